@@ -1,0 +1,247 @@
+/*
+ * af.h -- C ABI of libautofreeze: AutoFreeze's per-iteration freezing hot path
+ * (arXiv 2102.01386) on NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (section / equation /
+ * algorithm named beside it); S:n = SPEC.md line n; Qn = the readings of
+ * SURVEY.md §8(c), restated in DESIGN.md.
+ *
+ * The path:
+ *   af_layer_norms        per step: Delta += g over the active segments (P:196
+ *                         §3.1.1 "we accumulate gradients for each layer");
+ *                         at the interval end: per-segment sum of squares of
+ *                         Delta_T = Delta + g (the norm of Eq. 1), and with
+ *                         P > 1 ranks the exchange of the per-segment partials.
+ *   af_update_and_decide  Eq. 1, the N-th percentile threshold
+ *                         (Alg. 1) and the prefix-only freeze scan
+ *                         (Alg. 1), state roll, decision record.
+ *   af_cache_put / get    the Storage Manager's write / read of frozen-prefix
+ *                         activations keyed by original example id with
+ *                         evict-on-read (§3.2), one partition per GPU
+ *                         (§3.4 "each GPU manages its own cache").
+ *
+ * Conventions for every entry point:
+ *  - Returns af_status; never prints, throws or aborts.
+ *  - Argument / state errors are reported synchronously and ENQUEUE NOTHING.
+ *  - Device pointers are owned by the caller (e.g. torch tensors); the library
+ *    borrows them for the stream-ordered work it enqueues and never frees them.
+ *    The library owns only host metadata and (optionally) an NCCL communicator.
+ *  - Work is enqueued on the given cudaStream_t (passed as void*; NULL = legacy
+ *    default stream) and is asynchronous unless the entry says "synchronous".
+ *    All enqueued work is CUDA-graph capturable (no host syncs, no allocation).
+ *  - One af_ctx / af_cache per (process, device); handles are not thread-safe.
+ *  - There is no CPU fallback: if no CUDA device is usable, calls that must
+ *    touch the device return AF_ECUDA.
+ */
+#ifndef AF_H_
+#define AF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define AF_API __attribute__((visibility("default")))
+#else
+#define AF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  AF_OK = 0,
+  AF_EINVAL = 1,      /* bad argument (NULL, misaligned, out of range, bad layout)  */
+  AF_ESTATE = 2,      /* call out of order (e.g. decide without an interval end)     */
+  AF_EWORKSPACE = 3,  /* workspace / storage not bound                               */
+  AF_ECUDA = 4,       /* a CUDA runtime call failed (message: af_last_error)         */
+  AF_ENCCL = 5,       /* an NCCL call failed                                         */
+  AF_ENONFINITE = 6,  /* reserved: non-finite sums are reported in af_decision.flags */
+  AF_EOWNER = 7,      /* reserved: wrong-owner ids are reported by af_cache_status   */
+  AF_ERANGE = 8       /* a size does not fit the 64-bit / int32 limits               */
+} af_status;
+
+typedef enum { AF_DT_F32 = 0, AF_DT_BF16 = 1 } af_dtype;
+
+/* Segment kinds of the flat gradient buffer, in the order PRE* POOL+ HEAD*.
+ * POOL = a transformer block, the paper's "layer" (§2.2); PRE = the
+ * embeddings, frozen together with the first block (§4.1, Q11);
+ * HEAD = pooler + classifier, never frozen (Q12). */
+typedef enum { AF_SEG_PRE = 0, AF_SEG_POOL = 1, AF_SEG_HEAD = 2 } af_seg_kind;
+
+/* What "accumulated gradients Delta" means (Q1).  DELTA is the paper's reading:
+ * the elementwise vector sum over the interval, then its L2 norm (P:196, P:632:
+ * the 453 MB accumulator is one fp32 copy of the model).  STEP_SUMSQ is the
+ * alternative reading sum_t ||g_t||^2 (no Delta buffer). */
+typedef enum { AF_ACC_DELTA = 0, AF_ACC_STEP_SUMSQ = 1 } af_acc_mode;
+
+/* Percentile method (Q4): LINEAR = numpy's default "linear" (Hyndman-Fan type 7,
+ * numpy's two-branch lerp, bit-identical to numpy.percentile); NEAREST_RANK =
+ * the value of ordinal rank ceil(N/100 * n) (S:176 flag). */
+typedef enum { AF_PCT_LINEAR = 0, AF_PCT_NEAREST_RANK = 1 } af_pct_method;
+
+#define AF_MAX_SEGMENTS 256
+#define AF_MAX_WORLD 64
+
+/* af_layer_norms / af_update_and_decide flags */
+#define AF_INTERVAL_END 0x1u /* this step ends the evaluation interval (every k/5 iterations) */
+#define AF_DRY_RUN 0x2u      /* do all the work but commit no state: Delta stays armed, f/prev/T unchanged */
+
+/* af_decision.flags */
+#define AF_DEC_FIRST_INTERVAL 0x1u /* T == 0: norms recorded, no decision (Q9)            */
+#define AF_DEC_SKIPPED_FEW 0x2u    /* fewer than min_active active POOL layers (Q10)       */
+#define AF_DEC_NEAR_TIE 0x4u       /* a scanned eta within tie_rel_eps*thr of the threshold (Q16) */
+#define AF_DEC_NONFINITE 0x8u      /* a sum of squares was Inf/NaN: state unchanged (Q8)          */
+#define AF_DEC_DRY_RUN 0x10u       /* produced under AF_DRY_RUN                                    */
+
+/* af_cache_status device error flags (sticky) */
+#define AF_CACHE_ERR_RANGE 0x1u /* an id outside [0, num_examples)               */
+#define AF_CACHE_ERR_OWNER 0x2u /* an id with id % world != rank (P:335 partition) */
+
+typedef struct {
+  int32_t n_segments;          /* L, 1..AF_MAX_SEGMENTS                                   */
+  const int64_t *seg_offsets;  /* host, L+1 element offsets; [0] = 0, strictly increasing */
+  const int32_t *seg_kinds;    /* host, L kinds (af_seg_kind) in the order PRE* POOL+ HEAD* */
+  af_dtype grad_dtype;         /* dtype of the flat gradient buffer                       */
+} af_layout;
+
+typedef struct {
+  double percentile;       /* N of Alg. 1, in (0, 100]; the paper's default is 50 */
+  af_pct_method pct_method;
+  af_acc_mode acc_mode;
+  double tie_rel_eps;      /* near-tie window, e.g. 1e-5 (north_star)                 */
+  int32_t min_active;      /* skip the test below this many active POOL layers; >= 1 (default 2) */
+  int32_t rank, world;     /* this process's shard of the flat buffer; world in [1, AF_MAX_WORLD] */
+} af_config;
+
+/* The decision record of one interval (Alg. 1 output + the quantities that
+ * produced it).  Arrays are indexed by segment; entries >= n_segments are 0. */
+typedef struct {
+  int32_t interval;          /* T of the evaluated interval (0-based, continuous across epochs, Q15) */
+  int32_t boundary_before;   /* f: frozen POOL count before the decision                   */
+  int32_t boundary_after;    /* f + k (the newly frozen prefix), or f if nothing committed  */
+  int32_t n_active;          /* active POOL layers considered (P:174 activeLayers)          */
+  double threshold;          /* N-th percentile of eta over the active POOL (NaN if none)  */
+  uint32_t flags;            /* AF_DEC_*                                                   */
+  int32_t near_tie_seg;      /* first segment flagged NEAR_TIE, or -1                       */
+  double sumsq[AF_MAX_SEGMENTS]; /* ||Delta_T,l||^2 (0 for frozen segments)                 */
+  double norm[AF_MAX_SEGMENTS];  /* ||Delta_T,l||                                          */
+  double eta[AF_MAX_SEGMENTS];   /* Eq. 1 per segment, 0 where the previous norm is 0      */
+} af_decision;
+
+/* Host-side description of a created context (no device access). */
+typedef struct {
+  int32_t n_segments, n_pool, rank, world;
+  int64_t n_total;                  /* elements of the full flat buffer                  */
+  int64_t shard_begin, shard_end;   /* this rank's element range (multiples of 8 except n) */
+  int32_t n_tiles;                  /* segment-aligned tiles of the shard                */
+  int32_t tile_elems;               /* nominal tile size in elements                     */
+  int32_t first_tile_of_pool[AF_MAX_SEGMENTS + 1]; /* first active tile when f = j frozen */
+} af_info;
+
+typedef struct af_ctx af_ctx;
+typedef struct af_cache af_cache;
+
+/* ---- freezing module ------------------------------------------------------ */
+
+/* Host only (no device access).  Validates and copies the layout (offsets
+ * strictly increasing from 0, kinds in the order PRE* POOL+ HEAD* with >= 1
+ * POOL), the config, builds the segment-aligned tile table of this rank's
+ * contiguous shard [floor(r*n/P) rounded down to 8, ...).
+ * AF_EINVAL on any violation; *out untouched on error. */
+AF_API af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **out);
+
+/* Host only.  Bytes of the two caller-owned device buffers:
+ * accum = the fp32 Delta shard (n_local * 4 B; 0 in STEP_SUMSQ mode);
+ * scratch = device state, tile table, partials, exchange rows, decision ring. */
+AF_API af_status af_ctx_workspace_bytes(const af_ctx *ctx, size_t *accum_bytes, size_t *scratch_bytes);
+
+/* Host only.  Fills *info. */
+AF_API af_status af_ctx_info(const af_ctx *ctx, af_info *info);
+
+/* Synchronous.  Binds caller-allocated device buffers (256-byte aligned, sizes
+ * from af_ctx_workspace_bytes, on the current device) and initialises the
+ * device state (T = 0, f = 0).  accum may be NULL iff accum_bytes == 0. */
+AF_API af_status af_ctx_bind(af_ctx *ctx, void *accum_dev, void *scratch_dev);
+
+/* Synchronous, collective over all `world` ranks.  Creates the library's NCCL
+ * communicator from a 128-byte ncclUniqueId produced by af_nccl_unique_id on
+ * rank 0 and broadcast by the caller (e.g. torch.distributed).  Without a
+ * communicator a world > 1 context runs in "external exchange" mode: the caller
+ * fills the other ranks' rows of af_ctx_exchange_rows before deciding. */
+AF_API af_status af_nccl_unique_id(void *id_128B);
+AF_API af_status af_ctx_set_comm(af_ctx *ctx, const void *nccl_unique_id_128B);
+
+/* Device pointer of the exchange matrix ss_all[world][n_segments] (fp64, row r
+ * = rank r's per-segment partial sums) inside the bound scratch. */
+AF_API af_status af_ctx_exchange_rows(af_ctx *ctx, double **ss_all_dev);
+
+/* One training step.  grad_dev = the FULL flat gradient
+ * buffer (n_total elements of grad_dtype, 16-byte aligned; only this rank's
+ * shard is read).  Frozen segments (PRE and POOL[0..f) once f >= 1, read from
+ * device state) are skipped.  Without AF_INTERVAL_END: Delta <- Delta + g
+ * (Delta <- g on the first step of an interval).  With AF_INTERVAL_END: the
+ * per-segment fp64 sums of squares of Delta_T = Delta + g are formed (Delta is
+ * not written back: the next interval restarts it), then (world > 1 with a
+ * communicator) all-gathered.  AF_DRY_RUN: the next step still sees Delta armed. */
+AF_API af_status af_layer_norms(af_ctx *ctx, const void *grad_dev, uint32_t flags, void *stream);
+
+/* Eq. 1, threshold, prefix scan and state roll on the gathered sums (a5-a9).
+ * AF_ESTATE unless an AF_INTERVAL_END af_layer_norms precedes it.  With
+ * out_host != NULL (page-locked host memory, e.g. torch pin_memory) the record
+ * is copied there asynchronously; it is valid once the stream reaches this
+ * point.  AF_DRY_RUN: everything is computed and recorded, nothing committed. */
+AF_API af_status af_update_and_decide(af_ctx *ctx, uint32_t flags, af_decision *out_host, void *stream);
+
+/* Synchronous.  Serialise / restore {T, f, prev norms, Delta-armed flag}
+ * (checkpoint at interval boundaries is exact).  With buf == NULL, get_state
+ * stores the required size in *len. */
+AF_API af_status af_get_state(af_ctx *ctx, void *buf, size_t *len);
+AF_API af_status af_set_state(af_ctx *ctx, const void *buf, size_t len);
+
+AF_API af_status af_ctx_destroy(af_ctx *ctx);
+
+/* ---- storage manager (activation cache) ----------------------------------- */
+
+/* Host only.  A direct-mapped HBM cache of this rank's ids {id : id % world ==
+ * rank, 0 <= id < num_examples}, slot = id / world, rows of row_bytes (a
+ * positive multiple of 16). */
+AF_API af_status af_cache_create(int64_t num_examples, int64_t row_bytes, int32_t rank, int32_t world,
+                          af_cache **out);
+AF_API af_status af_cache_storage_bytes(const af_cache *c, size_t *payload_bytes, size_t *meta_bytes);
+/* Synchronous: binds caller-owned device storage and clears every record. */
+AF_API af_status af_cache_bind(af_cache *c, void *payload_dev, void *meta_dev);
+
+/* Write n rows (rows_dev: n x row_bytes, 16-byte aligned) for the unique
+ * original ids ids_dev[0..n) (int64, device) at depth >= 1 = the frozen POOL
+ * count whose output the rows hold ("the output of the forward pass up
+ * to layer L is written to cache").  Ids outside this rank's partition set a
+ * sticky error flag and are skipped. */
+AF_API af_status af_cache_put(af_cache *c, const int64_t *ids_dev, int32_t n, const void *rows_dev,
+                       int32_t depth, void *stream);
+
+/* Read n unique ids: for a valid record copy it to rows_out_dev[i] and set
+ * depth_out_dev[i] = its depth, then evict it if depth < cur_boundary (P:276:
+ * the frozen count grew since it was written); otherwise depth_out_dev[i] = -1
+ * and rows_out_dev[i] is untouched. */
+AF_API af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
+                       void *rows_out_dev, int32_t *depth_out_dev, void *stream);
+
+/* Synchronous: sticky AF_CACHE_ERR_* flags and the count of valid records. */
+AF_API af_status af_cache_status(af_cache *c, uint32_t *device_error_flags, int64_t *n_valid);
+AF_API af_status af_cache_destroy(af_cache *c);
+
+/* Cache-vs-recompute rule (§3.2): 1 iff frozen_layers *
+ * t_layer_fwd_s > t_batch_read_s, else 0 (also 0 for negative inputs). */
+AF_API int af_should_cache(int32_t frozen_layers, double t_layer_fwd_s, double t_batch_read_s);
+
+AF_API const char *af_status_str(af_status s);
+/* Thread-local text of the last AF_ECUDA / AF_ENCCL / AF_EINVAL cause. */
+AF_API const char *af_last_error(void);
+/* Library version, e.g. "0.1.0". */
+AF_API const char *af_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AF_H_ */

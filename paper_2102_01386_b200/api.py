@@ -1,0 +1,209 @@
+"""Thin Python binding over libautofreeze (include/af.h), same names as the ABI.
+
+PyTorch supplies device memory (workspace, cache storage), streams/events and
+torch.distributed for the NCCL-id bootstrap.  Every step of the path runs in the
+library's sm_100a kernels; nothing here computes.
+"""
+import ctypes
+from ctypes import byref, c_int64, c_size_t, c_uint32, c_void_p
+
+import torch
+
+from . import _lib as L
+from ._lib import check, lib
+
+_DTYPES = {"f32": L.AF_DT_F32, "fp32": L.AF_DT_F32, torch.float32: L.AF_DT_F32,
+           "bf16": L.AF_DT_BF16, torch.bfloat16: L.AF_DT_BF16}
+_PCT = {"linear": L.AF_PCT_LINEAR, "nearest_rank": L.AF_PCT_NEAREST_RANK}
+_ACC = {"delta": L.AF_ACC_DELTA, "step_sumsq": L.AF_ACC_STEP_SUMSQ}
+
+
+def _stream_handle(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return c_void_p(s.cuda_stream)
+
+
+def decision_to_dict(rec, n_segments):
+    return dict(interval=rec.interval, boundary_before=rec.boundary_before,
+                boundary_after=rec.boundary_after, n_active=rec.n_active,
+                threshold=rec.threshold, flags=rec.flags, near_tie_seg=rec.near_tie_seg,
+                sumsq=list(rec.sumsq[:n_segments]), norm=list(rec.norm[:n_segments]),
+                eta=list(rec.eta[:n_segments]))
+
+
+class FreezingModule:
+    """af_ctx: the per-GPU Freezing Module (§3.4, Alg. 1).
+
+    offsets: L+1 element offsets of the flat gradient buffer; kinds: L segment
+    kinds (0 PRE, 1 POOL, 2 HEAD) in the order PRE* POOL+ HEAD*."""
+
+    def __init__(self, offsets, kinds, grad_dtype="bf16", percentile=50.0, pct_method="linear",
+                 acc_mode="delta", tie_rel_eps=1e-5, min_active=2, rank=0, world=1, device=None,
+                 bind=True):
+        self.offsets = [int(o) for o in offsets]
+        self.kinds = [int(k) for k in kinds]
+        self.n_segments = len(self.kinds)
+        self._offs = (ctypes.c_int64 * len(self.offsets))(*self.offsets)
+        self._kinds = (ctypes.c_int32 * max(1, len(self.kinds)))(*self.kinds)
+        lay = L.AfLayout(len(self.kinds), self._offs, self._kinds, _DTYPES[grad_dtype])
+        cfg = L.AfConfig(float(percentile), _PCT[pct_method], _ACC[acc_mode], float(tie_rel_eps),
+                         int(min_active), int(rank), int(world))
+        h = c_void_p()
+        check(lib.af_ctx_create(byref(lay), byref(cfg), byref(h)), "af_ctx_create")
+        self._h = h
+        self.grad_dtype = _DTYPES[grad_dtype]
+        self.rank, self.world = int(rank), int(world)
+        a, s = c_size_t(), c_size_t()
+        check(lib.af_ctx_workspace_bytes(h, byref(a), byref(s)), "af_ctx_workspace_bytes")
+        self.accum_bytes, self.scratch_bytes = a.value, s.value
+        self.device = device
+        self.accum = self.scratch = None
+        self._rec_host = None
+        self._event = None
+        if bind:
+            self.bind(device)
+
+    # -- setup -------------------------------------------------------------------
+    def info(self):
+        i = L.AfInfo()
+        check(lib.af_ctx_info(self._h, byref(i)), "af_ctx_info")
+        return dict(n_segments=i.n_segments, n_pool=i.n_pool, rank=i.rank, world=i.world,
+                    n_total=i.n_total, shard_begin=i.shard_begin, shard_end=i.shard_end,
+                    n_tiles=i.n_tiles, tile_elems=i.tile_elems,
+                    first_tile_of_pool=list(i.first_tile_of_pool[:i.n_pool + 1]))
+
+    def bind(self, device=None):
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        with torch.cuda.device(dev):
+            self.accum = torch.empty(max(1, self.accum_bytes), dtype=torch.uint8, device=dev)
+            self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device=dev)
+            check(lib.af_ctx_bind(self._h, c_void_p(self.accum.data_ptr() if self.accum_bytes else 0),
+                                  c_void_p(self.scratch.data_ptr())), "af_ctx_bind")
+        self._rec_host = torch.empty(ctypes.sizeof(L.AfDecision), dtype=torch.uint8, pin_memory=True)
+        self._event = torch.cuda.Event()
+
+    def set_comm(self, group=None):
+        """Collective: create the library's NCCL communicator (rank 0 makes the id,
+        torch.distributed broadcasts it over `group`)."""
+        import torch.distributed as dist
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            buf = (ctypes.c_uint8 * 128)()
+            check(lib.af_nccl_unique_id(buf), "af_nccl_unique_id")
+            uid[:] = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        backend = dist.get_backend(group)
+        t = uid.to(self.device) if backend == "nccl" else uid
+        dist.broadcast(t, src=0, group=group)
+        raw = bytes(t.cpu().tolist())
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(raw)
+        with torch.cuda.device(self.device):
+            check(lib.af_ctx_set_comm(self._h, buf), "af_ctx_set_comm")
+
+    def exchange_rows(self):
+        """float64 view [world, L] of the exchange matrix inside the scratch buffer."""
+        p = c_void_p()
+        check(lib.af_ctx_exchange_rows(self._h, byref(p)), "af_ctx_exchange_rows")
+        off = p.value - self.scratch.data_ptr()
+        n = self.world * self.n_segments * 8
+        return self.scratch[off:off + n].view(torch.float64).view(self.world, self.n_segments)
+
+    # -- the hot path --------------------------------------------------------------
+    def layer_norms(self, grad, interval_end=False, dry_run=False, stream=None):
+        flags = (L.AF_INTERVAL_END if interval_end else 0) | (L.AF_DRY_RUN if dry_run else 0)
+        check(lib.af_layer_norms(self._h, c_void_p(grad.data_ptr()), flags, _stream_handle(stream)),
+              "af_layer_norms")
+
+    def update_and_decide(self, dry_run=False, stream=None, copy_record=True):
+        flags = L.AF_DRY_RUN if dry_run else 0
+        out = c_void_p(self._rec_host.data_ptr()) if copy_record else c_void_p(0)
+        check(lib.af_update_and_decide(self._h, flags, out, _stream_handle(stream)), "af_update_and_decide")
+        if copy_record:
+            self._event.record(stream if stream is not None else torch.cuda.current_stream())
+
+    def decision(self):
+        """The last copied decision record (waits for the stream to reach it)."""
+        self._event.synchronize()
+        rec = L.AfDecision.from_address(self._rec_host.data_ptr())
+        return decision_to_dict(rec, self.n_segments)
+
+    def get_state(self):
+        n = c_size_t()
+        check(lib.af_get_state(self._h, None, byref(n)), "af_get_state")
+        buf = ctypes.create_string_buffer(n.value)
+        check(lib.af_get_state(self._h, buf, byref(n)), "af_get_state")
+        return buf.raw[:n.value]
+
+    def set_state(self, blob):
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        check(lib.af_set_state(self._h, buf, len(blob)), "af_set_state")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.af_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ActivationCache:
+    """af_cache: the Storage Manager's HBM cache of frozen-prefix outputs for this
+    rank's ids (§3.2, P:335 partition by id mod world)."""
+
+    def __init__(self, num_examples, row_bytes, rank=0, world=1, device=None, bind=True):
+        h = c_void_p()
+        check(lib.af_cache_create(int(num_examples), int(row_bytes), int(rank), int(world), byref(h)),
+              "af_cache_create")
+        self._h = h
+        self.num_examples, self.row_bytes, self.rank, self.world = int(num_examples), int(row_bytes), rank, world
+        p, m = c_size_t(), c_size_t()
+        check(lib.af_cache_storage_bytes(h, byref(p), byref(m)), "af_cache_storage_bytes")
+        self.payload_bytes, self.meta_bytes = p.value, m.value
+        self.payload = self.meta = None
+        if bind:
+            self.bind(device)
+
+    def bind(self, device=None):
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        with torch.cuda.device(dev):
+            self.payload = torch.empty(max(16, self.payload_bytes), dtype=torch.uint8, device=dev)
+            self.meta = torch.empty(self.meta_bytes, dtype=torch.uint8, device=dev)
+            check(lib.af_cache_bind(self._h, c_void_p(self.payload.data_ptr()), c_void_p(self.meta.data_ptr())),
+                  "af_cache_bind")
+
+    def put(self, ids, rows, depth, stream=None):
+        n = int(ids.numel())
+        check(lib.af_cache_put(self._h, c_void_p(ids.data_ptr()), n, c_void_p(rows.data_ptr()), int(depth),
+                               _stream_handle(stream)), "af_cache_put")
+
+    def get(self, ids, cur_boundary, rows_out, depth_out, stream=None):
+        n = int(ids.numel())
+        check(lib.af_cache_get(self._h, c_void_p(ids.data_ptr()), n, int(cur_boundary),
+                               c_void_p(rows_out.data_ptr()), c_void_p(depth_out.data_ptr()),
+                               _stream_handle(stream)), "af_cache_get")
+
+    def status(self):
+        e, v = c_uint32(), c_int64()
+        check(lib.af_cache_status(self._h, byref(e), byref(v)), "af_cache_status")
+        return e.value, v.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.af_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def should_cache(frozen_layers, t_layer_fwd_s, t_batch_read_s):
+    """PAPER.md:230-235 §3.2 cache-vs-recompute rule, evaluated by the library."""
+    return bool(lib.af_should_cache(int(frozen_layers), float(t_layer_fwd_s), float(t_batch_read_s)))

@@ -1,0 +1,570 @@
+// af_api.cpp -- host side of the C ABI declared in include/af.h.
+//
+// Owns only host metadata (layout copy, shard bounds, tile table, host flags)
+// and the optional NCCL communicator; every device buffer is caller-owned.
+// Validation errors are synchronous and enqueue nothing.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "af_internal.h"
+
+using namespace af;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+af_status fail(af_status s, const char *what) {
+  g_last_error = what;
+  return s;
+}
+af_status cuda_fail(cudaError_t e, const char *where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return AF_ECUDA;
+}
+af_status nccl_fail(ncclResult_t r, const char *where) {
+  g_last_error = std::string(where) + ": " + ncclGetErrorString(r);
+  return AF_ENCCL;
+}
+
+#define AF_CUDA(call, where)                     \
+  do {                                           \
+    cudaError_t e_ = (call);                     \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int device_sm_count(int *sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  return static_cast<int>(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
+}
+
+}  // namespace
+
+struct af_ctx {
+  // layout / config (host copies)
+  int L = 0, n_pool = 0;
+  std::vector<int64_t> offs;
+  std::vector<int32_t> kinds, pool_seg;
+  af_dtype dtype = AF_DT_F32;
+  af_config cfg{};
+  int64_t n = 0, sb = 0, se = 0;
+  int tile_elems = 0;
+  std::vector<Tile> tiles;
+  std::vector<int32_t> seg_tile_begin, first_tile_of_f;
+  // workspace
+  size_t accum_bytes = 0, scratch_bytes = 0;
+  size_t o_state = 0, o_sched = 0, o_tiles = 0, o_ftf = 0, o_stb = 0, o_pool = 0, o_part = 0, o_ssall = 0,
+         o_ssacc = 0, o_last = 0, o_ring = 0;
+  float *accum = nullptr;
+  char *scratch = nullptr;
+  bool bound = false;
+  int grid = 0;
+  // host flags
+  bool armed = false;    // Delta / ss_acc hold this interval's partial sum
+  bool pending = false;  // an interval end awaits af_update_and_decide
+  ncclComm_t comm = nullptr;
+
+  template <typename T>
+  T *at(size_t o) const {
+    return reinterpret_cast<T *>(scratch + o);
+  }
+};
+
+struct af_cache {
+  int64_t num_examples = 0, row_bytes = 0, capacity = 0;
+  int32_t rank = 0, world = 1;
+  char *payload = nullptr;
+  char *meta = nullptr;  // [Sched | err | pad][CacheMeta x capacity]
+  bool bound = false;
+  int grid = 0;
+};
+
+static constexpr size_t kMetaHeader = 256;
+
+extern "C" {
+
+const char *af_status_str(af_status s) {
+  switch (s) {
+    case AF_OK: return "AF_OK";
+    case AF_EINVAL: return "AF_EINVAL";
+    case AF_ESTATE: return "AF_ESTATE";
+    case AF_EWORKSPACE: return "AF_EWORKSPACE";
+    case AF_ECUDA: return "AF_ECUDA";
+    case AF_ENCCL: return "AF_ENCCL";
+    case AF_ENONFINITE: return "AF_ENONFINITE";
+    case AF_EOWNER: return "AF_EOWNER";
+    case AF_ERANGE: return "AF_ERANGE";
+  }
+  return "AF_UNKNOWN";
+}
+
+const char *af_last_error(void) { return g_last_error.c_str(); }
+const char *af_version(void) { return "0.1.0"; }
+
+int af_should_cache(int32_t frozen_layers, double t_layer_fwd_s, double t_batch_read_s) {
+  if (frozen_layers <= 0 || !(t_layer_fwd_s >= 0.0) || !(t_batch_read_s >= 0.0)) return 0;
+  return static_cast<double>(frozen_layers) * t_layer_fwd_s > t_batch_read_s ? 1 : 0;
+}
+
+af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **out) {
+  if (!layout || !cfg || !out) return fail(AF_EINVAL, "NULL argument");
+  const int L = layout->n_segments;
+  if (L < 1 || L > AF_MAX_SEGMENTS) return fail(AF_EINVAL, "n_segments out of [1, AF_MAX_SEGMENTS]");
+  if (!layout->seg_offsets || !layout->seg_kinds) return fail(AF_EINVAL, "NULL offsets / kinds");
+  if (layout->grad_dtype != AF_DT_F32 && layout->grad_dtype != AF_DT_BF16) return fail(AF_EINVAL, "bad grad_dtype");
+  if (layout->seg_offsets[0] != 0) return fail(AF_EINVAL, "seg_offsets[0] must be 0");
+  for (int l = 0; l < L; ++l)
+    if (layout->seg_offsets[l + 1] <= layout->seg_offsets[l]) return fail(AF_EINVAL, "offsets not strictly increasing");
+  const int64_t n = layout->seg_offsets[L];
+  if (n > (int64_t(1) << 50)) return fail(AF_ERANGE, "n_total too large");
+  // kinds: PRE* POOL+ HEAD*
+  int phase = 0, n_pool = 0;
+  for (int l = 0; l < L; ++l) {
+    const int k = layout->seg_kinds[l];
+    if (k < AF_SEG_PRE || k > AF_SEG_HEAD) return fail(AF_EINVAL, "bad segment kind");
+    if (k < phase) return fail(AF_EINVAL, "segment kinds must be ordered PRE* POOL+ HEAD*");
+    if (k == AF_SEG_PRE && phase > AF_SEG_PRE) return fail(AF_EINVAL, "PRE after POOL/HEAD");
+    phase = k;
+    n_pool += (k == AF_SEG_POOL);
+  }
+  if (n_pool < 1) return fail(AF_EINVAL, "layout needs at least one POOL segment");
+  if (!(cfg->percentile > 0.0 && cfg->percentile <= 100.0)) return fail(AF_EINVAL, "percentile out of (0, 100]");
+  if (cfg->pct_method != AF_PCT_LINEAR && cfg->pct_method != AF_PCT_NEAREST_RANK)
+    return fail(AF_EINVAL, "bad pct_method");
+  if (cfg->acc_mode != AF_ACC_DELTA && cfg->acc_mode != AF_ACC_STEP_SUMSQ) return fail(AF_EINVAL, "bad acc_mode");
+  if (!(cfg->tie_rel_eps >= 0.0) || !std::isfinite(cfg->tie_rel_eps)) return fail(AF_EINVAL, "bad tie_rel_eps");
+  if (cfg->min_active < 1) return fail(AF_EINVAL, "min_active must be >= 1");
+  if (cfg->world < 1 || cfg->world > AF_MAX_WORLD) return fail(AF_EINVAL, "world out of [1, AF_MAX_WORLD]");
+  if (cfg->rank < 0 || cfg->rank >= cfg->world) return fail(AF_EINVAL, "rank out of [0, world)");
+
+  af_ctx *c = new (std::nothrow) af_ctx();
+  if (!c) return fail(AF_EINVAL, "out of host memory");
+  c->L = L;
+  c->n_pool = n_pool;
+  c->offs.assign(layout->seg_offsets, layout->seg_offsets + L + 1);
+  c->kinds.assign(layout->seg_kinds, layout->seg_kinds + L);
+  for (int l = 0; l < L; ++l)
+    if (c->kinds[l] == AF_SEG_POOL) c->pool_seg.push_back(l);
+  c->dtype = layout->grad_dtype;
+  c->cfg = *cfg;
+  c->n = n;
+  // contiguous shard, bounds rounded down to multiples of 8 elements
+  auto bound_of = [&](int r) -> int64_t {
+    if (r <= 0) return 0;
+    if (r >= cfg->world) return n;
+    const unsigned __int128 x = static_cast<unsigned __int128>(n) * static_cast<unsigned>(r) / cfg->world;
+    return static_cast<int64_t>(x) / kShardAlign * kShardAlign;
+  };
+  c->sb = bound_of(cfg->rank);
+  c->se = bound_of(cfg->rank + 1);
+  // segment-aligned tile table of the shard (tile edges on a global grid of tile_elems)
+  const int esz = (c->dtype == AF_DT_BF16) ? 2 : 4;
+  c->tile_elems = kTileBytes / esz;
+  const int64_t TE = c->tile_elems;
+  c->seg_tile_begin.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l) {
+    c->seg_tile_begin[l] = static_cast<int32_t>(c->tiles.size());
+    const int64_t lo = std::max(c->offs[l], c->sb), hi = std::min(c->offs[l + 1], c->se);
+    for (int64_t pos = lo; pos < hi;) {
+      const int64_t nxt = std::min(hi, (pos / TE + 1) * TE);
+      c->tiles.push_back(Tile{pos, nxt, l, 0});
+      pos = nxt;
+    }
+    if (c->tiles.size() > static_cast<size_t>(1) << 30) {
+      delete c;
+      return fail(AF_ERANGE, "too many tiles");
+    }
+  }
+  c->seg_tile_begin[L] = static_cast<int32_t>(c->tiles.size());
+  // first active tile when j POOL layers are frozen: PRE and POOL[0..j) skipped (Q11)
+  c->first_tile_of_f.assign(n_pool + 1, 0);
+  for (int j = 0; j <= n_pool; ++j) {
+    int first_seg = 0;
+    if (j > 0) first_seg = (j < n_pool) ? c->pool_seg[j] : c->pool_seg[n_pool - 1] + 1;
+    c->first_tile_of_f[j] = c->seg_tile_begin[first_seg];
+  }
+  // workspace layout
+  const int64_t n_local = c->se - c->sb;
+  c->accum_bytes = (cfg->acc_mode == AF_ACC_DELTA) ? static_cast<size_t>(n_local) * sizeof(float) : 0;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + (bytes ? bytes : 1), 256);
+    return at;
+  };
+  c->o_state = take(sizeof(DevState));
+  c->o_sched = take(4 * sizeof(Sched));
+  c->o_tiles = take(c->tiles.size() * sizeof(Tile));
+  c->o_ftf = take((n_pool + 1) * sizeof(int32_t));
+  c->o_stb = take((L + 1) * sizeof(int32_t));
+  c->o_pool = take(n_pool * sizeof(int32_t));
+  c->o_part = take(c->tiles.size() * sizeof(double));
+  c->o_ssall = take(static_cast<size_t>(cfg->world) * L * sizeof(double));
+  c->o_ssacc = take(L * sizeof(double));
+  c->o_last = take(sizeof(af_decision));
+  c->o_ring = take(kRing * sizeof(af_decision));
+  c->scratch_bytes = o;
+  *out = c;
+  return AF_OK;
+}
+
+af_status af_ctx_workspace_bytes(const af_ctx *c, size_t *accum_bytes, size_t *scratch_bytes) {
+  if (!c || !accum_bytes || !scratch_bytes) return fail(AF_EINVAL, "NULL argument");
+  *accum_bytes = c->accum_bytes;
+  *scratch_bytes = c->scratch_bytes;
+  return AF_OK;
+}
+
+af_status af_ctx_info(const af_ctx *c, af_info *info) {
+  if (!c || !info) return fail(AF_EINVAL, "NULL argument");
+  std::memset(info, 0, sizeof(*info));
+  info->n_segments = c->L;
+  info->n_pool = c->n_pool;
+  info->rank = c->cfg.rank;
+  info->world = c->cfg.world;
+  info->n_total = c->n;
+  info->shard_begin = c->sb;
+  info->shard_end = c->se;
+  info->n_tiles = static_cast<int32_t>(c->tiles.size());
+  info->tile_elems = c->tile_elems;
+  for (int j = 0; j <= c->n_pool; ++j) info->first_tile_of_pool[j] = c->first_tile_of_f[j];
+  return AF_OK;
+}
+
+af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
+  if (!c || !scratch_dev) return fail(AF_EINVAL, "NULL argument");
+  if (c->accum_bytes && !accum_dev) return fail(AF_EINVAL, "accum buffer required");
+  if (!aligned(scratch_dev, 256) || (accum_dev && !aligned(accum_dev, 256)))
+    return fail(AF_EINVAL, "workspace buffers must be 256-byte aligned");
+  int sms = 0, bps = 0;
+  cudaError_t e = static_cast<cudaError_t>(device_sm_count(&sms));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  e = static_cast<cudaError_t>(norms_max_blocks_per_sm(kEndDelta, c->dtype, &bps));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  c->grid = std::max(1, sms * std::max(1, bps));
+  c->accum = static_cast<float *>(accum_dev);
+  c->scratch = static_cast<char *>(scratch_dev);
+  AF_CUDA(cudaMemset(c->scratch, 0, c->scratch_bytes), "cudaMemset(scratch)");
+  if (!c->tiles.empty())
+    AF_CUDA(cudaMemcpy(c->scratch + c->o_tiles, c->tiles.data(), c->tiles.size() * sizeof(Tile),
+                       cudaMemcpyHostToDevice),
+            "cudaMemcpy(tiles)");
+  AF_CUDA(cudaMemcpy(c->scratch + c->o_ftf, c->first_tile_of_f.data(), c->first_tile_of_f.size() * 4,
+                     cudaMemcpyHostToDevice),
+          "cudaMemcpy(first_tile_of_f)");
+  AF_CUDA(cudaMemcpy(c->scratch + c->o_stb, c->seg_tile_begin.data(), c->seg_tile_begin.size() * 4,
+                     cudaMemcpyHostToDevice),
+          "cudaMemcpy(seg_tile_begin)");
+  AF_CUDA(cudaMemcpy(c->scratch + c->o_pool, c->pool_seg.data(), c->pool_seg.size() * 4, cudaMemcpyHostToDevice),
+          "cudaMemcpy(pool_seg)");
+  AF_CUDA(cudaDeviceSynchronize(), "bind");
+  c->bound = true;
+  c->armed = false;
+  c->pending = false;
+  return AF_OK;
+}
+
+af_status af_nccl_unique_id(void *id_128B) {
+  if (!id_128B) return fail(AF_EINVAL, "NULL argument");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(id_128B, &id, sizeof(id));
+  return AF_OK;
+}
+
+af_status af_ctx_set_comm(af_ctx *c, const void *id_128B) {
+  if (!c || !id_128B) return fail(AF_EINVAL, "NULL argument");
+  if (c->comm) return fail(AF_ESTATE, "communicator already set");
+  ncclUniqueId id;
+  std::memcpy(&id, id_128B, sizeof(id));
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = ncclCommInitRank(&comm, c->cfg.world, id, c->cfg.rank);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+  c->comm = comm;
+  return AF_OK;
+}
+
+af_status af_ctx_exchange_rows(af_ctx *c, double **ss_all_dev) {
+  if (!c || !ss_all_dev) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  *ss_all_dev = c->at<double>(c->o_ssall);
+  return AF_OK;
+}
+
+af_status af_layer_norms(af_ctx *c, const void *grad_dev, uint32_t flags, void *stream) {
+  if (!c) return fail(AF_EINVAL, "NULL ctx");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (!grad_dev || !aligned(grad_dev, 16)) return fail(AF_EINVAL, "grad must be a 16-byte aligned device pointer");
+  if (flags & ~(AF_INTERVAL_END | AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
+  const bool end = flags & AF_INTERVAL_END, dry = flags & AF_DRY_RUN;
+  int mode;
+  if (c->cfg.acc_mode == AF_ACC_DELTA)
+    mode = end ? kEndDelta : kAccum;
+  else
+    mode = kStepSq;
+  NormParams p{};
+  p.grad = grad_dev;
+  p.delta = c->accum;
+  p.shard_begin = c->sb;
+  p.tiles = c->at<Tile>(c->o_tiles);
+  p.n_tiles = static_cast<int32_t>(c->tiles.size());
+  p.L = c->L;
+  p.first_tile_of_f = c->at<int32_t>(c->o_ftf);
+  p.seg_tile_begin = c->at<int32_t>(c->o_stb);
+  p.state = c->at<DevState>(c->o_state);
+  p.sched = c->at<Sched>(c->o_sched);
+  p.partials = c->at<double>(c->o_part);
+  p.ss_out = c->at<double>(c->o_ssall) + static_cast<size_t>(c->cfg.rank) * c->L;
+  p.ss_acc = c->at<double>(c->o_ssacc);
+  p.n_pool = c->n_pool;
+  p.first = c->armed ? 0 : 1;
+  p.end = end ? 1 : 0;
+  p.commit = dry ? 0 : 1;
+  const int grid = std::max(1, std::min<int>(c->grid, std::max<int>(1, p.n_tiles)));
+  const int e = launch_norms(p, mode, c->dtype, grid, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "norms kernel launch");
+  if (end && c->cfg.world > 1 && c->comm) {
+    double *rows = c->at<double>(c->o_ssall);
+    ncclResult_t r = ncclAllGather(rows + static_cast<size_t>(c->cfg.rank) * c->L, rows, c->L, ncclFloat64, c->comm,
+                                   static_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+  }
+  if (!dry) c->armed = !end;
+  if (end) c->pending = true;
+  return AF_OK;
+}
+
+af_status af_update_and_decide(af_ctx *c, uint32_t flags, af_decision *out_host, void *stream) {
+  if (!c) return fail(AF_EINVAL, "NULL ctx");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (flags & ~(AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
+  if (!c->pending) return fail(AF_ESTATE, "af_update_and_decide without a preceding AF_INTERVAL_END");
+  const bool dry = flags & AF_DRY_RUN;
+  DecideParams p{};
+  p.ss_all = c->at<double>(c->o_ssall);
+  p.world = c->cfg.world;
+  p.L = c->L;
+  p.n_pool = c->n_pool;
+  p.pool_seg = c->at<int32_t>(c->o_pool);
+  p.state = c->at<DevState>(c->o_state);
+  p.last = c->at<af_decision>(c->o_last);
+  p.ring = c->at<af_decision>(c->o_ring);
+  p.percentile = c->cfg.percentile;
+  p.pct_method = c->cfg.pct_method;
+  p.tie_rel_eps = c->cfg.tie_rel_eps;
+  p.min_active = c->cfg.min_active;
+  p.commit = dry ? 0 : 1;
+  const int e = launch_decide(p, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "decide kernel launch");
+  if (out_host)
+    AF_CUDA(cudaMemcpyAsync(out_host, p.last, sizeof(af_decision), cudaMemcpyDeviceToHost,
+                            static_cast<cudaStream_t>(stream)),
+            "cudaMemcpyAsync(decision)");
+  if (!dry) c->pending = false;
+  return AF_OK;
+}
+
+struct StateBlob {
+  char magic[4];
+  int32_t version, L, world, rank, T, f, armed;
+  double prev[AF_MAX_SEGMENTS];
+  double ss_acc[AF_MAX_SEGMENTS];
+};
+
+af_status af_get_state(af_ctx *c, void *buf, size_t *len) {
+  if (!c || !len) return fail(AF_EINVAL, "NULL argument");
+  if (!buf) {
+    *len = sizeof(StateBlob);
+    return AF_OK;
+  }
+  if (*len < sizeof(StateBlob)) return fail(AF_EINVAL, "buffer too small");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  AF_CUDA(cudaDeviceSynchronize(), "get_state sync");
+  DevState st;
+  AF_CUDA(cudaMemcpy(&st, c->scratch + c->o_state, sizeof(st), cudaMemcpyDeviceToHost), "cudaMemcpy(state)");
+  StateBlob b{};
+  std::memcpy(b.magic, "AFS1", 4);
+  b.version = 1;
+  b.L = c->L;
+  b.world = c->cfg.world;
+  b.rank = c->cfg.rank;
+  b.T = st.T;
+  b.f = st.f;
+  b.armed = c->armed ? 1 : 0;
+  std::memcpy(b.prev, st.prev, sizeof(b.prev));
+  AF_CUDA(cudaMemcpy(b.ss_acc, c->scratch + c->o_ssacc, c->L * sizeof(double), cudaMemcpyDeviceToHost),
+          "cudaMemcpy(ss_acc)");
+  std::memcpy(buf, &b, sizeof(b));
+  *len = sizeof(b);
+  return AF_OK;
+}
+
+af_status af_set_state(af_ctx *c, const void *buf, size_t len) {
+  if (!c || !buf) return fail(AF_EINVAL, "NULL argument");
+  if (len < sizeof(StateBlob)) return fail(AF_EINVAL, "state blob too small");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  StateBlob b;
+  std::memcpy(&b, buf, sizeof(b));
+  if (std::memcmp(b.magic, "AFS1", 4) != 0 || b.version != 1) return fail(AF_EINVAL, "not an af state blob");
+  if (b.L != c->L) return fail(AF_EINVAL, "state blob has another segment count");
+  if (b.f < 0 || b.f > c->n_pool || b.T < 0) return fail(AF_EINVAL, "state blob out of range");
+  AF_CUDA(cudaDeviceSynchronize(), "set_state sync");
+  DevState st{};
+  st.T = b.T;
+  st.f = b.f;
+  std::memcpy(st.prev, b.prev, sizeof(st.prev));
+  AF_CUDA(cudaMemcpy(c->scratch + c->o_state, &st, sizeof(st), cudaMemcpyHostToDevice), "cudaMemcpy(state)");
+  AF_CUDA(cudaMemcpy(c->scratch + c->o_ssacc, b.ss_acc, c->L * sizeof(double), cudaMemcpyHostToDevice),
+          "cudaMemcpy(ss_acc)");
+  AF_CUDA(cudaDeviceSynchronize(), "set_state sync");
+  c->armed = b.armed != 0;
+  c->pending = false;
+  return AF_OK;
+}
+
+af_status af_ctx_destroy(af_ctx *c) {
+  if (!c) return fail(AF_EINVAL, "NULL ctx");
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  return AF_OK;
+}
+
+// ------------------------------------------------------------------ cache
+
+af_status af_cache_create(int64_t num_examples, int64_t row_bytes, int32_t rank, int32_t world, af_cache **out) {
+  if (!out) return fail(AF_EINVAL, "NULL argument");
+  if (num_examples < 0) return fail(AF_EINVAL, "num_examples < 0");
+  if (row_bytes <= 0 || row_bytes % 16 != 0) return fail(AF_EINVAL, "row_bytes must be a positive multiple of 16");
+  if (world < 1 || world > AF_MAX_WORLD || rank < 0 || rank >= world) return fail(AF_EINVAL, "bad rank/world");
+  af_cache *c = new (std::nothrow) af_cache();
+  if (!c) return fail(AF_EINVAL, "out of host memory");
+  c->num_examples = num_examples;
+  c->row_bytes = row_bytes;
+  c->rank = rank;
+  c->world = world;
+  c->capacity = (num_examples > rank) ? (num_examples - rank + world - 1) / world : 0;
+  const unsigned __int128 pb = static_cast<unsigned __int128>(c->capacity) * static_cast<uint64_t>(row_bytes);
+  if (pb > (static_cast<unsigned __int128>(1) << 60)) {
+    delete c;
+    return fail(AF_ERANGE, "cache too large");
+  }
+  *out = c;
+  return AF_OK;
+}
+
+af_status af_cache_storage_bytes(const af_cache *c, size_t *payload_bytes, size_t *meta_bytes) {
+  if (!c || !payload_bytes || !meta_bytes) return fail(AF_EINVAL, "NULL argument");
+  *payload_bytes = static_cast<size_t>(c->capacity) * static_cast<size_t>(c->row_bytes);
+  *meta_bytes = kMetaHeader + static_cast<size_t>(c->capacity) * sizeof(CacheMeta);
+  return AF_OK;
+}
+
+af_status af_cache_bind(af_cache *c, void *payload_dev, void *meta_dev) {
+  if (!c || !meta_dev || (c->capacity > 0 && !payload_dev)) return fail(AF_EINVAL, "NULL argument");
+  if ((payload_dev && !aligned(payload_dev, 16)) || !aligned(meta_dev, 256))
+    return fail(AF_EINVAL, "payload must be 16-byte and meta 256-byte aligned");
+  int sms = 0;
+  cudaError_t e = static_cast<cudaError_t>(device_sm_count(&sms));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  c->grid = std::max(1, sms);
+  c->payload = static_cast<char *>(payload_dev);
+  c->meta = static_cast<char *>(meta_dev);
+  AF_CUDA(cudaMemset(c->meta, 0, kMetaHeader + static_cast<size_t>(c->capacity) * sizeof(CacheMeta)),
+          "cudaMemset(meta)");
+  AF_CUDA(cudaDeviceSynchronize(), "cache bind");
+  c->bound = true;
+  return AF_OK;
+}
+
+static af_status cache_common(af_cache *c, const int64_t *ids, int32_t n, const void *rows, CacheParams &p) {
+  if (!c) return fail(AF_EINVAL, "NULL cache");
+  if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
+  if (n < 0) return fail(AF_EINVAL, "n < 0");
+  if (n > 0 && (!ids || !rows)) return fail(AF_EINVAL, "NULL ids / rows");
+  if (n > 0 && (!aligned(rows, 16) || !aligned(ids, 8))) return fail(AF_EINVAL, "rows must be 16-byte aligned");
+  p = CacheParams{};
+  p.payload = c->payload;
+  p.meta = reinterpret_cast<CacheMeta *>(c->meta + kMetaHeader);
+  p.sched = reinterpret_cast<Sched *>(c->meta);
+  p.err = reinterpret_cast<unsigned int *>(c->meta + sizeof(Sched));
+  p.ids = ids;
+  p.n = n;
+  p.row_bytes = c->row_bytes;
+  p.num_examples = c->num_examples;
+  p.rank = c->rank;
+  p.world = c->world;
+  return AF_OK;
+}
+
+af_status af_cache_put(af_cache *c, const int64_t *ids_dev, int32_t n, const void *rows_dev, int32_t depth,
+                       void *stream) {
+  CacheParams p;
+  af_status s = cache_common(c, ids_dev, n, rows_dev, p);
+  if (s != AF_OK) return s;
+  if (depth < 1) return fail(AF_EINVAL, "depth must be >= 1 (frozen POOL count)");
+  if (n == 0) return AF_OK;
+  p.src_rows = static_cast<const char *>(rows_dev);
+  p.depth = depth;
+  const int e = launch_cache_put(p, c->grid, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache put launch");
+  return AF_OK;
+}
+
+af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary, void *rows_out_dev,
+                       int32_t *depth_out_dev, void *stream) {
+  CacheParams p;
+  af_status s = cache_common(c, ids_dev, n, rows_out_dev, p);
+  if (s != AF_OK) return s;
+  if (n > 0 && !depth_out_dev) return fail(AF_EINVAL, "NULL depth_out");
+  if (cur_boundary < 0) return fail(AF_EINVAL, "cur_boundary < 0");
+  if (n == 0) return AF_OK;
+  p.dst_rows = static_cast<char *>(rows_out_dev);
+  p.depth_out = depth_out_dev;
+  p.cur_boundary = cur_boundary;
+  const int e = launch_cache_get(p, c->grid, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache get launch");
+  return AF_OK;
+}
+
+af_status af_cache_status(af_cache *c, uint32_t *device_error_flags, int64_t *n_valid) {
+  if (!c || !device_error_flags) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
+  AF_CUDA(cudaDeviceSynchronize(), "cache status sync");
+  unsigned int err = 0;
+  AF_CUDA(cudaMemcpy(&err, c->meta + sizeof(Sched), sizeof(err), cudaMemcpyDeviceToHost), "cudaMemcpy(err)");
+  *device_error_flags = err;
+  if (n_valid) {
+    std::vector<CacheMeta> m(static_cast<size_t>(c->capacity));
+    if (c->capacity)
+      AF_CUDA(cudaMemcpy(m.data(), c->meta + kMetaHeader, m.size() * sizeof(CacheMeta), cudaMemcpyDeviceToHost),
+              "cudaMemcpy(meta)");
+    int64_t v = 0;
+    for (const auto &x : m) v += (x.valid != 0);
+    *n_valid = v;
+  }
+  return AF_OK;
+}
+
+af_status af_cache_destroy(af_cache *c) {
+  if (!c) return fail(AF_EINVAL, "NULL cache");
+  delete c;
+  return AF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,236 @@
+// af_cache.cu -- Storage Manager put/get kernels.
+//
+// The paper's storage manager writes the frozen prefix's output for every
+// processed example at the original index and reads it back by original index
+// in the next epoch, evicting a record on read when the frozen depth grew
+// (§3.2).  Here the store is an HBM-resident direct-mapped
+// table per GPU (slot = id / world for the ids id % world == rank, §3.4).
+//
+// Data movement is pure bytes (bit-exact) and HBM-bound: 2 * rows * row_bytes.
+// Each CTA drives a TMA bulk-copy ring (cp.async.bulk global->shared with an
+// mbarrier transaction count, then cp.async.bulk shared->global in bulk groups),
+// STAGES x 32 KiB of shared memory, one elected lane issuing, so up to
+// STAGES-1 chunk loads and the matching stores are in flight per SM without
+// register staging.  Work items are (row, 32 KiB chunk) pairs dealt round-robin
+// to a persistent grid of one CTA per SM.  Get evictions are applied by the
+// last CTA to finish, after every chunk has read the record's meta word, so all
+// chunks of a row agree on hit/miss.
+#include <cuda_runtime.h>
+
+#include "af_internal.h"
+
+namespace af {
+namespace {
+
+constexpr int kStages = 6;
+constexpr int kChunk = 32 * 1024;
+constexpr int kMaxDesc = 512;
+
+struct Desc {
+  const char *src;
+  char *dst;
+  uint32_t bytes;
+  uint32_t ok;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Lane 0 streams the ok descriptors through the ring.  `seq` counts loads over
+// the whole launch so that stage s = seq % kStages and its mbarrier parity
+// (seq / kStages) & 1 stay consistent across descriptor batches.
+__device__ void pump(const Desc *descs, int m, unsigned char *stage_buf, uint64_t *bars, uint32_t &seq) {
+  // gather the ok items' indices on the fly
+  int load_i = 0;          // next descriptor to load
+  uint32_t base = seq;     // sequence number of the first ok item of this batch
+  uint32_t n_ok = 0;
+  for (int i = 0; i < m; ++i) n_ok += descs[i].ok;
+  auto next_ok = [&](int i) {
+    while (i < m && !descs[i].ok) ++i;
+    return i;
+  };
+  // prologue: up to kStages-1 loads ahead
+  uint32_t loaded = 0;
+  load_i = next_ok(0);
+  while (loaded < n_ok && loaded < kStages - 1) {
+    const uint32_t u = base + loaded;
+    const int s = u % kStages;
+    mbar_expect_tx(&bars[s], descs[load_i].bytes);
+    bulk_g2s(stage_buf + static_cast<size_t>(s) * kChunk, descs[load_i].src, descs[load_i].bytes, &bars[s]);
+    ++loaded;
+    load_i = next_ok(load_i + 1);
+  }
+  int store_i = next_ok(0);
+  for (uint32_t q = 0; q < n_ok; ++q) {
+    const uint32_t u = base + q;
+    const int s = u % kStages;
+    mbar_wait(&bars[s], (u / kStages) & 1u);
+    bulk_s2g(descs[store_i].dst, stage_buf + static_cast<size_t>(s) * kChunk, descs[store_i].bytes);
+    store_i = next_ok(store_i + 1);
+    if (loaded < n_ok) {
+      bulk_wait_read1();  // the store that last used the stage we refill has read its bytes
+      const uint32_t v = base + loaded;
+      const int sv = v % kStages;
+      mbar_expect_tx(&bars[sv], descs[load_i].bytes);
+      bulk_g2s(stage_buf + static_cast<size_t>(sv) * kChunk, descs[load_i].src, descs[load_i].bytes, &bars[sv]);
+      ++loaded;
+      load_i = next_ok(load_i + 1);
+    }
+  }
+  bulk_wait_read0();  // the next batch may reuse every stage
+  seq = base + n_ok;
+}
+
+template <bool PUT>
+__global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
+  unsigned char *stage_buf = smem + 128;
+  Desc *descs = reinterpret_cast<Desc *>(stage_buf + static_cast<size_t>(kStages) * kChunk);
+  __shared__ int s_last;
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const int64_t n_items = static_cast<int64_t>(p.n) * p.n_chunks;
+  const int64_t G = gridDim.x;
+  const int64_t my_items = (n_items > blockIdx.x) ? (n_items - blockIdx.x + G - 1) / G : 0;
+  uint32_t seq = 0;
+  for (int64_t kb = 0; kb < my_items; kb += kMaxDesc) {
+    const int m = static_cast<int>((my_items - kb) < kMaxDesc ? (my_items - kb) : kMaxDesc);
+    for (int q = lane; q < m; q += 32) {
+      const int64_t j = blockIdx.x + (kb + q) * G;
+      const int i = static_cast<int>(j / p.n_chunks);
+      const int c = static_cast<int>(j % p.n_chunks);
+      const int64_t id = p.ids[i];
+      Desc dsc{nullptr, nullptr, 0u, 0u};
+      bool ok = true;
+      if (id < 0 || id >= p.num_examples) {
+        if (c == 0) atomicOr(p.err, AF_CACHE_ERR_RANGE);
+        ok = false;
+      } else if (id % p.world != p.rank) {
+        if (c == 0) atomicOr(p.err, AF_CACHE_ERR_OWNER);
+        ok = false;
+      }
+      const int64_t off = static_cast<int64_t>(c) * p.chunk_bytes;
+      const int64_t rem = p.row_bytes - off;
+      dsc.bytes = static_cast<uint32_t>(rem < p.chunk_bytes ? rem : p.chunk_bytes);
+      if (ok) {
+        const int64_t slot = id / p.world;
+        char *rec = p.payload + slot * p.row_bytes + off;
+        if (PUT) {
+          dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+          dsc.dst = rec;
+          dsc.ok = 1u;
+          if (c == 0) {
+            CacheMeta m2;
+            m2.depth = p.depth;
+            m2.valid = 1;
+            p.meta[slot] = m2;
+          }
+        } else {
+          const int2 mv = __ldcg(reinterpret_cast<const int2 *>(p.meta) + slot);  // {depth, valid}
+          const bool hit = mv.y != 0;
+          if (c == 0) p.depth_out[i] = hit ? mv.x : -1;
+          if (hit) {
+            dsc.src = rec;
+            dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+            dsc.ok = 1u;
+          }
+        }
+      } else if (!PUT && c == 0) {
+        p.depth_out[i] = -1;
+      }
+      descs[q] = dsc;
+    }
+    __syncwarp();
+    if (lane == 0) pump(descs, m, stage_buf, bars, seq);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    bulk_wait_all();  // all stores complete before the CTA retires its shared memory
+    __threadfence();
+    const unsigned int d = atomicAdd(&p.sched->done, 1u);
+    s_last = (d == gridDim.x - 1);
+  }
+  __syncwarp();
+  if (!s_last) return;
+  __threadfence();
+  if (lane == 0) p.sched->done = 0;
+  if (!PUT) {
+    // evict on read: the frozen count grew beyond the record's depth
+    for (int i = lane; i < p.n; i += 32) {
+      const int64_t id = p.ids[i];
+      if (id < 0 || id >= p.num_examples || id % p.world != p.rank) continue;
+      const int64_t slot = id / p.world;
+      const int2 mv = __ldcg(reinterpret_cast<const int2 *>(p.meta) + slot);
+      if (mv.y != 0 && mv.x < p.cur_boundary) p.meta[slot].valid = 0;
+    }
+  }
+}
+
+}  // namespace
+
+int cache_smem_bytes() { return 128 + kStages * kChunk + kMaxDesc * static_cast<int>(sizeof(Desc)); }
+
+template <bool PUT>
+static int launch_cache(const CacheParams &p0, int grid, void *stream) {
+  CacheParams p = p0;
+  p.chunk_bytes = kChunk;
+  p.n_chunks = static_cast<int32_t>((p.row_bytes + kChunk - 1) / kChunk);
+  const int64_t items = static_cast<int64_t>(p.n) * p.n_chunks;
+  if (items < grid) grid = static_cast<int>(items);
+  if (grid < 1) grid = 1;
+  const int smem = cache_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(cache_kernel<PUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  cache_kernel<PUT><<<grid, 32, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_cache_put(const CacheParams &p, int grid, void *stream) { return launch_cache<true>(p, grid, stream); }
+int launch_cache_get(const CacheParams &p, int grid, void *stream) { return launch_cache<false>(p, grid, stream); }
+
+}  // namespace af

@@ -1,0 +1,109 @@
+// af_internal.h -- structures shared by the host library and the sm_100a kernels.
+// Not part of the ABI (include/af.h is).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/af.h"
+
+namespace af {
+
+constexpr int kNormBlock = 256;          // threads per CTA of the streaming kernels
+constexpr int kTileBytes = 64 * 1024;    // nominal gradient bytes per tile
+constexpr int kRing = 16;                // decision records kept on the device
+constexpr int kShardAlign = 8;           // shard bounds are multiples of 8 elements (32 B fp32 Delta)
+
+// A segment-aligned tile: global element range [begin, end) inside one segment.
+struct Tile {
+  int64_t begin, end;
+  int32_t seg, pad;
+};
+static_assert(sizeof(Tile) == 24, "tile layout");
+
+// Dynamic tile scheduler of one kernel family; reset by the last CTA of each launch.
+struct Sched {
+  unsigned int next, done;
+  unsigned int pad[30];
+};
+
+// Device-resident freezing state (lives in the caller-bound scratch buffer).
+struct DevState {
+  int32_t T;         // completed intervals
+  int32_t f;         // frozen POOL count (the boundary)
+  uint32_t sticky;   // reserved
+  int32_t pad;
+  double prev[AF_MAX_SEGMENTS];  // ||Delta_{T-1,l}||
+};
+
+enum Mode : int { kAccum = 0, kEndDelta = 1, kStepSq = 2 };
+
+// Arguments of the streaming kernels (accumulate / interval-end sum of squares).
+struct NormParams {
+  const void *grad;          // full flat buffer base
+  float *delta;              // Delta shard base: element i lives at delta[i - shard_begin]
+  int64_t shard_begin;
+  const Tile *tiles;
+  int32_t n_tiles;
+  int32_t L;
+  const int32_t *first_tile_of_f;  // [n_pool + 1]
+  const int32_t *seg_tile_begin;   // [L + 1]
+  const DevState *state;           // reads f
+  Sched *sched;
+  double *partials;                // [n_tiles]
+  double *ss_out;                  // [L] this rank's row of the exchange matrix
+  double *ss_acc;                  // [L] STEP_SUMSQ accumulator
+  int32_t n_pool;
+  int32_t first;                   // first step of the interval (Delta not read)
+  int32_t end;                     // interval end (STEP_SUMSQ: publish ss_acc)
+  int32_t commit;                  // STEP_SUMSQ: store ss_acc
+};
+
+// Arguments of the single-CTA decision kernel.
+struct DecideParams {
+  const double *ss_all;   // [world][L]
+  int32_t world, L, n_pool;
+  const int32_t *pool_seg;  // [n_pool] segment index of POOL layer j
+  DevState *state;
+  af_decision *last;        // device copy of the latest record
+  af_decision *ring;        // [kRing]
+  double percentile;
+  int32_t pct_method;
+  double tie_rel_eps;
+  int32_t min_active;
+  int32_t commit;           // 0 under AF_DRY_RUN
+};
+
+// Cache records: one 8-byte meta word per slot.
+struct CacheMeta {
+  int32_t depth;
+  int32_t valid;
+};
+
+struct CacheParams {
+  char *payload;            // [capacity][row_bytes]
+  CacheMeta *meta;          // [capacity]
+  unsigned int *err;        // sticky flags
+  Sched *sched;
+  const int64_t *ids;
+  int32_t n;
+  int64_t row_bytes;
+  int32_t chunk_bytes;
+  int32_t n_chunks;         // chunks per row
+  int64_t num_examples;
+  int32_t rank, world;
+  const char *src_rows;     // put: rows to write
+  char *dst_rows;           // get: output rows
+  int32_t *depth_out;       // get
+  int32_t depth;            // put
+  int32_t cur_boundary;     // get
+};
+
+// Launchers (defined in the .cu files).  Return cudaError_t as int.
+int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *stream);
+int launch_decide(const DecideParams &p, void *stream);
+int launch_cache_put(const CacheParams &p, int grid, void *stream);
+int launch_cache_get(const CacheParams &p, int grid, void *stream);
+int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks);
+int cache_smem_bytes();
+
+}  // namespace af

@@ -1,0 +1,284 @@
+// af_norms.cu -- the streaming kernels of the freezing hot path (sm_100a).
+//
+//   kAccum    Delta <- Delta + g (Delta <- g on the first step)      P:196 §3.1.1, §4.5
+//   kEndDelta partial[tile] = sum (Delta + g)^2 in fp64, no write-back  Eq. 1 norm
+//   kStepSq   partial[tile] = sum g^2 (alternative reading Q1)
+//
+// HBM-bound elementwise/reduction work: no tensor cores (nothing is a
+// contraction).  Design:
+//  * persistent grid sized from the occupancy query (148 SMs x resident CTAs),
+//    dynamic tile scheduler (one atomic per 64 KiB tile, prefetched one tile
+//    ahead, reset by the last CTA) -- balances the two dies' speed spread;
+//  * 128-bit streaming loads/stores (ld/st .cs), 4 vectors in flight per thread;
+//  * tiles never straddle a segment, so each tile's fp64 partial belongs to one
+//    layer; the partial's reduction order is fixed by the thread mapping
+//    (4 fp64 lane accumulators -> xor-shuffle tree -> 8 warps in order), so the
+//    result does not depend on which CTA ran the tile: deterministic, no atomics
+//    on the result path;
+//  * each fp32 Delta_T value widens exactly to fp64 and is squared-accumulated
+//    with one DFMA (the square is exact; only the accumulation rounds), giving
+//    norms good to ~1e-15 relative (eta needs < 5e-11);
+//  * frozen tiles (segments before the device-resident boundary f) are skipped;
+//  * the last CTA to finish sums each segment's partials in tile order.
+#include <cuda_runtime.h>
+
+#include "af_internal.h"
+
+namespace af {
+namespace {
+
+template <typename GT>
+struct VT;
+template <>
+struct VT<float> {
+  static constexpr int VE = 4;  // elements per 16-byte vector
+};
+template <>
+struct VT<uint16_t> {
+  static constexpr int VE = 8;
+};
+
+__device__ __forceinline__ float g_scalar(const float *g, int64_t i) { return __ldcs(g + i); }
+__device__ __forceinline__ float g_scalar(const uint16_t *g, int64_t i) {
+  return __uint_as_float(static_cast<uint32_t>(__ldcs(reinterpret_cast<const unsigned short *>(g) + i)) << 16);
+}
+
+template <int VE>
+__device__ __forceinline__ void unpack(const uint4 &v, float (&x)[VE]);
+template <>
+__device__ __forceinline__ void unpack<4>(const uint4 &v, float (&x)[4]) {
+  x[0] = __uint_as_float(v.x);
+  x[1] = __uint_as_float(v.y);
+  x[2] = __uint_as_float(v.z);
+  x[3] = __uint_as_float(v.w);
+}
+template <>
+__device__ __forceinline__ void unpack<8>(const uint4 &v, float (&x)[8]) {
+  // bf16 -> fp32 is exact: the bf16 bits are the high half of the fp32 word.
+  x[0] = __uint_as_float(v.x << 16);
+  x[1] = __uint_as_float(v.x & 0xFFFF0000u);
+  x[2] = __uint_as_float(v.y << 16);
+  x[3] = __uint_as_float(v.y & 0xFFFF0000u);
+  x[4] = __uint_as_float(v.z << 16);
+  x[5] = __uint_as_float(v.z & 0xFFFF0000u);
+  x[6] = __uint_as_float(v.w << 16);
+  x[7] = __uint_as_float(v.w & 0xFFFF0000u);
+}
+
+// x^2 accumulated in fp64: exact widening, exact square, one rounding per add.
+__device__ __forceinline__ double sq_acc(float x, double acc) {
+  const double xd = static_cast<double>(x);
+  return __fma_rn(xd, xd, acc);
+}
+
+template <int MODE, typename GT, bool RD>
+__device__ __forceinline__ void elem(const NormParams &p, const GT *g, float *d, int64_t i,
+                                     double &acc) {
+  const float gv = g_scalar(g, i);
+  if (MODE == kStepSq) {
+    acc = sq_acc(gv, acc);
+    return;
+  }
+  const float x = RD ? __fadd_rn(d[i], gv) : gv;
+  if (MODE == kAccum)
+    d[i] = x;
+  else
+    acc = sq_acc(x, acc);
+}
+
+template <int MODE, typename GT, bool RD>
+__device__ __forceinline__ double process_tile(const NormParams &p, const Tile &t) {
+  constexpr int VE = VT<GT>::VE;
+  constexpr int U = 4;  // vectors in flight per thread
+  const GT *__restrict__ g = static_cast<const GT *>(p.grad);
+  // Delta is indexed by global element i at d[i]; the shard base offset is applied
+  // through the pointer (shard_begin is a multiple of 8, keeping 16 B alignment).
+  float *__restrict__ d = p.delta - p.shard_begin;
+  const int64_t b = t.begin, e = t.end;
+  int64_t vb = ((b + VE - 1) / VE) * VE;
+  int64_t ve = (e / VE) * VE;
+  if (vb > ve) vb = ve = e;  // shorter than one aligned vector: all scalar
+  const int tid = threadIdx.x;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+
+  // unaligned segment edges (< VE elements each): scalar
+  const int nh = static_cast<int>(vb - b), nt = static_cast<int>(e - ve);
+  if (tid < nh) elem<MODE, GT, RD>(p, g, d, b + tid, a0);
+  if (tid >= 128 && tid - 128 < nt) elem<MODE, GT, RD>(p, g, d, ve + (tid - 128), a1);
+
+  const int64_t nch = (ve - vb) / VE;
+  const uint4 *gb = reinterpret_cast<const uint4 *>(g + vb);
+  float4 *db = reinterpret_cast<float4 *>(d + vb);
+  constexpr int DV = VE / 4;  // float4 of Delta per vector of g
+  for (int64_t c0 = tid; c0 < nch; c0 += U * kNormBlock) {
+    uint4 gv[U];
+    float4 dv[U][DV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = c0 + static_cast<int64_t>(u) * kNormBlock;
+      if (c < nch) {
+        gv[u] = __ldcs(gb + c);
+        if (RD) {
+#pragma unroll
+          for (int q = 0; q < DV; ++q) dv[u][q] = __ldcs(db + c * DV + q);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = c0 + static_cast<int64_t>(u) * kNormBlock;
+      if (c < nch) {
+        float x[VE];
+        unpack<VE>(gv[u], x);
+        if (MODE == kStepSq) {
+#pragma unroll
+          for (int k = 0; k < VE; k += 4) {
+            a0 = sq_acc(x[k + 0], a0);
+            a1 = sq_acc(x[k + 1], a1);
+            a2 = sq_acc(x[k + 2], a2);
+            a3 = sq_acc(x[k + 3], a3);
+          }
+          continue;
+        }
+        if (RD) {
+#pragma unroll
+          for (int q = 0; q < DV; ++q) {
+            x[4 * q + 0] = __fadd_rn(dv[u][q].x, x[4 * q + 0]);
+            x[4 * q + 1] = __fadd_rn(dv[u][q].y, x[4 * q + 1]);
+            x[4 * q + 2] = __fadd_rn(dv[u][q].z, x[4 * q + 2]);
+            x[4 * q + 3] = __fadd_rn(dv[u][q].w, x[4 * q + 3]);
+          }
+        }
+        if (MODE == kAccum) {
+#pragma unroll
+          for (int q = 0; q < DV; ++q)
+            __stcs(db + c * DV + q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < VE; k += 4) {
+            a0 = sq_acc(x[k + 0], a0);
+            a1 = sq_acc(x[k + 1], a1);
+            a2 = sq_acc(x[k + 2], a2);
+            a3 = sq_acc(x[k + 3], a3);
+          }
+        }
+      }
+    }
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;  // identical on every lane (fp add is commutative)
+}
+
+template <int MODE, typename GT, bool RD>
+__global__ void __launch_bounds__(kNormBlock) norms_kernel(const NormParams p) {
+  __shared__ int s_tile[2];
+  __shared__ double s_red[kNormBlock / 32];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int f = p.state->f;
+  f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
+  const int first_tile = p.first_tile_of_f[f];
+
+  if (tid == 0) s_tile[0] = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+  __syncthreads();
+  for (int it = 0;; ++it) {
+    const int tile = s_tile[it & 1];
+    if (tile >= p.n_tiles) break;
+    if (tid == 0) s_tile[(it + 1) & 1] = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+    const Tile t = p.tiles[tile];
+    const double v = process_tile<MODE, GT, RD>(p, t);
+    if (MODE != kAccum) {
+      const double w = warp_sum(v);
+      if (lane == 0) s_red[warp] = w;
+      __syncthreads();
+      if (tid == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < kNormBlock / 32; ++k) s += s_red[k];
+        p.partials[tile] = s;
+      }
+    }
+    __syncthreads();
+  }
+
+  // grid completion: the last CTA resets the scheduler and finalises per segment
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int d = atomicAdd(&p.sched->done, 1u);
+    s_last = (d == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) {
+    p.sched->next = 0;
+    p.sched->done = 0;
+  }
+  if (MODE == kAccum) return;
+  for (int l = warp; l < p.L; l += kNormBlock / 32) {
+    int tb = p.seg_tile_begin[l];
+    tb = tb < first_tile ? first_tile : tb;
+    const int te = p.seg_tile_begin[l + 1];
+    double s = 0.0;
+#pragma unroll 8
+    for (int t = tb + lane; t < te; t += 32) s += __ldcg(p.partials + t);
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (MODE == kEndDelta) {
+        p.ss_out[l] = s;
+      } else {
+        const double a = p.first ? s : p.ss_acc[l] + s;
+        if (p.commit) p.ss_acc[l] = a;
+        if (p.end) p.ss_out[l] = a;
+      }
+    }
+  }
+}
+
+template <int MODE, typename GT, bool RD>
+int launch_one(const NormParams &p, int grid, void *stream) {
+  norms_kernel<MODE, GT, RD><<<grid, kNormBlock, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  return static_cast<int>(cudaGetLastError());
+}
+
+template <typename GT>
+int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
+  const bool rd = !p.first;
+  switch (mode) {
+    case kAccum:
+      return rd ? launch_one<kAccum, GT, true>(p, grid, stream) : launch_one<kAccum, GT, false>(p, grid, stream);
+    case kEndDelta:
+      return rd ? launch_one<kEndDelta, GT, true>(p, grid, stream)
+                : launch_one<kEndDelta, GT, false>(p, grid, stream);
+    case kStepSq:
+      return launch_one<kStepSq, GT, false>(p, grid, stream);
+  }
+  return static_cast<int>(cudaErrorInvalidValue);
+}
+
+}  // namespace
+
+int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *stream) {
+  if (grad_dtype == AF_DT_BF16) return launch_dt<uint16_t>(p, mode, grid, stream);
+  return launch_dt<float>(p, mode, grid, stream);
+}
+
+int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks) {
+  cudaError_t e;
+  if (grad_dtype == AF_DT_BF16)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kEndDelta, uint16_t, true>,
+                                                      kNormBlock, 0);
+  else
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kEndDelta, float, true>,
+                                                      kNormBlock, 0);
+  (void)mode;
+  return static_cast<int>(e);
+}
+
+}  // namespace af

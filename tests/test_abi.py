@@ -1,0 +1,177 @@
+"""C-ABI tests that need no GPU: the library loads, exports exactly what
+include/af.h declares, validates arguments synchronously, and computes its
+host-side shard / tile tables correctly."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2102_01386_b200 as af
+from paper_2102_01386_b200 import _lib as L
+from afinputs import bert_layout, tiny_layout, uniform_layout
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "af.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return set(re.findall(r"^AF_API\s+[\w\s\*]+?\b(af_\w+)\(", src, flags=re.M))
+
+
+def test_library_exports_every_declared_symbol():
+    decl = declared_symbols()
+    assert len(decl) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", af.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert decl <= exported, decl - exported
+    assert {s for s in exported if s.startswith("af_")} == decl  # nothing undeclared leaks
+    assert decl == set(L.SIGNATURES), decl ^ set(L.SIGNATURES)
+
+
+def test_struct_sizes_match_header_layout():
+    assert ctypes.sizeof(L.AfDecision) == 4 * 4 + 8 + 4 + 4 + 3 * 8 * 256
+    assert ctypes.sizeof(L.AfConfig) == 40
+
+
+def test_status_strings_and_version():
+    assert L.lib.af_status_str(L.AF_EINVAL) == b"AF_EINVAL"
+    assert L.lib.af_version() == b"0.1.0"
+
+
+def test_should_cache_printed_examples(golden):
+    for k, tf, tr, want in golden("spec_examples.json")["should_cache"]["cases"]:
+        assert af.should_cache(k, tf, tr) == want
+
+
+def _create(offsets, kinds, dt=L.AF_DT_F32, **cfg):
+    offs = (ctypes.c_int64 * len(offsets))(*offsets)
+    knd = (ctypes.c_int32 * max(1, len(kinds)))(*kinds)
+    lay = L.AfLayout(len(kinds), offs, knd, dt)
+    c = dict(percentile=50.0, pct_method=0, acc_mode=0, tie_rel_eps=1e-5, min_active=2, rank=0, world=1)
+    c.update(cfg)
+    conf = L.AfConfig(c["percentile"], c["pct_method"], c["acc_mode"], c["tie_rel_eps"], c["min_active"],
+                      c["rank"], c["world"])
+    h = ctypes.c_void_p()
+    st = L.lib.af_ctx_create(ctypes.byref(lay), ctypes.byref(conf), ctypes.byref(h))
+    if st == L.AF_OK:
+        L.lib.af_ctx_destroy(h)
+    return st
+
+
+@pytest.mark.parametrize("offsets,kinds,cfg", [
+    ([0, 10], [1], {}),
+    ([0, 5, 10, 20], [0, 1, 2], {}),
+    ([0, 5, 10, 20], [1, 1, 1], dict(percentile=100.0, pct_method=1, acc_mode=1, world=8, rank=7)),
+])
+def test_create_accepts_valid(offsets, kinds, cfg):
+    assert _create(offsets, kinds, **cfg) == L.AF_OK
+
+
+@pytest.mark.parametrize("offsets,kinds,cfg", [
+    ([0, 10], [0], {}),                        # no POOL
+    ([1, 10], [1], {}),                        # offsets[0] != 0
+    ([0, 10, 10], [1, 1], {}),                 # not strictly increasing
+    ([0, 5, 10], [1, 0], {}),                  # PRE after POOL
+    ([0, 5, 10, 15], [1, 2, 1], {}),           # POOL after HEAD
+    ([0, 5, 10], [1, 3], {}),                  # bad kind
+    ([0, 10], [1], dict(percentile=0.0)),
+    ([0, 10], [1], dict(percentile=100.5)),
+    ([0, 10], [1], dict(percentile=float("nan"))),
+    ([0, 10], [1], dict(pct_method=7)),
+    ([0, 10], [1], dict(acc_mode=2)),
+    ([0, 10], [1], dict(min_active=0)),
+    ([0, 10], [1], dict(tie_rel_eps=-1.0)),
+    ([0, 10], [1], dict(world=0)),
+    ([0, 10], [1], dict(world=2, rank=2)),
+    ([0, 10], [1], dict(world=65)),
+])
+def test_create_rejects_invalid(offsets, kinds, cfg):
+    assert _create(offsets, kinds, **cfg) == L.AF_EINVAL
+
+
+def test_create_rejects_too_many_segments_and_bad_dtype():
+    offs = list(range(0, 258))
+    assert _create(offs, [1] * 257) == L.AF_EINVAL
+    assert _create([0, 10], [1], dt=5) == L.AF_EINVAL
+
+
+def test_null_arguments():
+    assert L.lib.af_ctx_create(None, None, None) == L.AF_EINVAL
+    assert L.lib.af_layer_norms(None, None, 0, None) == L.AF_EINVAL
+    assert L.lib.af_update_and_decide(None, 0, None, None) == L.AF_EINVAL
+    assert L.lib.af_cache_create(10, 64, 0, 1, None) == L.AF_EINVAL
+
+
+def _expected_tiles(lay, sb, se, tile_elems):
+    n = 0
+    for l in range(lay.n_segments):
+        lo, hi = max(lay.offsets[l], sb), min(lay.offsets[l + 1], se)
+        pos = lo
+        while pos < hi:
+            pos = min(hi, (pos // tile_elems + 1) * tile_elems)
+            n += 1
+    return n
+
+
+@pytest.mark.parametrize("which,dt", [("base", "bf16"), ("large", "f32"), ("base", "f32")])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_shards_cover_buffer_and_tiles_are_segment_aligned(which, dt, world):
+    lay = bert_layout(which)
+    prev_end = 0
+    total_tiles = 0
+    for r in range(world):
+        fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, rank=r, world=world, bind=False)
+        i = fm.info()
+        assert i["shard_begin"] == prev_end
+        assert i["shard_begin"] % 8 == 0
+        prev_end = i["shard_end"]
+        assert i["tile_elems"] * (2 if dt == "bf16" else 4) == 64 * 1024
+        assert i["n_tiles"] == _expected_tiles(lay, i["shard_begin"], i["shard_end"], i["tile_elems"])
+        assert fm.accum_bytes == 4 * (i["shard_end"] - i["shard_begin"])
+        ft = i["first_tile_of_pool"]
+        assert ft == sorted(ft) and ft[0] == 0
+        total_tiles += i["n_tiles"]
+        # balanced within one shard-alignment unit
+        assert abs((i["shard_end"] - i["shard_begin"]) - lay.n / world) <= 8
+        fm.close()
+    assert prev_end == lay.n
+
+
+def test_first_tile_skips_embedding_with_first_block():
+    lay = bert_layout("base")
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="bf16", bind=False)
+    i = fm.info()
+    te = i["tile_elems"]
+    pre_tiles = -(-lay.seg_len(0) // te)
+    blk_tiles = _expected_tiles(bert_layout("base"), lay.offsets[1], lay.offsets[2], te)
+    assert i["first_tile_of_pool"][1] == pre_tiles + blk_tiles
+    assert i["first_tile_of_pool"][0] == 0
+
+
+def test_step_sumsq_needs_no_accumulator():
+    lay = tiny_layout()
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="f32", acc_mode="step_sumsq", bind=False)
+    assert fm.accum_bytes == 0
+
+
+def test_unbound_calls_report_workspace():
+    lay = uniform_layout(1 << 12, 4)
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="f32", bind=False)
+    buf = (ctypes.c_float * 16)()
+    assert L.lib.af_layer_norms(fm._h, ctypes.addressof(buf) // 16 * 16 + 16, 1, None) == L.AF_EWORKSPACE
+    assert L.lib.af_update_and_decide(fm._h, 0, None, None) == L.AF_EWORKSPACE
+
+
+def test_cache_create_validation_and_sizes():
+    h = ctypes.c_void_p()
+    assert L.lib.af_cache_create(100, 100, 0, 1, ctypes.byref(h)) == L.AF_EINVAL   # not a multiple of 16
+    assert L.lib.af_cache_create(100, 64, 3, 2, ctypes.byref(h)) == L.AF_EINVAL    # rank >= world
+    assert L.lib.af_cache_create(-1, 64, 0, 1, ctypes.byref(h)) == L.AF_EINVAL
+    c = af.ActivationCache(100_000, 196_608, rank=3, world=8, bind=False)
+    assert c.payload_bytes == 12_500 * 196_608
+    assert c.meta_bytes == 256 + 12_500 * 8
+    c2 = af.ActivationCache(10, 64, rank=3, world=4, bind=False)       # ids 3, 7
+    assert c2.payload_bytes == 2 * 64

@@ -1,0 +1,364 @@
+"""GPU parity: the sm_100a path (through the C ABI) vs the fp64 oracle on the
+same seeded inputs.  Run on a B200 with `pytest -m gpu`."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from afinputs import (bert_grad_step, bert_layout, tiny_grad_step, tiny_layout, uniform_layout,
+                      f32_to_bf16_bits)
+from gpu_util import canon, compare_records, delta_host, to_device_grad
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2102_01386_b200  # noqa: F401  (loads libautofreeze.so; fails loudly if missing)
+    torch.cuda.set_device(0)
+
+
+def _fm(lay, dt, **kw):
+    import paper_2102_01386_b200 as af
+    return af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, **kw)
+
+
+def _oracle(lay, dt, **kw):
+    m = {"percentile": kw.get("percentile", 50.0), "tie_rel_eps": kw.get("tie_rel_eps", 1e-5),
+         "min_active": kw.get("min_active", 2)}
+    m["pct_method"] = O.PCT_NEAREST_RANK if kw.get("pct_method") == "nearest_rank" else O.PCT_LINEAR
+    m["acc_mode"] = O.ACC_STEP_SUMSQ if kw.get("acc_mode") == "step_sumsq" else O.ACC_DELTA
+    return O.Freezer(lay.offsets, lay.kinds, O.DT_BF16 if dt == "bf16" else O.DT_F32, **m)
+
+
+def run_both(lay, dt, step_fn, schedule, check_delta=True, **kw):
+    """schedule = list of steps-per-interval; step_fn(T, t) -> numpy gradient."""
+    fm, oz = _fm(lay, dt, **kw), _oracle(lay, dt, **kw)
+    n_local = lay.n
+    ties, recs = 0, []
+    for T, S in enumerate(schedule):
+        for t in range(S):
+            g = step_fn(T, t)
+            end = t == S - 1
+            fm.layer_norms(to_device_grad(g, dt), interval_end=end)
+            oz.layer_norms(g, end)
+            if check_delta and not end and oz.delta is not None:
+                torch.cuda.synchronize()
+                assert np.array_equal(delta_host(fm, n_local), oz.delta), f"Delta T={T} t={t}"
+        fm.update_and_decide()
+        gr, orr = fm.decision(), oz.update_and_decide()
+        ties += compare_records(gr, orr, lay.n_segments, tag=f"T={T}")
+        recs.append((gr, orr))
+    return recs, ties, fm, oz
+
+
+# ---------------------------------------------------------------- closed-form tiny trace
+
+def test_tiny_trace_matches_closed_form(golden):
+    g = golden("tiny_trace.json")
+    lay = tiny_layout()
+    recs, ties, _, _ = run_both(lay, "f32", lambda T, t: tiny_grad_step(lay, 0, T, t), [4] * 10)
+    assert [r[0]["boundary_after"] for r in recs] == g["boundary_after"]
+    for T in range(1, 9):
+        assert round(recs[T][0]["threshold"], 6) == pytest.approx(g["threshold_T1_to_T8"][T - 1])
+    assert ties == 0
+
+
+def test_tiny_trace_step_sumsq_reading():
+    lay = tiny_layout()
+    recs, _, _, _ = run_both(lay, "f32", lambda T, t: tiny_grad_step(lay, 0, T, t), [4] * 10,
+                             acc_mode="step_sumsq")
+    paper = [0, 0, 0, 1, 1, 2, 2, 2, 3, 3]
+    assert [r[0]["boundary_after"] for r in recs] != paper       # Q1 discriminator
+
+
+# ---------------------------------------------------------------- ragged layouts, several tiles
+
+def _ragged_layout():
+    # odd sizes: unaligned segment edges for both 8-element bf16 and 4-element fp32 vectors
+    return uniform_layout(1_000_003, 7, pre=123_457, head=777)
+
+
+def _decaying_step(lay, dt, seed):
+    rng_scale = np.random.default_rng(seed).random(lay.n_segments) * 0.5 + 0.3
+
+    def fn(T, t):
+        rng = np.random.default_rng([seed, T, t])
+        x = rng.standard_normal(lay.n).astype(np.float32)
+        amp = np.repeat((rng_scale ** T).astype(np.float32), np.diff(lay.offsets))
+        x *= amp * np.float32(1e-3)
+        return f32_to_bf16_bits(x) if dt == "bf16" else x
+    return fn
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_ragged_multi_tile_parity(dt):
+    lay = _ragged_layout()
+    recs, ties, _, oz = run_both(lay, dt, _decaying_step(lay, dt, 7), [3, 1, 2, 3, 2, 4, 1, 3])
+    assert max(r[0]["boundary_after"] for r in recs) >= 1      # the frozen-skip path ran
+    assert oz.f == recs[-1][0]["boundary_after"]
+
+
+@pytest.mark.parametrize("pct_method,N", [("linear", 25.0), ("linear", 75.0), ("nearest_rank", 50.0)])
+def test_percentile_variants_parity(pct_method, N):
+    lay = uniform_layout(200_000, 12, pre=5000, head=333)
+    run_both(lay, "f32", _decaying_step(lay, "f32", 3), [2] * 8, percentile=N, pct_method=pct_method)
+
+
+def test_step_sumsq_ragged_parity():
+    lay = _ragged_layout()
+    run_both(lay, "bf16", _decaying_step(lay, "bf16", 11), [2, 3, 1, 2], acc_mode="step_sumsq",
+             check_delta=False)
+
+
+def test_tiny_and_edge_layouts():
+    # segments shorter than one vector, a single POOL, and one-element segments
+    for lay in (uniform_layout(37, 5, pre=3, head=2), uniform_layout(9, 1, pre=0, head=0),
+                uniform_layout(64 * 1024 + 13, 3, pre=1, head=1)):
+        for dt in ("f32", "bf16"):
+            run_both(lay, dt, _decaying_step(lay, dt, 5), [2, 2, 1, 3])
+
+
+# ---------------------------------------------------------------- decide kernel bit-exactness
+
+@pytest.mark.parametrize("seed", range(4))
+def test_threshold_bit_identical_to_numpy(seed):
+    """Inject arbitrary per-segment sums through the exchange rows: the decide
+    kernel's threshold and k must equal the oracle's (numpy) bit for bit."""
+    rng = np.random.default_rng(seed)
+    for trial in range(25):
+        n_pool = int(rng.integers(2, 60))
+        lay = uniform_layout(n_pool * 16, n_pool)
+        N = float(rng.choice([50.0, 25.0, 75.0, float(rng.uniform(1, 100))]))
+        method = "nearest_rank" if trial % 5 == 4 else "linear"
+        fm = _fm(lay, "f32", percentile=N, pct_method=method)
+        oz = _oracle(lay, "f32", percentile=N, pct_method=method)
+        g = torch.zeros(lay.n, device="cuda")
+        rows = fm.exchange_rows()
+        for T in range(3):
+            ss = rng.random(n_pool) * 10.0 ** rng.integers(-6, 3)
+            if T == 2 and trial % 3 == 0:
+                ss[: n_pool // 2] = oz.prev[: n_pool // 2] ** 2    # exact ties at eta = 0
+            fm.layer_norms(g, interval_end=True)
+            rows.copy_(torch.from_numpy(ss).view(1, -1))
+            fm.update_and_decide()
+            gr = fm.decision()
+            oz.pending = ss.copy()
+            orr = oz.update_and_decide()
+            assert gr["boundary_after"] == orr["boundary_after"]
+            assert gr["flags"] == orr["flags"]
+            assert np.array_equal(np.array(gr["norm"]), orr["norm"])
+            assert np.array_equal(np.array(gr["eta"]), orr["eta"])
+            if not math.isnan(orr["threshold"]):
+                assert gr["threshold"] == orr["threshold"], (trial, T, N, method)
+
+
+# ---------------------------------------------------------------- semantics
+
+def test_dry_run_and_state_roundtrip():
+    lay = uniform_layout(300_001, 6, pre=1001, head=55)
+    step = _decaying_step(lay, "f32", 2)
+    fm = _fm(lay, "f32")
+    for T in range(3):
+        fm.layer_norms(to_device_grad(step(T, 0), "f32"))
+        fm.layer_norms(to_device_grad(step(T, 1), "f32"), interval_end=True)
+        fm.update_and_decide()
+    blob = fm.get_state()
+    d0 = fm.decision()
+    # dry-run repetitions: identical records, nothing committed
+    g = to_device_grad(step(3, 0), "f32")
+    recs = []
+    for _ in range(3):
+        fm.layer_norms(g, interval_end=True, dry_run=True)
+        fm.update_and_decide(dry_run=True)
+        recs.append(fm.decision())
+    assert all(r["flags"] & O.FLAG_DRY_RUN for r in recs)
+    assert canon(recs[0]) == canon(recs[1]) == canon(recs[2])
+    assert fm.get_state() == blob
+    assert recs[0]["boundary_before"] == d0["boundary_after"]
+    # restore into a fresh context and continue identically
+    fm2 = _fm(lay, "f32")
+    fm2.set_state(blob)
+    for m in (fm, fm2):
+        m.layer_norms(g, interval_end=True)
+        m.update_and_decide()
+    assert canon(fm.decision()) == canon(fm2.decision())
+
+
+def test_decide_without_interval_end_is_estate():
+    import paper_2102_01386_b200 as af
+    lay = tiny_layout()
+    fm = _fm(lay, "f32")
+    with pytest.raises(af.AfError) as e:
+        fm.update_and_decide()
+    assert e.value.status == 2
+
+
+def test_nonfinite_gradient_leaves_state():
+    lay = tiny_layout()
+    fm = _fm(lay, "f32")
+    g = torch.ones(lay.n, device="cuda")
+    fm.layer_norms(g, interval_end=True)
+    fm.update_and_decide()
+    blob = fm.get_state()
+    g[7] = float("inf")
+    fm.layer_norms(g, interval_end=True)
+    fm.update_and_decide()
+    r = fm.decision()
+    assert r["flags"] & O.FLAG_NONFINITE
+    assert fm.get_state() == blob
+
+
+def test_deterministic_bits():
+    lay = _ragged_layout()
+    step = _decaying_step(lay, "bf16", 9)
+    outs = []
+    for _ in range(2):
+        fm = _fm(lay, "bf16")
+        rs = []
+        for T in range(4):
+            fm.layer_norms(to_device_grad(step(T, 0), "bf16"))
+            fm.layer_norms(to_device_grad(step(T, 1), "bf16"), interval_end=True)
+            fm.update_and_decide()
+            rs.append(canon(fm.decision()))
+        outs.append(rs)
+    assert outs[0] == outs[1]
+
+
+# ---------------------------------------------------------------- fake multi-GPU on one GPU
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_fake_sharded_parity(P):
+    """P contexts (ranks 0..P-1) on one GPU, external exchange: every rank reaches
+    the bit-identical decision; matches the P = 1 oracle within the contract."""
+    lay = _ragged_layout()
+    step = _decaying_step(lay, "bf16", 4)
+    fms = [_fm(lay, "bf16", rank=r, world=P) for r in range(P)]
+    oz = _oracle(lay, "bf16")
+    for T in range(5):
+        for t in range(2):
+            gnp = step(T, t)
+            g = to_device_grad(gnp, "bf16")
+            for fm in fms:
+                fm.layer_norms(g, interval_end=(t == 1))
+            oz.layer_norms(gnp, t == 1)
+        rows = [fm.exchange_rows() for fm in fms]
+        gathered = torch.stack([rows[r][r].clone() for r in range(P)])
+        for fm, rw in zip(fms, rows):
+            rw.copy_(gathered)
+            fm.update_and_decide()
+        decs = [fm.decision() for fm in fms]
+        assert all(canon(d) == canon(decs[0]) for d in decs[1:])
+        compare_records(decs[0], oz.update_and_decide(), lay.n_segments, tag=f"P={P} T={T}")
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+
+@pytest.mark.parametrize("which,dt", [("base", "bf16"), ("large", "f32")])
+def test_bert_full_size_parity(which, dt):
+    """configs[1] / configs[2] at full size in the bench's launch configuration:
+    every per-layer norm vs the oracle on the same generated gradients."""
+    lay = bert_layout(which)
+    step = lambda T, t: bert_grad_step(lay, 0, T, t, dtype=dt)  # noqa: E731
+    recs, ties, fm, oz = run_both(lay, dt, step, [2, 2, 1], check_delta=False)
+    # Delta after one accumulate step equals the oracle's bit for bit
+    g0, g1 = step(5, 0), step(5, 1)
+    fm.layer_norms(to_device_grad(g0, dt))
+    fm.layer_norms(to_device_grad(g1, dt))
+    oz.layer_norms(g0, False)
+    oz.layer_norms(g1, False)
+    torch.cuda.synchronize()
+    assert np.array_equal(delta_host(fm, lay.n), oz.delta)
+
+
+# ---------------------------------------------------------------- activation cache
+
+def _cache_pair(num, row_bytes, rank=0, world=1):
+    import paper_2102_01386_b200 as af
+    return af.ActivationCache(num, row_bytes, rank=rank, world=world), O.Cache(num, row_bytes, rank, world)
+
+
+def _ids(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.int64)).cuda()
+
+
+def test_cache_script_matches_oracle(golden):
+    from afinputs import cache_rows
+    g = golden("spec_examples.json")["cache_script"]
+    gc, oc = _cache_pair(1000, 196_608)
+    ids = np.array([3, 7, 42, 999, 0])
+    rows = cache_rows(0, 1, len(ids), 196_608)
+    gc.put(_ids(ids), torch.from_numpy(rows).cuda(), g["put_depth"])
+    oc.put(ids, rows, g["put_depth"])
+    for q, bnd in (([3, 5, 42], 4), ([3, 42, 999, 0, 7], 7), ([3, 7], 7)):
+        out_g = torch.full((len(q), 196_608), 77, dtype=torch.uint8, device="cuda")
+        dep_g = torch.zeros(len(q), dtype=torch.int32, device="cuda")
+        gc.get(_ids(q), bnd, out_g, dep_g)
+        out_o = np.full((len(q), 196_608), 77, np.uint8)
+        dep_o = oc.get(q, bnd, out_o)
+        assert np.array_equal(dep_g.cpu().numpy(), dep_o)
+        assert np.array_equal(out_g.cpu().numpy(), out_o)
+    # re-cache deeper, then hit without eviction
+    gc.put(_ids([3]), torch.from_numpy(rows[:1]).cuda(), 7)
+    oc.put([3], rows[:1], 7)
+    dep_g = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out_g = torch.zeros((1, 196_608), dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        gc.get(_ids([3]), 7, out_g, dep_g)
+        assert dep_g.item() == 7
+    assert gc.status() == (0, len(oc.store))
+
+
+@pytest.mark.parametrize("rank,world", [(0, 1), (1, 4)])
+def test_cache_epoch_parity(rank, world):
+    from afinputs import cache_rows, epoch_permutation, rank_ids
+    num, rb = 3000, 4096 + 16
+    gc, oc = _cache_pair(num, rb, rank, world)
+    mine = rank_ids(num, rank, world)
+    for epoch, (depth, bnd) in enumerate([(4, 4), (4, 7), (7, 7)]):
+        perm = epoch_permutation(0, epoch, mine)
+        for b0 in range(0, len(perm), 97):
+            ids = perm[b0:b0 + 97]
+            out_g = torch.full((len(ids), rb), 5, dtype=torch.uint8, device="cuda")
+            dep_g = torch.zeros(len(ids), dtype=torch.int32, device="cuda")
+            gc.get(_ids(ids), bnd, out_g, dep_g)
+            out_o = np.full((len(ids), rb), 5, np.uint8)
+            dep_o = oc.get(ids, bnd, out_o)
+            assert np.array_equal(dep_g.cpu().numpy(), dep_o)
+            assert np.array_equal(out_g.cpu().numpy(), out_o)
+            miss = ids[dep_o < 0]
+            rows = cache_rows(epoch, b0, len(miss), rb)
+            if len(miss):
+                gc.put(_ids(miss), torch.from_numpy(rows).cuda(), depth)
+                oc.put(miss, rows, depth)
+    assert gc.status() == (0, len(oc.store))
+
+
+def test_cache_owner_and_range_errors():
+    gc, oc = _cache_pair(10, 64, rank=1, world=4)
+    rows = torch.zeros((4, 64), dtype=torch.uint8, device="cuda")
+    gc.put(_ids([1, 5, 2, 11]), rows, 1)
+    oc.put([1, 5, 2, 11], rows.cpu().numpy(), 1)
+    err, valid = gc.status()
+    assert err == oc.error_flags == 3 and valid == 2
+    gc.put(_ids([]), rows[:0], 1)      # empty call: no-op
+
+
+def test_cache_large_gather_parity():
+    from afinputs import cache_rows
+    num, rb = 20_000, 196_608
+    gc, oc = _cache_pair(num, rb)
+    ids = np.random.default_rng(1).permutation(num)[:1024]
+    rows = cache_rows(3, 3, len(ids), rb)
+    gc.put(_ids(ids), torch.from_numpy(rows).cuda(), 3)
+    q = np.random.default_rng(2).permutation(ids)
+    out = torch.empty((len(q), rb), dtype=torch.uint8, device="cuda")
+    dep = torch.empty(len(q), dtype=torch.int32, device="cuda")
+    gc.get(_ids(q), 3, out, dep)
+    pos = {int(x): i for i, x in enumerate(ids)}
+    want = rows[[pos[int(x)] for x in q]]
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert np.all(dep.cpu().numpy() == 3)
