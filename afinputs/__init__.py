@@ -16,12 +16,12 @@ Neither `oracle/` nor the CUDA package imports the other; both may import this.
 from .layouts import (SEG_PRE, SEG_POOL, SEG_HEAD, Layout, bert_layout, tiny_layout,
                       uniform_layout)
 from .gen import (splitmix64, hash_u64, tiny_dyadic_ints, tiny_schedule_a, tiny_grad_step,
-                  bert_grad_step, f32_to_bf16_bits, bf16_bits_to_f32, cache_rows,
+                  bert_grad_step, segment_rho, f32_to_bf16_bits, bf16_bits_to_f32, cache_rows,
                   rank_ids, epoch_permutation)
 
 __all__ = [
     "SEG_PRE", "SEG_POOL", "SEG_HEAD", "Layout", "bert_layout", "tiny_layout",
     "uniform_layout", "splitmix64", "hash_u64", "tiny_dyadic_ints", "tiny_schedule_a",
-    "tiny_grad_step", "bert_grad_step", "f32_to_bf16_bits", "bf16_bits_to_f32",
+    "tiny_grad_step", "bert_grad_step", "segment_rho", "f32_to_bf16_bits", "bf16_bits_to_f32",
     "cache_rows", "rank_ids", "epoch_permutation",
 ]

@@ -84,7 +84,7 @@ def bf16_bits_to_f32(b):
     return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
 
 
-def _seg_rho(layout):
+def segment_rho(layout):
     pool = [l for l, k in enumerate(layout.kinds) if k == SEG_POOL]
     B = len(pool)
     rho = np.empty(layout.n_segments)
@@ -108,7 +108,7 @@ def bert_grad_step(layout, seed, T, t, dtype="bf16", sparse_rows=4096, lo=0, hi=
     rng = np.random.default_rng([int(seed), int(T), int(t), 0xAF])
     u = rng.random(layout.n, dtype=np.float32)[lo:hi]
     x = u * np.float32(2.0) - np.float32(1.0)
-    rho = _seg_rho(layout)
+    rho = segment_rho(layout)
     for l in range(layout.n_segments):
         b, e = max(layout.offsets[l], lo), min(layout.offsets[l + 1], hi)
         if b >= e:

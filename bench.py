@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""Benchmark of the AutoFreeze freezing hot path on B200 (BASELINE.json metric:
+"per-layer grad-norm+decide GB/s (% of HBM peak) at 1/2/4/8 B200; cache GB/s").
+
+One step = one pass of every SURVEY.md §8(a) row over one batch of synthetic
+input, through the C ABI:
+  a2   af_layer_norms            Delta += g over the rank's shard    n_loc*(s_g+8) B
+  a3-4 af_layer_norms(END)       fp64 sum of squares of Delta + g    n_loc*(s_g+4) B
+                                 (+ NCCL all-gather of the L partials when N > 1)
+  a5-9 af_update_and_decide      Eq. 1, percentile, prefix scan, record copy
+  a11  af_cache_get              B rows by example id                 2*B*row B
+  a10  af_cache_put              B rows by example id                 2*B*row B
+Timed steps run under AF_DRY_RUN (every rep does the same work: Delta stays
+armed, the decision is computed and recorded but not committed; boundary f = 0
+so every segment is active -- the worst case).  value = algorithmic bytes of
+all ranks / max-over-ranks device time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload bert-large-f32|bert-base-bf16]
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+    python bench.py --impl reference      # the fp64 CPU oracle, same metric (rank 0 only)
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "per-layer grad-norm+decide GB/s (% of HBM peak) at 1/2/4/8 B200; cache GB/s"
+ROW_BYTES = 128 * 768 * 2          # BERT-base hidden 768, seq 128, bf16 (configs[3])
+NUM_EXAMPLES = 100_000
+GLOBAL_CACHE_BATCH = 256
+
+WORKLOADS = {
+    "bert-large-f32": ("large", "f32"),   # configs[2]: BERT-large fp32, sharded over N GPUs
+    "bert-base-bf16": ("base", "bf16"),   # configs[1]: BERT-base bf16, 1 GPU
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="bert-large-f32", choices=sorted(WORKLOADS))
+    ap.add_argument("--cache-batch", type=int, default=GLOBAL_CACHE_BATCH)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks (NVML, in-process)
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons every 10 ms during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            pr = torch.cuda.get_device_properties(index)
+            try:
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:  # noqa: BLE001
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ synthetic inputs on the device
+
+def device_grad(lay, dt, seed, device, T=1):
+    """Synthetic gradient of the workload's shape (DESIGN.md input recipe:
+    sigma_l(T) * U(-1, 1) per segment), drawn on the device with torch's RNG
+    (bench only; the parity tests use afinputs/numpy)."""
+    import torch
+    from afinputs import segment_rho
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    x = torch.rand(lay.n, generator=gen, device=device, dtype=torch.float32).mul_(2).sub_(1)
+    sizes = torch.tensor([lay.seg_len(l) for l in range(lay.n_segments)], device=device)
+    sig = torch.tensor([1e-3 * (1 + 0.9 * r ** T) for r in segment_rho(lay)], device=device,
+                       dtype=torch.float32)
+    x.mul_(torch.repeat_interleave(sig, sizes))
+    return x.to(torch.bfloat16) if dt == "bf16" else x
+
+
+def algorithmic_bytes(n_loc, s_g, rows, row_bytes):
+    return {"accumulate": n_loc * (s_g + 8), "grad_norm": n_loc * (s_g + 4), "decide": 0,
+            "cache_get": 2 * rows * row_bytes, "cache_put": 2 * rows * row_bytes}
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2102_01386_b200 as af
+    from afinputs import bert_layout
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    which, dt = WORKLOADS[args.workload]
+    lay = bert_layout(which)
+    s_g = 2 if dt == "bf16" else 4
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, rank=rank, world=world, device=dev)
+    if world > 1:
+        fm.set_comm()
+    info = fm.info()
+    n_loc = info["shard_end"] - info["shard_begin"]
+    grads = [device_grad(lay, dt, 1000 + k, dev) for k in range(2)]
+    # activation cache partition of this rank (id mod world)
+    B = max(1, args.cache_batch // world)
+    cache = af.ActivationCache(NUM_EXAMPLES, ROW_BYTES, rank=rank, world=world, device=dev)
+    my_ids = torch.arange(rank, NUM_EXAMPLES, world, device=dev, dtype=torch.int64)
+    perm = my_ids[torch.randperm(my_ids.numel(), device=dev)]
+    rows = torch.randint(0, 256, (B, ROW_BYTES), dtype=torch.uint8, device=dev)
+    out_rows = torch.empty_like(rows)
+    depth_out = torch.empty(B, dtype=torch.int32, device=dev)
+    # populate every slot once (untimed) at depth 4: gets hit and never evict (boundary 4)
+    for b0 in range(0, my_ids.numel(), 4096):
+        ids_b = my_ids[b0:b0 + 4096]
+        src = rows.repeat((ids_b.numel() + B - 1) // B, 1)[: ids_b.numel()].contiguous()
+        cache.put(ids_b, src, 4)
+    n_batches = my_ids.numel() // B
+    id_batches = [perm[i * B:(i + 1) * B].contiguous() for i in range(max(1, n_batches))]
+    # one committed interval so that T = 1 and every dry-run decide does the full test
+    fm.layer_norms(grads[0])
+    fm.layer_norms(grads[1], interval_end=True)
+    fm.update_and_decide()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    n_ev = 6
+
+    def step(i, evs=None):
+        g = grads[i & 1]
+        ids = id_batches[i % len(id_batches)]
+        if evs: evs[0].record(stream)
+        fm.layer_norms(g, dry_run=True)
+        if evs: evs[1].record(stream)
+        fm.layer_norms(grads[(i + 1) & 1], interval_end=True, dry_run=True)
+        if evs: evs[2].record(stream)
+        fm.update_and_decide(dry_run=True)
+        if evs: evs[3].record(stream)
+        cache.get(ids, 4, out_rows, depth_out)
+        if evs: evs[4].record(stream)
+        cache.put(ids, rows, 4)
+        if evs: evs[5].record(stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0.record(stream)
+        for i in range(args.steps):
+            step(i, evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms_local = t0.elapsed_time(t1)
+    phases = ["accumulate", "grad_norm", "decide", "cache_get", "cache_put"]
+    ph_ms = {p: sum(e[k].elapsed_time(e[k + 1]) for e in evs) / args.steps for k, p in enumerate(phases)}
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_per_step = ms / args.steps
+    bytes_rank = algorithmic_bytes(n_loc, s_g, B, ROW_BYTES)
+    step_bytes_all = sum(bytes_rank.values()) * world   # every rank moves ~the same bytes
+    value = step_bytes_all / (ms_per_step * 1e-3) / 1e9
+    peak, peak_src = measured_peaks()
+    # dominant kernel roofline (per-launch CUDA-event durations on the launch stream)
+    dom = max(("accumulate", "grad_norm", "cache_get", "cache_put"), key=lambda p: ph_ms[p])
+    ach = bytes_rank[dom] / (ph_ms[dom] * 1e-3) / 1e9
+    phase_report = {p: {"ms": round(ph_ms[p], 5),
+                        "gbs": (round(bytes_rank[p] / (ph_ms[p] * 1e-3) / 1e9, 1) if bytes_rank[p] else None),
+                        "frac_of_peak": (round(bytes_rank[p] / (ph_ms[p] * 1e-3) / 1e9 / peak, 4)
+                                         if bytes_rank[p] else None)} for p in phases}
+    gn_dec_ms = ph_ms["grad_norm"] + ph_ms["decide"]
+    gn_dec = bytes_rank["grad_norm"] / (gn_dec_ms * 1e-3) / 1e9
+    cache_gbs = (bytes_rank["cache_get"] + bytes_rank["cache_put"]) / (
+        (ph_ms["cache_get"] + ph_ms["cache_put"]) * 1e-3) / 1e9
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": ("bf16" if dt == "bf16" else "f32") + "+f64",
+        "data": "synthetic (seeded device RNG, BERT layer layout, DESIGN.md input recipe)",
+        "config": {"workload": f"{args.workload}" + ("-sharded" if world > 1 else ""),
+                   "n_elements": lay.n, "segments": lay.n_segments, "n_local": n_loc,
+                   "cache": {"examples": NUM_EXAMPLES, "row_bytes": ROW_BYTES, "rows_per_rank_step": B},
+                   "boundary_f": 0, "parallelism": f"shard{world}",
+                   "l2": "inputs larger than L2: each step streams >= 4 GB/rank through the 126 MB L2"},
+        "grad_norm_decide_gbs": round(gn_dec, 1),
+        "grad_norm_decide_frac_of_hbm_peak": round(gn_dec / peak, 4),
+        "cache_gbs": round(cache_gbs, 1),
+        "phases": phase_report,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_rank[dom]},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clk.summary(),
+    }
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(lay, dt, s_g, B, budget_s=12.0)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist):
+    """Same metric through the public API with HOST buffers: every step copies the
+    rank's gradient shard, the cache rows and ids from pinned host memory and
+    reads the decision record and the fetched rows back."""
+    import torch
+    sb, se = info["shard_begin"], info["shard_end"]
+    n_loc = se - sb
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    host_g = [torch.empty(n_loc, dtype=tdt, pin_memory=True) for _ in range(2)]
+    for k in range(2):
+        host_g[k].copy_(device_grad(lay, dt, 2000 + k, dev)[sb:se].cpu())
+    dev_g = torch.zeros(lay.n, dtype=tdt, device=dev)          # full buffer; shard refreshed per step
+    host_rows = rows.cpu().pin_memory()
+    host_ids = [b.cpu().pin_memory() for b in id_batches[:8]]
+    dev_ids = torch.empty(B, dtype=torch.int64, device=dev)
+    dev_rows = torch.empty_like(rows)
+    out_rows = torch.empty_like(rows)
+    depth_out = torch.empty(B, dtype=torch.int32, device=dev)
+    host_out = torch.empty_like(host_rows)
+    host_depth = torch.empty(B, dtype=torch.int32, pin_memory=True)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        dev_g[sb:se].copy_(host_g[i & 1], non_blocking=True)
+        fm.layer_norms(dev_g, dry_run=True)
+        dev_g[sb:se].copy_(host_g[(i + 1) & 1], non_blocking=True)
+        fm.layer_norms(dev_g, interval_end=True, dry_run=True)
+        fm.update_and_decide(dry_run=True)                    # record -> pinned host (D2H)
+        dev_ids.copy_(host_ids[i % len(host_ids)], non_blocking=True)
+        cache.get(dev_ids, 4, out_rows, depth_out)
+        host_out.copy_(out_rows, non_blocking=True)
+        host_depth.copy_(depth_out, non_blocking=True)
+        dev_rows.copy_(host_rows, non_blocking=True)
+        cache.put(dev_ids, dev_rows, 4)
+
+    for i in range(2):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(steps):
+        step(i)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    bytes_all = sum(algorithmic_bytes(n_loc, s_g, B, ROW_BYTES).values()) * world
+    h2d = 2 * n_loc * s_g + B * ROW_BYTES + B * 8
+    d2h = 6184 + B * ROW_BYTES + B * 4
+    return {"value": round(bytes_all / (ms / steps * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": round(ms / steps, 4), "steps": steps,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+
+# ------------------------------------------------------------------ the oracle (CPU baseline / reference arm)
+
+def oracle_step_runner(lay, dt, s_g, B, n_sample):
+    """The oracle as it stands, on the first n_sample elements of the workload's
+    flat buffer (a prefix of its segments) plus B cache rows."""
+    import numpy as np
+
+    import oracle as O
+    from afinputs import bert_grad_step, cache_rows
+    offs = [o for o in lay.offsets if o < n_sample] + [n_sample]
+    kinds = lay.kinds[:len(offs) - 1]
+    if O.SEG_POOL not in kinds:           # keep a valid layout: treat the sample as one POOL
+        kinds = [O.SEG_POOL] * len(kinds)
+    kinds = [k if k != O.SEG_HEAD else O.SEG_POOL for k in kinds]
+    fz = O.Freezer(offs, kinds, O.DT_BF16 if dt == "bf16" else O.DT_F32)
+    g = [bert_grad_step(lay, 0, 0, t, dtype=dt, hi=n_sample) for t in range(2)]
+    cache = O.Cache(NUM_EXAMPLES, ROW_BYTES)
+    ids = np.arange(B)
+    rows = cache_rows(0, 0, B, ROW_BYTES)
+    out = np.empty_like(rows)
+    fz.layer_norms(g[0], False)
+    fz.layer_norms(g[1], True)
+    fz.update_and_decide()
+    cache.put(ids, rows, 4)
+
+    def step(i):
+        fz.layer_norms(g[i & 1], False, dry_run=True)
+        fz.layer_norms(g[(i + 1) & 1], True, dry_run=True)
+        fz.update_and_decide(dry_run=True)
+        cache.get(ids, 4, out)
+        cache.put(ids, rows, 4)
+    nbytes = sum(algorithmic_bytes(n_sample, s_g, B, ROW_BYTES).values())
+    return step, nbytes
+
+
+def cpu_baseline(lay, dt, s_g, B, budget_s=12.0):
+    n_sample = min(lay.n, 48_000_000)
+    step, nbytes = oracle_step_runner(lay, dt, s_g, B, n_sample)
+    step(0)
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        step(k)
+        k += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt_s = (time.perf_counter() - t0) / k
+    return {"value": round(nbytes / dt_s / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{k} oracle steps on the first {n_sample:,} elements of the {lay.name} flat buffer "
+                      f"(+{B} cache rows), numpy single-threaded, {dt_s:.3f} s/step"}
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the fp64 CPU oracle as it stands, on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    from afinputs import bert_layout
+    which, dt = WORKLOADS[args.workload]
+    lay = bert_layout(which)
+    s_g = 2 if dt == "bf16" else 4
+    B = max(1, args.cache_batch // max(1, args.gpus))
+    total_budget = 150.0
+    n_probe = 4_000_000
+    step, nb = oracle_step_runner(lay, dt, s_g, B, n_probe)
+    t = time.perf_counter()
+    step(0)
+    per_elem = (time.perf_counter() - t) / n_probe
+    per_step = total_budget / max(1, args.steps + args.warmup)
+    n_sample = int(min(lay.n, max(1_000_000, per_step / per_elem)))
+    step, nbytes = oracle_step_runner(lay, dt, s_g, B, n_sample)
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        step(i)
+    el = time.perf_counter() - t0
+    value = nbytes * args.steps / el / 1e9
+    sample = (f"each step: oracle on the first {n_sample:,} of {lay.n:,} elements of the {lay.name} "
+              f"flat buffer + {B} cache rows (numpy, single-threaded)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": ("bf16" if dt == "bf16" else "f32") + "+f64", "data": "synthetic",
+        "config": {"workload": args.workload, "n_elements": lay.n, "sample_elements": n_sample},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()
