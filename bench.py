@@ -190,10 +190,13 @@ def run_ours(args, rank, world, local):
         cache.put(ids_b, src, 4)
     n_batches = my_ids.numel() // B
     id_batches = [perm[i * B:(i + 1) * B].contiguous() for i in range(max(1, n_batches))]
-    # one committed interval so that T = 1 and every dry-run decide does the full test
+    # one committed interval so that T = 1 and every dry-run decide does the full test,
+    # then one committed accumulate step so that Delta is armed: every dry-run
+    # accumulate reads+writes Delta and every dry-run interval end reads it.
     fm.layer_norms(grads[0])
     fm.layer_norms(grads[1], interval_end=True)
     fm.update_and_decide()
+    fm.layer_norms(grads[0])
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     n_ev = 6
@@ -369,6 +372,7 @@ def oracle_step_runner(lay, dt, s_g, B, n_sample):
     fz.layer_norms(g[0], False)
     fz.layer_norms(g[1], True)
     fz.update_and_decide()
+    fz.layer_norms(g[0], False)          # arm Delta (as the GPU arm does)
     cache.put(ids, rows, 4)
 
     def step(i):

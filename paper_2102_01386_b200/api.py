@@ -86,17 +86,8 @@ class FreezingModule:
     def set_comm(self, group=None):
         """Collective: create the library's NCCL communicator (rank 0 makes the id,
         torch.distributed broadcasts it over `group`)."""
-        import torch.distributed as dist
-        uid = torch.zeros(128, dtype=torch.uint8)
-        if self.rank == 0:
-            buf = (ctypes.c_uint8 * 128)()
-            check(lib.af_nccl_unique_id(buf), "af_nccl_unique_id")
-            uid[:] = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
-        backend = dist.get_backend(group)
-        t = uid.to(self.device) if backend == "nccl" else uid
-        dist.broadcast(t, src=0, group=group)
-        raw = bytes(t.cpu().tolist())
-        buf = (ctypes.c_uint8 * 128).from_buffer_copy(raw)
+        uid = bootstrap_nccl_id(self.rank, group, self.device)
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         with torch.cuda.device(self.device):
             check(lib.af_ctx_set_comm(self._h, buf), "af_ctx_set_comm")
 
@@ -202,6 +193,24 @@ class ActivationCache:
             self.close()
         except Exception:
             pass
+
+
+def bootstrap_nccl_id(rank, group=None, device=None):
+    """Rank 0 creates a 128-byte ncclUniqueId through the library; torch.distributed
+    broadcasts it to every rank of `group` (gloo: CPU tensor, nccl: device tensor)."""
+    import torch.distributed as dist
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        buf = (ctypes.c_uint8 * 128)()
+        check(lib.af_nccl_unique_id(buf), "af_nccl_unique_id")
+        uid = torch.frombuffer(bytearray(bytes(buf)), dtype=torch.uint8).clone()
+    if dist.get_backend(group) == "nccl":
+        t = uid.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+        dist.broadcast(t, src=0, group=group)
+        uid = t.cpu()
+    else:
+        dist.broadcast(uid, src=0, group=group)
+    return bytes(uid.tolist())
 
 
 def should_cache(frozen_layers, t_layer_fwd_s, t_batch_read_s):

@@ -77,6 +77,8 @@ struct af_ctx {
   bool armed = false;    // Delta / ss_acc hold this interval's partial sum
   bool pending = false;  // an interval end awaits af_update_and_decide
   ncclComm_t comm = nullptr;
+  const void *rec_host = nullptr;  // last out_host pointer and its mapped device alias
+  af_decision *rec_host_dev = nullptr;
 
   template <typename T>
   T *at(size_t o) const {
@@ -88,7 +90,7 @@ struct af_cache {
   int64_t num_examples = 0, row_bytes = 0, capacity = 0;
   int32_t rank = 0, world = 1;
   char *payload = nullptr;
-  char *meta = nullptr;  // [Sched | err | pad][CacheMeta x capacity]
+  char *meta = nullptr;  // [err | pad to 256 B][CacheMeta x capacity]
   bool bound = false;
   int grid = 0;
 };
@@ -370,9 +372,20 @@ af_status af_update_and_decide(af_ctx *c, uint32_t flags, af_decision *out_host,
   p.tie_rel_eps = c->cfg.tie_rel_eps;
   p.min_active = c->cfg.min_active;
   p.commit = dry ? 0 : 1;
+  // page-locked host memory is device-addressable (UVA): the kernel writes the record there
+  // directly; otherwise fall back to an async copy.
+  if (out_host && out_host != c->rec_host) {
+    cudaPointerAttributes a{};
+    c->rec_host = out_host;
+    c->rec_host_dev = nullptr;
+    if (cudaPointerGetAttributes(&a, out_host) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer)
+      c->rec_host_dev = static_cast<af_decision *>(a.devicePointer);
+    cudaGetLastError();  // clear a sticky "invalid value" from unregistered pointers
+  }
+  p.host = out_host ? c->rec_host_dev : nullptr;
   const int e = launch_decide(p, stream);
   if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "decide kernel launch");
-  if (out_host)
+  if (out_host && !p.host)
     AF_CUDA(cudaMemcpyAsync(out_host, p.last, sizeof(af_decision), cudaMemcpyDeviceToHost,
                             static_cast<cudaStream_t>(stream)),
             "cudaMemcpyAsync(decision)");
@@ -501,8 +514,7 @@ static af_status cache_common(af_cache *c, const int64_t *ids, int32_t n, const 
   p = CacheParams{};
   p.payload = c->payload;
   p.meta = reinterpret_cast<CacheMeta *>(c->meta + kMetaHeader);
-  p.sched = reinterpret_cast<Sched *>(c->meta);
-  p.err = reinterpret_cast<unsigned int *>(c->meta + sizeof(Sched));
+  p.err = reinterpret_cast<unsigned int *>(c->meta);
   p.ids = ids;
   p.n = n;
   p.row_bytes = c->row_bytes;
@@ -547,7 +559,7 @@ af_status af_cache_status(af_cache *c, uint32_t *device_error_flags, int64_t *n_
   if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
   AF_CUDA(cudaDeviceSynchronize(), "cache status sync");
   unsigned int err = 0;
-  AF_CUDA(cudaMemcpy(&err, c->meta + sizeof(Sched), sizeof(err), cudaMemcpyDeviceToHost), "cudaMemcpy(err)");
+  AF_CUDA(cudaMemcpy(&err, c->meta, sizeof(err), cudaMemcpyDeviceToHost), "cudaMemcpy(err)");
   *device_error_flags = err;
   if (n_valid) {
     std::vector<CacheMeta> m(static_cast<size_t>(c->capacity));

@@ -12,9 +12,9 @@
 // STAGES x 32 KiB of shared memory, one elected lane issuing, so up to
 // STAGES-1 chunk loads and the matching stores are in flight per SM without
 // register staging.  Work items are (row, 32 KiB chunk) pairs dealt round-robin
-// to a persistent grid of one CTA per SM.  Get evictions are applied by the
-// last CTA to finish, after every chunk has read the record's meta word, so all
-// chunks of a row agree on hit/miss.
+// to a persistent grid of one CTA per SM.  A get evicts a record only after
+// every chunk of its row has read the meta word (a per-record reader count,
+// fenced), so all chunks of a row agree on hit/miss.
 #include <cuda_runtime.h>
 
 #include "af_internal.h"
@@ -126,7 +126,6 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
   unsigned char *stage_buf = smem + 128;
   Desc *descs = reinterpret_cast<Desc *>(stage_buf + static_cast<size_t>(kStages) * kChunk);
-  __shared__ int s_last;
   const int lane = threadIdx.x;
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
@@ -164,20 +163,22 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
           dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
           dsc.dst = rec;
           dsc.ok = 1u;
-          if (c == 0) {
-            CacheMeta m2;
-            m2.depth = p.depth;
-            m2.valid = 1;
-            p.meta[slot] = m2;
-          }
+          if (c == 0) *reinterpret_cast<int2 *>(p.meta + slot) = make_int2(p.depth, 1);  // {depth, valid}
         } else {
-          const int2 mv = __ldcg(reinterpret_cast<const int2 *>(p.meta) + slot);  // {depth, valid}
+          const int4 mv = __ldcg(reinterpret_cast<const int4 *>(p.meta) + slot);  // {depth, valid, readers, -}
           const bool hit = mv.y != 0;
           if (c == 0) p.depth_out[i] = hit ? mv.x : -1;
           if (hit) {
             dsc.src = rec;
             dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
             dsc.ok = 1u;
+            // evict on read once every chunk of the row has read the record
+            __threadfence();
+            const unsigned int seen = atomicAdd(&p.meta[slot].readers, 1u);
+            if (seen == static_cast<unsigned int>(p.n_chunks) - 1u) {
+              if (mv.x < p.cur_boundary) p.meta[slot].valid = 0;
+              p.meta[slot].readers = 0u;
+            }
           }
         }
       } else if (!PUT && c == 0) {
@@ -189,26 +190,7 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
     if (lane == 0) pump(descs, m, stage_buf, bars, seq);
     __syncwarp();
   }
-  if (lane == 0) {
-    bulk_wait_all();  // all stores complete before the CTA retires its shared memory
-    __threadfence();
-    const unsigned int d = atomicAdd(&p.sched->done, 1u);
-    s_last = (d == gridDim.x - 1);
-  }
-  __syncwarp();
-  if (!s_last) return;
-  __threadfence();
-  if (lane == 0) p.sched->done = 0;
-  if (!PUT) {
-    // evict on read: the frozen count grew beyond the record's depth
-    for (int i = lane; i < p.n; i += 32) {
-      const int64_t id = p.ids[i];
-      if (id < 0 || id >= p.num_examples || id % p.world != p.rank) continue;
-      const int64_t slot = id / p.world;
-      const int2 mv = __ldcg(reinterpret_cast<const int2 *>(p.meta) + slot);
-      if (mv.y != 0 && mv.x < p.cur_boundary) p.meta[slot].valid = 0;
-    }
-  }
+  if (lane == 0) bulk_wait_all();  // all stores complete before the CTA retires its shared memory
 }
 
 }  // namespace

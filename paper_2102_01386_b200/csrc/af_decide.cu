@@ -128,10 +128,11 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(const DecidePara
   const int k = nonfinite ? 0 : s_k;
   const int f_new = f + k;
 
-  // record (device copy + ring) -- every thread writes its segment's entries
-  af_decision *recs[2] = {p.last, p.ring + (T % kRing)};
-  for (int q = 0; q < 2; ++q) {
+  // record: device copy, ring slot and (if mapped) the caller's pinned host struct
+  af_decision *recs[3] = {p.last, p.ring + (T % kRing), p.host};
+  for (int q = 0; q < 3; ++q) {
     af_decision *r = recs[q];
+    if (r == nullptr) continue;
     if (t < AF_MAX_SEGMENTS) {
       r->sumsq[t] = (t < L) ? ss : 0.0;
       r->norm[t] = (t < L) ? nrm : 0.0;

@@ -66,6 +66,7 @@ struct DecideParams {
   DevState *state;
   af_decision *last;        // device copy of the latest record
   af_decision *ring;        // [kRing]
+  af_decision *host;        // mapped page-locked host record or nullptr
   double percentile;
   int32_t pct_method;
   double tie_rel_eps;
@@ -73,17 +74,20 @@ struct DecideParams {
   int32_t commit;           // 0 under AF_DRY_RUN
 };
 
-// Cache records: one 8-byte meta word per slot.
+// Cache records: one 16-byte meta word per slot.  `readers` counts the chunks
+// of a get that have read {depth, valid}; the last one applies the eviction.
 struct CacheMeta {
   int32_t depth;
   int32_t valid;
+  uint32_t readers;
+  uint32_t pad;
 };
+static_assert(sizeof(CacheMeta) == 16, "cache meta layout");
 
 struct CacheParams {
   char *payload;            // [capacity][row_bytes]
   CacheMeta *meta;          // [capacity]
   unsigned int *err;        // sticky flags
-  Sched *sched;
   const int64_t *ids;
   int32_t n;
   int64_t row_bytes;

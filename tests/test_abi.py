@@ -172,6 +172,6 @@ def test_cache_create_validation_and_sizes():
     assert L.lib.af_cache_create(-1, 64, 0, 1, ctypes.byref(h)) == L.AF_EINVAL
     c = af.ActivationCache(100_000, 196_608, rank=3, world=8, bind=False)
     assert c.payload_bytes == 12_500 * 196_608
-    assert c.meta_bytes == 256 + 12_500 * 8
+    assert c.meta_bytes == 256 + 12_500 * 16
     c2 = af.ActivationCache(10, 64, rank=3, world=4, bind=False)       # ids 3, 7
     assert c2.payload_bytes == 2 * 64
