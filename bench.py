@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cache-sweep", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly (no CUDA graphs)")
+    ap.add_argument("--sweep", action="store_true",
+                    help="configs[4]: layers x elements sweep, one JSON line per point (not the bench line)")
     return ap.parse_args()
 
 
@@ -148,6 +152,17 @@ def device_grad(lay, dt, seed, device, T=1):
     return x.to(torch.bfloat16) if dt == "bf16" else x
 
 
+def ncu_traffic(workload, phase):
+    """roofline.traffic: DRAM bytes per launch of this kernel from the committed
+    `ncu --set full` capture (profiles/traffic.json, tools/traffic_from_ncu.py)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))[workload][phase]
+        return {"traffic": round(d["bytes_per_launch"]), "traffic_source": "profiles/traffic.json <- " + d["source"]}
+    except Exception:  # noqa: BLE001
+        return {"traffic": None}
+
+
 def algorithmic_bytes(n_loc, s_g, rows, row_bytes):
     return {"accumulate": n_loc * (s_g + 8), "grad_norm": n_loc * (s_g + 4), "decide": 0,
             "cache_get": 2 * rows * row_bytes, "cache_put": 2 * rows * row_bytes}
@@ -216,12 +231,27 @@ def run_ours(args, rank, world, local):
         cache.put(ids, rows, 4)
         if evs: evs[5].record(stream)
 
+    # the timed loop replays CUDA graphs of one step each (8 graphs rotate the id batches)
+    graphs = []
+    if not args.no_graph:
+        for i in range(min(8, len(id_batches))):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                step(i)
+            graphs.append(gph)
+        torch.cuda.synchronize()
+
+    def run(i):
+        if graphs:
+            graphs[i % len(graphs)].replay()
+        else:
+            step(i)
+
     for i in range(args.warmup):
-        step(i)
+        run(i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -229,14 +259,20 @@ def run_ours(args, rank, world, local):
             dist.barrier()
         t0.record(stream)
         for i in range(args.steps):
-            step(i, evs[i])
+            run(i)
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     ms_local = t0.elapsed_time(t1)
+    # per-phase breakdown: a second, eagerly launched pass with CUDA events between calls
+    n_ph = max(1, min(args.steps, 100))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(n_ph)]
+    for i in range(n_ph):
+        step(i, evs[i])
+    torch.cuda.synchronize()
     phases = ["accumulate", "grad_norm", "decide", "cache_get", "cache_put"]
-    ph_ms = {p: sum(e[k].elapsed_time(e[k + 1]) for e in evs) / args.steps for k, p in enumerate(phases)}
+    ph_ms = {p: sum(e[k].elapsed_time(e[k + 1]) for e in evs) / n_ph for k, p in enumerate(phases)}
     ms = ms_local
     if world > 1:
         t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
@@ -267,17 +303,21 @@ def run_ours(args, rank, world, local):
                    "n_elements": lay.n, "segments": lay.n_segments, "n_local": n_loc,
                    "cache": {"examples": NUM_EXAMPLES, "row_bytes": ROW_BYTES, "rows_per_rank_step": B},
                    "boundary_f": 0, "parallelism": f"shard{world}",
+                   "launch": "eager" if args.no_graph else "CUDA graph per step (8 graphs rotating id batches)",
                    "l2": "inputs larger than L2: each step streams >= 4 GB/rank through the 126 MB L2"},
         "grad_norm_decide_gbs": round(gn_dec, 1),
         "grad_norm_decide_frac_of_hbm_peak": round(gn_dec / peak, 4),
         "cache_gbs": round(cache_gbs, 1),
         "phases": phase_report,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_rank[dom]},
+                     "frac": round(ach / peak, 4), "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_rank[dom],
+                     **ncu_traffic(args.workload if world == 1 else None, dom)},
         "gpu_launches": 5 * args.steps,
         "clocks": clk.summary(),
     }
+    if not args.no_cache_sweep:
+        result["cache_gbs_by_batch"] = cache_sweep(cache, my_ids, rows, dev, world, dist)
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -287,6 +327,97 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(32, 256, 1024, 4096), reps=20):
+    """Cache get / put GB/s (2 x rows x row_bytes per call) per batch size on this
+    rank's partition (all hits, no eviction: boundary == depth)."""
+    import torch
+    out = {}
+    B0 = rows.shape[0]
+    big = rows.repeat((max(batches) + B0 - 1) // B0, 1)[: max(batches)].contiguous()
+    peak, _ = measured_peaks()
+    for B in batches:
+        if B > my_ids.numel():
+            continue
+        ids = my_ids[torch.randperm(my_ids.numel(), device=dev)[:B]].contiguous()
+        src = big[:B]
+        dst = torch.empty_like(src)
+        dep = torch.empty(B, dtype=torch.int32, device=dev)
+        for _ in range(3):
+            cache.put(ids, src, 4)
+            cache.get(ids, 4, dst, dep)
+        res = {}
+        for name, fn in (("put", lambda: cache.put(ids, src, 4)), ("get", lambda: cache.get(ids, 4, dst, dep))):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
+            torch.cuda.synchronize()
+            for r in range(reps):
+                ev[2 * r].record()
+                fn()
+                ev[2 * r + 1].record()
+            torch.cuda.synchronize()
+            ms = statistics.median(ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(reps))
+            gbs = 2 * B * ROW_BYTES / (ms * 1e-3) / 1e9
+            res[name] = {"us": round(ms * 1e3, 2), "gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4)}
+        out[str(B)] = res
+    return out
+
+
+def run_sweep(args, local):
+    """configs[4]: uniform layouts, L in {1,2,4,12,24,48} POOL segments x n in
+    {1M..1B} elements, fp32 and bf16, one GPU; accumulate and interval-end GB/s."""
+    import torch
+
+    import paper_2102_01386_b200 as af
+    from afinputs import uniform_layout
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    peak, src = measured_peaks()
+    for dt in ("f32", "bf16"):
+        s_g = 2 if dt == "bf16" else 4
+        for n in (1 << 20, 1 << 22, 1 << 24, 1 << 26, 1 << 28, 1 << 30):
+            if n * (s_g + 4) > 9e9:
+                continue
+            g = device_grad(uniform_layout(n, 1), dt, 7, dev)
+            for L in (1, 2, 4, 12, 24, 48):
+                lay = uniform_layout(n, L)
+                fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, device=dev)
+                fm.layer_norms(g)
+                fm.layer_norms(g, interval_end=True)
+                fm.update_and_decide()
+                fm.layer_norms(g)                    # arm Delta
+                reps = max(5, min(200, int(2e10 / (n * (s_g + 8)))))
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                for _ in range(3):
+                    fm.layer_norms(g, dry_run=True)
+                    fm.layer_norms(g, interval_end=True, dry_run=True)
+                    fm.update_and_decide(dry_run=True)
+                torch.cuda.synchronize()
+                ev[0].record()
+                for _ in range(reps):
+                    fm.layer_norms(g, dry_run=True)
+                ev[1].record()
+                for _ in range(reps):
+                    fm.layer_norms(g, interval_end=True, dry_run=True)
+                    fm.update_and_decide(dry_run=True)
+                ev[2].record()
+                torch.cuda.synchronize()
+                acc_ms = ev[0].elapsed_time(ev[1]) / reps
+                end_ms = ev[1].elapsed_time(ev[2]) / reps
+                acc = n * (s_g + 8) / (acc_ms * 1e-3) / 1e9
+                gnd = n * (s_g + 4) / (end_ms * 1e-3) / 1e9
+                resident = n * (s_g + 4) < 126e6
+                print(json.dumps({"sweep": "configs[4]", "dtype": dt, "n": n, "layers": L, "reps": reps,
+                                  "accumulate_us": round(acc_ms * 1e3, 2), "accumulate_gbs": round(acc, 1),
+                                  "accumulate_frac": round(acc / peak, 4),
+                                  "grad_norm_decide_us": round(end_ms * 1e3, 2),
+                                  "grad_norm_decide_gbs": round(gnd, 1), "grad_norm_decide_frac": round(gnd / peak, 4),
+                                  "regime": "L2-resident / latency-bound" if resident else "HBM",
+                                  "peak": peak, "peak_source": src}), flush=True)
+                fm.close()
+                del fm
+            del g
+            torch.cuda.empty_cache()
 
 
 def run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist):
@@ -446,6 +577,9 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.sweep:
+        run_sweep(args, local)
         return
     run_ours(args, rank, world, local)
 

@@ -109,7 +109,7 @@ class FreezingModule:
         flags = L.AF_DRY_RUN if dry_run else 0
         out = c_void_p(self._rec_host.data_ptr()) if copy_record else c_void_p(0)
         check(lib.af_update_and_decide(self._h, flags, out, _stream_handle(stream)), "af_update_and_decide")
-        if copy_record:
+        if copy_record and not torch.cuda.is_current_stream_capturing():
             self._event.record(stream if stream is not None else torch.cuda.current_stream())
 
     def decision(self):

@@ -206,8 +206,13 @@ static int launch_cache(const CacheParams &p0, int grid, void *stream) {
   if (items < grid) grid = static_cast<int>(items);
   if (grid < 1) grid = 1;
   const int smem = cache_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(cache_kernel<PUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return static_cast<int>(e);
+  // once per process and kernel (not a stream operation: keep it out of CUDA-graph captures)
+  static int attr_set = 0;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(cache_kernel<PUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    attr_set = 1;
+  }
   cache_kernel<PUT><<<grid, 32, smem, static_cast<cudaStream_t>(stream)>>>(p);
   return static_cast<int>(cudaGetLastError());
 }

@@ -7,8 +7,8 @@
 // HBM-bound elementwise/reduction work: no tensor cores (nothing is a
 // contraction).  Design:
 //  * persistent grid sized from the occupancy query (148 SMs x resident CTAs),
-//    dynamic tile scheduler (one atomic per 64 KiB tile, prefetched one tile
-//    ahead, reset by the last CTA) -- balances the two dies' speed spread;
+//    dynamic tile scheduler (one atomic per 64 KiB tile, index two tiles and
+//    descriptor one tile ahead, reset by the last CTA) -- balances the two dies;
 //  * 128-bit streaming loads/stores (ld/st .cs), 4 vectors in flight per thread;
 //  * tiles never straddle a segment, so each tile's fp64 partial belongs to one
 //    layer; the partial's reduction order is fixed by the thread mapping
@@ -176,7 +176,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 template <int MODE, typename GT, bool RD>
 __global__ void __launch_bounds__(kNormBlock) norms_kernel(const NormParams p) {
-  __shared__ int s_tile[2];
+  __shared__ int s_tile[3];
+  __shared__ Tile s_desc[3];
   __shared__ double s_red[kNormBlock / 32];
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -184,14 +185,33 @@ __global__ void __launch_bounds__(kNormBlock) norms_kernel(const NormParams p) {
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int first_tile = p.first_tile_of_f[f];
 
-  if (tid == 0) s_tile[0] = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+  // Tile scheduler, two tiles of lookahead: while tile `it` is processed, thread 0
+  // has the atomic for tile it+2 and the descriptor load of tile it+1 in flight and
+  // publishes them only after its share of tile `it`, so no warp waits on them.
+  if (tid == 0) {
+    const int t0 = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+    s_tile[0] = t0;
+    if (t0 < p.n_tiles) s_desc[0] = p.tiles[t0];
+    s_tile[1] = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+  }
   __syncthreads();
   for (int it = 0;; ++it) {
-    const int tile = s_tile[it & 1];
+    const int slot = it % 3, slot1 = (it + 1) % 3, slot2 = (it + 2) % 3;
+    const int tile = s_tile[slot];
     if (tile >= p.n_tiles) break;
-    if (tid == 0) s_tile[(it + 1) & 1] = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
-    const Tile t = p.tiles[tile];
+    const Tile t = s_desc[slot];
+    int next2 = 0;
+    Tile d1{0, 0, 0, 0};
+    if (tid == 0) {
+      next2 = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+      const int n1 = s_tile[slot1];
+      if (n1 < p.n_tiles) d1 = p.tiles[n1];
+    }
     const double v = process_tile<MODE, GT, RD>(p, t);
+    if (tid == 0) {
+      s_tile[slot2] = next2;
+      s_desc[slot1] = d1;
+    }
     if (MODE != kAccum) {
       const double w = warp_sum(v);
       if (lane == 0) s_red[warp] = w;
