@@ -5,9 +5,9 @@
 One step = one pass of every SURVEY.md §8(a) row over one batch of synthetic
 input, through the C ABI:
   a2   af_layer_norms            Delta += g over the rank's shard    n_loc*(s_g+8) B
-  a3-4 af_layer_norms(END)       fp64 sum of squares of Delta + g    n_loc*(s_g+4) B
-                                 (+ NCCL all-gather of the L partials when N > 1)
-  a5-9 af_update_and_decide      Eq. 1, percentile, prefix scan, record copy
+  a3-9 af_interval_end           fp64 sum of squares of Delta + g,   n_loc*(s_g+4) B
+                                 Eq. 1, percentile, prefix scan, record (ONE kernel at N = 1;
+                                 kernel + NCCL all-gather of the L partials + decide at N > 1)
   a11  af_cache_get              B rows by example id                 2*B*row B
   a10  af_cache_put              B rows by example id                 2*B*row B
 Timed steps run under AF_DRY_RUN (every rep does the same work: Delta stays
@@ -164,7 +164,7 @@ def ncu_traffic(workload, phase):
 
 
 def algorithmic_bytes(n_loc, s_g, rows, row_bytes):
-    return {"accumulate": n_loc * (s_g + 8), "grad_norm": n_loc * (s_g + 4), "decide": 0,
+    return {"accumulate": n_loc * (s_g + 8), "grad_norm_decide": n_loc * (s_g + 4),
             "cache_get": 2 * rows * row_bytes, "cache_put": 2 * rows * row_bytes}
 
 
@@ -214,22 +214,20 @@ def run_ours(args, rank, world, local):
     fm.layer_norms(grads[0])
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    n_ev = 6
+    n_ev = 5
 
     def step(i, evs=None):
         g = grads[i & 1]
         ids = id_batches[i % len(id_batches)]
         if evs: evs[0].record(stream)
-        fm.layer_norms(g, dry_run=True)
+        fm.layer_norms(g, dry_run=True)                               # a2
         if evs: evs[1].record(stream)
-        fm.layer_norms(grads[(i + 1) & 1], interval_end=True, dry_run=True)
+        fm.interval_end(grads[(i + 1) & 1], dry_run=True)             # a3-a9 (fused at N=1)
         if evs: evs[2].record(stream)
-        fm.update_and_decide(dry_run=True)
+        cache.get(ids, 4, out_rows, depth_out)                        # a11
         if evs: evs[3].record(stream)
-        cache.get(ids, 4, out_rows, depth_out)
+        cache.put(ids, rows, 4)                                       # a10
         if evs: evs[4].record(stream)
-        cache.put(ids, rows, 4)
-        if evs: evs[5].record(stream)
 
     # the timed loop replays CUDA graphs of one step each (8 graphs rotate the id batches)
     graphs = []
@@ -271,7 +269,7 @@ def run_ours(args, rank, world, local):
     for i in range(n_ph):
         step(i, evs[i])
     torch.cuda.synchronize()
-    phases = ["accumulate", "grad_norm", "decide", "cache_get", "cache_put"]
+    phases = ["accumulate", "grad_norm_decide", "cache_get", "cache_put"]
     ph_ms = {p: sum(e[k].elapsed_time(e[k + 1]) for e in evs) / n_ph for k, p in enumerate(phases)}
     ms = ms_local
     if world > 1:
@@ -284,14 +282,14 @@ def run_ours(args, rank, world, local):
     value = step_bytes_all / (ms_per_step * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
     # dominant kernel roofline (per-launch CUDA-event durations on the launch stream)
-    dom = max(("accumulate", "grad_norm", "cache_get", "cache_put"), key=lambda p: ph_ms[p])
+    dom = max(("accumulate", "grad_norm_decide", "cache_get", "cache_put"), key=lambda p: ph_ms[p])
     ach = bytes_rank[dom] / (ph_ms[dom] * 1e-3) / 1e9
     phase_report = {p: {"ms": round(ph_ms[p], 5),
                         "gbs": (round(bytes_rank[p] / (ph_ms[p] * 1e-3) / 1e9, 1) if bytes_rank[p] else None),
                         "frac_of_peak": (round(bytes_rank[p] / (ph_ms[p] * 1e-3) / 1e9 / peak, 4)
                                          if bytes_rank[p] else None)} for p in phases}
-    gn_dec_ms = ph_ms["grad_norm"] + ph_ms["decide"]
-    gn_dec = bytes_rank["grad_norm"] / (gn_dec_ms * 1e-3) / 1e9
+    gn_dec_ms = ph_ms["grad_norm_decide"]
+    gn_dec = bytes_rank["grad_norm_decide"] / (gn_dec_ms * 1e-3) / 1e9
     cache_gbs = (bytes_rank["cache_get"] + bytes_rank["cache_put"]) / (
         (ph_ms["cache_get"] + ph_ms["cache_put"]) * 1e-3) / 1e9
     result = {
@@ -313,7 +311,7 @@ def run_ours(args, rank, world, local):
                      "frac": round(ach / peak, 4), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_rank[dom],
                      **ncu_traffic(args.workload if world == 1 else None, dom)},
-        "gpu_launches": 5 * args.steps,
+        "gpu_launches": (4 if world == 1 else 5) * args.steps,
         "clocks": clk.summary(),
     }
     if not args.no_cache_sweep:
@@ -390,16 +388,14 @@ def run_sweep(args, local):
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                 for _ in range(3):
                     fm.layer_norms(g, dry_run=True)
-                    fm.layer_norms(g, interval_end=True, dry_run=True)
-                    fm.update_and_decide(dry_run=True)
+                    fm.interval_end(g, dry_run=True)
                 torch.cuda.synchronize()
                 ev[0].record()
                 for _ in range(reps):
                     fm.layer_norms(g, dry_run=True)
                 ev[1].record()
                 for _ in range(reps):
-                    fm.layer_norms(g, interval_end=True, dry_run=True)
-                    fm.update_and_decide(dry_run=True)
+                    fm.interval_end(g, dry_run=True)
                 ev[2].record()
                 torch.cuda.synchronize()
                 acc_ms = ev[0].elapsed_time(ev[1]) / reps
@@ -447,8 +443,7 @@ def run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world
         dev_g[sb:se].copy_(host_g[i & 1], non_blocking=True)
         fm.layer_norms(dev_g, dry_run=True)
         dev_g[sb:se].copy_(host_g[(i + 1) & 1], non_blocking=True)
-        fm.layer_norms(dev_g, interval_end=True, dry_run=True)
-        fm.update_and_decide(dry_run=True)                    # record -> pinned host (D2H)
+        fm.interval_end(dev_g, dry_run=True)                  # record -> pinned host (D2H)
         dev_ids.copy_(host_ids[i % len(host_ids)], non_blocking=True)
         cache.get(dev_ids, 4, out_rows, depth_out)
         host_out.copy_(out_rows, non_blocking=True)

@@ -193,6 +193,16 @@ AF_API af_status af_layer_norms(af_ctx *ctx, const void *grad_dev, uint32_t flag
  * point.  AF_DRY_RUN: everything is computed and recorded, nothing committed. */
 AF_API af_status af_update_and_decide(af_ctx *ctx, uint32_t flags, af_decision *out_host, void *stream);
 
+/* Fused interval end: exactly af_layer_norms(AF_INTERVAL_END |
+ * flags) followed by af_update_and_decide(flags), same results and state.  With
+ * world == 1 it is ONE kernel launch: the CTA that completes a segment's last
+ * tile sums that segment, and the grid's last CTA runs the decision (no second
+ * launch, no host involvement).  With world > 1: kernel, NCCL all-gather (when a
+ * communicator is set; otherwise the caller must use the two-call form to fill
+ * the exchange rows), decide kernel.  flags: AF_DRY_RUN only. */
+AF_API af_status af_interval_end(af_ctx *ctx, const void *grad_dev, uint32_t flags, af_decision *out_host,
+                                 void *stream);
+
 /* Synchronous.  Serialise / restore {T, f, prev norms, Delta-armed flag}
  * (checkpoint at interval boundaries is exact).  With buf == NULL, get_state
  * stores the required size in *len. */

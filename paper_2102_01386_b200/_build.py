@@ -1,6 +1,7 @@
 """Build libautofreeze.so in-tree with nvcc for sm_100a (no JIT cache).
 
-`python -m paper_2102_01386_b200._build [--force] [-v]`
+`python paper_2102_01386_b200/_build.py [--force] [-v] [--ptxas]` (run by path:
+importing the package loads the library this script builds).
 """
 import os
 import subprocess
@@ -56,6 +57,7 @@ def build(force=False, verbose=False, ptxas_verbose=False):
            "-cudart", "static"]
     if ptxas_verbose:
         cmd += ["-Xptxas", "-v"]
+    cmd += os.environ.get("AF_NVCC_EXTRA", "").split()
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)

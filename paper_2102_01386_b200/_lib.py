@@ -57,6 +57,7 @@ SIGNATURES = {
     "af_ctx_exchange_rows": (c_int, [c_void_p, POINTER(c_void_p)]),
     "af_layer_norms": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p]),
     "af_update_and_decide": (c_int, [c_void_p, c_uint32, c_void_p, c_void_p]),
+    "af_interval_end": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_get_state": (c_int, [c_void_p, c_void_p, POINTER(c_size_t)]),
     "af_set_state": (c_int, [c_void_p, c_void_p, c_size_t]),
     "af_ctx_destroy": (c_int, [c_void_p]),

@@ -112,6 +112,16 @@ class FreezingModule:
         if copy_record and not torch.cuda.is_current_stream_capturing():
             self._event.record(stream if stream is not None else torch.cuda.current_stream())
 
+    def interval_end(self, grad, dry_run=False, stream=None, copy_record=True):
+        """af_interval_end: the interval-end step and the decision in one call
+        (one kernel launch when world == 1)."""
+        flags = L.AF_DRY_RUN if dry_run else 0
+        out = c_void_p(self._rec_host.data_ptr()) if copy_record else c_void_p(0)
+        check(lib.af_interval_end(self._h, c_void_p(grad.data_ptr()), flags, out, _stream_handle(stream)),
+              "af_interval_end")
+        if copy_record and not torch.cuda.is_current_stream_capturing():
+            self._event.record(stream if stream is not None else torch.cuda.current_stream())
+
     def decision(self):
         """The last copied decision record (waits for the stream to reach it)."""
         self._event.synchronize()

@@ -68,11 +68,11 @@ struct af_ctx {
   // workspace
   size_t accum_bytes = 0, scratch_bytes = 0;
   size_t o_state = 0, o_sched = 0, o_tiles = 0, o_ftf = 0, o_stb = 0, o_pool = 0, o_part = 0, o_ssall = 0,
-         o_ssacc = 0, o_last = 0, o_ring = 0;
+         o_ssacc = 0, o_last = 0, o_ring = 0, o_segdone = 0;
   float *accum = nullptr;
   char *scratch = nullptr;
   bool bound = false;
-  int grid = 0;
+  int grid[3] = {0, 0, 0};  // persistent grid per streaming-kernel mode (occupancy x SMs)
   // host flags
   bool armed = false;    // Delta / ss_acc hold this interval's partial sum
   bool pending = false;  // an interval end awaits af_update_and_decide
@@ -183,7 +183,7 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
     const int64_t lo = std::max(c->offs[l], c->sb), hi = std::min(c->offs[l + 1], c->se);
     for (int64_t pos = lo; pos < hi;) {
       const int64_t nxt = std::min(hi, (pos / TE + 1) * TE);
-      c->tiles.push_back(Tile{pos, nxt, l, 0});
+      c->tiles.push_back(Tile{pos, nxt, l, 0, 0, 0});
       pos = nxt;
     }
     if (c->tiles.size() > static_cast<size_t>(1) << 30) {
@@ -192,6 +192,10 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
     }
   }
   c->seg_tile_begin[L] = static_cast<int32_t>(c->tiles.size());
+  for (auto &t : c->tiles) {
+    t.seg_first = c->seg_tile_begin[t.seg];
+    t.seg_end = c->seg_tile_begin[t.seg + 1];
+  }
   // first active tile when j POOL layers are frozen: PRE and POOL[0..j) skipped (Q11)
   c->first_tile_of_f.assign(n_pool + 1, 0);
   for (int j = 0; j <= n_pool; ++j) {
@@ -219,6 +223,7 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   c->o_ssacc = take(L * sizeof(double));
   c->o_last = take(sizeof(af_decision));
   c->o_ring = take(kRing * sizeof(af_decision));
+  c->o_segdone = take(L * sizeof(unsigned int));
   c->scratch_bytes = o;
   *out = c;
   return AF_OK;
@@ -252,12 +257,15 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
   if (c->accum_bytes && !accum_dev) return fail(AF_EINVAL, "accum buffer required");
   if (!aligned(scratch_dev, 256) || (accum_dev && !aligned(accum_dev, 256)))
     return fail(AF_EINVAL, "workspace buffers must be 256-byte aligned");
-  int sms = 0, bps = 0;
+  int sms = 0;
   cudaError_t e = static_cast<cudaError_t>(device_sm_count(&sms));
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
-  e = static_cast<cudaError_t>(norms_max_blocks_per_sm(kEndDelta, c->dtype, &bps));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-  c->grid = std::max(1, sms * std::max(1, bps));
+  for (int m = 0; m < 3; ++m) {
+    int bps = 0;
+    e = static_cast<cudaError_t>(norms_max_blocks_per_sm(m, c->dtype, &bps));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    c->grid[m] = std::max(1, sms * std::max(1, bps));
+  }
   c->accum = static_cast<float *>(accum_dev);
   c->scratch = static_cast<char *>(scratch_dev);
   AF_CUDA(cudaMemset(c->scratch, 0, c->scratch_bytes), "cudaMemset(scratch)");
@@ -309,17 +317,11 @@ af_status af_ctx_exchange_rows(af_ctx *c, double **ss_all_dev) {
   return AF_OK;
 }
 
-af_status af_layer_norms(af_ctx *c, const void *grad_dev, uint32_t flags, void *stream) {
-  if (!c) return fail(AF_EINVAL, "NULL ctx");
-  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
-  if (!grad_dev || !aligned(grad_dev, 16)) return fail(AF_EINVAL, "grad must be a 16-byte aligned device pointer");
-  if (flags & ~(AF_INTERVAL_END | AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
-  const bool end = flags & AF_INTERVAL_END, dry = flags & AF_DRY_RUN;
-  int mode;
-  if (c->cfg.acc_mode == AF_ACC_DELTA)
-    mode = end ? kEndDelta : kAccum;
-  else
-    mode = kStepSq;
+}  // extern "C"
+
+namespace {
+
+NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   NormParams p{};
   p.grad = grad_dev;
   p.delta = c->accum;
@@ -334,30 +336,20 @@ af_status af_layer_norms(af_ctx *c, const void *grad_dev, uint32_t flags, void *
   p.partials = c->at<double>(c->o_part);
   p.ss_out = c->at<double>(c->o_ssall) + static_cast<size_t>(c->cfg.rank) * c->L;
   p.ss_acc = c->at<double>(c->o_ssacc);
+  p.seg_done = c->at<unsigned int>(c->o_segdone);
   p.n_pool = c->n_pool;
   p.first = c->armed ? 0 : 1;
   p.end = end ? 1 : 0;
   p.commit = dry ? 0 : 1;
-  const int grid = std::max(1, std::min<int>(c->grid, std::max<int>(1, p.n_tiles)));
-  const int e = launch_norms(p, mode, c->dtype, grid, stream);
-  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "norms kernel launch");
-  if (end && c->cfg.world > 1 && c->comm) {
-    double *rows = c->at<double>(c->o_ssall);
-    ncclResult_t r = ncclAllGather(rows + static_cast<size_t>(c->cfg.rank) * c->L, rows, c->L, ncclFloat64, c->comm,
-                                   static_cast<cudaStream_t>(stream));
-    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
-  }
-  if (!dry) c->armed = !end;
-  if (end) c->pending = true;
-  return AF_OK;
+  return p;
 }
 
-af_status af_update_and_decide(af_ctx *c, uint32_t flags, af_decision *out_host, void *stream) {
-  if (!c) return fail(AF_EINVAL, "NULL ctx");
-  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
-  if (flags & ~(AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
-  if (!c->pending) return fail(AF_ESTATE, "af_update_and_decide without a preceding AF_INTERVAL_END");
-  const bool dry = flags & AF_DRY_RUN;
+int norm_mode(const af_ctx *c, bool end) {
+  if (c->cfg.acc_mode == AF_ACC_DELTA) return end ? kEndDelta : kAccum;
+  return kStepSq;
+}
+
+DecideParams decide_params(af_ctx *c, bool dry, af_decision *out_host) {
   DecideParams p{};
   p.ss_all = c->at<double>(c->o_ssall);
   p.world = c->cfg.world;
@@ -372,8 +364,8 @@ af_status af_update_and_decide(af_ctx *c, uint32_t flags, af_decision *out_host,
   p.tie_rel_eps = c->cfg.tie_rel_eps;
   p.min_active = c->cfg.min_active;
   p.commit = dry ? 0 : 1;
-  // page-locked host memory is device-addressable (UVA): the kernel writes the record there
-  // directly; otherwise fall back to an async copy.
+  // page-locked host memory is device-addressable (UVA): the kernel writes the record
+  // there directly; otherwise the caller gets an async copy after the kernel.
   if (out_host && out_host != c->rec_host) {
     cudaPointerAttributes a{};
     c->rec_host = out_host;
@@ -383,13 +375,96 @@ af_status af_update_and_decide(af_ctx *c, uint32_t flags, af_decision *out_host,
     cudaGetLastError();  // clear a sticky "invalid value" from unregistered pointers
   }
   p.host = out_host ? c->rec_host_dev : nullptr;
-  const int e = launch_decide(p, stream);
-  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "decide kernel launch");
+  return p;
+}
+
+af_status copy_record_if_unmapped(af_ctx *c, const DecideParams &p, af_decision *out_host, void *stream) {
   if (out_host && !p.host)
     AF_CUDA(cudaMemcpyAsync(out_host, p.last, sizeof(af_decision), cudaMemcpyDeviceToHost,
                             static_cast<cudaStream_t>(stream)),
             "cudaMemcpyAsync(decision)");
+  return AF_OK;
+}
+
+af_status allgather_rows(af_ctx *c, void *stream) {
+  if (c->cfg.world > 1 && c->comm) {
+    double *rows = c->at<double>(c->o_ssall);
+    ncclResult_t r = ncclAllGather(rows + static_cast<size_t>(c->cfg.rank) * c->L, rows, c->L, ncclFloat64, c->comm,
+                                   static_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+  }
+  return AF_OK;
+}
+
+af_status check_norm_args(af_ctx *c, const void *grad_dev) {
+  if (!c) return fail(AF_EINVAL, "NULL ctx");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (!grad_dev || !aligned(grad_dev, 16)) return fail(AF_EINVAL, "grad must be a 16-byte aligned device pointer");
+  return AF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+af_status af_layer_norms(af_ctx *c, const void *grad_dev, uint32_t flags, void *stream) {
+  af_status st = check_norm_args(c, grad_dev);
+  if (st != AF_OK) return st;
+  if (flags & ~(AF_INTERVAL_END | AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
+  const bool end = flags & AF_INTERVAL_END, dry = flags & AF_DRY_RUN;
+  const int mode = norm_mode(c, end);
+  NormParams p = norm_params(c, grad_dev, end, dry);
+  const int grid = std::max(1, std::min<int>(c->grid[mode], std::max<int>(1, p.n_tiles)));
+  const int e = launch_norms(p, mode, c->dtype, grid, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "norms kernel launch");
+  if (end) {
+    st = allgather_rows(c, stream);
+    if (st != AF_OK) return st;
+  }
+  if (!dry) c->armed = !end;
+  if (end) c->pending = true;
+  return AF_OK;
+}
+
+af_status af_update_and_decide(af_ctx *c, uint32_t flags, af_decision *out_host, void *stream) {
+  if (!c) return fail(AF_EINVAL, "NULL ctx");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (flags & ~(AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
+  if (!c->pending) return fail(AF_ESTATE, "af_update_and_decide without a preceding AF_INTERVAL_END");
+  const bool dry = flags & AF_DRY_RUN;
+  DecideParams p = decide_params(c, dry, out_host);
+  const int e = launch_decide(p, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "decide kernel launch");
+  af_status st = copy_record_if_unmapped(c, p, out_host, stream);
+  if (st != AF_OK) return st;
   if (!dry) c->pending = false;
+  return AF_OK;
+}
+
+af_status af_interval_end(af_ctx *c, const void *grad_dev, uint32_t flags, af_decision *out_host, void *stream) {
+  af_status st = check_norm_args(c, grad_dev);
+  if (st != AF_OK) return st;
+  if (flags & ~(AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
+  const bool dry = flags & AF_DRY_RUN;
+  if (c->cfg.world > 1) {  // kernel + all-gather + decide kernel
+    if (!c->comm) return fail(AF_ESTATE, "af_interval_end with world > 1 needs a communicator (af_ctx_set_comm)");
+    st = af_layer_norms(c, grad_dev, AF_INTERVAL_END | flags, stream);
+    if (st != AF_OK) return st;
+    return af_update_and_decide(c, flags, out_host, stream);
+  }
+  const int mode = norm_mode(c, true);
+  NormParams p = norm_params(c, grad_dev, true, dry);
+  p.fuse_decide = 1;
+  p.dec = decide_params(c, dry, out_host);
+  const int grid = std::max(1, std::min<int>(c->grid[mode], std::max<int>(1, p.n_tiles)));
+  const int e = launch_norms(p, mode, c->dtype, grid, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "fused interval-end kernel launch");
+  st = copy_record_if_unmapped(c, p.dec, out_host, stream);
+  if (st != AF_OK) return st;
+  if (!dry) {
+    c->armed = false;
+    c->pending = false;
+  }
   return AF_OK;
 }
 

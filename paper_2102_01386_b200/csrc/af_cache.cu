@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
     fence_mbar_init();
   }
   __syncwarp();
+  pdl_wait();  // ids, rows and the meta words may come from the preceding kernels
 
   const int64_t n_items = static_cast<int64_t>(p.n) * p.n_chunks;
   const int64_t G = gridDim.x;
@@ -190,6 +191,7 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
     if (lane == 0) pump(descs, m, stage_buf, bars, seq);
     __syncwarp();
   }
+  pdl_launch_dependents();
   if (lane == 0) bulk_wait_all();  // all stores complete before the CTA retires its shared memory
 }
 
@@ -213,8 +215,8 @@ static int launch_cache(const CacheParams &p0, int grid, void *stream) {
     if (e != cudaSuccess) return static_cast<int>(e);
     attr_set = 1;
   }
-  cache_kernel<PUT><<<grid, 32, smem, static_cast<cudaStream_t>(stream)>>>(p);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(launch_pdl(cache_kernel<PUT>, dim3(grid), dim3(32), static_cast<size_t>(smem),
+                                     static_cast<cudaStream_t>(stream), p));
 }
 
 int launch_cache_put(const CacheParams &p, int grid, void *stream) { return launch_cache<true>(p, grid, stream); }

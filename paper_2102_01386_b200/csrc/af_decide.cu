@@ -1,169 +1,22 @@
-// af_decide.cu -- the single-CTA decision kernel.
-//
-// Alg. 1 on the gathered per-segment sums of squares:
-//   ss_l   = sum_r ss_all[r][l] in rank order 0..P-1 (identical on every rank)
-//   norm_l = sqrt(ss_l)                                   (correctly rounded)
-//   eta_l  = |norm_{T-1,l} - norm_{T,l}| / norm_{T-1,l}     Eq. 1; 0 if prev = 0 (Q7)
-//   thr    = N-th percentile of eta over the active POOL  Alg. 1; numpy "linear" (Q4)
-//   k      = leading active POOL layers with eta < thr    Alg. 1 P:182-190 (break at first failure)
-//   f     <- f + k; prev <- norm; T <- T + 1              roll (Q13)
-// All fp64 arithmetic uses explicit round-to-nearest intrinsics so nvcc cannot
-// contract it into FMAs: the threshold is bit-identical to numpy.percentile
-// given the same eta values.  Latency-bound: one CTA, 256 threads, L <= 256.
+// af_decide.cu -- the standalone single-CTA decision kernel (world > 1, or the
+// unfused af_update_and_decide call); the logic lives in af_decide.cuh.
 #include <cuda_runtime.h>
 
-#include "af_internal.h"
+#include "af_decide.cuh"
 
 namespace af {
 namespace {
 
-constexpr int kDecideThreads = 256;
-
 __global__ void __launch_bounds__(kDecideThreads) decide_kernel(const DecideParams p) {
-  __shared__ double s_eta[AF_MAX_SEGMENTS];
-  __shared__ double s_act[AF_MAX_SEGMENTS];
-  __shared__ double s_sorted[AF_MAX_SEGMENTS];
-  __shared__ double s_thr;
-  __shared__ int s_k, s_near, s_nonfinite;
-  __shared__ unsigned int s_flags;
-
-  const int t = threadIdx.x;
-  const int L = p.L;
-  const int T = p.state->T;
-  int f = p.state->f;
-  f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
-  const int n_act = p.n_pool - f;
-
-  if (t == 0) s_nonfinite = 0;
-  __syncthreads();
-
-  double ss = 0.0, nrm = 0.0, et = 0.0;
-  if (t < L) {
-    for (int r = 0; r < p.world; ++r) ss = __dadd_rn(ss, p.ss_all[r * L + t]);
-    nrm = __dsqrt_rn(ss);
-    const double pv = p.state->prev[t];
-    et = (pv == 0.0) ? 0.0 : __ddiv_rn(fabs(__dsub_rn(pv, nrm)), pv);
-    s_eta[t] = et;
-    if (!isfinite(ss)) s_nonfinite = 1;  // benign race: every writer stores 1
-  }
-  __syncthreads();
-  if (t < n_act) s_act[t] = s_eta[p.pool_seg[f + t]];
-  __syncthreads();
-
-  const bool nonfinite = s_nonfinite != 0;
-  unsigned int flags = p.commit ? 0u : AF_DEC_DRY_RUN;
-  bool decide = false;
-  if (nonfinite)
-    flags |= AF_DEC_NONFINITE;
-  else if (T == 0)
-    flags |= AF_DEC_FIRST_INTERVAL;
-  else if (n_act < p.min_active)
-    flags |= AF_DEC_SKIPPED_FEW;
-  else
-    decide = true;
-
-  if (decide) {
-    // rank sort of the active eta values (ties broken by position; values are finite)
-    if (t < n_act) {
-      const double v = s_act[t];
-      int r = 0;
-      for (int j = 0; j < n_act; ++j) {
-        const double w = s_act[j];
-        r += (w < v) || (w == v && j < t);
-      }
-      s_sorted[r] = v;
-    }
-    __syncthreads();
-    if (t == 0) {
-      const int n = n_act;
-      double thr;
-      if (p.pct_method == AF_PCT_NEAREST_RANK) {
-        int rank = static_cast<int>(ceil(__dmul_rn(__ddiv_rn(p.percentile, 100.0), static_cast<double>(n))));
-        rank = rank < 1 ? 1 : (rank > n ? n : rank);
-        thr = s_sorted[rank - 1];
-      } else {
-        // numpy "linear": h = (n-1) * (N/100); gamma = h - floor(h); two-branch lerp
-        const double q = __ddiv_rn(p.percentile, 100.0);
-        const double h = __dmul_rn(static_cast<double>(n - 1), q);
-        if (h >= static_cast<double>(n - 1)) {
-          thr = s_sorted[n - 1];
-        } else {
-          const double fl = floor(h);
-          const int lo = static_cast<int>(fl);
-          const double gm = __dsub_rn(h, fl);
-          const double a = s_sorted[lo], b = s_sorted[lo + 1];
-          const double dba = __dsub_rn(b, a);
-          thr = (gm >= 0.5) ? __dsub_rn(b, __dmul_rn(dba, __dsub_rn(1.0, gm))) : __dadd_rn(a, __dmul_rn(dba, gm));
-        }
-      }
-      // Alg. 1 scan with break; near-tie window over the comparisons that decide k
-      int k = 0, near = -1;
-      unsigned int fl2 = 0;
-      const double win = __dmul_rn(p.tie_rel_eps, thr);
-      for (int i = 0; i < n; ++i) {
-        const double e = s_act[i];
-        const double dd = fabs(__dsub_rn(e, thr));
-        if (dd > 0.0 && dd <= win) {
-          fl2 |= AF_DEC_NEAR_TIE;
-          if (near < 0) near = p.pool_seg[f + i];
-        }
-        if (e < thr)
-          ++k;
-        else
-          break;
-      }
-      s_thr = thr;
-      s_k = k;
-      s_near = near;
-      s_flags = fl2;
-    }
-  } else if (t == 0) {
-    s_thr = __longlong_as_double(0x7FF8000000000000LL);  // NaN: no threshold
-    s_k = 0;
-    s_near = -1;
-    s_flags = 0;
-  }
-  __syncthreads();
-  flags |= s_flags;
-  const int k = nonfinite ? 0 : s_k;
-  const int f_new = f + k;
-
-  // record: device copy, ring slot and (if mapped) the caller's pinned host struct
-  af_decision *recs[3] = {p.last, p.ring + (T % kRing), p.host};
-  for (int q = 0; q < 3; ++q) {
-    af_decision *r = recs[q];
-    if (r == nullptr) continue;
-    if (t < AF_MAX_SEGMENTS) {
-      r->sumsq[t] = (t < L) ? ss : 0.0;
-      r->norm[t] = (t < L) ? nrm : 0.0;
-      r->eta[t] = (t < L) ? et : 0.0;
-    }
-    if (t == 0) {
-      r->interval = T;
-      r->boundary_before = f;
-      r->boundary_after = f_new;
-      r->n_active = n_act;
-      r->threshold = s_thr;
-      r->flags = flags;
-      r->near_tie_seg = s_near;
-    }
-  }
-  // commit (not under AF_DRY_RUN, not on non-finite sums)
-  if (p.commit && !nonfinite) {
-    __syncthreads();  // every thread has read state->prev / T / f
-    if (t < L) p.state->prev[t] = nrm;
-    if (t == 0) {
-      p.state->T = T + 1;
-      p.state->f = f_new;
-    }
-  }
+  pdl_wait();  // the sums come from the preceding kernel / all-gather
+  pdl_launch_dependents();
+  decide_block(p);
 }
 
 }  // namespace
 
 int launch_decide(const DecideParams &p, void *stream) {
-  decide_kernel<<<1, kDecideThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(launch_pdl(decide_kernel, dim3(1), dim3(kDecideThreads), 0, static_cast<cudaStream_t>(stream), p));
 }
 
 }  // namespace af

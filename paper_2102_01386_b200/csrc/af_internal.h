@@ -14,11 +14,12 @@ constexpr int kRing = 16;                // decision records kept on the device
 constexpr int kShardAlign = 8;           // shard bounds are multiples of 8 elements (32 B fp32 Delta)
 
 // A segment-aligned tile: global element range [begin, end) inside one segment.
-struct Tile {
+// 32 bytes so a descriptor moves with two 16-byte cp.async copies.
+struct alignas(16) Tile {
   int64_t begin, end;
-  int32_t seg, pad;
+  int32_t seg, seg_first, seg_end, pad;  // seg_first/seg_end: the segment's tile range [seg_first, seg_end)
 };
-static_assert(sizeof(Tile) == 24, "tile layout");
+static_assert(sizeof(Tile) == 32, "tile layout");
 
 // Dynamic tile scheduler of one kernel family; reset by the last CTA of each launch.
 struct Sched {
@@ -36,6 +37,22 @@ struct DevState {
 };
 
 enum Mode : int { kAccum = 0, kEndDelta = 1, kStepSq = 2 };
+
+// Arguments of the single-CTA decision kernel.
+struct DecideParams {
+  const double *ss_all;   // [world][L]
+  int32_t world, L, n_pool;
+  const int32_t *pool_seg;  // [n_pool] segment index of POOL layer j
+  DevState *state;
+  af_decision *last;        // device copy of the latest record
+  af_decision *ring;        // [kRing]
+  af_decision *host;        // mapped page-locked host record or nullptr
+  double percentile;
+  int32_t pct_method;
+  double tie_rel_eps;
+  int32_t min_active;
+  int32_t commit;           // 0 under AF_DRY_RUN
+};
 
 // Arguments of the streaming kernels (accumulate / interval-end sum of squares).
 struct NormParams {
@@ -56,22 +73,9 @@ struct NormParams {
   int32_t first;                   // first step of the interval (Delta not read)
   int32_t end;                     // interval end (STEP_SUMSQ: publish ss_acc)
   int32_t commit;                  // STEP_SUMSQ: store ss_acc
-};
-
-// Arguments of the single-CTA decision kernel.
-struct DecideParams {
-  const double *ss_all;   // [world][L]
-  int32_t world, L, n_pool;
-  const int32_t *pool_seg;  // [n_pool] segment index of POOL layer j
-  DevState *state;
-  af_decision *last;        // device copy of the latest record
-  af_decision *ring;        // [kRing]
-  af_decision *host;        // mapped page-locked host record or nullptr
-  double percentile;
-  int32_t pct_method;
-  double tie_rel_eps;
-  int32_t min_active;
-  int32_t commit;           // 0 under AF_DRY_RUN
+  unsigned int *seg_done;          // [L] per-segment tile completion counters
+  int32_t fuse_decide;             // world == 1 fused interval end: last CTA decides
+  DecideParams dec;
 };
 
 // Cache records: one 16-byte meta word per slot.  `readers` counts the chunks
@@ -101,6 +105,31 @@ struct CacheParams {
   int32_t depth;            // put
   int32_t cur_boundary;     // get
 };
+
+#ifdef __CUDACC__
+// Programmatic dependent launch: our kernels are launched with programmatic stream
+// serialization, so a kernel may be scheduled while its predecessor drains; each
+// kernel calls pdl_wait() before touching global memory the predecessor may write
+// (a no-op when launched without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+template <typename K, typename... Args>
+inline cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+#endif
 
 // Launchers (defined in the .cu files).  Return cudaError_t as int.
 int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *stream);

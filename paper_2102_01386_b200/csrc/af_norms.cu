@@ -19,13 +19,54 @@
 //    with one DFMA (the square is exact; only the accumulation rounds), giving
 //    norms good to ~1e-15 relative (eta needs < 5e-11);
 //  * frozen tiles (segments before the device-resident boundary f) are skipped;
-//  * the last CTA to finish sums each segment's partials in tile order.
+//  * the CTA that completes a segment's last active tile sums that segment's
+//    partials (a per-segment counter), overlapped with the other CTAs; the last
+//    CTA of the grid only fills frozen segments and, for the fused interval end
+//    (world == 1), runs the decision (af_decide.cuh) -- one launch per interval.
+//  * programmatic dependent launch: pdl_wait() before the first dependent read.
 #include <cuda_runtime.h>
 
+#include "af_decide.cuh"
 #include "af_internal.h"
+
+// Tunables (compile-time; defaults chosen from the B200 variant sweep in
+// profiles/r01_v3_variants.jsonl): vectors in flight per thread
+// and load cache hints.
+#ifndef AF_U_END
+#define AF_U_END 4
+#endif
+#ifndef AF_U_ACC
+#define AF_U_ACC 8
+#endif
+#ifndef AF_G_HINT  // 0: ld.global.cs   1: ld.global.nc.L1::no_allocate.L2::256B
+#define AF_G_HINT 1
+#endif
+#ifndef AF_D_HINT_END
+#define AF_D_HINT_END 0
+#endif
+#ifndef AF_MINB_END
+#define AF_MINB_END 1
+#endif
 
 namespace af {
 namespace {
+
+template <int HINT>
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
+  if (HINT == 0) return __ldcs(p);
+  uint4 r;
+  // read-only for the kernel's lifetime: non-coherent path, no L1 allocation, 256 B L2 prefetch
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+template <int HINT>
+__device__ __forceinline__ float4 ld_stream(const float4 *p) {
+  if (HINT == 0) return __ldcs(p);
+  const uint4 u = ld_stream<HINT>(reinterpret_cast<const uint4 *>(p));
+  return make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
+}
 
 template <typename GT>
 struct VT;
@@ -89,7 +130,8 @@ __device__ __forceinline__ void elem(const NormParams &p, const GT *g, float *d,
 template <int MODE, typename GT, bool RD>
 __device__ __forceinline__ double process_tile(const NormParams &p, const Tile &t) {
   constexpr int VE = VT<GT>::VE;
-  constexpr int U = 4;  // vectors in flight per thread
+  constexpr int U = (MODE == kAccum) ? AF_U_ACC : AF_U_END;  // vectors in flight per thread
+  constexpr int DH = (MODE == kAccum) ? 0 : AF_D_HINT_END;     // Delta is rewritten by kAccum
   const GT *__restrict__ g = static_cast<const GT *>(p.grad);
   // Delta is indexed by global element i at d[i]; the shard base offset is applied
   // through the pointer (shard_begin is a multiple of 8, keeping 16 B alignment).
@@ -117,10 +159,10 @@ __device__ __forceinline__ double process_tile(const NormParams &p, const Tile &
     for (int u = 0; u < U; ++u) {
       const int64_t c = c0 + static_cast<int64_t>(u) * kNormBlock;
       if (c < nch) {
-        gv[u] = __ldcs(gb + c);
+        gv[u] = ld_stream<AF_G_HINT>(gb + c);
         if (RD) {
 #pragma unroll
-          for (int q = 0; q < DV; ++q) dv[u][q] = __ldcs(db + c * DV + q);
+          for (int q = 0; q < DV; ++q) dv[u][q] = ld_stream<DH>(db + c * DV + q);
         }
       }
     }
@@ -174,20 +216,49 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;  // identical on every lane (fp add is commutative)
 }
 
+// One segment's sum: its active tiles' partials in tile order, summed by the
+// whole CTA in a fixed thread mapping (thread k takes tiles tb+k, tb+k+256, ...,
+// then the xor tree and the 8 warps in order) -- deterministic whichever CTA runs it.
+template <int MODE>
+__device__ __noinline__ void finish_segment(const NormParams &p, int l, int tb, int te, double *s_red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double a = 0.0;
+  for (int k = tb + tid; k < te; k += kNormBlock) a += __ldcg(p.partials + k);
+  a = warp_sum(a);
+  if (lane == 0) s_red[warp] = a;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kNormBlock / 32; ++k) s += s_red[k];
+    if (MODE == kEndDelta) {
+      p.ss_out[l] = s;
+    } else {
+      const double acc = p.first ? s : p.ss_acc[l] + s;
+      if (p.commit) p.ss_acc[l] = acc;
+      if (p.end) p.ss_out[l] = acc;
+    }
+    p.seg_done[l] = 0u;  // every tile of the segment has been counted: reset for the next launch
+  }
+  __syncthreads();
+}
+
 template <int MODE, typename GT, bool RD>
-__global__ void __launch_bounds__(kNormBlock) norms_kernel(const NormParams p) {
+__global__ void __launch_bounds__(kNormBlock, (MODE == kAccum) ? 1 : AF_MINB_END) norms_kernel(const NormParams p) {
   __shared__ int s_tile[3];
   __shared__ Tile s_desc[3];
   __shared__ double s_red[kNormBlock / 32];
-  __shared__ int s_last;
+  __shared__ int s_last, s_fin, s_fin_tb, s_fin_te;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_wait();  // f, Delta and the counters are written by the preceding kernels
   int f = p.state->f;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int first_tile = p.first_tile_of_f[f];
 
   // Tile scheduler, two tiles of lookahead: while tile `it` is processed, thread 0
-  // has the atomic for tile it+2 and the descriptor load of tile it+1 in flight and
-  // publishes them only after its share of tile `it`, so no warp waits on them.
+  // has the atomic for tile it+2 (one register) and an async copy (cp.async) of
+  // tile it+1's descriptor into shared memory in flight; both land before the
+  // end-of-tile barrier, so no warp waits on them and no registers hold them.
   if (tid == 0) {
     const int t0 = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
     s_tile[0] = t0;
@@ -201,16 +272,23 @@ __global__ void __launch_bounds__(kNormBlock) norms_kernel(const NormParams p) {
     if (tile >= p.n_tiles) break;
     const Tile t = s_desc[slot];
     int next2 = 0;
-    Tile d1{0, 0, 0, 0};
     if (tid == 0) {
       next2 = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
       const int n1 = s_tile[slot1];
-      if (n1 < p.n_tiles) d1 = p.tiles[n1];
+      if (n1 < p.n_tiles) {
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_desc[slot1]));
+        const Tile *src = p.tiles + n1;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16u),
+                     "l"(reinterpret_cast<const char *>(src) + 16)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
     const double v = process_tile<MODE, GT, RD>(p, t);
     if (tid == 0) {
       s_tile[slot2] = next2;
-      s_desc[slot1] = d1;
+      asm volatile("cp.async.wait_all;" ::: "memory");
     }
     if (MODE != kAccum) {
       const double w = warp_sum(v);
@@ -221,12 +299,27 @@ __global__ void __launch_bounds__(kNormBlock) norms_kernel(const NormParams p) {
 #pragma unroll
         for (int k = 0; k < kNormBlock / 32; ++k) s += s_red[k];
         p.partials[tile] = s;
+        // segment completion count: the CTA that adds the segment's last active
+        // tile sums the segment right away (overlapped with the other CTAs' tiles)
+        __threadfence();
+        const int tb = t.seg_first < first_tile ? first_tile : t.seg_first;
+        const unsigned int seen = atomicAdd(&p.seg_done[t.seg], 1u);
+        s_fin = (seen == static_cast<unsigned int>(t.seg_end - tb) - 1u) ? t.seg : -1;
+        s_fin_tb = tb;
+        s_fin_te = t.seg_end;
+      }
+      __syncthreads();
+      if (s_fin >= 0) {
+        __threadfence();
+        finish_segment<MODE>(p, s_fin, s_fin_tb, s_fin_te, s_red);
       }
     }
     __syncthreads();
   }
+  pdl_launch_dependents();
 
-  // grid completion: the last CTA resets the scheduler and finalises per segment
+  // grid completion: the last CTA resets the scheduler, fills segments with no
+  // active tile and (fused interval end, world == 1) runs the decision
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -241,30 +334,28 @@ __global__ void __launch_bounds__(kNormBlock) norms_kernel(const NormParams p) {
     p.sched->done = 0;
   }
   if (MODE == kAccum) return;
-  for (int l = warp; l < p.L; l += kNormBlock / 32) {
+  for (int l = tid; l < p.L; l += kNormBlock) {
     int tb = p.seg_tile_begin[l];
     tb = tb < first_tile ? first_tile : tb;
-    const int te = p.seg_tile_begin[l + 1];
-    double s = 0.0;
-#pragma unroll 8
-    for (int t = tb + lane; t < te; t += 32) s += __ldcg(p.partials + t);
-    s = warp_sum(s);
-    if (lane == 0) {
-      if (MODE == kEndDelta) {
-        p.ss_out[l] = s;
-      } else {
-        const double a = p.first ? s : p.ss_acc[l] + s;
-        if (p.commit) p.ss_acc[l] = a;
-        if (p.end) p.ss_out[l] = a;
-      }
+    if (p.seg_tile_begin[l + 1] > tb) continue;  // summed by its finishing CTA
+    if (MODE == kEndDelta) {
+      p.ss_out[l] = 0.0;
+    } else {
+      const double acc = p.first ? 0.0 : p.ss_acc[l];
+      if (p.commit) p.ss_acc[l] = acc;
+      if (p.end) p.ss_out[l] = acc;
     }
+  }
+  if (p.fuse_decide) {
+    __syncthreads();
+    decide_block(p.dec);
   }
 }
 
 template <int MODE, typename GT, bool RD>
 int launch_one(const NormParams &p, int grid, void *stream) {
-  norms_kernel<MODE, GT, RD><<<grid, kNormBlock, 0, static_cast<cudaStream_t>(stream)>>>(p);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(
+      launch_pdl(norms_kernel<MODE, GT, RD>, dim3(grid), dim3(kNormBlock), 0, static_cast<cudaStream_t>(stream), p));
 }
 
 template <typename GT>
@@ -289,16 +380,24 @@ int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *
   return launch_dt<float>(p, mode, grid, stream);
 }
 
-int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks) {
+template <typename GT>
+static int occ_dt(int mode, int *blocks) {
   cudaError_t e;
-  if (grad_dtype == AF_DT_BF16)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kEndDelta, uint16_t, true>,
-                                                      kNormBlock, 0);
-  else
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kEndDelta, float, true>,
-                                                      kNormBlock, 0);
-  (void)mode;
+  switch (mode) {
+    case kAccum:
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kAccum, GT, true>, kNormBlock, 0);
+      break;
+    case kEndDelta:
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kEndDelta, GT, true>, kNormBlock, 0);
+      break;
+    default:
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kStepSq, GT, false>, kNormBlock, 0);
+  }
   return static_cast<int>(e);
+}
+
+int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks) {
+  return grad_dtype == AF_DT_BF16 ? occ_dt<uint16_t>(mode, blocks) : occ_dt<float>(mode, blocks);
 }
 
 }  // namespace af

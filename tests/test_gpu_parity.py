@@ -156,6 +156,50 @@ def test_threshold_bit_identical_to_numpy(seed):
                 assert gr["threshold"] == orr["threshold"], (trial, T, N, method)
 
 
+# ---------------------------------------------------------------- fused interval end
+
+@pytest.mark.parametrize("dt,acc", [("bf16", "delta"), ("f32", "delta"), ("bf16", "step_sumsq")])
+def test_fused_interval_end_equals_two_calls(dt, acc):
+    """af_interval_end (one launch at world 1) == af_layer_norms(END) + af_update_and_decide,
+    bit for bit, and matches the oracle."""
+    lay = _ragged_layout()
+    step = _decaying_step(lay, dt, 21)
+    a, b = _fm(lay, dt, acc_mode=acc), _fm(lay, dt, acc_mode=acc)
+    oz = _oracle(lay, dt, acc_mode=acc)
+    for T, S in enumerate([2, 1, 3, 2, 2, 3, 1, 2]):
+        for t in range(S):
+            gnp = step(T, t)
+            g = to_device_grad(gnp, dt)
+            end = t == S - 1
+            if end:
+                a.layer_norms(g, interval_end=True)
+                a.update_and_decide()
+                b.interval_end(g)
+            else:
+                a.layer_norms(g)
+                b.layer_norms(g)
+            oz.layer_norms(gnp, end)
+        ra, rb = a.decision(), b.decision()
+        assert canon(ra) == canon(rb), T
+        compare_records(rb, oz.update_and_decide(), lay.n_segments, tag=f"T={T}")
+    # dry-run repetitions through the fused call commit nothing
+    blob = b.get_state()
+    g = to_device_grad(step(9, 0), dt)
+    b.interval_end(g, dry_run=True)
+    r1 = canon(b.decision())
+    b.interval_end(g, dry_run=True)
+    assert canon(b.decision()) == r1 and b.get_state() == blob
+
+
+def test_fused_interval_end_needs_comm_when_sharded():
+    import paper_2102_01386_b200 as af
+    lay = tiny_layout()
+    fm = _fm(lay, "f32", rank=0, world=2)
+    with pytest.raises(af.AfError) as e:
+        fm.interval_end(torch.zeros(lay.n, device="cuda"))
+    assert e.value.status == 2
+
+
 # ---------------------------------------------------------------- semantics
 
 def test_dry_run_and_state_roundtrip():

@@ -21,7 +21,7 @@ def phase_of(kernel):
     if "norms_kernel<0" in kernel:
         return "accumulate"
     if "norms_kernel<1" in kernel:
-        return "grad_norm"
+        return "grad_norm_decide"
     if "norms_kernel<2" in kernel:
         return "step_sumsq"
     if "cache_kernel<1>" in kernel or "cache_kernel<true>" in kernel:

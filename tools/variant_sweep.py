@@ -1,0 +1,60 @@
+#!/usr/bin/env python
+"""Build libautofreeze with each compile-time variant and time the streaming
+kernels through bench.py (run on the GPU box).  Prints one JSON line per
+(variant, workload) with the per-phase GB/s; the default build is restored at
+the end.
+
+    python tools/variant_sweep.py [--steps 200] > gpurun_out/variants.jsonl
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+VARIANTS = {
+    "default": "",
+    "g_nc": "-DAF_G_HINT=1",
+    "g_nc_d_nc": "-DAF_G_HINT=1 -DAF_D_HINT_END=1",
+    "g_nc_d_nc_u8": "-DAF_G_HINT=1 -DAF_D_HINT_END=1 -DAF_U_END=8",
+    "g_nc_d_nc_u8_minb2": "-DAF_G_HINT=1 -DAF_D_HINT_END=1 -DAF_U_END=8 -DAF_MINB_END=2",
+    "g_nc_d_nc_minb3": "-DAF_G_HINT=1 -DAF_D_HINT_END=1 -DAF_MINB_END=3",
+    "g_nc_d_nc_minb4": "-DAF_G_HINT=1 -DAF_D_HINT_END=1 -DAF_MINB_END=4",
+    "g_nc_acc_u2": "-DAF_G_HINT=1 -DAF_U_ACC=2",
+    "g_nc_acc_u8": "-DAF_G_HINT=1 -DAF_U_ACC=8",
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--only", nargs="*")
+    a = ap.parse_args()
+    sys.path.insert(0, ROOT)
+    for name, extra in VARIANTS.items():
+        if a.only and name not in a.only:
+            continue
+        env = dict(os.environ, AF_NVCC_EXTRA=extra)
+        subprocess.run([sys.executable, os.path.join(ROOT, "paper_2102_01386_b200", "_build.py"), "--force"], cwd=ROOT, env=env,
+                       check=True)
+        for wl in ("bert-large-f32", "bert-base-bf16"):
+            r = subprocess.run([sys.executable, "bench.py", "--workload", wl, "--steps", str(a.steps), "--warmup", "10",
+                                "--no-e2e", "--no-cpu-baseline", "--no-cache-sweep"], cwd=ROOT,
+                               capture_output=True, text=True)
+            try:
+                d = json.loads(r.stdout.strip().splitlines()[-1])
+            except Exception:  # noqa: BLE001
+                print(json.dumps({"variant": name, "workload": wl, "error": r.stderr[-2000:]}), flush=True)
+                continue
+            ph = d["phases"]
+            print(json.dumps({"variant": name, "flags": extra, "workload": wl, "value": d["value"],
+                              "ms_per_step": d["ms_per_step"],
+                              "accumulate_gbs": ph["accumulate"]["gbs"], "grad_norm_gbs": ph["grad_norm_decide"]["gbs"],
+                              "accumulate_ms": ph["accumulate"]["ms"], "grad_norm_ms": ph["grad_norm_decide"]["ms"],
+                              "clocks": d.get("clocks")}), flush=True)
+    subprocess.run([sys.executable, os.path.join(ROOT, "paper_2102_01386_b200", "_build.py"), "--force"], cwd=ROOT, check=True)
+
+
+if __name__ == "__main__":
+    main()
