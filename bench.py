@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cache-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly (no CUDA graphs)")
+    ap.add_argument("--unfused", action="store_true",
+                    help="interval end as af_layer_norms(END) + af_update_and_decide (two launches)")
     ap.add_argument("--sweep", action="store_true",
                     help="configs[4]: layers x elements sweep, one JSON line per point (not the bench line)")
     return ap.parse_args()
@@ -222,7 +224,11 @@ def run_ours(args, rank, world, local):
         if evs: evs[0].record(stream)
         fm.layer_norms(g, dry_run=True)                               # a2
         if evs: evs[1].record(stream)
-        fm.interval_end(grads[(i + 1) & 1], dry_run=True)             # a3-a9 (fused at N=1)
+        if args.unfused:
+            fm.layer_norms(grads[(i + 1) & 1], interval_end=True, dry_run=True)
+            fm.update_and_decide(dry_run=True)
+        else:
+            fm.interval_end(grads[(i + 1) & 1], dry_run=True)         # a3-a9 (fused at N=1)
         if evs: evs[2].record(stream)
         cache.get(ids, 4, out_rows, depth_out)                        # a11
         if evs: evs[3].record(stream)

@@ -68,7 +68,7 @@ struct af_ctx {
   // workspace
   size_t accum_bytes = 0, scratch_bytes = 0;
   size_t o_state = 0, o_sched = 0, o_tiles = 0, o_ftf = 0, o_stb = 0, o_pool = 0, o_part = 0, o_ssall = 0,
-         o_ssacc = 0, o_last = 0, o_ring = 0, o_segdone = 0;
+         o_ssacc = 0, o_last = 0, o_ring = 0;
   float *accum = nullptr;
   char *scratch = nullptr;
   bool bound = false;
@@ -223,7 +223,6 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   c->o_ssacc = take(L * sizeof(double));
   c->o_last = take(sizeof(af_decision));
   c->o_ring = take(kRing * sizeof(af_decision));
-  c->o_segdone = take(L * sizeof(unsigned int));
   c->scratch_bytes = o;
   *out = c;
   return AF_OK;
@@ -336,7 +335,6 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   p.partials = c->at<double>(c->o_part);
   p.ss_out = c->at<double>(c->o_ssall) + static_cast<size_t>(c->cfg.rank) * c->L;
   p.ss_acc = c->at<double>(c->o_ssacc);
-  p.seg_done = c->at<unsigned int>(c->o_segdone);
   p.n_pool = c->n_pool;
   p.first = c->armed ? 0 : 1;
   p.end = end ? 1 : 0;

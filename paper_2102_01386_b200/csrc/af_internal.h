@@ -73,7 +73,6 @@ struct NormParams {
   int32_t first;                   // first step of the interval (Delta not read)
   int32_t end;                     // interval end (STEP_SUMSQ: publish ss_acc)
   int32_t commit;                  // STEP_SUMSQ: store ss_acc
-  unsigned int *seg_done;          // [L] per-segment tile completion counters
   int32_t fuse_decide;             // world == 1 fused interval end: last CTA decides
   DecideParams dec;
 };

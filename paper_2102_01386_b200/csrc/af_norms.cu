@@ -19,10 +19,9 @@
 //    with one DFMA (the square is exact; only the accumulation rounds), giving
 //    norms good to ~1e-15 relative (eta needs < 5e-11);
 //  * frozen tiles (segments before the device-resident boundary f) are skipped;
-//  * the CTA that completes a segment's last active tile sums that segment's
-//    partials (a per-segment counter), overlapped with the other CTAs; the last
-//    CTA of the grid only fills frozen segments and, for the fused interval end
-//    (world == 1), runs the decision (af_decide.cuh) -- one launch per interval.
+//  * the last CTA of the grid sums each segment's partials in tile order and,
+//    for the fused interval end (world == 1), runs the decision
+//    (af_decide.cuh) -- one launch per interval.
 //  * programmatic dependent launch: pdl_wait() before the first dependent read.
 #include <cuda_runtime.h>
 
@@ -216,39 +215,12 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;  // identical on every lane (fp add is commutative)
 }
 
-// One segment's sum: its active tiles' partials in tile order, summed by the
-// whole CTA in a fixed thread mapping (thread k takes tiles tb+k, tb+k+256, ...,
-// then the xor tree and the 8 warps in order) -- deterministic whichever CTA runs it.
-template <int MODE>
-__device__ __noinline__ void finish_segment(const NormParams &p, int l, int tb, int te, double *s_red) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double a = 0.0;
-  for (int k = tb + tid; k < te; k += kNormBlock) a += __ldcg(p.partials + k);
-  a = warp_sum(a);
-  if (lane == 0) s_red[warp] = a;
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < kNormBlock / 32; ++k) s += s_red[k];
-    if (MODE == kEndDelta) {
-      p.ss_out[l] = s;
-    } else {
-      const double acc = p.first ? s : p.ss_acc[l] + s;
-      if (p.commit) p.ss_acc[l] = acc;
-      if (p.end) p.ss_out[l] = acc;
-    }
-    p.seg_done[l] = 0u;  // every tile of the segment has been counted: reset for the next launch
-  }
-  __syncthreads();
-}
-
 template <int MODE, typename GT, bool RD>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum) ? 1 : AF_MINB_END) norms_kernel(const NormParams p) {
   __shared__ int s_tile[3];
   __shared__ Tile s_desc[3];
   __shared__ double s_red[kNormBlock / 32];
-  __shared__ int s_last, s_fin, s_fin_tb, s_fin_te;
+  __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_wait();  // f, Delta and the counters are written by the preceding kernels
   int f = p.state->f;
@@ -299,27 +271,14 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum) ? 1 : AF_MINB_END
 #pragma unroll
         for (int k = 0; k < kNormBlock / 32; ++k) s += s_red[k];
         p.partials[tile] = s;
-        // segment completion count: the CTA that adds the segment's last active
-        // tile sums the segment right away (overlapped with the other CTAs' tiles)
-        __threadfence();
-        const int tb = t.seg_first < first_tile ? first_tile : t.seg_first;
-        const unsigned int seen = atomicAdd(&p.seg_done[t.seg], 1u);
-        s_fin = (seen == static_cast<unsigned int>(t.seg_end - tb) - 1u) ? t.seg : -1;
-        s_fin_tb = tb;
-        s_fin_te = t.seg_end;
-      }
-      __syncthreads();
-      if (s_fin >= 0) {
-        __threadfence();
-        finish_segment<MODE>(p, s_fin, s_fin_tb, s_fin_te, s_red);
       }
     }
     __syncthreads();
   }
   pdl_launch_dependents();
 
-  // grid completion: the last CTA resets the scheduler, fills segments with no
-  // active tile and (fused interval end, world == 1) runs the decision
+  // grid completion: the last CTA resets the scheduler, sums the segments and
+  // (fused interval end, world == 1) runs the decision
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -334,16 +293,24 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum) ? 1 : AF_MINB_END
     p.sched->done = 0;
   }
   if (MODE == kAccum) return;
-  for (int l = tid; l < p.L; l += kNormBlock) {
+  // each segment's active tiles' partials in tile order: one warp per segment,
+  // lane-strided with 8 loads in flight, then the xor tree (deterministic)
+  for (int l = warp; l < p.L; l += kNormBlock / 32) {
     int tb = p.seg_tile_begin[l];
     tb = tb < first_tile ? first_tile : tb;
-    if (p.seg_tile_begin[l + 1] > tb) continue;  // summed by its finishing CTA
-    if (MODE == kEndDelta) {
-      p.ss_out[l] = 0.0;
-    } else {
-      const double acc = p.first ? 0.0 : p.ss_acc[l];
-      if (p.commit) p.ss_acc[l] = acc;
-      if (p.end) p.ss_out[l] = acc;
+    const int te = p.seg_tile_begin[l + 1];
+    double s = 0.0;
+#pragma unroll 8
+    for (int k = tb + lane; k < te; k += 32) s += __ldcg(p.partials + k);
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (MODE == kEndDelta) {
+        p.ss_out[l] = s;
+      } else {
+        const double acc = p.first ? s : p.ss_acc[l] + s;
+        if (p.commit) p.ss_acc[l] = acc;
+        if (p.end) p.ss_out[l] = acc;
+      }
     }
   }
   if (p.fuse_decide) {
