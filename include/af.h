@@ -93,6 +93,9 @@ typedef enum { AF_PCT_LINEAR = 0, AF_PCT_NEAREST_RANK = 1 } af_pct_method;
 #define AF_DEC_NEAR_TIE 0x4u       /* a scanned eta within tie_rel_eps*thr of the threshold (Q16) */
 #define AF_DEC_NONFINITE 0x8u      /* a sum of squares was Inf/NaN: state unchanged (Q8)          */
 #define AF_DEC_DRY_RUN 0x10u       /* produced under AF_DRY_RUN                                    */
+#define AF_DEC_EXCHANGE_TIMEOUT 0x20u /* a peer never published its row (sticky): nothing committed  */
+
+#define AF_IPC_HANDLE_BYTES 128
 
 /* af_cache_status device error flags (sticky) */
 #define AF_CACHE_ERR_RANGE 0x1u /* an id outside [0, num_examples)               */
@@ -175,6 +178,23 @@ AF_API af_status af_ctx_set_comm(af_ctx *ctx, const void *nccl_unique_id_128B);
 /* Device pointer of the exchange matrix ss_all[world][n_segments] (fp64, row r
  * = rank r's per-segment partial sums) inside the bound scratch. */
 AF_API af_status af_ctx_exchange_rows(af_ctx *ctx, double **ss_all_dev);
+
+/* NVLink one-shot exchange, replacing the all-gather:
+ * every rank registers every rank's exchange buffers (double-buffered rows +
+ * epoch flags inside the scratch).  Then at each interval end the CTA that
+ * finishes the per-segment sums writes this rank's L partials straight into
+ * every peer's memory over NVLink (P2P stores), publishes its epoch in every
+ * peer's flag slot (st.release.sys) and waits for all ranks' epochs
+ * (ld.acquire.sys, bounded spin: a missing peer sets AF_DEC_EXCHANGE_TIMEOUT
+ * instead of hanging) -- af_interval_end is ONE kernel at any world size.
+ * _ipc: synchronous, collective; `handles` = world x AF_IPC_HANDLE_BYTES in rank
+ * order, each from af_ctx_exchange_ipc_handle on that rank (exchanged by the
+ * caller, e.g. torch.distributed.all_gather_object).  _local: every rank's ctx
+ * lives in this process (single-process multi-GPU with peer access, or several
+ * ranks sharing one GPU).  Takes precedence over an NCCL communicator. */
+AF_API af_status af_ctx_exchange_ipc_handle(af_ctx *ctx, void *handle_out);
+AF_API af_status af_ctx_set_peers_ipc(af_ctx *ctx, const void *handles);
+AF_API af_status af_ctx_set_peers_local(af_ctx *ctx, af_ctx *const *peers);
 
 /* One training step.  grad_dev = the FULL flat gradient
  * buffer (n_total elements of grad_dtype, 16-byte aligned; only this rank's

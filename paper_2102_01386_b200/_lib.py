@@ -19,6 +19,8 @@ AF_ACC_DELTA, AF_ACC_STEP_SUMSQ = 0, 1
 AF_PCT_LINEAR, AF_PCT_NEAREST_RANK = 0, 1
 AF_INTERVAL_END, AF_DRY_RUN = 0x1, 0x2
 AF_DEC_FIRST_INTERVAL, AF_DEC_SKIPPED_FEW, AF_DEC_NEAR_TIE, AF_DEC_NONFINITE, AF_DEC_DRY_RUN = 1, 2, 4, 8, 16
+AF_DEC_EXCHANGE_TIMEOUT = 32
+AF_IPC_HANDLE_BYTES = 128
 AF_CACHE_ERR_RANGE, AF_CACHE_ERR_OWNER = 1, 2
 
 
@@ -55,6 +57,9 @@ SIGNATURES = {
     "af_nccl_unique_id": (c_int, [c_void_p]),
     "af_ctx_set_comm": (c_int, [c_void_p, c_void_p]),
     "af_ctx_exchange_rows": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "af_ctx_exchange_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "af_ctx_set_peers_ipc": (c_int, [c_void_p, c_void_p]),
+    "af_ctx_set_peers_local": (c_int, [c_void_p, c_void_p]),
     "af_layer_norms": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p]),
     "af_update_and_decide": (c_int, [c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_interval_end": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p, c_void_p]),

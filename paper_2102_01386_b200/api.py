@@ -91,6 +91,26 @@ class FreezingModule:
         with torch.cuda.device(self.device):
             check(lib.af_ctx_set_comm(self._h, buf), "af_ctx_set_comm")
 
+    def set_peers_local(self, peers):
+        """Register every rank's context living in this process (ranks sharing one
+        GPU, or single-process multi-GPU with peer access) for the NVLink one-shot
+        exchange."""
+        arr = (c_void_p * len(peers))(*[p._h.value for p in peers])
+        check(lib.af_ctx_set_peers_local(self._h, arr), "af_ctx_set_peers_local")
+
+    def set_peers_ipc(self, group=None):
+        """Collective: exchange CUDA IPC handles of every rank's exchange buffers
+        through torch.distributed and register them (one-shot NVLink exchange)."""
+        import torch.distributed as dist
+        h = (ctypes.c_uint8 * L.AF_IPC_HANDLE_BYTES)()
+        with torch.cuda.device(self.device):
+            check(lib.af_ctx_exchange_ipc_handle(self._h, h), "af_ctx_exchange_ipc_handle")
+        allh = [None] * self.world
+        dist.all_gather_object(allh, bytes(h), group=group)
+        buf = (ctypes.c_uint8 * (L.AF_IPC_HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(allh))
+        with torch.cuda.device(self.device):
+            check(lib.af_ctx_set_peers_ipc(self._h, buf), "af_ctx_set_peers_ipc")
+
     def exchange_rows(self):
         """float64 view [world, L] of the exchange matrix inside the scratch buffer."""
         p = c_void_p()

@@ -4,6 +4,7 @@
 // and the optional NCCL communicator; every device buffer is caller-owned.
 // Validation errors are synchronous and enqueue nothing.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -68,7 +69,8 @@ struct af_ctx {
   // workspace
   size_t accum_bytes = 0, scratch_bytes = 0;
   size_t o_state = 0, o_sched = 0, o_tiles = 0, o_ftf = 0, o_stb = 0, o_pool = 0, o_part = 0, o_ssall = 0,
-         o_ssacc = 0, o_last = 0, o_ring = 0;
+         o_ssacc = 0, o_last = 0, o_ring = 0, o_xrows = 0,
+         o_xflags = 0, o_peer_rows = 0, o_peer_flags = 0;
   float *accum = nullptr;
   char *scratch = nullptr;
   bool bound = false;
@@ -79,6 +81,8 @@ struct af_ctx {
   ncclComm_t comm = nullptr;
   const void *rec_host = nullptr;  // last out_host pointer and its mapped device alias
   af_decision *rec_host_dev = nullptr;
+  bool peers = false;               // NVLink one-shot exchange registered
+  std::vector<void *> ipc_opened;   // peer allocations opened with cudaIpcOpenMemHandle
 
   template <typename T>
   T *at(size_t o) const {
@@ -223,6 +227,10 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   c->o_ssacc = take(L * sizeof(double));
   c->o_last = take(sizeof(af_decision));
   c->o_ring = take(kRing * sizeof(af_decision));
+  c->o_xrows = take(2 * static_cast<size_t>(cfg->world) * L * sizeof(double));
+  c->o_xflags = take(static_cast<size_t>(cfg->world) * sizeof(unsigned long long));
+  c->o_peer_rows = take(static_cast<size_t>(cfg->world) * sizeof(void *));
+  c->o_peer_flags = take(static_cast<size_t>(cfg->world) * sizeof(void *));
   c->scratch_bytes = o;
   *out = c;
   return AF_OK;
@@ -339,6 +347,14 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   p.first = c->armed ? 0 : 1;
   p.end = end ? 1 : 0;
   p.commit = dry ? 0 : 1;
+  if (c->peers) {
+    p.xworld = c->cfg.world;
+    p.xrank = c->cfg.rank;
+    p.xrows = c->at<double>(c->o_xrows);
+    p.peer_rows = c->at<double *const>(c->o_peer_rows);
+    p.xflags = c->at<unsigned long long>(c->o_xflags);
+    p.peer_flags = c->at<unsigned long long *const>(c->o_peer_flags);
+  }
   return p;
 }
 
@@ -349,7 +365,8 @@ int norm_mode(const af_ctx *c, bool end) {
 
 DecideParams decide_params(af_ctx *c, bool dry, af_decision *out_host) {
   DecideParams p{};
-  p.ss_all = c->at<double>(c->o_ssall);
+  p.ss_all = c->peers ? c->at<double>(c->o_xrows) : c->at<double>(c->o_ssall);
+  p.xparity = c->peers ? 1 : 0;
   p.world = c->cfg.world;
   p.L = c->L;
   p.n_pool = c->n_pool;
@@ -385,7 +402,7 @@ af_status copy_record_if_unmapped(af_ctx *c, const DecideParams &p, af_decision 
 }
 
 af_status allgather_rows(af_ctx *c, void *stream) {
-  if (c->cfg.world > 1 && c->comm) {
+  if (c->cfg.world > 1 && c->comm && !c->peers) {
     double *rows = c->at<double>(c->o_ssall);
     ncclResult_t r = ncclAllGather(rows + static_cast<size_t>(c->cfg.rank) * c->L, rows, c->L, ncclFloat64, c->comm,
                                    static_cast<cudaStream_t>(stream));
@@ -444,8 +461,9 @@ af_status af_interval_end(af_ctx *c, const void *grad_dev, uint32_t flags, af_de
   if (st != AF_OK) return st;
   if (flags & ~(AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
   const bool dry = flags & AF_DRY_RUN;
-  if (c->cfg.world > 1) {  // kernel + all-gather + decide kernel
-    if (!c->comm) return fail(AF_ESTATE, "af_interval_end with world > 1 needs a communicator (af_ctx_set_comm)");
+  if (c->cfg.world > 1 && !c->peers) {  // kernel + all-gather + decide kernel
+    if (!c->comm)
+      return fail(AF_ESTATE, "af_interval_end with world > 1 needs peers (af_ctx_set_peers_*) or a communicator");
     st = af_layer_norms(c, grad_dev, AF_INTERVAL_END | flags, stream);
     if (st != AF_OK) return st;
     return af_update_and_decide(c, flags, out_host, stream);
@@ -464,6 +482,89 @@ af_status af_interval_end(af_ctx *c, const void *grad_dev, uint32_t flags, af_de
     c->pending = false;
   }
   return AF_OK;
+}
+
+struct IpcHandle {  // AF_IPC_HANDLE_BYTES
+  cudaIpcMemHandle_t h;
+  uint64_t offset;  // scratch offset inside the exported allocation
+  int32_t rank, world, L, pad;
+};
+static_assert(sizeof(IpcHandle) <= AF_IPC_HANDLE_BYTES, "ipc handle size");
+
+static af_status upload_peers(af_ctx *c, const std::vector<char *> &scratch_of) {
+  std::vector<double *> rows(c->cfg.world);
+  std::vector<unsigned long long *> flags(c->cfg.world);
+  for (int r = 0; r < c->cfg.world; ++r) {
+    rows[r] = reinterpret_cast<double *>(scratch_of[r] + c->o_xrows);
+    flags[r] = reinterpret_cast<unsigned long long *>(scratch_of[r] + c->o_xflags);
+  }
+  AF_CUDA(cudaMemcpy(c->scratch + c->o_peer_rows, rows.data(), rows.size() * sizeof(void *), cudaMemcpyHostToDevice),
+          "cudaMemcpy(peer rows)");
+  AF_CUDA(cudaMemcpy(c->scratch + c->o_peer_flags, flags.data(), flags.size() * sizeof(void *),
+                     cudaMemcpyHostToDevice),
+          "cudaMemcpy(peer flags)");
+  AF_CUDA(cudaDeviceSynchronize(), "set peers");
+  c->peers = true;
+  return AF_OK;
+}
+
+af_status af_ctx_exchange_ipc_handle(af_ctx *c, void *handle_out) {
+  if (!c || !handle_out) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  // base of the allocation holding the scratch buffer (the caller's allocator may
+  // sub-allocate): driver entry point resolved at run time (libcuda is loaded by cudart)
+  typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
+  static GetRange get_range = reinterpret_cast<GetRange>(dlsym(RTLD_DEFAULT, "cuMemGetAddressRange_v2"));
+  if (!get_range) return fail(AF_ECUDA, "cuMemGetAddressRange_v2 not found (no CUDA driver loaded)");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(c->scratch)) != 0)
+    return fail(AF_ECUDA, "cuMemGetAddressRange failed");
+  IpcHandle h{};
+  AF_CUDA(cudaIpcGetMemHandle(&h.h, reinterpret_cast<void *>(base)), "cudaIpcGetMemHandle");
+  h.offset = reinterpret_cast<unsigned long long>(c->scratch) - base;
+  h.rank = c->cfg.rank;
+  h.world = c->cfg.world;
+  h.L = c->L;
+  std::memset(handle_out, 0, AF_IPC_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  return AF_OK;
+}
+
+af_status af_ctx_set_peers_ipc(af_ctx *c, const void *handles) {
+  if (!c || !handles) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (c->peers) return fail(AF_ESTATE, "peers already set");
+  std::vector<char *> scratch_of(c->cfg.world, nullptr);
+  for (int r = 0; r < c->cfg.world; ++r) {
+    IpcHandle h;
+    std::memcpy(&h, static_cast<const char *>(handles) + static_cast<size_t>(r) * AF_IPC_HANDLE_BYTES, sizeof(h));
+    if (h.rank != r || h.world != c->cfg.world || h.L != c->L) return fail(AF_EINVAL, "peer handle mismatch");
+    if (r == c->cfg.rank) {
+      scratch_of[r] = c->scratch;
+      continue;
+    }
+    void *p = nullptr;
+    AF_CUDA(cudaIpcOpenMemHandle(&p, h.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    c->ipc_opened.push_back(p);
+    scratch_of[r] = static_cast<char *>(p) + h.offset;
+  }
+  return upload_peers(c, scratch_of);
+}
+
+af_status af_ctx_set_peers_local(af_ctx *c, af_ctx *const *peers) {
+  if (!c || !peers) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (c->peers) return fail(AF_ESTATE, "peers already set");
+  std::vector<char *> scratch_of(c->cfg.world, nullptr);
+  for (int r = 0; r < c->cfg.world; ++r) {
+    const af_ctx *q = peers[r];
+    if (!q || !q->bound || q->cfg.rank != r || q->cfg.world != c->cfg.world || q->L != c->L ||
+        q->o_xrows != c->o_xrows || q->o_xflags != c->o_xflags)
+      return fail(AF_EINVAL, "peer context mismatch");
+    scratch_of[r] = q->scratch;
+  }
+  return upload_peers(c, scratch_of);
 }
 
 struct StateBlob {
@@ -527,6 +628,7 @@ af_status af_set_state(af_ctx *c, const void *buf, size_t len) {
 af_status af_ctx_destroy(af_ctx *c) {
   if (!c) return fail(AF_EINVAL, "NULL ctx");
   if (c->comm) ncclCommDestroy(c->comm);
+  for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   delete c;
   return AF_OK;
 }

@@ -35,6 +35,7 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
   const int t = threadIdx.x;
   const int L = p.L;
   const int T = p.state->T;
+  const double *ss_all = p.ss_all + (p.xparity ? (p.state->epoch & 1ull) * p.world * p.L : 0);
   int f = p.state->f;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int n_act = p.n_pool - f;
@@ -44,7 +45,7 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
 
   double ss = 0.0, nrm = 0.0, et = 0.0;
   if (t < L) {
-    for (int r = 0; r < p.world; ++r) ss = __dadd_rn(ss, __ldcg(p.ss_all + r * L + t));
+    for (int r = 0; r < p.world; ++r) ss = __dadd_rn(ss, __ldcg(ss_all + r * L + t));
     nrm = __dsqrt_rn(ss);
     const double pv = p.state->prev[t];
     et = (pv == 0.0) ? 0.0 : __ddiv_rn(fabs(__dsub_rn(pv, nrm)), pv);
@@ -55,17 +56,20 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
   if (t < n_act) s_act[t] = s_eta[p.pool_seg[f + t]];
   __syncthreads();
 
-  const bool nonfinite = s_nonfinite != 0;
+  const bool xfail = p.xparity && (p.state->sticky & 1u);  // a peer never arrived
+  const bool nonfinite = s_nonfinite != 0 || xfail;
   unsigned int flags = p.commit ? 0u : AF_DEC_DRY_RUN;
+  if (xfail) flags |= AF_DEC_EXCHANGE_TIMEOUT;
   bool decide = false;
-  if (nonfinite)
-    flags |= AF_DEC_NONFINITE;
-  else if (T == 0)
-    flags |= AF_DEC_FIRST_INTERVAL;
-  else if (n_act < p.min_active)
-    flags |= AF_DEC_SKIPPED_FEW;
-  else
-    decide = true;
+  if (s_nonfinite != 0) flags |= AF_DEC_NONFINITE;
+  if (!nonfinite) {
+    if (T == 0)
+      flags |= AF_DEC_FIRST_INTERVAL;
+    else if (n_act < p.min_active)
+      flags |= AF_DEC_SKIPPED_FEW;
+    else
+      decide = true;
+  }
 
   if (decide) {
     // rank sort of the active eta values (ties broken by position; values are finite)

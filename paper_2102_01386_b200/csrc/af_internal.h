@@ -33,6 +33,7 @@ struct DevState {
   int32_t f;         // frozen POOL count (the boundary)
   uint32_t sticky;   // reserved
   int32_t pad;
+  unsigned long long epoch;      // peer-exchange epoch: interval ends seen (identical on all ranks)
   double prev[AF_MAX_SEGMENTS];  // ||Delta_{T-1,l}||
 };
 
@@ -52,6 +53,7 @@ struct DecideParams {
   double tie_rel_eps;
   int32_t min_active;
   int32_t commit;           // 0 under AF_DRY_RUN
+  int32_t xparity;          // peer exchange: rows live in buffer (state->epoch & 1) of 2
 };
 
 // Arguments of the streaming kernels (accumulate / interval-end sum of squares).
@@ -73,7 +75,15 @@ struct NormParams {
   int32_t first;                   // first step of the interval (Delta not read)
   int32_t end;                     // interval end (STEP_SUMSQ: publish ss_acc)
   int32_t commit;                  // STEP_SUMSQ: store ss_acc
-  int32_t fuse_decide;             // world == 1 fused interval end: last CTA decides
+  int32_t fuse_decide;             // fused interval end: the last CTA decides
+  // NVLink one-shot exchange (peers registered): the last CTA writes this rank's
+  // row into every peer's double-buffered exchange matrix, raises its flag there
+  // and waits for all peers' flags before deciding.
+  int32_t xworld, xrank;           // xworld == 0: no peer exchange
+  double *xrows;                   // local exchange matrices [2][world][L]
+  double *const *peer_rows;        // [world] device pointers to each rank's xrows
+  unsigned long long *xflags;      // local flags [world]: epoch reached by each rank
+  unsigned long long *const *peer_flags;  // [world] pointers to each rank's xflags
   DecideParams dec;
 };
 

@@ -1,0 +1,75 @@
+"""Two processes on one GPU exchange their per-segment partials through CUDA IPC
+mappings of each other's exchange buffers (the multi-process form of the
+NVLink one-shot exchange)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    try:
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import numpy as np
+        import oracle as O
+        import paper_2102_01386_b200 as af
+        from afinputs import tiny_grad_step, tiny_layout
+        lay = tiny_layout()
+        fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="f32", rank=rank, world=world)
+        fm.set_peers_ipc()
+        oz = O.Freezer(lay.offsets, lay.kinds, O.DT_F32)
+        out = []
+        for T in range(4):
+            for t in range(4):
+                g = tiny_grad_step(lay, 0, T, t)
+                gd = torch.from_numpy(g).cuda()
+                if t == 3:
+                    fm.interval_end(gd)
+                else:
+                    fm.layer_norms(gd)
+                oz.layer_norms(g, t == 3)
+            d = fm.decision()
+            o = oz.update_and_decide()
+            assert not d["flags"] & 32, "exchange timeout"
+            assert d["boundary_after"] == o["boundary_after"]
+            np.testing.assert_allclose(d["norm"], o["norm"], rtol=1e-12)
+            out.append((d["boundary_after"], d["norm"]))
+        allr = [None] * world
+        dist.all_gather_object(allr, out)
+        assert allr[0] == allr[1]
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.timeout(600)
+def test_two_processes_ipc_exchange_one_gpu():
+    assert torch.cuda.is_available()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=500) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res

@@ -406,3 +406,45 @@ def test_cache_large_gather_parity():
     want = rows[[pos[int(x)] for x in q]]
     assert np.array_equal(out.cpu().numpy(), want)
     assert np.all(dep.cpu().numpy() == 3)
+
+
+# ---------------------------------------------------------------- NVLink one-shot exchange (NEXT 2)
+
+def _run_peer_ranks(P, fused, intervals=5, dt="bf16"):
+    lay = _ragged_layout()
+    step = _decaying_step(lay, dt, 31)
+    fms = [_fm(lay, dt, rank=r, world=P) for r in range(P)]
+    for fm in fms:
+        fm.set_peers_local(fms)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    oz = _oracle(lay, dt)
+    for T in range(intervals):
+        for t in range(2):
+            gnp = step(T, t)
+            g = to_device_grad(gnp, dt)
+            torch.cuda.synchronize()
+            for fm, s in zip(fms, streams):          # ranks run concurrently on their streams
+                with torch.cuda.stream(s):
+                    if t == 1 and fused:
+                        fm.interval_end(g, stream=s)
+                    elif t == 1:
+                        fm.layer_norms(g, interval_end=True, stream=s)
+                        fm.update_and_decide(stream=s)
+                    else:
+                        fm.layer_norms(g, stream=s)
+            torch.cuda.synchronize()
+            oz.layer_norms(gnp, t == 1)
+        decs = [fm.decision() for fm in fms]
+        assert not any(d["flags"] & 32 for d in decs), "exchange timeout"
+        assert all(canon(d) == canon(decs[0]) for d in decs[1:])
+        compare_records(decs[0], oz.update_and_decide(), lay.n_segments, tag=f"P={P} T={T}")
+    return fms
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("fused", [True, False])
+def test_peer_exchange_ranks_on_one_gpu(P, fused):
+    """P ranks in one process (concurrent streams) exchange their partials through
+    each other's memory inside the interval-end kernel; identical decisions on all
+    ranks, oracle parity."""
+    _run_peer_ranks(P, fused)
