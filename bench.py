@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cache-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly (no CUDA graphs)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: per-layer partial exchange (in-kernel NVLink P2P, or NCCL all-gather)")
     ap.add_argument("--unfused", action="store_true",
                     help="interval end as af_layer_norms(END) + af_update_and_decide (two launches)")
     ap.add_argument("--sweep", action="store_true",
@@ -187,8 +189,18 @@ def run_ours(args, rank, world, local):
     lay = bert_layout(which)
     s_g = 2 if dt == "bf16" else 4
     fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, rank=rank, world=world, device=dev)
+    exchange = "none"
     if world > 1:
-        fm.set_comm()
+        # NVLink one-shot exchange inside the interval-end kernel (CUDA IPC peer
+        # mappings); NCCL all-gather as the fallback
+        try:
+            if args.exchange != "p2p":
+                raise RuntimeError("nccl requested")
+            fm.set_peers_ipc()
+            exchange = "p2p"
+        except Exception:  # noqa: BLE001
+            fm.set_comm()
+            exchange = "nccl"
     info = fm.info()
     n_loc = info["shard_end"] - info["shard_begin"]
     grads = [device_grad(lay, dt, 1000 + k, dev) for k in range(2)]
@@ -306,7 +318,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": f"{args.workload}" + ("-sharded" if world > 1 else ""),
                    "n_elements": lay.n, "segments": lay.n_segments, "n_local": n_loc,
                    "cache": {"examples": NUM_EXAMPLES, "row_bytes": ROW_BYTES, "rows_per_rank_step": B},
-                   "boundary_f": 0, "parallelism": f"shard{world}",
+                   "boundary_f": 0, "parallelism": f"shard{world}", "exchange": exchange,
                    "launch": "eager" if args.no_graph else "CUDA graph per step (8 graphs rotating id batches)",
                    "l2": "inputs larger than L2: each step streams >= 4 GB/rank through the 126 MB L2"},
         "grad_norm_decide_gbs": round(gn_dec, 1),
@@ -317,7 +329,7 @@ def run_ours(args, rank, world, local):
                      "frac": round(ach / peak, 4), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_rank[dom],
                      **ncu_traffic(args.workload if world == 1 else None, dom)},
-        "gpu_launches": (4 if world == 1 else 5) * args.steps,
+        "gpu_launches": (4 if (world == 1 or exchange == "p2p") else 5) * args.steps,
         "clocks": clk.summary(),
     }
     if not args.no_cache_sweep:

@@ -4,7 +4,6 @@
 // and the optional NCCL communicator; every device buffer is caller-owned.
 // Validation errors are synchronous and enqueue nothing.
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -514,8 +513,11 @@ af_status af_ctx_exchange_ipc_handle(af_ctx *c, void *handle_out) {
   // base of the allocation holding the scratch buffer (the caller's allocator may
   // sub-allocate): driver entry point resolved at run time (libcuda is loaded by cudart)
   typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
-  static GetRange get_range = reinterpret_cast<GetRange>(dlsym(RTLD_DEFAULT, "cuMemGetAddressRange_v2"));
-  if (!get_range) return fail(AF_ECUDA, "cuMemGetAddressRange_v2 not found (no CUDA driver loaded)");
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  AF_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(AF_ECUDA, "cuMemGetAddressRange entry point not found");
+  GetRange get_range = reinterpret_cast<GetRange>(fn);
   unsigned long long base = 0;
   size_t size = 0;
   if (get_range(&base, &size, reinterpret_cast<unsigned long long>(c->scratch)) != 0)
