@@ -64,6 +64,16 @@ def parse():
     return ap.parse_args()
 
 
+def max_over_ranks(x, dev):
+    """Max of a float over all ranks (device tensor for NCCL, CPU tensor for gloo)."""
+    import torch
+    import torch.distributed as dist
+    on = dev if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], device=on, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -181,10 +191,17 @@ def run_ours(args, rank, world, local):
     import paper_2102_01386_b200 as af
     from afinputs import bert_layout
 
+    local = local % max(1, torch.cuda.device_count())   # ranks may share a GPU (functional check)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # AF_BENCH_BACKEND=gloo lets several ranks share one GPU for a functional
+        # check of the N > 1 flow (NCCL refuses two ranks on one device)
+        backend = os.environ.get("AF_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     which, dt = WORKLOADS[args.workload]
     lay = bert_layout(which)
     s_g = 2 if dt == "bf16" else 4
@@ -291,9 +308,7 @@ def run_ours(args, rank, world, local):
     ph_ms = {p: sum(e[k].elapsed_time(e[k + 1]) for e in evs) / n_ph for k, p in enumerate(phases)}
     ms = ms_local
     if world > 1:
-        t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
+        ms = max_over_ranks(ms_local, dev)
     ms_per_step = ms / args.steps
     bytes_rank = algorithmic_bytes(n_loc, s_g, B, ROW_BYTES)
     step_bytes_all = sum(bytes_rank.values()) * world   # every rank moves ~the same bytes
@@ -482,9 +497,7 @@ def run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
+        ms = max_over_ranks(ms, dev)
     bytes_all = sum(algorithmic_bytes(n_loc, s_g, B, ROW_BYTES).values()) * world
     h2d = 2 * n_loc * s_g + B * ROW_BYTES + B * 8
     d2h = 6184 + B * ROW_BYTES + B * 4

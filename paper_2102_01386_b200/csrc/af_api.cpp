@@ -215,21 +215,23 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
     o = align_up(o + (bytes ? bytes : 1), 256);
     return at;
   };
+  // rank-independent part first (its offsets are identical on every rank: peers
+  // address each other's exchange buffers by these offsets), then the tile tables
   c->o_state = take(sizeof(DevState));
   c->o_sched = take(4 * sizeof(Sched));
-  c->o_tiles = take(c->tiles.size() * sizeof(Tile));
-  c->o_ftf = take((n_pool + 1) * sizeof(int32_t));
-  c->o_stb = take((L + 1) * sizeof(int32_t));
-  c->o_pool = take(n_pool * sizeof(int32_t));
-  c->o_part = take(c->tiles.size() * sizeof(double));
-  c->o_ssall = take(static_cast<size_t>(cfg->world) * L * sizeof(double));
-  c->o_ssacc = take(L * sizeof(double));
-  c->o_last = take(sizeof(af_decision));
-  c->o_ring = take(kRing * sizeof(af_decision));
   c->o_xrows = take(2 * static_cast<size_t>(cfg->world) * L * sizeof(double));
   c->o_xflags = take(static_cast<size_t>(cfg->world) * sizeof(unsigned long long));
   c->o_peer_rows = take(static_cast<size_t>(cfg->world) * sizeof(void *));
   c->o_peer_flags = take(static_cast<size_t>(cfg->world) * sizeof(void *));
+  c->o_ssall = take(static_cast<size_t>(cfg->world) * L * sizeof(double));
+  c->o_ssacc = take(L * sizeof(double));
+  c->o_last = take(sizeof(af_decision));
+  c->o_ring = take(kRing * sizeof(af_decision));
+  c->o_ftf = take((n_pool + 1) * sizeof(int32_t));
+  c->o_stb = take((L + 1) * sizeof(int32_t));
+  c->o_pool = take(n_pool * sizeof(int32_t));
+  c->o_tiles = take(c->tiles.size() * sizeof(Tile));
+  c->o_part = take(c->tiles.size() * sizeof(double));
   c->scratch_bytes = o;
   *out = c;
   return AF_OK;
@@ -485,7 +487,8 @@ af_status af_interval_end(af_ctx *c, const void *grad_dev, uint32_t flags, af_de
 
 struct IpcHandle {  // AF_IPC_HANDLE_BYTES
   cudaIpcMemHandle_t h;
-  uint64_t offset;  // scratch offset inside the exported allocation
+  uint64_t offset;                 // scratch offset inside the exported allocation
+  uint64_t xrows_off, xflags_off;  // exchange-area offsets inside the scratch
   int32_t rank, world, L, pad;
 };
 static_assert(sizeof(IpcHandle) <= AF_IPC_HANDLE_BYTES, "ipc handle size");
@@ -525,6 +528,8 @@ af_status af_ctx_exchange_ipc_handle(af_ctx *c, void *handle_out) {
   IpcHandle h{};
   AF_CUDA(cudaIpcGetMemHandle(&h.h, reinterpret_cast<void *>(base)), "cudaIpcGetMemHandle");
   h.offset = reinterpret_cast<unsigned long long>(c->scratch) - base;
+  h.xrows_off = c->o_xrows;
+  h.xflags_off = c->o_xflags;
   h.rank = c->cfg.rank;
   h.world = c->cfg.world;
   h.L = c->L;
@@ -541,7 +546,9 @@ af_status af_ctx_set_peers_ipc(af_ctx *c, const void *handles) {
   for (int r = 0; r < c->cfg.world; ++r) {
     IpcHandle h;
     std::memcpy(&h, static_cast<const char *>(handles) + static_cast<size_t>(r) * AF_IPC_HANDLE_BYTES, sizeof(h));
-    if (h.rank != r || h.world != c->cfg.world || h.L != c->L) return fail(AF_EINVAL, "peer handle mismatch");
+    if (h.rank != r || h.world != c->cfg.world || h.L != c->L || h.xrows_off != c->o_xrows ||
+        h.xflags_off != c->o_xflags)
+      return fail(AF_EINVAL, "peer handle mismatch");
     if (r == c->cfg.rank) {
       scratch_of[r] = c->scratch;
       continue;
