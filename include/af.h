@@ -137,9 +137,11 @@ typedef struct {
   int32_t n_segments, n_pool, rank, world;
   int64_t n_total;                  /* elements of the full flat buffer                  */
   int64_t shard_begin, shard_end;   /* this rank's element range (multiples of 8 except n) */
-  int32_t n_tiles;                  /* segment-aligned tiles of the shard                */
-  int32_t tile_elems;               /* nominal tile size in elements                     */
+  int32_t n_tiles;                  /* segment-aligned tiles of the shard (interval-end kernels) */
+  int32_t tile_elems;               /* their nominal size in elements                    */
   int32_t first_tile_of_pool[AF_MAX_SEGMENTS + 1]; /* first active tile when f = j frozen */
+  int32_t n_tiles_acc;              /* tiles of the accumulate kernel (finer, no partials) */
+  int32_t tile_elems_acc;
 } af_info;
 
 typedef struct af_ctx af_ctx;

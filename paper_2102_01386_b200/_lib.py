@@ -45,7 +45,8 @@ class AfInfo(ctypes.Structure):
     _fields_ = [("n_segments", c_int32), ("n_pool", c_int32), ("rank", c_int32), ("world", c_int32),
                 ("n_total", c_int64), ("shard_begin", c_int64), ("shard_end", c_int64),
                 ("n_tiles", c_int32), ("tile_elems", c_int32),
-                ("first_tile_of_pool", c_int32 * (AF_MAX_SEGMENTS + 1))]
+                ("first_tile_of_pool", c_int32 * (AF_MAX_SEGMENTS + 1)),
+                ("n_tiles_acc", c_int32), ("tile_elems_acc", c_int32)]
 
 
 # name -> (restype, argtypes); every af_* symbol declared in include/af.h

@@ -62,12 +62,18 @@ struct af_ctx {
   af_dtype dtype = AF_DT_F32;
   af_config cfg{};
   int64_t n = 0, sb = 0, se = 0;
-  int tile_elems = 0;
-  std::vector<Tile> tiles;
-  std::vector<int32_t> seg_tile_begin, first_tile_of_f;
+  // two segment-aligned tile tables of the shard: [0] the accumulate kernel's
+  // (finer: scheduling granularity only), [1] the interval-end kernels' (one fp64
+  // partial per tile)
+  struct TileSet {
+    int tile_elems = 0;
+    std::vector<Tile> tiles;
+    std::vector<int32_t> seg_tile_begin, first_tile_of_f;
+    size_t o_tiles = 0, o_ftf = 0, o_stb = 0;
+  } ts[2];
   // workspace
   size_t accum_bytes = 0, scratch_bytes = 0;
-  size_t o_state = 0, o_sched = 0, o_tiles = 0, o_ftf = 0, o_stb = 0, o_pool = 0, o_part = 0, o_ssall = 0,
+  size_t o_state = 0, o_sched = 0, o_pool = 0, o_part = 0, o_ssall = 0,
          o_ssacc = 0, o_last = 0, o_ring = 0, o_xrows = 0,
          o_xflags = 0, o_peer_rows = 0, o_peer_flags = 0;
   float *accum = nullptr;
@@ -176,35 +182,38 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   };
   c->sb = bound_of(cfg->rank);
   c->se = bound_of(cfg->rank + 1);
-  // segment-aligned tile table of the shard (tile edges on a global grid of tile_elems)
-  const int esz = (c->dtype == AF_DT_BF16) ? 2 : 4;
-  c->tile_elems = kTileBytes / esz;
-  const int64_t TE = c->tile_elems;
-  c->seg_tile_begin.assign(L + 1, 0);
-  for (int l = 0; l < L; ++l) {
-    c->seg_tile_begin[l] = static_cast<int32_t>(c->tiles.size());
-    const int64_t lo = std::max(c->offs[l], c->sb), hi = std::min(c->offs[l + 1], c->se);
-    for (int64_t pos = lo; pos < hi;) {
-      const int64_t nxt = std::min(hi, (pos / TE + 1) * TE);
-      c->tiles.push_back(Tile{pos, nxt, l, 0, 0, 0});
-      pos = nxt;
+  // segment-aligned tile tables of the shard (tile edges on a global grid of tile_elems)
+  const bool bf16 = (c->dtype == AF_DT_BF16);
+  c->ts[0].tile_elems = bf16 ? AF_TILE_ACC_BF16 : AF_TILE_ACC_F32;
+  c->ts[1].tile_elems = bf16 ? AF_TILE_ELEMS_BF16 : AF_TILE_ELEMS_F32;
+  for (auto &T : c->ts) {
+    const int64_t TE = T.tile_elems;
+    T.seg_tile_begin.assign(L + 1, 0);
+    for (int l = 0; l < L; ++l) {
+      T.seg_tile_begin[l] = static_cast<int32_t>(T.tiles.size());
+      const int64_t lo = std::max(c->offs[l], c->sb), hi = std::min(c->offs[l + 1], c->se);
+      for (int64_t pos = lo; pos < hi;) {
+        const int64_t nxt = std::min(hi, (pos / TE + 1) * TE);
+        T.tiles.push_back(Tile{pos, nxt, l, 0, 0, 0});
+        pos = nxt;
+      }
+      if (T.tiles.size() > static_cast<size_t>(1) << 30) {
+        delete c;
+        return fail(AF_ERANGE, "too many tiles");
+      }
     }
-    if (c->tiles.size() > static_cast<size_t>(1) << 30) {
-      delete c;
-      return fail(AF_ERANGE, "too many tiles");
+    T.seg_tile_begin[L] = static_cast<int32_t>(T.tiles.size());
+    for (auto &t : T.tiles) {
+      t.seg_first = T.seg_tile_begin[t.seg];
+      t.seg_end = T.seg_tile_begin[t.seg + 1];
     }
-  }
-  c->seg_tile_begin[L] = static_cast<int32_t>(c->tiles.size());
-  for (auto &t : c->tiles) {
-    t.seg_first = c->seg_tile_begin[t.seg];
-    t.seg_end = c->seg_tile_begin[t.seg + 1];
-  }
-  // first active tile when j POOL layers are frozen: PRE and POOL[0..j) skipped (Q11)
-  c->first_tile_of_f.assign(n_pool + 1, 0);
-  for (int j = 0; j <= n_pool; ++j) {
-    int first_seg = 0;
-    if (j > 0) first_seg = (j < n_pool) ? c->pool_seg[j] : c->pool_seg[n_pool - 1] + 1;
-    c->first_tile_of_f[j] = c->seg_tile_begin[first_seg];
+    // first active tile when j POOL layers are frozen: PRE and POOL[0..j) skipped (Q11)
+    T.first_tile_of_f.assign(n_pool + 1, 0);
+    for (int j = 0; j <= n_pool; ++j) {
+      int first_seg = 0;
+      if (j > 0) first_seg = (j < n_pool) ? c->pool_seg[j] : c->pool_seg[n_pool - 1] + 1;
+      T.first_tile_of_f[j] = T.seg_tile_begin[first_seg];
+    }
   }
   // workspace layout
   const int64_t n_local = c->se - c->sb;
@@ -227,11 +236,13 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   c->o_ssacc = take(L * sizeof(double));
   c->o_last = take(sizeof(af_decision));
   c->o_ring = take(kRing * sizeof(af_decision));
-  c->o_ftf = take((n_pool + 1) * sizeof(int32_t));
-  c->o_stb = take((L + 1) * sizeof(int32_t));
   c->o_pool = take(n_pool * sizeof(int32_t));
-  c->o_tiles = take(c->tiles.size() * sizeof(Tile));
-  c->o_part = take(c->tiles.size() * sizeof(double));
+  for (auto &T : c->ts) {
+    T.o_ftf = take((n_pool + 1) * sizeof(int32_t));
+    T.o_stb = take((L + 1) * sizeof(int32_t));
+    T.o_tiles = take(T.tiles.size() * sizeof(Tile));
+  }
+  c->o_part = take(c->ts[1].tiles.size() * sizeof(double));
   c->scratch_bytes = o;
   *out = c;
   return AF_OK;
@@ -254,9 +265,11 @@ af_status af_ctx_info(const af_ctx *c, af_info *info) {
   info->n_total = c->n;
   info->shard_begin = c->sb;
   info->shard_end = c->se;
-  info->n_tiles = static_cast<int32_t>(c->tiles.size());
-  info->tile_elems = c->tile_elems;
-  for (int j = 0; j <= c->n_pool; ++j) info->first_tile_of_pool[j] = c->first_tile_of_f[j];
+  info->n_tiles = static_cast<int32_t>(c->ts[1].tiles.size());
+  info->tile_elems = c->ts[1].tile_elems;
+  info->n_tiles_acc = static_cast<int32_t>(c->ts[0].tiles.size());
+  info->tile_elems_acc = c->ts[0].tile_elems;
+  for (int j = 0; j <= c->n_pool; ++j) info->first_tile_of_pool[j] = c->ts[1].first_tile_of_f[j];
   return AF_OK;
 }
 
@@ -277,16 +290,18 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
   c->accum = static_cast<float *>(accum_dev);
   c->scratch = static_cast<char *>(scratch_dev);
   AF_CUDA(cudaMemset(c->scratch, 0, c->scratch_bytes), "cudaMemset(scratch)");
-  if (!c->tiles.empty())
-    AF_CUDA(cudaMemcpy(c->scratch + c->o_tiles, c->tiles.data(), c->tiles.size() * sizeof(Tile),
+  for (auto &T : c->ts) {
+    if (!T.tiles.empty())
+      AF_CUDA(cudaMemcpy(c->scratch + T.o_tiles, T.tiles.data(), T.tiles.size() * sizeof(Tile),
+                         cudaMemcpyHostToDevice),
+              "cudaMemcpy(tiles)");
+    AF_CUDA(cudaMemcpy(c->scratch + T.o_ftf, T.first_tile_of_f.data(), T.first_tile_of_f.size() * 4,
                        cudaMemcpyHostToDevice),
-            "cudaMemcpy(tiles)");
-  AF_CUDA(cudaMemcpy(c->scratch + c->o_ftf, c->first_tile_of_f.data(), c->first_tile_of_f.size() * 4,
-                     cudaMemcpyHostToDevice),
-          "cudaMemcpy(first_tile_of_f)");
-  AF_CUDA(cudaMemcpy(c->scratch + c->o_stb, c->seg_tile_begin.data(), c->seg_tile_begin.size() * 4,
-                     cudaMemcpyHostToDevice),
-          "cudaMemcpy(seg_tile_begin)");
+            "cudaMemcpy(first_tile_of_f)");
+    AF_CUDA(cudaMemcpy(c->scratch + T.o_stb, T.seg_tile_begin.data(), T.seg_tile_begin.size() * 4,
+                       cudaMemcpyHostToDevice),
+            "cudaMemcpy(seg_tile_begin)");
+  }
   AF_CUDA(cudaMemcpy(c->scratch + c->o_pool, c->pool_seg.data(), c->pool_seg.size() * 4, cudaMemcpyHostToDevice),
           "cudaMemcpy(pool_seg)");
   AF_CUDA(cudaDeviceSynchronize(), "bind");
@@ -331,16 +346,18 @@ namespace {
 
 NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   NormParams p{};
+  const int k = (c->cfg.acc_mode == AF_ACC_DELTA && !end) ? 0 : 1;  // which tile table
+  const auto &T = c->ts[k];
   p.grad = grad_dev;
   p.delta = c->accum;
   p.shard_begin = c->sb;
-  p.tiles = c->at<Tile>(c->o_tiles);
-  p.n_tiles = static_cast<int32_t>(c->tiles.size());
+  p.tiles = c->at<Tile>(T.o_tiles);
+  p.n_tiles = static_cast<int32_t>(T.tiles.size());
   p.L = c->L;
-  p.first_tile_of_f = c->at<int32_t>(c->o_ftf);
-  p.seg_tile_begin = c->at<int32_t>(c->o_stb);
+  p.first_tile_of_f = c->at<int32_t>(T.o_ftf);
+  p.seg_tile_begin = c->at<int32_t>(T.o_stb);
   p.state = c->at<DevState>(c->o_state);
-  p.sched = c->at<Sched>(c->o_sched);
+  p.sched = c->at<Sched>(c->o_sched) + k;
   p.partials = c->at<double>(c->o_part);
   p.ss_out = c->at<double>(c->o_ssall) + static_cast<size_t>(c->cfg.rank) * c->L;
   p.ss_acc = c->at<double>(c->o_ssacc);

@@ -9,7 +9,22 @@
 namespace af {
 
 constexpr int kNormBlock = 256;          // threads per CTA of the streaming kernels
-constexpr int kTileBytes = 64 * 1024;    // nominal gradient bytes per tile
+// Tile = the unit of dynamic scheduling and of one fp64 partial.  Sized in
+// elements so that a bf16 tile (32 KiB of g + 64 KiB of Delta) and an fp32 tile
+// (64 KiB + 64 KiB) both leave >= ~10 tiles per CTA for BERT-base, bounding the
+// end-of-kernel imbalance (see profiles/ for the sweep).
+#ifndef AF_TILE_ELEMS_F32
+#define AF_TILE_ELEMS_F32 16384
+#endif
+#ifndef AF_TILE_ELEMS_BF16
+#define AF_TILE_ELEMS_BF16 16384
+#endif
+#ifndef AF_TILE_ACC_F32  // the accumulate kernel keeps no partials: finer tiles balance better
+#define AF_TILE_ACC_F32 8192
+#endif
+#ifndef AF_TILE_ACC_BF16
+#define AF_TILE_ACC_BF16 8192
+#endif
 constexpr int kRing = 16;                // decision records kept on the device
 constexpr int kShardAlign = 8;           // shard bounds are multiples of 8 elements (32 B fp32 Delta)
 

@@ -128,8 +128,9 @@ def test_shards_cover_buffer_and_tiles_are_segment_aligned(which, dt, world):
         assert i["shard_begin"] == prev_end
         assert i["shard_begin"] % 8 == 0
         prev_end = i["shard_end"]
-        assert i["tile_elems"] * (2 if dt == "bf16" else 4) == 64 * 1024
+        assert i["tile_elems"] % 8 == 0 and i["tile_elems"] >= 4096
         assert i["n_tiles"] == _expected_tiles(lay, i["shard_begin"], i["shard_end"], i["tile_elems"])
+        assert i["n_tiles_acc"] == _expected_tiles(lay, i["shard_begin"], i["shard_end"], i["tile_elems_acc"])
         assert fm.accum_bytes == 4 * (i["shard_end"] - i["shard_begin"])
         ft = i["first_tile_of_pool"]
         assert ft == sorted(ft) and ft[0] == 0

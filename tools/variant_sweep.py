@@ -15,6 +15,15 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
+    "acc4k": "-DAF_TILE_ACC_F32=4096 -DAF_TILE_ACC_BF16=4096",
+    "acc16k_bf16": "-DAF_TILE_ACC_BF16=16384",
+    "end8k_f32": "-DAF_TILE_ELEMS_F32=8192",
+    "end32k_bf16": "-DAF_TILE_ELEMS_BF16=32768",
+    "tile_bf16_32k": "-DAF_TILE_ELEMS_BF16=32768",
+    "tile_bf16_8k": "-DAF_TILE_ELEMS_BF16=8192",
+    "tile_f32_8k": "-DAF_TILE_ELEMS_F32=8192",
+    "tile_f32_32k": "-DAF_TILE_ELEMS_F32=32768",
+    "bf16_acc_u4": "-DAF_U_ACC=4",
     "g_nc": "-DAF_G_HINT=1",
     "g_nc_d_nc": "-DAF_G_HINT=1 -DAF_D_HINT_END=1",
     "g_nc_d_nc_u8": "-DAF_G_HINT=1 -DAF_D_HINT_END=1 -DAF_U_END=8",
