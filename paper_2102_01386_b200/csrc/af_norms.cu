@@ -215,6 +215,88 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;  // identical on every lane (fp add is commutative)
 }
 
+// The last CTA's work after the grid has drained: per-segment sums, the optional
+// NVLink one-shot exchange and the fused decision.  Not inlined, so its
+// registers do not raise the streaming loop's (occupancy) budget.
+template <int MODE>
+__device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, double *s_red_unused) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  (void)s_red_unused;
+  // peer exchange: this interval end's epoch selects the exchange buffer
+  const bool xchg = p.xworld > 1 && p.end;
+  __shared__ unsigned long long s_epoch;
+  double *ss_row = p.ss_out;
+  if (xchg) {
+    if (tid == 0) {
+      DevState *st = const_cast<DevState *>(p.state);
+      s_epoch = st->epoch + 1ull;
+      st->epoch = s_epoch;
+    }
+    __syncthreads();
+    ss_row = p.xrows + (s_epoch & 1ull) * p.xworld * p.L + static_cast<size_t>(p.xrank) * p.L;
+  }
+  // each segment's active tiles' partials in tile order: one warp per segment,
+  // lane-strided with 8 loads in flight, then the xor tree (deterministic)
+  for (int l = warp; l < p.L; l += kNormBlock / 32) {
+    int tb = p.seg_tile_begin[l];
+    tb = tb < first_tile ? first_tile : tb;
+    const int te = p.seg_tile_begin[l + 1];
+    double s = 0.0;
+#pragma unroll 8
+    for (int k = tb + lane; k < te; k += 32) s += __ldcg(p.partials + k);
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (MODE == kEndDelta) {
+        ss_row[l] = s;
+      } else {
+        const double acc = p.first ? s : p.ss_acc[l] + s;
+        if (p.commit) p.ss_acc[l] = acc;
+        if (p.end) ss_row[l] = acc;
+      }
+    }
+  }
+  if (xchg) {
+    // NVLink one-shot exchange: push this rank's row into every peer's matrix
+    // (P x L fp64 stores over peer memory), publish the epoch in every peer's
+    // flag slot for this rank, then wait until every rank's epoch has arrived.
+    __syncthreads();
+    const unsigned long long e = s_epoch;
+    const size_t off = (e & 1ull) * p.xworld * p.L + static_cast<size_t>(p.xrank) * p.L;
+    for (int i = tid; i < p.xworld * p.L; i += kNormBlock) {
+      const int r = i / p.L, l = i % p.L;
+      p.peer_rows[r][off + l] = ss_row[l];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid < p.xworld) {
+      unsigned long long *flag = p.peer_flags[tid] + p.xrank;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
+    }
+    __shared__ int s_timeout;
+    if (tid == 0) s_timeout = 0;
+    __syncthreads();
+    if (tid < p.xworld) {
+      const unsigned long long *flag = p.xflags + tid;
+      unsigned long long v = 0;
+      for (long long spin = 0;; ++spin) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+        if (v >= e) break;
+        if (spin > (1ll << 22)) {  // ~seconds: a peer never arrived -- flag it, do not hang the GPU
+          s_timeout = 1;
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    if (s_timeout && tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 1u);
+  }
+  if (p.fuse_decide) {
+    __syncthreads();
+    decide_block(p.dec);
+  }
+}
+
 template <int MODE, typename GT, bool RD>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum) ? 1 : AF_MINB_END) norms_kernel(const NormParams p) {
   __shared__ int s_tile[3];
@@ -293,79 +375,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum) ? 1 : AF_MINB_END
     p.sched->done = 0;
   }
   if (MODE == kAccum) return;
-  // peer exchange: this interval end's epoch selects the exchange buffer
-  const bool xchg = p.xworld > 1 && p.end;
-  __shared__ unsigned long long s_epoch;
-  double *ss_row = p.ss_out;
-  if (xchg) {
-    if (tid == 0) {
-      DevState *st = const_cast<DevState *>(p.state);
-      s_epoch = st->epoch + 1ull;
-      st->epoch = s_epoch;
-    }
-    __syncthreads();
-    ss_row = p.xrows + (s_epoch & 1ull) * p.xworld * p.L + static_cast<size_t>(p.xrank) * p.L;
-  }
-  // each segment's active tiles' partials in tile order: one warp per segment,
-  // lane-strided with 8 loads in flight, then the xor tree (deterministic)
-  for (int l = warp; l < p.L; l += kNormBlock / 32) {
-    int tb = p.seg_tile_begin[l];
-    tb = tb < first_tile ? first_tile : tb;
-    const int te = p.seg_tile_begin[l + 1];
-    double s = 0.0;
-#pragma unroll 8
-    for (int k = tb + lane; k < te; k += 32) s += __ldcg(p.partials + k);
-    s = warp_sum(s);
-    if (lane == 0) {
-      if (MODE == kEndDelta) {
-        ss_row[l] = s;
-      } else {
-        const double acc = p.first ? s : p.ss_acc[l] + s;
-        if (p.commit) p.ss_acc[l] = acc;
-        if (p.end) ss_row[l] = acc;
-      }
-    }
-  }
-  if (xchg) {
-    // NVLink one-shot exchange: push this rank's row into every peer's matrix
-    // (P x L fp64 stores over peer memory), publish the epoch in every peer's
-    // flag slot for this rank, then wait until every rank's epoch has arrived.
-    __syncthreads();
-    const unsigned long long e = s_epoch;
-    const size_t off = (e & 1ull) * p.xworld * p.L + static_cast<size_t>(p.xrank) * p.L;
-    for (int i = tid; i < p.xworld * p.L; i += kNormBlock) {
-      const int r = i / p.L, l = i % p.L;
-      p.peer_rows[r][off + l] = ss_row[l];
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (tid < p.xworld) {
-      unsigned long long *flag = p.peer_flags[tid] + p.xrank;
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
-    }
-    __shared__ int s_timeout;
-    if (tid == 0) s_timeout = 0;
-    __syncthreads();
-    if (tid < p.xworld) {
-      const unsigned long long *flag = p.xflags + tid;
-      unsigned long long v = 0;
-      for (long long spin = 0;; ++spin) {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-        if (v >= e) break;
-        if (spin > (1ll << 22)) {  // ~seconds: a peer never arrived -- flag it, do not hang the GPU
-          s_timeout = 1;
-          break;
-        }
-        __nanosleep(64);
-      }
-    }
-    __syncthreads();
-    if (s_timeout && tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 1u);
-  }
-  if (p.fuse_decide) {
-    __syncthreads();
-    decide_block(p.dec);
-  }
+  last_cta_tail<MODE>(p, first_tile, s_red);
 }
 
 template <int MODE, typename GT, bool RD>

@@ -15,6 +15,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
+    "minb3": "-DAF_MINB_END=3",
+    "u2": "-DAF_U_END=2",
+    "ghint0": "-DAF_G_HINT=0",
+    "ghint0_minb3": "-DAF_G_HINT=0 -DAF_MINB_END=3",
     "acc4k": "-DAF_TILE_ACC_F32=4096 -DAF_TILE_ACC_BF16=4096",
     "acc16k_bf16": "-DAF_TILE_ACC_BF16=16384",
     "end8k_f32": "-DAF_TILE_ELEMS_F32=8192",
