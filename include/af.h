@@ -259,6 +259,35 @@ AF_API af_status af_cache_put(af_cache *c, const int64_t *ids_dev, int32_t n, co
 AF_API af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
                        void *rows_out_dev, int32_t *depth_out_dev, void *stream);
 
+/* Storage-manager tiers and admission (§3.2).
+ * Host only, before af_cache_storage_bytes / af_cache_bind: room for I =
+ * hbm_rows + host_rows records (I may be < D = the rank's owned ids): hbm_rows in
+ * the HBM payload, host_rows in a page-locked, device-mapped host tier (the
+ * paper's spill to CPU memory / disk).  Records are allocated from a free list on
+ * put (HBM slots first); a put of a NEW id when every slot is taken is dropped,
+ * in call order (drop-newest) -- the store never exceeds I; rewriting an
+ * existing id reuses its slot; an evict-on-read returns the slot (the paper's
+ * re-cache balance).  Each call is planned by a one-CTA kernel (block scans in
+ * call order, deterministic), then copied by the TMA kernel.  Without this call
+ * the cache is direct-mapped with room for every owned id. */
+AF_API af_status af_cache_set_capacity(af_cache *c, int64_t hbm_rows, int64_t host_rows);
+AF_API af_status af_cache_host_bytes(const af_cache *c, size_t *host_bytes);
+/* Synchronous: binds the caller-owned page-locked host tier (cudaHostAlloc /
+ * torch pin_memory: device-mapped under UVA), 16-byte aligned. */
+AF_API af_status af_cache_bind_host(af_cache *c, void *host_pinned);
+
+typedef struct {
+  uint32_t error_flags;      /* sticky AF_CACHE_ERR_* */
+  uint32_t pad;
+  int64_t partition;         /* D: ids owned by this rank */
+  int64_t capacity;          /* I: record slots (== D when direct-mapped) */
+  int64_t n_valid, n_hbm, n_host;
+  int64_t n_dropped;         /* puts refused for lack of room (tiered) */
+  int64_t free_slots;
+} af_cache_info;
+/* Synchronous: counters of the store. */
+AF_API af_status af_cache_stats(af_cache *c, af_cache_info *out);
+
 /* Synchronous: sticky AF_CACHE_ERR_* flags and the count of valid records. */
 AF_API af_status af_cache_status(af_cache *c, uint32_t *device_error_flags, int64_t *n_valid);
 AF_API af_status af_cache_destroy(af_cache *c);

@@ -294,13 +294,21 @@ class Cache:
     output written with its depth L = frozen POOL count at write time.
     A read returns the record and evicts it when the current frozen count is
     greater than the record's depth (Q22).  With P GPUs each GPU owns
-    the ids with id mod P == rank ("each GPU manages its own cache")."""
+    the ids with id mod P == rank ("each GPU manages its own cache").
 
-    def __init__(self, num_examples, row_bytes, rank=0, world=1):
+    capacity = I (None: every owned id fits): "When the dataset (D points) is
+    larger than the disk space available, we save I points"; a put of a
+    NEW id into a full store is dropped, in call order (drop-newest), so
+    the store never exceeds I; rewriting an existing id (re-cache deeper) always
+    succeeds, and an evict-on-read frees room (P:277 re-cache balance)."""
+
+    def __init__(self, num_examples, row_bytes, rank=0, world=1, capacity=None):
         self.num_examples, self.row_bytes = int(num_examples), int(row_bytes)
         self.rank, self.world = int(rank), int(world)
+        self.capacity = None if capacity is None else int(capacity)
         self.store = {}
         self.error_flags = 0
+        self.dropped = 0
 
     def _check(self, i):
         if i < 0 or i >= self.num_examples:
@@ -314,8 +322,13 @@ class Cache:
     def put(self, ids, rows, depth):
         rows = np.asarray(rows, dtype=np.uint8).reshape(len(ids), self.row_bytes)
         for i, ex in enumerate(ids):
-            if self._check(int(ex)):
-                self.store[int(ex)] = (int(depth), rows[i].copy())
+            ex = int(ex)
+            if not self._check(ex):
+                continue
+            if ex not in self.store and self.capacity is not None and len(self.store) >= self.capacity:
+                self.dropped += 1
+                continue
+            self.store[ex] = (int(depth), rows[i].copy())
 
     def get(self, ids, cur_boundary, out):
         depth_out = np.full(len(ids), MISS, dtype=np.int32)

@@ -49,6 +49,12 @@ class AfInfo(ctypes.Structure):
                 ("n_tiles_acc", c_int32), ("tile_elems_acc", c_int32)]
 
 
+class AfCacheInfo(ctypes.Structure):
+    _fields_ = [("error_flags", c_uint32), ("pad", c_uint32), ("partition", c_int64), ("capacity", c_int64),
+                ("n_valid", c_int64), ("n_hbm", c_int64), ("n_host", c_int64), ("n_dropped", c_int64),
+                ("free_slots", c_int64)]
+
+
 # name -> (restype, argtypes); every af_* symbol declared in include/af.h
 SIGNATURES = {
     "af_ctx_create": (c_int, [POINTER(AfLayout), POINTER(AfConfig), POINTER(c_void_p)]),
@@ -73,6 +79,10 @@ SIGNATURES = {
     "af_cache_put": (c_int, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),
     "af_cache_get": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     "af_cache_status": (c_int, [c_void_p, POINTER(c_uint32), POINTER(c_int64)]),
+    "af_cache_set_capacity": (c_int, [c_void_p, c_int64, c_int64]),
+    "af_cache_host_bytes": (c_int, [c_void_p, POINTER(c_size_t)]),
+    "af_cache_bind_host": (c_int, [c_void_p, c_void_p]),
+    "af_cache_stats": (c_int, [c_void_p, POINTER(AfCacheInfo)]),
     "af_cache_destroy": (c_int, [c_void_p]),
     "af_should_cache": (c_int, [c_int32, c_double, c_double]),
     "af_status_str": (c_char_p, [c_int]),

@@ -173,19 +173,29 @@ class FreezingModule:
 
 
 class ActivationCache:
-    """af_cache: the Storage Manager's HBM cache of frozen-prefix outputs for this
-    rank's ids (§3.2, P:335 partition by id mod world)."""
+    """af_cache: the Storage Manager's cache of frozen-prefix outputs for this
+    rank's ids (§3.2, P:335 partition by id mod world).
 
-    def __init__(self, num_examples, row_bytes, rank=0, world=1, device=None, bind=True):
+    Direct-mapped in HBM by default (room for every owned id).  With
+    hbm_rows/host_rows it is tiered with admission (af_cache_set_capacity): room
+    for I = hbm_rows + host_rows records, the host part in page-locked memory;
+    puts of new ids beyond I are dropped (drop-newest)."""
+
+    def __init__(self, num_examples, row_bytes, rank=0, world=1, device=None, bind=True,
+                 hbm_rows=None, host_rows=0):
         h = c_void_p()
         check(lib.af_cache_create(int(num_examples), int(row_bytes), int(rank), int(world), byref(h)),
               "af_cache_create")
         self._h = h
         self.num_examples, self.row_bytes, self.rank, self.world = int(num_examples), int(row_bytes), rank, world
-        p, m = c_size_t(), c_size_t()
+        self.tiered = hbm_rows is not None or host_rows
+        if self.tiered:
+            check(lib.af_cache_set_capacity(h, int(hbm_rows or 0), int(host_rows)), "af_cache_set_capacity")
+        p, m, hb = c_size_t(), c_size_t(), c_size_t()
         check(lib.af_cache_storage_bytes(h, byref(p), byref(m)), "af_cache_storage_bytes")
-        self.payload_bytes, self.meta_bytes = p.value, m.value
-        self.payload = self.meta = None
+        check(lib.af_cache_host_bytes(h, byref(hb)), "af_cache_host_bytes")
+        self.payload_bytes, self.meta_bytes, self.host_bytes = p.value, m.value, hb.value
+        self.payload = self.meta = self.host_tier = None
         if bind:
             self.bind(device)
 
@@ -197,6 +207,9 @@ class ActivationCache:
             self.meta = torch.empty(self.meta_bytes, dtype=torch.uint8, device=dev)
             check(lib.af_cache_bind(self._h, c_void_p(self.payload.data_ptr()), c_void_p(self.meta.data_ptr())),
                   "af_cache_bind")
+            if self.host_bytes:
+                self.host_tier = torch.empty(self.host_bytes, dtype=torch.uint8, pin_memory=True)
+                check(lib.af_cache_bind_host(self._h, c_void_p(self.host_tier.data_ptr())), "af_cache_bind_host")
 
     def put(self, ids, rows, depth, stream=None):
         n = int(ids.numel())
@@ -209,10 +222,23 @@ class ActivationCache:
                                c_void_p(rows_out.data_ptr()), c_void_p(depth_out.data_ptr()),
                                _stream_handle(stream)), "af_cache_get")
 
+    def get_async(self, ids, cur_boundary, rows_out, depth_out, stream):
+        """Prefetch (the paper's reader process, Fig. 8): enqueue the get on a side
+        stream and return an event the consumer stream waits on."""
+        self.get(ids, cur_boundary, rows_out, depth_out, stream=stream)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return ev
+
     def status(self):
         e, v = c_uint32(), c_int64()
         check(lib.af_cache_status(self._h, byref(e), byref(v)), "af_cache_status")
         return e.value, v.value
+
+    def stats(self):
+        i = L.AfCacheInfo()
+        check(lib.af_cache_stats(self._h, byref(i)), "af_cache_stats")
+        return {k: getattr(i, k) for k, _ in L.AfCacheInfo._fields_ if k != "pad"}
 
     def close(self):
         if getattr(self, "_h", None):
@@ -224,6 +250,28 @@ class ActivationCache:
             self.close()
         except Exception:
             pass
+
+
+def calibrate_read_seconds(row_bytes, batch_rows, device=None, reps=10):
+    """Measured time to read one cached batch (af_cache_get of batch_rows hits) on
+    this device: the t_batch_read of the cache-vs-recompute rule (PAPER.md:230-235:
+    "few iterations of training can indicate how many layers ... need to be frozen
+    before caching becomes advantageous")."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    c = ActivationCache(batch_rows, row_bytes, device=dev)
+    ids = torch.arange(batch_rows, device=dev, dtype=torch.int64)
+    rows = torch.zeros((batch_rows, row_bytes), dtype=torch.uint8, device=dev)
+    out = torch.empty_like(rows)
+    dep = torch.empty(batch_rows, dtype=torch.int32, device=dev)
+    c.put(ids, rows, 1)
+    c.get(ids, 1, out, dep)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        c.get(ids, 1, out, dep)
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / reps * 1e-3
 
 
 def bootstrap_nccl_id(rank, group=None, device=None):

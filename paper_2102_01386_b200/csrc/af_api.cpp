@@ -96,15 +96,29 @@ struct af_ctx {
 };
 
 struct af_cache {
-  int64_t num_examples = 0, row_bytes = 0, capacity = 0;
+  int64_t num_examples = 0, row_bytes = 0;
+  int64_t capacity = 0;  // owned ids of this rank (the partition size D_local)
   int32_t rank = 0, world = 1;
+  // tiered mode (af_cache_set_capacity): I = hbm_rows + host_rows < D slots
+  bool tiered = false;
+  int64_t hbm_rows = 0, host_rows = 0;
+  int32_t max_batch = 65536;  // rows per plan pass (larger calls are split)
   char *payload = nullptr;
-  char *meta = nullptr;  // [err | pad to 256 B][CacheMeta x capacity]
-  bool bound = false;
+  char *meta = nullptr;  // [CacheHeader | pad to 256 B][CacheMeta x capacity][free x I][rowslot x max_batch]
+  char *host = nullptr;  // device alias of the page-locked host tier
+  bool bound = false, host_bound = false;
   int grid = 0;
+  size_t meta_bytes() const {
+    size_t b = kMetaHeaderBytes + static_cast<size_t>(capacity) * sizeof(CacheMeta);
+    if (tiered) b += static_cast<size_t>(hbm_rows + host_rows) * 4 + static_cast<size_t>(max_batch) * 4;
+    return b;
+  }
+  size_t o_free() const { return kMetaHeaderBytes + static_cast<size_t>(capacity) * sizeof(CacheMeta); }
+  size_t o_rowslot() const { return o_free() + static_cast<size_t>(hbm_rows + host_rows) * 4; }
+  static constexpr size_t kMetaHeaderBytes = 256;
 };
 
-static constexpr size_t kMetaHeader = 256;
+static constexpr size_t kMetaHeader = af_cache::kMetaHeaderBytes;
 
 extern "C" {
 
@@ -682,15 +696,49 @@ af_status af_cache_create(int64_t num_examples, int64_t row_bytes, int32_t rank,
   return AF_OK;
 }
 
+af_status af_cache_set_capacity(af_cache *c, int64_t hbm_rows, int64_t host_rows) {
+  if (!c) return fail(AF_EINVAL, "NULL cache");
+  if (c->bound) return fail(AF_ESTATE, "set the capacity before binding storage");
+  if (hbm_rows < 0 || host_rows < 0 || hbm_rows + host_rows < 1) return fail(AF_EINVAL, "bad capacity");
+  if (hbm_rows + host_rows > (int64_t(1) << 31) - 1) return fail(AF_ERANGE, "capacity too large");
+  c->tiered = true;
+  c->hbm_rows = hbm_rows;
+  c->host_rows = host_rows;
+  return AF_OK;
+}
+
 af_status af_cache_storage_bytes(const af_cache *c, size_t *payload_bytes, size_t *meta_bytes) {
   if (!c || !payload_bytes || !meta_bytes) return fail(AF_EINVAL, "NULL argument");
-  *payload_bytes = static_cast<size_t>(c->capacity) * static_cast<size_t>(c->row_bytes);
-  *meta_bytes = kMetaHeader + static_cast<size_t>(c->capacity) * sizeof(CacheMeta);
+  const int64_t rows = c->tiered ? c->hbm_rows : c->capacity;
+  *payload_bytes = static_cast<size_t>(rows) * static_cast<size_t>(c->row_bytes);
+  *meta_bytes = c->meta_bytes();
+  return AF_OK;
+}
+
+af_status af_cache_host_bytes(const af_cache *c, size_t *host_bytes) {
+  if (!c || !host_bytes) return fail(AF_EINVAL, "NULL argument");
+  *host_bytes = static_cast<size_t>(c->tiered ? c->host_rows : 0) * static_cast<size_t>(c->row_bytes);
+  return AF_OK;
+}
+
+af_status af_cache_bind_host(af_cache *c, void *host_pinned) {
+  if (!c || !host_pinned) return fail(AF_EINVAL, "NULL argument");
+  if (!c->tiered || c->host_rows == 0) return fail(AF_ESTATE, "no host tier configured");
+  if (!aligned(host_pinned, 16)) return fail(AF_EINVAL, "host tier must be 16-byte aligned");
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, host_pinned);
+  if (e != cudaSuccess || a.type != cudaMemoryTypeHost || !a.devicePointer) {
+    cudaGetLastError();
+    return fail(AF_EINVAL, "host tier must be page-locked, device-mapped memory (cudaHostAlloc / pin_memory)");
+  }
+  c->host = static_cast<char *>(a.devicePointer);
+  c->host_bound = true;
   return AF_OK;
 }
 
 af_status af_cache_bind(af_cache *c, void *payload_dev, void *meta_dev) {
-  if (!c || !meta_dev || (c->capacity > 0 && !payload_dev)) return fail(AF_EINVAL, "NULL argument");
+  const int64_t rows = c ? (c->tiered ? c->hbm_rows : c->capacity) : 0;
+  if (!c || !meta_dev || (rows > 0 && !payload_dev)) return fail(AF_EINVAL, "NULL argument");
   if ((payload_dev && !aligned(payload_dev, 16)) || !aligned(meta_dev, 256))
     return fail(AF_EINVAL, "payload must be 16-byte and meta 256-byte aligned");
   int sms = 0;
@@ -699,8 +747,17 @@ af_status af_cache_bind(af_cache *c, void *payload_dev, void *meta_dev) {
   c->grid = std::max(1, sms);
   c->payload = static_cast<char *>(payload_dev);
   c->meta = static_cast<char *>(meta_dev);
-  AF_CUDA(cudaMemset(c->meta, 0, kMetaHeader + static_cast<size_t>(c->capacity) * sizeof(CacheMeta)),
-          "cudaMemset(meta)");
+  AF_CUDA(cudaMemset(c->meta, 0, c->meta_bytes()), "cudaMemset(meta)");
+  if (c->tiered) {
+    // every record slot free: the stack pops slot 0 first (HBM before host)
+    const int32_t I = static_cast<int32_t>(c->hbm_rows + c->host_rows);
+    std::vector<int32_t> fr(static_cast<size_t>(I));
+    for (int32_t k = 0; k < I; ++k) fr[k] = I - 1 - k;
+    AF_CUDA(cudaMemcpy(c->meta + c->o_free(), fr.data(), fr.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy(free)");
+    CacheHeader h{};
+    h.top = I;
+    AF_CUDA(cudaMemcpy(c->meta, &h, sizeof(h), cudaMemcpyHostToDevice), "cudaMemcpy(header)");
+  }
   AF_CUDA(cudaDeviceSynchronize(), "cache bind");
   c->bound = true;
   return AF_OK;
@@ -725,6 +782,43 @@ static af_status cache_common(af_cache *c, const int64_t *ids, int32_t n, const 
   return AF_OK;
 }
 
+static af_status cache_tiered(af_cache *c, CacheParams &p, bool put, void *stream) {
+  if (c->host_rows > 0 && !c->host_bound) return fail(AF_EWORKSPACE, "host tier not bound (af_cache_bind_host)");
+  const int32_t n_all = p.n;
+  for (int32_t b0 = 0; b0 < n_all; b0 += c->max_batch) {
+    const int32_t n = std::min(c->max_batch, n_all - b0);
+    CachePlanParams q{};
+    q.meta = p.meta;
+    q.hdr = reinterpret_cast<CacheHeader *>(c->meta);
+    q.free_slots = reinterpret_cast<int32_t *>(c->meta + c->o_free());
+    q.rowslot = reinterpret_cast<int32_t *>(c->meta + c->o_rowslot());
+    q.ids = p.ids + b0;
+    q.n = n;
+    q.put = put ? 1 : 0;
+    q.depth = p.depth;
+    q.cur_boundary = p.cur_boundary;
+    q.depth_out = put ? nullptr : p.depth_out + b0;
+    q.num_examples = c->num_examples;
+    q.rank = c->rank;
+    q.world = c->world;
+    int e = launch_cache_plan(q, stream);
+    if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache plan launch");
+    CacheParams r = p;
+    r.ids = p.ids + b0;
+    r.n = n;
+    r.rowslot = q.rowslot;
+    r.host = c->host;
+    r.hbm_rows = c->hbm_rows;
+    if (put)
+      r.src_rows = p.src_rows + static_cast<int64_t>(b0) * c->row_bytes;
+    else
+      r.dst_rows = p.dst_rows + static_cast<int64_t>(b0) * c->row_bytes;
+    e = put ? launch_cache_put(r, c->grid, stream) : launch_cache_get(r, c->grid, stream);
+    if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache copy launch");
+  }
+  return AF_OK;
+}
+
 af_status af_cache_put(af_cache *c, const int64_t *ids_dev, int32_t n, const void *rows_dev, int32_t depth,
                        void *stream) {
   CacheParams p;
@@ -734,6 +828,7 @@ af_status af_cache_put(af_cache *c, const int64_t *ids_dev, int32_t n, const voi
   if (n == 0) return AF_OK;
   p.src_rows = static_cast<const char *>(rows_dev);
   p.depth = depth;
+  if (c->tiered) return cache_tiered(c, p, true, stream);
   const int e = launch_cache_put(p, c->grid, stream);
   if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache put launch");
   return AF_OK;
@@ -750,8 +845,36 @@ af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t c
   p.dst_rows = static_cast<char *>(rows_out_dev);
   p.depth_out = depth_out_dev;
   p.cur_boundary = cur_boundary;
+  if (c->tiered) return cache_tiered(c, p, false, stream);
   const int e = launch_cache_get(p, c->grid, stream);
   if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache get launch");
+  return AF_OK;
+}
+
+af_status af_cache_stats(af_cache *c, af_cache_info *out) {
+  if (!c || !out) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
+  AF_CUDA(cudaDeviceSynchronize(), "cache stats sync");
+  CacheHeader h{};
+  AF_CUDA(cudaMemcpy(&h, c->meta, sizeof(h), cudaMemcpyDeviceToHost), "cudaMemcpy(header)");
+  std::vector<CacheMeta> m(static_cast<size_t>(c->capacity));
+  if (c->capacity)
+    AF_CUDA(cudaMemcpy(m.data(), c->meta + kMetaHeader, m.size() * sizeof(CacheMeta), cudaMemcpyDeviceToHost),
+            "cudaMemcpy(meta)");
+  std::memset(out, 0, sizeof(*out));
+  out->error_flags = h.err;
+  out->partition = c->capacity;
+  out->capacity = c->tiered ? c->hbm_rows + c->host_rows : c->capacity;
+  for (const auto &x : m) {
+    if (!x.valid) continue;
+    out->n_valid++;
+    if (c->tiered && x.slot >= c->hbm_rows)
+      out->n_host++;
+    else
+      out->n_hbm++;
+  }
+  out->n_dropped = c->tiered ? h.dropped : 0;
+  out->free_slots = c->tiered ? h.top : c->capacity - out->n_valid;
   return AF_OK;
 }
 
@@ -760,7 +883,7 @@ af_status af_cache_status(af_cache *c, uint32_t *device_error_flags, int64_t *n_
   if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
   AF_CUDA(cudaDeviceSynchronize(), "cache status sync");
   unsigned int err = 0;
-  AF_CUDA(cudaMemcpy(&err, c->meta, sizeof(err), cudaMemcpyDeviceToHost), "cudaMemcpy(err)");
+  AF_CUDA(cudaMemcpy(&err, c->meta, sizeof(err), cudaMemcpyDeviceToHost), "cudaMemcpy(err)");  // CacheHeader.err
   *device_error_flags = err;
   if (n_valid) {
     std::vector<CacheMeta> m(static_cast<size_t>(c->capacity));

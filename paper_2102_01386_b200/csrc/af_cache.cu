@@ -157,7 +157,23 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
       const int64_t off = static_cast<int64_t>(c) * p.chunk_bytes;
       const int64_t rem = p.row_bytes - off;
       dsc.bytes = static_cast<uint32_t>(rem < p.chunk_bytes ? rem : p.chunk_bytes);
-      if (ok) {
+      if (ok && p.rowslot) {
+        // tiered: the plan kernel resolved the row's slot (and its meta / eviction)
+        const int32_t slot = p.rowslot[i];
+        if (slot >= 0) {
+          char *rec = (slot < p.hbm_rows ? p.payload + static_cast<int64_t>(slot) * p.row_bytes
+                                         : p.host + (static_cast<int64_t>(slot) - p.hbm_rows) * p.row_bytes) +
+                      off;
+          if (PUT) {
+            dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+            dsc.dst = rec;
+          } else {
+            dsc.src = rec;
+            dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+          }
+          dsc.ok = 1u;
+        }
+      } else if (ok) {
         const int64_t slot = id / p.world;
         char *rec = p.payload + slot * p.row_bytes + off;
         if (PUT) {
@@ -182,8 +198,8 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
             }
           }
         }
-      } else if (!PUT && c == 0) {
-        p.depth_out[i] = -1;
+      } else if (!PUT && c == 0 && !p.rowslot) {
+        p.depth_out[i] = -1;  // (tiered: the plan kernel wrote depth_out)
       }
       descs[q] = dsc;
     }
@@ -193,6 +209,115 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
   }
   pdl_launch_dependents();
   if (lane == 0) bulk_wait_all();  // all stores complete before the CTA retires its shared memory
+}
+
+
+// Tiered-mode plan (one CTA, 1024 threads): resolves every row of the call in call
+// order with block-wide exclusive scans, so slot allocation and freeing are
+// deterministic.  put: existing record -> its slot (re-cache deeper); new id ->
+// the next free slot (HBM slots are handed out first), or dropped when none is
+// left (drop-newest; the store never exceeds its capacity).  get:
+// hit -> depth_out and the slot; hits with depth < cur_boundary are evicted and
+// their slots pushed back (P:277 re-cache balance).
+constexpr int kPlanThreads = 1024;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int *s_warp, int &total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = (lane < kPlanThreads / 32) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= o) w += y;
+    }
+    s_warp[lane] = w;  // inclusive warp prefix
+  }
+  __syncthreads();
+  const int before = (warp > 0 ? s_warp[warp - 1] : 0) + x - v;
+  total = s_warp[kPlanThreads / 32 - 1];
+  __syncthreads();
+  return before;
+}
+
+__global__ void __launch_bounds__(kPlanThreads) cache_plan_kernel(const CachePlanParams p) {
+  __shared__ int s_warp[32];
+  __shared__ int s_top;
+  __shared__ unsigned int s_dropped;
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    s_top = p.hdr->top;
+    s_dropped = 0u;
+  }
+  __syncthreads();
+  for (int base = 0; base < p.n; base += kPlanThreads) {
+    const int i = base + threadIdx.x;
+    int need = 0, slot = -1;
+    int64_t lid = -1;
+    int4 m = make_int4(0, 0, 0, -1);
+    if (i < p.n) {
+      const int64_t id = p.ids[i];
+      if (id < 0 || id >= p.num_examples) {
+        atomicOr(&p.hdr->err, AF_CACHE_ERR_RANGE);
+      } else if (id % p.world != p.rank) {
+        atomicOr(&p.hdr->err, AF_CACHE_ERR_OWNER);
+      } else {
+        lid = id / p.world;
+        m = __ldcg(reinterpret_cast<const int4 *>(p.meta) + lid);
+        if (p.put) {
+          if (m.y) slot = m.w;
+          else need = 1;
+        } else {
+          if (m.y) {
+            slot = m.w;
+            p.depth_out[i] = m.x;
+            need = (m.x < p.cur_boundary) ? 1 : 0;
+          } else {
+            p.depth_out[i] = -1;
+          }
+        }
+      }
+    }
+    int total = 0;
+    const int k = block_exclusive_scan(need, s_warp, total);
+    const int top = s_top;
+    if (i < p.n) {
+      if (p.put) {
+        if (need) slot = (k < top) ? p.free_slots[top - 1 - k] : -1;
+        p.rowslot[i] = slot;
+        if (slot >= 0) reinterpret_cast<int4 *>(p.meta)[lid] = make_int4(p.depth, 1, 0, slot);
+      } else {
+        p.rowslot[i] = slot;
+        if (need) {
+          p.free_slots[top + k] = slot;
+          reinterpret_cast<int4 *>(p.meta)[lid] = make_int4(m.x, 0, 0, -1);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (p.put) {
+        const int got = total < top ? total : top;
+        s_dropped += static_cast<unsigned int>(total - got);
+        s_top = top - got;
+      } else {
+        s_top = top + total;
+      }
+    }
+    __syncthreads();
+  }
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    p.hdr->top = s_top;
+    p.hdr->dropped += s_dropped;
+  }
 }
 
 }  // namespace
@@ -222,4 +347,11 @@ static int launch_cache(const CacheParams &p0, int grid, void *stream) {
 int launch_cache_put(const CacheParams &p, int grid, void *stream) { return launch_cache<true>(p, grid, stream); }
 int launch_cache_get(const CacheParams &p, int grid, void *stream) { return launch_cache<false>(p, grid, stream); }
 
+}  // namespace af
+
+namespace af {
+int launch_cache_plan(const CachePlanParams &p, void *stream) {
+  return static_cast<int>(launch_pdl(cache_plan_kernel, dim3(1), dim3(kPlanThreads), 0,
+                                     static_cast<cudaStream_t>(stream), p));
+}
 }  // namespace af

@@ -102,13 +102,23 @@ struct NormParams {
   DecideParams dec;
 };
 
-// Cache records: one 16-byte meta word per slot.  `readers` counts the chunks
-// of a get that have read {depth, valid}; the last one applies the eviction.
+// Cache records: one 16-byte meta word per owned id.  Direct mode: `readers`
+// counts the chunks of a get that have read {depth, valid}; the last one applies
+// the eviction.  Tiered mode: `slot` is the record's storage slot (HBM slots
+// first, then page-locked host slots), assigned by the plan kernel.
 struct CacheMeta {
   int32_t depth;
   int32_t valid;
   uint32_t readers;
-  uint32_t pad;
+  int32_t slot;
+};
+
+// Tiered cache header words (after the sticky error word at offset 0).
+struct CacheHeader {
+  unsigned int err;       // sticky AF_CACHE_ERR_* flags
+  int32_t top;            // free-slot stack height
+  unsigned int dropped;   // puts of new ids refused because every slot was taken
+  unsigned int pad;
 };
 static_assert(sizeof(CacheMeta) == 16, "cache meta layout");
 
@@ -128,6 +138,25 @@ struct CacheParams {
   int32_t *depth_out;       // get
   int32_t depth;            // put
   int32_t cur_boundary;     // get
+  // tiered mode (rowslot != nullptr): the plan kernel already resolved each row's slot
+  const int32_t *rowslot;   // [n] slot per row of the call, -1 = skip
+  char *host;               // device alias of the page-locked host tier
+  int64_t hbm_rows;         // slots [0, hbm_rows) in `payload`, the rest in `host`
+};
+
+struct CachePlanParams {
+  CacheMeta *meta;
+  CacheHeader *hdr;
+  int32_t *free_slots;      // [hbm_rows + host_rows] stack
+  int32_t *rowslot;         // [n] out
+  const int64_t *ids;
+  int32_t n;
+  int32_t put;              // 1: put (allocate), 0: get (hit, depth, evict)
+  int32_t depth;
+  int32_t cur_boundary;
+  int32_t *depth_out;
+  int64_t num_examples;
+  int32_t rank, world;
 };
 
 #ifdef __CUDACC__
@@ -160,6 +189,7 @@ int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *
 int launch_decide(const DecideParams &p, void *stream);
 int launch_cache_put(const CacheParams &p, int grid, void *stream);
 int launch_cache_get(const CacheParams &p, int grid, void *stream);
+int launch_cache_plan(const CachePlanParams &p, void *stream);
 int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks);
 int cache_smem_bytes();
 

@@ -448,3 +448,64 @@ def test_peer_exchange_ranks_on_one_gpu(P, fused):
     each other's memory inside the interval-end kernel; identical decisions on all
     ranks, oracle parity."""
     _run_peer_ranks(P, fused)
+
+
+# ---------------------------------------------------------------- tiered cache with admission (NEXT 3)
+
+def test_cache_admission_printed_example_gpu():
+    """D = 100, room for I = 60 -> exactly 60 stored, 40 dropped."""
+    import paper_2102_01386_b200 as af
+    gc = af.ActivationCache(100, 64, hbm_rows=40, host_rows=20)
+    oc = O.Cache(100, 64, capacity=60)
+    rows = torch.randint(0, 256, (100, 64), dtype=torch.uint8, device="cuda")
+    gc.put(_ids(np.arange(100)), rows, 1)
+    oc.put(np.arange(100), rows.cpu().numpy(), 1)
+    st = gc.stats()
+    assert st["n_valid"] == len(oc.store) == 60 and st["n_dropped"] == oc.dropped == 40
+    assert st["n_hbm"] == 40 and st["n_host"] == 20 and st["free_slots"] == 0
+    out = torch.zeros_like(rows)
+    dep = torch.zeros(100, dtype=torch.int32, device="cuda")
+    gc.get(_ids(np.arange(100)), 1, out, dep)
+    oo = np.zeros((100, 64), np.uint8)
+    do = oc.get(np.arange(100), 1, oo)
+    assert np.array_equal(dep.cpu().numpy(), do) and np.array_equal(out.cpu().numpy(), oo)
+
+
+@pytest.mark.parametrize("rank,world,hbm,host", [(0, 1, 300, 200), (2, 4, 100, 150), (0, 1, 0, 400)])
+def test_tiered_cache_epochs_match_oracle(rank, world, hbm, host):
+    """Scripted epochs with boundary changes: evict-on-read frees slots that the
+    re-cache of the same epoch reuses; drops, depths and bytes match the oracle."""
+    import paper_2102_01386_b200 as af
+    from afinputs import cache_rows, epoch_permutation, rank_ids
+    num, rb = 3000, 1024 + 16
+    gc = af.ActivationCache(num, rb, rank=rank, world=world, hbm_rows=hbm, host_rows=host)
+    oc = O.Cache(num, rb, rank, world, capacity=hbm + host)
+    mine = rank_ids(num, rank, world)
+    for epoch, (depth, bnd) in enumerate([(4, 4), (4, 7), (7, 7), (7, 9)]):
+        perm = epoch_permutation(1, epoch, mine)
+        for b0 in range(0, len(perm), 113):
+            ids = perm[b0:b0 + 113]
+            out_g = torch.full((len(ids), rb), 3, dtype=torch.uint8, device="cuda")
+            dep_g = torch.zeros(len(ids), dtype=torch.int32, device="cuda")
+            gc.get(_ids(ids), bnd, out_g, dep_g)
+            out_o = np.full((len(ids), rb), 3, np.uint8)
+            dep_o = oc.get(ids, bnd, out_o)
+            assert np.array_equal(dep_g.cpu().numpy(), dep_o)
+            assert np.array_equal(out_g.cpu().numpy(), out_o)
+            miss = ids[dep_o < 0]
+            if len(miss):
+                rows = cache_rows(epoch, b0, len(miss), rb)
+                gc.put(_ids(miss), torch.from_numpy(rows).cuda(), depth)
+                oc.put(miss, rows, depth)
+        st = gc.stats()
+        assert st["n_valid"] == len(oc.store) and st["n_dropped"] == oc.dropped, (epoch, st, oc.dropped)
+        assert st["n_valid"] <= hbm + host and st["n_hbm"] <= hbm and st["n_host"] <= host
+        assert st["n_valid"] + st["free_slots"] == hbm + host
+    assert oc.dropped > 0                                   # admission was exercised
+
+
+def test_calibrate_read_seconds_and_should_cache():
+    import paper_2102_01386_b200 as af
+    t = af.calibrate_read_seconds(196_608, 256)
+    assert 1e-6 < t < 1e-2
+    assert af.should_cache(3, 0.011, t) and not af.should_cache(0, 0.011, t)

@@ -353,3 +353,38 @@ def test_cache_owner_partition():
     c.put([1, 5, 2, 11], np.zeros((4, 16), np.uint8), 1)
     assert c.error_flags == O.CACHE_ERR_OWNER | O.CACHE_ERR_RANGE
     assert sorted(c.store) == [1, 5]
+
+
+def test_cache_admission_printed_example():
+    # S:276 [PAPER P:276]: D = 100 records, room for I = 60 -> exactly 60 stored,
+    # the rest dropped without error (drop-newest in call order).
+    c = O.Cache(100, 16, capacity=60)
+    rows = np.zeros((100, 16), np.uint8)
+    c.put(np.arange(100), rows, 1)
+    assert len(c.store) == 60 and c.dropped == 40
+    assert sorted(c.store) == list(range(60))
+
+
+def test_cache_capacity_and_recache_balance_invariants():
+    # capacity never exceeded; during a deepening epoch the records
+    # written never exceed those evicted on read plus the initial free room.
+    rng = np.random.default_rng(0)
+    D, I = 500, 200
+    c = O.Cache(D, 16, capacity=I)
+    ids = rng.permutation(D)
+    c.put(ids, np.zeros((D, 16), np.uint8), 2)
+    assert len(c.store) == I
+    free0 = I - len(c.store)
+    evicted = written = 0
+    for b0 in range(0, D, 50):
+        batch = rng.permutation(D)[b0:b0 + 50]
+        out = np.zeros((len(batch), 16), np.uint8)
+        before = len(c.store)
+        d = c.get(batch, 5, out)                      # boundary 2 -> 5: hits are evicted
+        evicted += before - len(c.store)
+        miss = batch[d < 0]
+        n_before = len(c.store)
+        c.put(batch, np.ones((len(batch), 16), np.uint8), 5)
+        written += len(c.store) - n_before
+        assert len(c.store) <= I
+        assert written <= evicted + free0
