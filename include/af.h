@@ -225,6 +225,27 @@ AF_API af_status af_update_and_decide(af_ctx *ctx, uint32_t flags, af_decision *
 AF_API af_status af_interval_end(af_ctx *ctx, const void *grad_dev, uint32_t flags, af_decision *out_host,
                                  void *stream);
 
+/* AdamW hyper-parameters of one optimizer step (step = t >= 1 for the bias corrections). */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;
+  int32_t step;
+} af_adamw;
+
+/* the Delta accumulate fused into the optimizer that
+ * already reads g.  One pass over this rank's shard of the active segments:
+ * AdamW (decoupled weight decay; fp32, round-to-nearest, in the order
+ *   p <- p*(1-lr*wd); m <- m*b1 + g*(1-b1); v <- v*b2 + (g*g)*(1-b2);
+ *   p <- p - (lr/(1-b1^t)) * (m / (sqrt(v)/sqrt(1-b2^t) + eps)) )
+ * on params/exp_avg/exp_avg_sq (FULL flat fp32 buffers, n_total elements, 16-byte
+ * aligned; frozen segments are not touched -- requires_grad=False), and either
+ * Delta += g (flags = 0) or, with AF_INTERVAL_END, the interval end of
+ * af_interval_end (sums of squares of Delta + g, exchange, decision, record) in
+ * the same kernel.  Saves the separate read of g per step (s_g bytes per element).
+ * With world > 1 the caller all-gathers the updated parameter shards (ZeRO-1). */
+AF_API af_status af_adamw_step(af_ctx *ctx, float *params_dev, float *exp_avg_dev, float *exp_avg_sq_dev,
+                               const void *grad_dev, const af_adamw *hp, uint32_t flags, af_decision *out_host,
+                               void *stream);
+
 /* Synchronous.  Serialise / restore {T, f, prev norms, Delta-armed flag}
  * (checkpoint at interval boundaries is exact).  With buf == NULL, get_state
  * stores the required size in *len. */

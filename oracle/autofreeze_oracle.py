@@ -48,6 +48,7 @@ __all__ = [
     "FLAG_DRY_RUN", "CACHE_ERR_RANGE", "CACHE_ERR_OWNER", "MISS",
     "widen", "accumulate", "segment_sumsq", "layer_norm", "eta", "percentile_threshold",
     "prefix_scan", "should_cache", "active_segments", "Freezer", "Cache", "OracleStateError",
+    "adamw_constants", "adamw_step",
 ]
 
 SEG_PRE, SEG_POOL, SEG_HEAD = 0, 1, 2
@@ -156,6 +157,31 @@ def active_segments(kinds, f):
         else:
             out.append(l)
     return out
+
+
+# ---------------------------------------------------------------- optimizer (NEXT 1 fusion)
+
+def adamw_constants(lr, beta1, beta2, eps, weight_decay, step):
+    """The fp32 constants of one AdamW step, each computed in fp64 from the fp32
+    hyper-parameters and rounded once (the ABI's af_adamw_step contract).
+    Reading: the paper fine-tunes BERT with PyTorch and names only the
+    LR schedule; AdamW with decoupled weight decay is BERT's optimizer."""
+    f32 = np.float32
+    lr, b1, b2, eps, wd = (float(f32(x)) for x in (lr, beta1, beta2, eps, weight_decay))
+    return dict(decay=f32(1.0 - lr * wd), beta1=f32(b1), omb1=f32(1.0 - b1), beta2=f32(b2), omb2=f32(1.0 - b2),
+                step_size=f32(lr / (1.0 - b1 ** step)), sqrt_bc2=f32(math.sqrt(1.0 - b2 ** step)), eps=f32(eps))
+
+
+def adamw_step(p, m, v, g32, c):
+    """AdamW (Loshchilov & Hutter; PyTorch's order: decay, moments, bias-corrected
+    update) in fp32, one IEEE rounding per operation, no fused multiply-add:
+      p <- p*decay; m <- m*b1 + g*(1-b1); v <- v*b2 + (g*g)*(1-b2)
+      p <- p - step_size * (m / (sqrt(v)/sqrt_bc2 + eps))       (in place)"""
+    p *= c["decay"]
+    m[...] = m * c["beta1"] + g32 * c["omb1"]
+    v[...] = v * c["beta2"] + (g32 * g32) * c["omb2"]
+    den = np.sqrt(v) / c["sqrt_bc2"] + c["eps"]
+    p -= c["step_size"] * (m / den)
 
 
 # ---------------------------------------------------------------- freezing module
@@ -278,6 +304,14 @@ class Freezer:
         if not dry_run:
             self.pending = None
         return rec
+
+    def adamw_active(self, p, m, v, g, c):
+        """The optimizer step restricted to the active segments (frozen layers have
+        requires_grad=False and are not updated, P:33)."""
+        g32 = widen(g, self.grad_dtype)
+        for l in active_segments(self.kinds, self.f):
+            lo, hi = self.seg(l)
+            adamw_step(p[lo:hi], m[lo:hi], v[lo:hi], g32[lo:hi], c)
 
     # convenience for whole-trace tests
     def run_interval(self, grads):

@@ -49,6 +49,11 @@ class AfInfo(ctypes.Structure):
                 ("n_tiles_acc", c_int32), ("tile_elems_acc", c_int32)]
 
 
+class AfAdamW(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
+                ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float), ("step", c_int32)]
+
+
 class AfCacheInfo(ctypes.Structure):
     _fields_ = [("error_flags", c_uint32), ("pad", c_uint32), ("partition", c_int64), ("capacity", c_int64),
                 ("n_valid", c_int64), ("n_hbm", c_int64), ("n_host", c_int64), ("n_dropped", c_int64),
@@ -70,6 +75,8 @@ SIGNATURES = {
     "af_layer_norms": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p]),
     "af_update_and_decide": (c_int, [c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_interval_end": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p, c_void_p]),
+    "af_adamw_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(AfAdamW), c_uint32,
+                              c_void_p, c_void_p]),
     "af_get_state": (c_int, [c_void_p, c_void_p, POINTER(c_size_t)]),
     "af_set_state": (c_int, [c_void_p, c_void_p, c_size_t]),
     "af_ctx_destroy": (c_int, [c_void_p]),

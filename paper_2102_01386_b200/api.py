@@ -143,6 +143,19 @@ class FreezingModule:
         if copy_record and not torch.cuda.is_current_stream_capturing():
             self._event.record(stream if stream is not None else torch.cuda.current_stream())
 
+    def adamw_step(self, params, exp_avg, exp_avg_sq, grad, lr, step, beta1=0.9, beta2=0.999, eps=1e-8,
+                   weight_decay=0.0, interval_end=False, dry_run=False, stream=None, copy_record=True):
+        """af_adamw_step: AdamW on this rank's shard fused with the Delta accumulate
+        (or, with interval_end=True, with the whole interval end and decision)."""
+        hp = L.AfAdamW(float(lr), float(beta1), float(beta2), float(eps), float(weight_decay), int(step))
+        flags = (L.AF_INTERVAL_END if interval_end else 0) | (L.AF_DRY_RUN if dry_run else 0)
+        out = c_void_p(self._rec_host.data_ptr()) if (copy_record and interval_end) else c_void_p(0)
+        check(lib.af_adamw_step(self._h, c_void_p(params.data_ptr()), c_void_p(exp_avg.data_ptr()),
+                                c_void_p(exp_avg_sq.data_ptr()), c_void_p(grad.data_ptr()), byref(hp), flags, out,
+                                _stream_handle(stream)), "af_adamw_step")
+        if interval_end and copy_record and not torch.cuda.is_current_stream_capturing():
+            self._event.record(stream if stream is not None else torch.cuda.current_stream())
+
     def decision(self):
         """The last copied decision record (waits for the stream to reach it)."""
         self._event.synchronize()

@@ -79,7 +79,7 @@ struct af_ctx {
   float *accum = nullptr;
   char *scratch = nullptr;
   bool bound = false;
-  int grid[3] = {0, 0, 0};  // persistent grid per streaming-kernel mode (occupancy x SMs)
+  int grid[kNumModes] = {0, 0, 0, 0, 0};  // persistent grid per streaming-kernel mode (occupancy x SMs)
   // host flags
   bool armed = false;    // Delta / ss_acc hold this interval's partial sum
   bool pending = false;  // an interval end awaits af_update_and_decide
@@ -295,7 +295,7 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
   int sms = 0;
   cudaError_t e = static_cast<cudaError_t>(device_sm_count(&sms));
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
-  for (int m = 0; m < 3; ++m) {
+  for (int m = 0; m < kNumModes; ++m) {
     int bps = 0;
     e = static_cast<cudaError_t>(norms_max_blocks_per_sm(m, c->dtype, &bps));
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
@@ -470,6 +470,62 @@ af_status af_layer_norms(af_ctx *c, const void *grad_dev, uint32_t flags, void *
   }
   if (!dry) c->armed = !end;
   if (end) c->pending = true;
+  return AF_OK;
+}
+
+af_status af_adamw_step(af_ctx *c, float *params_dev, float *exp_avg_dev, float *exp_avg_sq_dev,
+                        const void *grad_dev, const af_adamw *hp, uint32_t flags, af_decision *out_host,
+                        void *stream) {
+  af_status st = check_norm_args(c, grad_dev);
+  if (st != AF_OK) return st;
+  if (!hp || !params_dev || !exp_avg_dev || !exp_avg_sq_dev) return fail(AF_EINVAL, "NULL argument");
+  if (!aligned(params_dev, 16) || !aligned(exp_avg_dev, 16) || !aligned(exp_avg_sq_dev, 16))
+    return fail(AF_EINVAL, "optimizer buffers must be 16-byte aligned");
+  if (c->cfg.acc_mode != AF_ACC_DELTA) return fail(AF_ESTATE, "af_adamw_step needs acc_mode AF_ACC_DELTA");
+  if (flags & ~(AF_INTERVAL_END | AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
+  if (hp->step < 1 || !(hp->beta1 >= 0.f && hp->beta1 < 1.f) || !(hp->beta2 >= 0.f && hp->beta2 < 1.f) ||
+      !(hp->eps > 0.f) || !(hp->lr >= 0.f) || !(hp->weight_decay >= 0.f))
+    return fail(AF_EINVAL, "bad AdamW hyper-parameters");
+  const bool end = flags & AF_INTERVAL_END, dry = flags & AF_DRY_RUN;
+  if (end && c->cfg.world > 1 && !c->peers && !c->comm)
+    return fail(AF_ESTATE, "interval end with world > 1 needs peers or a communicator");
+  const int mode = end ? kAdamEnd : kAdamAccum;
+  NormParams p = norm_params(c, grad_dev, end, dry);
+  p.params = params_dev;
+  p.exp_avg = exp_avg_dev;
+  p.exp_avg_sq = exp_avg_sq_dev;
+  // constants rounded once to fp32 (the oracle rounds the same fp64 values)
+  const double lr = hp->lr, b1 = hp->beta1, b2 = hp->beta2;
+  p.adam.decay = static_cast<float>(1.0 - lr * static_cast<double>(hp->weight_decay));
+  p.adam.beta1 = hp->beta1;
+  p.adam.one_minus_beta1 = static_cast<float>(1.0 - b1);
+  p.adam.beta2 = hp->beta2;
+  p.adam.one_minus_beta2 = static_cast<float>(1.0 - b2);
+  p.adam.step_size = static_cast<float>(lr / (1.0 - std::pow(b1, hp->step)));
+  p.adam.sqrt_bc2 = static_cast<float>(std::sqrt(1.0 - std::pow(b2, hp->step)));
+  p.adam.eps = hp->eps;
+  const bool fuse = end && (c->cfg.world == 1 || c->peers);
+  if (fuse) {
+    p.fuse_decide = 1;
+    p.dec = decide_params(c, dry, out_host);
+  }
+  const int grid = std::max(1, std::min<int>(c->grid[mode], std::max<int>(1, p.n_tiles)));
+  const int e = launch_norms(p, mode, c->dtype, grid, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "fused AdamW kernel launch");
+  if (fuse) {
+    st = copy_record_if_unmapped(c, p.dec, out_host, stream);
+    if (st != AF_OK) return st;
+    if (!dry) c->armed = false;
+    return AF_OK;
+  }
+  if (end) {  // NCCL path: all-gather then the decide kernel
+    st = allgather_rows(c, stream);
+    if (st != AF_OK) return st;
+    if (!dry) c->armed = false;
+    c->pending = true;
+    return af_update_and_decide(c, flags & AF_DRY_RUN, out_host, stream);
+  }
+  if (!dry) c->armed = true;
   return AF_OK;
 }
 

@@ -52,7 +52,18 @@ struct DevState {
   double prev[AF_MAX_SEGMENTS];  // ||Delta_{T-1,l}||
 };
 
-enum Mode : int { kAccum = 0, kEndDelta = 1, kStepSq = 2 };
+enum Mode : int { kAccum = 0, kEndDelta = 1, kStepSq = 2, kAdamAccum = 3, kAdamEnd = 4 };
+constexpr int kNumModes = 5;
+
+// AdamW constants of one step, rounded once to fp32 on the host (NEXT 1 fusion).
+struct AdamConst {
+  float decay;      // 1 - lr * weight_decay
+  float beta1, one_minus_beta1;
+  float beta2, one_minus_beta2;
+  float step_size;  // lr / (1 - beta1^t)
+  float sqrt_bc2;   // sqrt(1 - beta2^t)
+  float eps;
+};
 
 // Arguments of the single-CTA decision kernel.
 struct DecideParams {
@@ -91,6 +102,9 @@ struct NormParams {
   int32_t end;                     // interval end (STEP_SUMSQ: publish ss_acc)
   int32_t commit;                  // STEP_SUMSQ: store ss_acc
   int32_t fuse_decide;             // fused interval end: the last CTA decides
+  // kAdamAccum / kAdamEnd: AdamW update of the same elements (full flat fp32 buffers)
+  float *params, *exp_avg, *exp_avg_sq;
+  AdamConst adam;
   // NVLink one-shot exchange (peers registered): the last CTA writes this rank's
   // row into every peer's double-buffered exchange matrix, raises its flag there
   // and waits for all peers' flags before deciding.

@@ -209,6 +209,101 @@ __device__ __forceinline__ double process_tile(const NormParams &p, const Tile &
   return (a0 + a1) + (a2 + a3);
 }
 
+
+// AdamW on one element in fp32 with explicit round-to-nearest operations (no
+// contraction), in the order of the oracle's definition (oracle.adamw_step):
+//   p <- p * decay;  m <- m*b1 + g*(1-b1);  v <- v*b2 + (g*g)*(1-b2)
+//   p <- p - step_size * (m / (sqrt(v) / sqrt_bc2 + eps))
+__device__ __forceinline__ void adamw_elem(const AdamConst &c, float g, float &pw, float &m, float &v) {
+  pw = __fmul_rn(pw, c.decay);
+  m = __fadd_rn(__fmul_rn(m, c.beta1), __fmul_rn(g, c.one_minus_beta1));
+  v = __fadd_rn(__fmul_rn(v, c.beta2), __fmul_rn(__fmul_rn(g, g), c.one_minus_beta2));
+  const float den = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), c.sqrt_bc2), c.eps);
+  pw = __fsub_rn(pw, __fmul_rn(c.step_size, __fdiv_rn(m, den)));
+}
+
+// NEXT 1: the Delta accumulate (or, at the interval end, the
+// fp64 sum of squares of Delta + g) fused into the AdamW update that already
+// reads g -- one pass over g, Delta, p, m, v instead of two kernels reading g.
+template <bool END, typename GT, bool RD>
+__device__ __forceinline__ double process_tile_adam(const NormParams &p, const Tile &t) {
+  constexpr int VE = VT<GT>::VE;
+  constexpr int DV = VE / 4;
+  const GT *__restrict__ g = static_cast<const GT *>(p.grad);
+  float *__restrict__ d = p.delta - p.shard_begin;
+  float *__restrict__ pw = p.params;
+  float *__restrict__ mm = p.exp_avg;
+  float *__restrict__ vv = p.exp_avg_sq;
+  const int64_t b = t.begin, e = t.end;
+  int64_t vb = ((b + VE - 1) / VE) * VE;
+  int64_t ve = (e / VE) * VE;
+  if (vb > ve) vb = ve = e;
+  const int tid = threadIdx.x;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  auto scalar = [&](int64_t i, double &acc) {
+    const float gf = g_scalar(g, i);
+    const float x = RD ? __fadd_rn(d[i], gf) : gf;
+    if (END)
+      acc = sq_acc(x, acc);
+    else
+      d[i] = x;
+    float pv = pw[i], mv = mm[i], vv2 = vv[i];
+    adamw_elem(p.adam, gf, pv, mv, vv2);
+    pw[i] = pv;
+    mm[i] = mv;
+    vv[i] = vv2;
+  };
+  const int nh = static_cast<int>(vb - b), nt = static_cast<int>(e - ve);
+  if (tid < nh) scalar(b + tid, a0);
+  if (tid >= 128 && tid - 128 < nt) scalar(ve + (tid - 128), a1);
+  const int64_t nch = (ve - vb) / VE;
+  const uint4 *gb = reinterpret_cast<const uint4 *>(g + vb);
+  float4 *db = reinterpret_cast<float4 *>(d + vb);
+  float4 *pb = reinterpret_cast<float4 *>(pw + vb);
+  float4 *mb = reinterpret_cast<float4 *>(mm + vb);
+  float4 *vb4 = reinterpret_cast<float4 *>(vv + vb);
+  for (int64_t c = tid; c < nch; c += kNormBlock) {
+    const uint4 gv = ld_stream<AF_G_HINT>(gb + c);
+    float4 dv[DV], pv[DV], mv[DV], v2[DV];
+#pragma unroll
+    for (int q = 0; q < DV; ++q) {
+      if (RD) dv[q] = __ldcs(db + c * DV + q);
+      pv[q] = __ldcs(pb + c * DV + q);
+      mv[q] = __ldcs(mb + c * DV + q);
+      v2[q] = __ldcs(vb4 + c * DV + q);
+    }
+    float x[VE];
+    unpack<VE>(gv, x);
+#pragma unroll
+    for (int q = 0; q < DV; ++q) {
+      float gq[4] = {x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]};
+      float dq[4] = {gq[0], gq[1], gq[2], gq[3]};
+      if (RD) {
+        dq[0] = __fadd_rn(dv[q].x, gq[0]);
+        dq[1] = __fadd_rn(dv[q].y, gq[1]);
+        dq[2] = __fadd_rn(dv[q].z, gq[2]);
+        dq[3] = __fadd_rn(dv[q].w, gq[3]);
+      }
+      if (END) {
+        a0 = sq_acc(dq[0], a0);
+        a1 = sq_acc(dq[1], a1);
+        a2 = sq_acc(dq[2], a2);
+        a3 = sq_acc(dq[3], a3);
+      } else {
+        __stcs(db + c * DV + q, make_float4(dq[0], dq[1], dq[2], dq[3]));
+      }
+      adamw_elem(p.adam, gq[0], pv[q].x, mv[q].x, v2[q].x);
+      adamw_elem(p.adam, gq[1], pv[q].y, mv[q].y, v2[q].y);
+      adamw_elem(p.adam, gq[2], pv[q].z, mv[q].z, v2[q].z);
+      adamw_elem(p.adam, gq[3], pv[q].w, mv[q].w, v2[q].w);
+      __stcs(pb + c * DV + q, pv[q]);
+      __stcs(mb + c * DV + q, mv[q]);
+      __stcs(vb4 + c * DV + q, v2[q]);
+    }
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
@@ -298,7 +393,8 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
 }
 
 template <int MODE, typename GT, bool RD>
-__global__ void __launch_bounds__(kNormBlock, (MODE == kAccum) ? 1 : AF_MINB_END) norms_kernel(const NormParams p) {
+__global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAccum) ? 1 : AF_MINB_END)
+    norms_kernel(const NormParams p) {
   __shared__ int s_tile[3];
   __shared__ Tile s_desc[3];
   __shared__ double s_red[kNormBlock / 32];
@@ -339,12 +435,16 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum) ? 1 : AF_MINB_END
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    const double v = process_tile<MODE, GT, RD>(p, t);
+    double v;
+    if constexpr (MODE == kAdamAccum || MODE == kAdamEnd)
+      v = process_tile_adam<MODE == kAdamEnd, GT, RD>(p, t);
+    else
+      v = process_tile<MODE, GT, RD>(p, t);
     if (tid == 0) {
       s_tile[slot2] = next2;
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    if (MODE != kAccum) {
+    if (MODE != kAccum && MODE != kAdamAccum) {
       const double w = warp_sum(v);
       if (lane == 0) s_red[warp] = w;
       __syncthreads();
@@ -374,8 +474,8 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum) ? 1 : AF_MINB_END
     p.sched->next = 0;
     p.sched->done = 0;
   }
-  if (MODE == kAccum) return;
-  last_cta_tail<MODE>(p, first_tile, s_red);
+  if (MODE == kAccum || MODE == kAdamAccum) return;
+  last_cta_tail<(MODE == kAdamEnd) ? kEndDelta : MODE>(p, first_tile, s_red);
 }
 
 template <int MODE, typename GT, bool RD>
@@ -395,6 +495,11 @@ int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
                 : launch_one<kEndDelta, GT, false>(p, grid, stream);
     case kStepSq:
       return launch_one<kStepSq, GT, false>(p, grid, stream);
+    case kAdamAccum:
+      return rd ? launch_one<kAdamAccum, GT, true>(p, grid, stream)
+                : launch_one<kAdamAccum, GT, false>(p, grid, stream);
+    case kAdamEnd:
+      return rd ? launch_one<kAdamEnd, GT, true>(p, grid, stream) : launch_one<kAdamEnd, GT, false>(p, grid, stream);
   }
   return static_cast<int>(cudaErrorInvalidValue);
 }
@@ -415,6 +520,12 @@ static int occ_dt(int mode, int *blocks) {
       break;
     case kEndDelta:
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kEndDelta, GT, true>, kNormBlock, 0);
+      break;
+    case kAdamAccum:
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kAdamAccum, GT, true>, kNormBlock, 0);
+      break;
+    case kAdamEnd:
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kAdamEnd, GT, true>, kNormBlock, 0);
       break;
     default:
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kStepSq, GT, false>, kNormBlock, 0);

@@ -509,3 +509,39 @@ def test_calibrate_read_seconds_and_should_cache():
     t = af.calibrate_read_seconds(196_608, 256)
     assert 1e-6 < t < 1e-2
     assert af.should_cache(3, 0.011, t) and not af.should_cache(0, 0.011, t)
+
+
+# ---------------------------------------------------------------- AdamW fused with the accumulate (NEXT 1)
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_fused_adamw_bit_exact_and_decisions(dt):
+    """af_adamw_step: params / moments / Delta bit-exact vs the fp32 oracle
+    (same operation order, one rounding each), decisions as the oracle's, frozen
+    segments left untouched."""
+    lay = _ragged_layout()
+    step = _decaying_step(lay, dt, 41)
+    fm = _fm(lay, dt)
+    oz = _oracle(lay, dt)
+    rng = np.random.default_rng(3)
+    p0 = rng.standard_normal(lay.n).astype(np.float32)
+    P, M, V = p0.copy(), np.zeros(lay.n, np.float32), np.zeros(lay.n, np.float32)
+    tp, tm, tv = (torch.from_numpy(x.copy()).cuda() for x in (P, M, V))
+    k = 0
+    for T, S in enumerate([2, 3, 1, 2, 2, 3, 2]):
+        for t in range(S):
+            k += 1
+            gnp = step(T, t)
+            end = t == S - 1
+            c = O.adamw_constants(1e-3, 0.9, 0.999, 1e-8, 0.01, k)
+            oz.adamw_active(P, M, V, gnp, c)                 # on the layers active before this step
+            oz.layer_norms(gnp, end)
+            fm.adamw_step(tp, tm, tv, to_device_grad(gnp, dt), lr=1e-3, step=k, weight_decay=0.01,
+                          interval_end=end)
+            if not end:
+                torch.cuda.synchronize()
+                assert np.array_equal(delta_host(fm, lay.n), oz.delta)
+        compare_records(fm.decision(), oz.update_and_decide(), lay.n_segments, tag=f"T={T}")
+        assert np.array_equal(tp.cpu().numpy(), P)
+        assert np.array_equal(tm.cpu().numpy(), M)
+        assert np.array_equal(tv.cpu().numpy(), V)
+    assert oz.f >= 1                                          # frozen prefix exercised

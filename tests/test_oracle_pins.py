@@ -388,3 +388,32 @@ def test_cache_capacity_and_recache_balance_invariants():
         written += len(c.store) - n_before
         assert len(c.store) <= I
         assert written <= evicted + free0
+
+
+# ------------------------------------------------------------------ AdamW (NEXT 1 fusion)
+
+def test_adamw_matches_torch_library_routine():
+    import torch
+    rng = np.random.default_rng(0)
+    n = 5000
+    p0 = rng.standard_normal(n).astype(np.float32)
+    p, m, v = p0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
+    tp = torch.nn.Parameter(torch.from_numpy(p0.copy()))
+    opt = torch.optim.AdamW([tp], lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01)
+    for step in range(1, 6):
+        g = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+        O.adamw_step(p, m, v, g, O.adamw_constants(1e-3, 0.9, 0.999, 1e-8, 0.01, step))
+        tp.grad = torch.from_numpy(g.copy())
+        opt.step()
+    np.testing.assert_allclose(p, tp.detach().numpy(), rtol=2e-6, atol=1e-7)
+
+
+def test_adamw_first_step_closed_form():
+    # zero moments, no decay: m = (1-b1) g, v = (1-b2) g^2, so the update is
+    # lr * g / (|g| + eps) up to fp32 rounding
+    g = np.array([1e-2, -3e-3, 2.5e-1, -1.0], np.float32)
+    p = np.zeros(4, np.float32)
+    m, v = np.zeros(4, np.float32), np.zeros(4, np.float32)
+    O.adamw_step(p, m, v, g, O.adamw_constants(1e-3, 0.9, 0.999, 1e-8, 0.0, 1))
+    want = -1e-3 * g.astype(np.float64) / (np.abs(g.astype(np.float64)) + 1e-8)
+    np.testing.assert_allclose(p, want, rtol=1e-6)
