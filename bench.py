@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cache-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly (no CUDA graphs)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-row probes (fused AdamW)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: per-layer partial exchange (in-kernel NVLink P2P, or NCCL all-gather)")
     ap.add_argument("--unfused", action="store_true",
@@ -349,6 +350,9 @@ def run_ours(args, rank, world, local):
     }
     if not args.no_cache_sweep:
         result["cache_gbs_by_batch"] = cache_sweep(cache, my_ids, rows, dev, world, dist)
+        result["cache_host_tier"] = host_tier_probe(rows, dev)
+    if not args.no_extras:
+        result["next1_fused_adamw"] = adamw_probe(fm, lay, dt, s_g, n_loc, grads, dev)
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -392,6 +396,60 @@ def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(32, 256, 1024, 4
             res[name] = {"us": round(ms * 1e3, 2), "gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4)}
         out[str(B)] = res
     return out
+
+
+def host_tier_probe(rows, dev, reps=10):
+    """Tiered storage manager (NEXT 3): put/get GB/s of the rows when every slot
+    lives in the page-locked host tier (PCIe / C2C bound)."""
+    import torch
+
+    import paper_2102_01386_b200 as af
+    B = rows.shape[0]
+    c = af.ActivationCache(B, ROW_BYTES, device=dev, hbm_rows=0, host_rows=B)
+    ids = torch.arange(B, device=dev, dtype=torch.int64)
+    out = torch.empty_like(rows)
+    dep = torch.empty(B, dtype=torch.int32, device=dev)
+    res = {}
+    for name, fn in (("put", lambda: c.put(ids, rows, 4)), ("get", lambda: c.get(ids, 4, out, dep))):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        ms = a.elapsed_time(b) / reps
+        res[name] = {"us": round(ms * 1e3, 1), "gbs": round(B * ROW_BYTES / (ms * 1e-3) / 1e9, 1),
+                     "note": "host-tier bytes crossing the link (one direction)"}
+    res["rows"] = B
+    return res
+
+
+def adamw_probe(fm, lay, dt, s_g, n_loc, grads, dev, reps=20):
+    """NEXT 1: AdamW fused with the Delta accumulate (af_adamw_step) on this rank's
+    shard: reads g, Delta, p, m, v and writes Delta, p, m, v -- s_g + 32 bytes per
+    element, one read of g instead of two kernels reading it."""
+    import torch
+    p = torch.zeros(lay.n, device=dev)
+    m = torch.zeros(lay.n, device=dev)
+    v = torch.zeros(lay.n, device=dev)
+    for k in range(2):
+        fm.adamw_step(p, m, v, grads[k & 1], lr=1e-5, step=k + 1, dry_run=True)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for k in range(reps):
+        fm.adamw_step(p, m, v, grads[k & 1], lr=1e-5, step=k + 3, dry_run=True)
+    b.record()
+    b.synchronize()
+    ms = a.elapsed_time(b) / reps
+    peak, _ = measured_peaks()
+    by = n_loc * (s_g + 32)
+    del p, m, v
+    return {"us": round(ms * 1e3, 1), "bytes_per_elem": s_g + 32, "gbs": round(by / (ms * 1e-3) / 1e9, 1),
+            "frac_of_peak": round(by / (ms * 1e-3) / 1e9 / peak, 4),
+            "saved_vs_unfused_bytes_per_elem": s_g}
 
 
 def run_sweep(args, local):
