@@ -297,6 +297,23 @@ AF_API af_status af_cache_host_bytes(const af_cache *c, size_t *host_bytes);
  * torch pin_memory: device-mapped under UVA), 16-byte aligned. */
 AF_API af_status af_cache_bind_host(af_cache *c, void *host_pinned);
 
+/* cross-GPU cache get / put for samplers that are not
+ * rank-affine.  Every rank registers every rank's direct-mapped store (CUDA IPC
+ * of payload + meta, handles exchanged by the caller; or contexts of one
+ * process); then *_global accept ANY id in [0, num_examples): the owner rank
+ * (id % world) store is read / written through its mapped memory -- TMA bulk
+ * copies and meta updates over NVLink peer memory, evict-on-read included (the
+ * reader count is a peer atomic).  The paper keeps caches per GPU to avoid data
+ * movement; this removes the need for a rank-affine sampler. */
+#define AF_CACHE_IPC_HANDLE_BYTES 256
+AF_API af_status af_cache_exchange_ipc_handle(af_cache *c, void *handle_out);
+AF_API af_status af_cache_set_peers_ipc(af_cache *c, const void *handles);
+AF_API af_status af_cache_set_peers_local(af_cache *c, af_cache *const *peers);
+AF_API af_status af_cache_put_global(af_cache *c, const int64_t *ids_dev, int32_t n, const void *rows_dev,
+                                     int32_t depth, void *stream);
+AF_API af_status af_cache_get_global(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
+                                     void *rows_out_dev, int32_t *depth_out_dev, void *stream);
+
 typedef struct {
   uint32_t error_flags;      /* sticky AF_CACHE_ERR_* */
   uint32_t pad;

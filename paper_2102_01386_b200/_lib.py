@@ -21,6 +21,7 @@ AF_INTERVAL_END, AF_DRY_RUN = 0x1, 0x2
 AF_DEC_FIRST_INTERVAL, AF_DEC_SKIPPED_FEW, AF_DEC_NEAR_TIE, AF_DEC_NONFINITE, AF_DEC_DRY_RUN = 1, 2, 4, 8, 16
 AF_DEC_EXCHANGE_TIMEOUT = 32
 AF_IPC_HANDLE_BYTES = 128
+AF_CACHE_IPC_HANDLE_BYTES = 256
 AF_CACHE_ERR_RANGE, AF_CACHE_ERR_OWNER = 1, 2
 
 
@@ -90,6 +91,11 @@ SIGNATURES = {
     "af_cache_host_bytes": (c_int, [c_void_p, POINTER(c_size_t)]),
     "af_cache_bind_host": (c_int, [c_void_p, c_void_p]),
     "af_cache_stats": (c_int, [c_void_p, POINTER(AfCacheInfo)]),
+    "af_cache_exchange_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "af_cache_set_peers_ipc": (c_int, [c_void_p, c_void_p]),
+    "af_cache_set_peers_local": (c_int, [c_void_p, c_void_p]),
+    "af_cache_put_global": (c_int, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),
+    "af_cache_get_global": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     "af_cache_destroy": (c_int, [c_void_p]),
     "af_should_cache": (c_int, [c_int32, c_double, c_double]),
     "af_status_str": (c_char_p, [c_int]),

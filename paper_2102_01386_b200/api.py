@@ -243,6 +243,33 @@ class ActivationCache:
         ev.record(stream)
         return ev
 
+    def set_peers_local(self, peers):
+        """NEXT 4: register every rank's cache living in this process."""
+        arr = (c_void_p * len(peers))(*[p._h.value for p in peers])
+        check(lib.af_cache_set_peers_local(self._h, arr), "af_cache_set_peers_local")
+
+    def set_peers_ipc(self, group=None):
+        """NEXT 4, collective: exchange CUDA IPC handles of every rank's store."""
+        import torch.distributed as dist
+        h = (ctypes.c_uint8 * L.AF_CACHE_IPC_HANDLE_BYTES)()
+        with torch.cuda.device(self.device):
+            check(lib.af_cache_exchange_ipc_handle(self._h, h), "af_cache_exchange_ipc_handle")
+        allh = [None] * self.world
+        dist.all_gather_object(allh, bytes(h), group=group)
+        buf = (ctypes.c_uint8 * (L.AF_CACHE_IPC_HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(allh))
+        with torch.cuda.device(self.device):
+            check(lib.af_cache_set_peers_ipc(self._h, buf), "af_cache_set_peers_ipc")
+
+    def put_global(self, ids, rows, depth, stream=None):
+        check(lib.af_cache_put_global(self._h, c_void_p(ids.data_ptr()), int(ids.numel()),
+                                      c_void_p(rows.data_ptr()), int(depth), _stream_handle(stream)),
+              "af_cache_put_global")
+
+    def get_global(self, ids, cur_boundary, rows_out, depth_out, stream=None):
+        check(lib.af_cache_get_global(self._h, c_void_p(ids.data_ptr()), int(ids.numel()), int(cur_boundary),
+                                      c_void_p(rows_out.data_ptr()), c_void_p(depth_out.data_ptr()),
+                                      _stream_handle(stream)), "af_cache_get_global")
+
     def status(self):
         e, v = c_uint32(), c_int64()
         check(lib.af_cache_status(self._h, byref(e), byref(v)), "af_cache_status")

@@ -107,12 +107,15 @@ struct af_cache {
   char *meta = nullptr;  // [CacheHeader | pad to 256 B][CacheMeta x capacity][free x I][rowslot x max_batch]
   char *host = nullptr;  // device alias of the page-locked host tier
   bool bound = false, host_bound = false;
+  bool peers = false;                // global get/put through peers' stores (NEXT 4)
+  std::vector<void *> ipc_opened;
   int grid = 0;
-  size_t meta_bytes() const {
+  size_t o_peer_table() const {
     size_t b = kMetaHeaderBytes + static_cast<size_t>(capacity) * sizeof(CacheMeta);
     if (tiered) b += static_cast<size_t>(hbm_rows + host_rows) * 4 + static_cast<size_t>(max_batch) * 4;
-    return b;
+    return (b + 255) / 256 * 256;
   }
+  size_t meta_bytes() const { return o_peer_table() + 2 * AF_MAX_WORLD * sizeof(void *); }
   size_t o_free() const { return kMetaHeaderBytes + static_cast<size_t>(capacity) * sizeof(CacheMeta); }
   size_t o_rowslot() const { return o_free() + static_cast<size_t>(hbm_rows + host_rows) * 4; }
   static constexpr size_t kMetaHeaderBytes = 256;
@@ -572,6 +575,36 @@ af_status af_interval_end(af_ctx *c, const void *grad_dev, uint32_t flags, af_de
   return AF_OK;
 }
 
+// CUDA IPC export of a pointer that may sit inside a larger allocation (the
+// caller's allocator sub-allocates): handle of the allocation base + offset.
+struct IpcRef {
+  cudaIpcMemHandle_t h;
+  uint64_t offset;
+};
+
+static af_status ipc_export(const void *ptr, IpcRef *out) {
+  typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  AF_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(AF_ECUDA, "cuMemGetAddressRange entry point not found");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<GetRange>(fn)(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0)
+    return fail(AF_ECUDA, "cuMemGetAddressRange failed");
+  AF_CUDA(cudaIpcGetMemHandle(&out->h, reinterpret_cast<void *>(base)), "cudaIpcGetMemHandle");
+  out->offset = reinterpret_cast<unsigned long long>(ptr) - base;
+  return AF_OK;
+}
+
+static af_status ipc_import(const IpcRef &r, std::vector<void *> &opened, char **out) {
+  void *p = nullptr;
+  AF_CUDA(cudaIpcOpenMemHandle(&p, r.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  opened.push_back(p);
+  *out = static_cast<char *>(p) + r.offset;
+  return AF_OK;
+}
+
 struct IpcHandle {  // AF_IPC_HANDLE_BYTES
   cudaIpcMemHandle_t h;
   uint64_t offset;                 // scratch offset inside the exported allocation
@@ -600,21 +633,12 @@ static af_status upload_peers(af_ctx *c, const std::vector<char *> &scratch_of) 
 af_status af_ctx_exchange_ipc_handle(af_ctx *c, void *handle_out) {
   if (!c || !handle_out) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
-  // base of the allocation holding the scratch buffer (the caller's allocator may
-  // sub-allocate): driver entry point resolved at run time (libcuda is loaded by cudart)
-  typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
-  void *fn = nullptr;
-  cudaDriverEntryPointQueryResult q{};
-  AF_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
-  if (!fn || q != cudaDriverEntryPointSuccess) return fail(AF_ECUDA, "cuMemGetAddressRange entry point not found");
-  GetRange get_range = reinterpret_cast<GetRange>(fn);
-  unsigned long long base = 0;
-  size_t size = 0;
-  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(c->scratch)) != 0)
-    return fail(AF_ECUDA, "cuMemGetAddressRange failed");
+  IpcRef r{};
+  af_status st = ipc_export(c->scratch, &r);
+  if (st != AF_OK) return st;
   IpcHandle h{};
-  AF_CUDA(cudaIpcGetMemHandle(&h.h, reinterpret_cast<void *>(base)), "cudaIpcGetMemHandle");
-  h.offset = reinterpret_cast<unsigned long long>(c->scratch) - base;
+  h.h = r.h;
+  h.offset = r.offset;
   h.xrows_off = c->o_xrows;
   h.xflags_off = c->o_xflags;
   h.rank = c->cfg.rank;
@@ -640,10 +664,8 @@ af_status af_ctx_set_peers_ipc(af_ctx *c, const void *handles) {
       scratch_of[r] = c->scratch;
       continue;
     }
-    void *p = nullptr;
-    AF_CUDA(cudaIpcOpenMemHandle(&p, h.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-    c->ipc_opened.push_back(p);
-    scratch_of[r] = static_cast<char *>(p) + h.offset;
+    af_status st = ipc_import(IpcRef{h.h, h.offset}, c->ipc_opened, &scratch_of[r]);
+    if (st != AF_OK) return st;
   }
   return upload_peers(c, scratch_of);
 }
@@ -953,8 +975,133 @@ af_status af_cache_status(af_cache *c, uint32_t *device_error_flags, int64_t *n_
   return AF_OK;
 }
 
+struct CacheIpcHandle {  // AF_CACHE_IPC_HANDLE_BYTES
+  IpcRef payload, meta;
+  int64_t num_examples, row_bytes;
+  int32_t rank, world;
+};
+static_assert(sizeof(CacheIpcHandle) <= AF_CACHE_IPC_HANDLE_BYTES, "cache ipc handle size");
+
+static af_status cache_upload_peers(af_cache *c, const std::vector<char *> &pay, const std::vector<char *> &met) {
+  std::vector<void *> tab(2 * AF_MAX_WORLD, nullptr);
+  for (int r = 0; r < c->world; ++r) {
+    tab[r] = pay[r];
+    tab[AF_MAX_WORLD + r] = met[r];
+  }
+  AF_CUDA(cudaMemcpy(c->meta + c->o_peer_table(), tab.data(), tab.size() * sizeof(void *), cudaMemcpyHostToDevice),
+          "cudaMemcpy(cache peers)");
+  AF_CUDA(cudaDeviceSynchronize(), "cache set peers");
+  c->peers = true;
+  return AF_OK;
+}
+
+af_status af_cache_exchange_ipc_handle(af_cache *c, void *handle_out) {
+  if (!c || !handle_out) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
+  if (c->tiered) return fail(AF_ESTATE, "global get/put needs the direct-mapped cache");
+  CacheIpcHandle h{};
+  af_status st = ipc_export(c->payload, &h.payload);
+  if (st != AF_OK) return st;
+  st = ipc_export(c->meta + kMetaHeader, &h.meta);
+  if (st != AF_OK) return st;
+  h.num_examples = c->num_examples;
+  h.row_bytes = c->row_bytes;
+  h.rank = c->rank;
+  h.world = c->world;
+  std::memset(handle_out, 0, AF_CACHE_IPC_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  return AF_OK;
+}
+
+af_status af_cache_set_peers_ipc(af_cache *c, const void *handles) {
+  if (!c || !handles) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
+  if (c->tiered) return fail(AF_ESTATE, "global get/put needs the direct-mapped cache");
+  if (c->peers) return fail(AF_ESTATE, "peers already set");
+  std::vector<char *> pay(c->world), met(c->world);
+  for (int r = 0; r < c->world; ++r) {
+    CacheIpcHandle h;
+    std::memcpy(&h, static_cast<const char *>(handles) + static_cast<size_t>(r) * AF_CACHE_IPC_HANDLE_BYTES,
+                sizeof(h));
+    if (h.rank != r || h.world != c->world || h.num_examples != c->num_examples || h.row_bytes != c->row_bytes)
+      return fail(AF_EINVAL, "peer cache handle mismatch");
+    if (r == c->rank) {
+      pay[r] = c->payload;
+      met[r] = c->meta + kMetaHeader;
+      continue;
+    }
+    af_status st = ipc_import(h.payload, c->ipc_opened, &pay[r]);
+    if (st != AF_OK) return st;
+    st = ipc_import(h.meta, c->ipc_opened, &met[r]);
+    if (st != AF_OK) return st;
+  }
+  return cache_upload_peers(c, pay, met);
+}
+
+af_status af_cache_set_peers_local(af_cache *c, af_cache *const *peers) {
+  if (!c || !peers) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
+  if (c->tiered) return fail(AF_ESTATE, "global get/put needs the direct-mapped cache");
+  if (c->peers) return fail(AF_ESTATE, "peers already set");
+  std::vector<char *> pay(c->world), met(c->world);
+  for (int r = 0; r < c->world; ++r) {
+    const af_cache *q = peers[r];
+    if (!q || !q->bound || q->tiered || q->rank != r || q->world != c->world || q->num_examples != c->num_examples ||
+        q->row_bytes != c->row_bytes)
+      return fail(AF_EINVAL, "peer cache mismatch");
+    pay[r] = q->payload;
+    met[r] = q->meta + kMetaHeader;
+  }
+  return cache_upload_peers(c, pay, met);
+}
+
+static af_status cache_global_common(af_cache *c) {
+  if (!c) return fail(AF_EINVAL, "NULL cache");
+  if (!c->peers) return fail(AF_ESTATE, "global get/put needs af_cache_set_peers_*");
+  return AF_OK;
+}
+
+af_status af_cache_put_global(af_cache *c, const int64_t *ids_dev, int32_t n, const void *rows_dev, int32_t depth,
+                              void *stream) {
+  af_status s = cache_global_common(c);
+  if (s != AF_OK) return s;
+  CacheParams p;
+  s = cache_common(c, ids_dev, n, rows_dev, p);
+  if (s != AF_OK) return s;
+  if (depth < 1) return fail(AF_EINVAL, "depth must be >= 1 (frozen POOL count)");
+  if (n == 0) return AF_OK;
+  p.src_rows = static_cast<const char *>(rows_dev);
+  p.depth = depth;
+  p.peer_payload = reinterpret_cast<char *const *>(c->meta + c->o_peer_table());
+  p.peer_meta = reinterpret_cast<CacheMeta *const *>(c->meta + c->o_peer_table() + AF_MAX_WORLD * sizeof(void *));
+  const int e = launch_cache_put(p, c->grid, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache put launch");
+  return AF_OK;
+}
+
+af_status af_cache_get_global(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
+                              void *rows_out_dev, int32_t *depth_out_dev, void *stream) {
+  af_status s = cache_global_common(c);
+  if (s != AF_OK) return s;
+  CacheParams p;
+  s = cache_common(c, ids_dev, n, rows_out_dev, p);
+  if (s != AF_OK) return s;
+  if (n > 0 && !depth_out_dev) return fail(AF_EINVAL, "NULL depth_out");
+  if (cur_boundary < 0) return fail(AF_EINVAL, "cur_boundary < 0");
+  if (n == 0) return AF_OK;
+  p.dst_rows = static_cast<char *>(rows_out_dev);
+  p.depth_out = depth_out_dev;
+  p.cur_boundary = cur_boundary;
+  p.peer_payload = reinterpret_cast<char *const *>(c->meta + c->o_peer_table());
+  p.peer_meta = reinterpret_cast<CacheMeta *const *>(c->meta + c->o_peer_table() + AF_MAX_WORLD * sizeof(void *));
+  const int e = launch_cache_get(p, c->grid, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache get launch");
+  return AF_OK;
+}
+
 af_status af_cache_destroy(af_cache *c) {
   if (!c) return fail(AF_EINVAL, "NULL cache");
+  for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   delete c;
   return AF_OK;
 }

@@ -147,9 +147,15 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
       const int64_t id = p.ids[i];
       Desc dsc{nullptr, nullptr, 0u, 0u};
       bool ok = true;
+      char *payload = p.payload;
+      CacheMeta *meta = p.meta;
       if (id < 0 || id >= p.num_examples) {
         if (c == 0) atomicOr(p.err, AF_CACHE_ERR_RANGE);
         ok = false;
+      } else if (p.peer_payload) {  // global: the owner's store, possibly a peer's
+        const int owner = static_cast<int>(id % p.world);
+        payload = p.peer_payload[owner];
+        meta = p.peer_meta[owner];
       } else if (id % p.world != p.rank) {
         if (c == 0) atomicOr(p.err, AF_CACHE_ERR_OWNER);
         ok = false;
@@ -175,14 +181,14 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
         }
       } else if (ok) {
         const int64_t slot = id / p.world;
-        char *rec = p.payload + slot * p.row_bytes + off;
+        char *rec = payload + slot * p.row_bytes + off;
         if (PUT) {
           dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
           dsc.dst = rec;
           dsc.ok = 1u;
-          if (c == 0) *reinterpret_cast<int2 *>(p.meta + slot) = make_int2(p.depth, 1);  // {depth, valid}
+          if (c == 0) *reinterpret_cast<int2 *>(meta + slot) = make_int2(p.depth, 1);  // {depth, valid}
         } else {
-          const int4 mv = __ldcg(reinterpret_cast<const int4 *>(p.meta) + slot);  // {depth, valid, readers, -}
+          const int4 mv = __ldcg(reinterpret_cast<const int4 *>(meta) + slot);  // {depth, valid, readers, -}
           const bool hit = mv.y != 0;
           if (c == 0) p.depth_out[i] = hit ? mv.x : -1;
           if (hit) {
@@ -191,10 +197,10 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
             dsc.ok = 1u;
             // evict on read once every chunk of the row has read the record
             __threadfence();
-            const unsigned int seen = atomicAdd(&p.meta[slot].readers, 1u);
+            const unsigned int seen = atomicAdd(&meta[slot].readers, 1u);
             if (seen == static_cast<unsigned int>(p.n_chunks) - 1u) {
-              if (mv.x < p.cur_boundary) p.meta[slot].valid = 0;
-              p.meta[slot].readers = 0u;
+              if (mv.x < p.cur_boundary) meta[slot].valid = 0;
+              meta[slot].readers = 0u;
             }
           }
         }

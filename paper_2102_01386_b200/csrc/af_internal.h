@@ -156,6 +156,10 @@ struct CacheParams {
   const int32_t *rowslot;   // [n] slot per row of the call, -1 = skip
   char *host;               // device alias of the page-locked host tier
   int64_t hbm_rows;         // slots [0, hbm_rows) in `payload`, the rest in `host`
+  // global mode (NEXT 4): any id; the owner's (id % world) store is reached through
+  // its mapped payload / meta (peer memory over NVLink)
+  char *const *peer_payload;     // [world]
+  CacheMeta *const *peer_meta;   // [world]
 };
 
 struct CachePlanParams {

@@ -173,7 +173,7 @@ def test_cache_create_validation_and_sizes():
     assert L.lib.af_cache_create(-1, 64, 0, 1, ctypes.byref(h)) == L.AF_EINVAL
     c = af.ActivationCache(100_000, 196_608, rank=3, world=8, bind=False)
     assert c.payload_bytes == 12_500 * 196_608
-    assert c.meta_bytes == 256 + 12_500 * 16
+    assert c.meta_bytes == (256 + 12_500 * 16 + 255) // 256 * 256 + 2 * 64 * 8
     c2 = af.ActivationCache(10, 64, rank=3, world=4, bind=False)       # ids 3, 7
     assert c2.payload_bytes == 2 * 64
 
@@ -182,7 +182,7 @@ def test_cache_tiered_capacity_validation_and_sizes():
     c = af.ActivationCache(100_000, 196_608, rank=0, world=8, bind=False, hbm_rows=1000, host_rows=500)
     assert c.payload_bytes == 1000 * 196_608
     assert c.host_bytes == 500 * 196_608
-    assert c.meta_bytes == 256 + 12_500 * 16 + (1500 + 65536) * 4
+    assert c.meta_bytes == (256 + 12_500 * 16 + (1500 + 65536) * 4 + 255) // 256 * 256 + 2 * 64 * 8
     h = ctypes.c_void_p()
     assert L.lib.af_cache_create(100, 64, 0, 1, ctypes.byref(h)) == L.AF_OK
     assert L.lib.af_cache_set_capacity(h, 0, 0) == L.AF_EINVAL

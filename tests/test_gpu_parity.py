@@ -545,3 +545,38 @@ def test_fused_adamw_bit_exact_and_decisions(dt):
         assert np.array_equal(tm.cpu().numpy(), M)
         assert np.array_equal(tv.cpu().numpy(), V)
     assert oz.f >= 1                                          # frozen prefix exercised
+
+
+# ---------------------------------------------------------------- cross-GPU cache get / put (NEXT 4)
+
+def test_global_cache_get_put_across_ranks():
+    """Ranks in one process (stores in each other's memory): a non-rank-affine
+    batch is put and read by ANY rank through the owners' stores, with the
+    owners' evict-on-read; bytes / depths / residency match one global oracle."""
+    import paper_2102_01386_b200 as af
+    from afinputs import cache_rows
+    P, num, rb = 3, 900, 2048 + 16
+    cs = [af.ActivationCache(num, rb, rank=r, world=P) for r in range(P)]
+    for c in cs:
+        c.set_peers_local(cs)
+    oc = O.Cache(num, rb)                      # the union of the partitions
+    rng = np.random.default_rng(7)
+    for epoch, (depth, bnd) in enumerate([(4, 4), (4, 7), (7, 7)]):
+        perm = rng.permutation(num)
+        for b, b0 in enumerate(range(0, num, 100)):
+            ids = perm[b0:b0 + 100]
+            c = cs[b % P]                        # the batch lands on any rank
+            out_g = torch.full((len(ids), rb), 1, dtype=torch.uint8, device="cuda")
+            dep_g = torch.zeros(len(ids), dtype=torch.int32, device="cuda")
+            c.get_global(_ids(ids), bnd, out_g, dep_g)
+            out_o = np.full((len(ids), rb), 1, np.uint8)
+            dep_o = oc.get(ids, bnd, out_o)
+            assert np.array_equal(dep_g.cpu().numpy(), dep_o)
+            assert np.array_equal(out_g.cpu().numpy(), out_o)
+            miss = ids[dep_o < 0]
+            if len(miss):
+                rows = cache_rows(epoch, b0, len(miss), rb)
+                c.put_global(_ids(miss), torch.from_numpy(rows).cuda(), depth)
+                oc.put(miss, rows, depth)
+        assert sum(c.status()[1] for c in cs) == len(oc.store)
+        assert all(c.status()[0] == 0 for c in cs)
