@@ -478,6 +478,249 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
   last_cta_tail<(MODE == kAdamEnd) ? kEndDelta : MODE>(p, first_tile, s_red);
 }
 
+
+// ---------------------------------------------------------------- TMA-staged variant
+//
+// Same work, tiles, scheduler and per-tile reduction order as norms_kernel, but
+// the vector body of each tile moves HBM -> shared memory with TMA bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx) in chunks of kTmaChunk elements
+// through a kTmaStages ring; thread 0 is the producer (it also fetches the
+// tiles) and every thread consumes from shared memory.  One CTA per SM; the
+// bytes in flight no longer depend on registers.  Unaligned segment edges are
+// read directly (as in norms_kernel).  kAccum writes Delta back with st.global.
+#ifndef AF_TMA
+#define AF_TMA 1  // 0: LDG kernels only; 1: TMA for the interval end; 2: also for the accumulate
+#endif
+constexpr int kTmaStages = 4;
+constexpr int kTmaChunk = 4096;
+
+struct StageMeta {
+  int64_t c0;         // first element of the chunk (aligned)
+  int64_t tb, te;     // the tile's element range (for the scalar edges)
+  int32_t tile, n;    // tile index (-1: no more work), elements in the chunk
+  int32_t first, last;
+};
+
+__device__ __forceinline__ uint32_t smem_u32a(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tma_mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32a(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tma_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32a(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32a(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32a(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32a(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32a(bar))
+      : "memory");
+}
+
+template <typename GT>
+__host__ __device__ constexpr int tma_stage_bytes() {
+  return kTmaChunk * static_cast<int>(sizeof(GT)) + kTmaChunk * 4;
+}
+template <typename GT>
+__host__ __device__ constexpr int tma_smem_bytes() {
+  return 1024 + kTmaStages * tma_stage_bytes<GT>();
+}
+
+template <int MODE, typename GT, bool RD>
+__global__ void __launch_bounds__(kNormBlock, 1) norms_tma_kernel(const NormParams p) {
+  static_assert(MODE == kAccum || MODE == kEndDelta, "TMA variant: accumulate and interval end");
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  constexpr int VE = VT<GT>::VE;
+  constexpr int DV = VE / 4;
+  constexpr int GB = kTmaChunk * static_cast<int>(sizeof(GT));
+  constexpr int SB = tma_stage_bytes<GT>();
+  uint64_t *full = reinterpret_cast<uint64_t *>(tsm);
+  uint64_t *empty = full + kTmaStages;
+  StageMeta *meta = reinterpret_cast<StageMeta *>(tsm + 128);
+  unsigned char *bufs = tsm + 1024;
+  __shared__ double s_red[kNormBlock / 32];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      tma_mbar_init(&full[s], 1);
+      tma_mbar_init(&empty[s], kNormBlock / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  int f = p.state->f;
+  f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
+  const int first_tile = p.first_tile_of_f[f];
+  const GT *__restrict__ g = static_cast<const GT *>(p.grad);
+  float *__restrict__ d = p.delta - p.shard_begin;
+
+  // producer state (thread 0)
+  uint32_t issued = 0;
+  int p_tile = -1, p_chunk = 0, p_nch = 0;
+  int64_t p_vb = 0, p_ve = 0, p_tb = 0, p_te = 0;
+  bool p_done = false;
+  auto produce = [&]() {
+    const int s = static_cast<int>(issued % kTmaStages);
+    if (issued >= static_cast<uint32_t>(kTmaStages)) tma_wait(&empty[s], ((issued / kTmaStages) - 1u) & 1u);
+    if (!p_done && p_chunk == p_nch) {
+      const int t = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+      if (t >= p.n_tiles) {
+        p_done = true;
+      } else {
+        const Tile tt = p.tiles[t];
+        p_tile = t;
+        p_tb = tt.begin;
+        p_te = tt.end;
+        p_vb = ((tt.begin + VE - 1) / VE) * VE;
+        p_ve = (tt.end / VE) * VE;
+        if (p_vb > p_ve) p_vb = p_ve = tt.end;
+        p_nch = static_cast<int>((p_ve - p_vb + kTmaChunk - 1) / kTmaChunk);
+        if (p_nch < 1) p_nch = 1;
+        p_chunk = 0;
+      }
+    }
+    StageMeta &m = meta[s];
+    if (p_done) {
+      m.tile = -1;
+      tma_arrive(&full[s]);
+    } else {
+      const int64_t c0 = p_vb + static_cast<int64_t>(p_chunk) * kTmaChunk;
+      const int64_t rem = p_ve - c0;
+      const int n = static_cast<int>(rem < kTmaChunk ? (rem > 0 ? rem : 0) : kTmaChunk);
+      m.c0 = c0;
+      m.tb = p_tb;
+      m.te = p_te;
+      m.tile = p_tile;
+      m.n = n;
+      m.first = (p_chunk == 0);
+      m.last = (p_chunk == p_nch - 1);
+      const uint32_t gbytes = static_cast<uint32_t>(n) * sizeof(GT), dbytes = RD ? static_cast<uint32_t>(n) * 4u : 0u;
+      tma_expect_tx(&full[s], gbytes + dbytes);
+      if (n > 0) {
+        unsigned char *st = bufs + static_cast<size_t>(s) * SB;
+        tma_g2s(st, g + c0, gbytes, &full[s]);
+        if (RD) tma_g2s(st + GB, d + c0, dbytes, &full[s]);
+      }
+      ++p_chunk;
+    }
+    ++issued;
+  };
+  if (tid == 0)
+    for (int i = 0; i < kTmaStages - 1; ++i) produce();
+
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (uint32_t k = 0;; ++k) {
+    if (tid == 0) produce();  // chunk k + stages - 1
+    const int s = static_cast<int>(k % kTmaStages);
+    tma_wait(&full[s], (k / kTmaStages) & 1u);
+    const StageMeta m = meta[s];
+    if (m.tile < 0) break;
+    const unsigned char *st = bufs + static_cast<size_t>(s) * SB;
+    const uint4 *gs = reinterpret_cast<const uint4 *>(st);
+    const float4 *ds = reinterpret_cast<const float4 *>(st + GB);
+    const int nv = m.n / VE;
+    for (int v = tid; v < nv; v += kNormBlock) {
+      float x[VE];
+      unpack<VE>(gs[v], x);
+      if (RD) {
+#pragma unroll
+        for (int q = 0; q < DV; ++q) {
+          const float4 dv = ds[v * DV + q];
+          x[4 * q + 0] = __fadd_rn(dv.x, x[4 * q + 0]);
+          x[4 * q + 1] = __fadd_rn(dv.y, x[4 * q + 1]);
+          x[4 * q + 2] = __fadd_rn(dv.z, x[4 * q + 2]);
+          x[4 * q + 3] = __fadd_rn(dv.w, x[4 * q + 3]);
+        }
+      }
+      if (MODE == kAccum) {
+        float4 *dst = reinterpret_cast<float4 *>(d + m.c0) + static_cast<int64_t>(v) * DV;
+#pragma unroll
+        for (int q = 0; q < DV; ++q) __stcs(dst + q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
+      } else {
+#pragma unroll
+        for (int k2 = 0; k2 < VE; k2 += 4) {
+          a0 = sq_acc(x[k2 + 0], a0);
+          a1 = sq_acc(x[k2 + 1], a1);
+          a2 = sq_acc(x[k2 + 2], a2);
+          a3 = sq_acc(x[k2 + 3], a3);
+        }
+      }
+    }
+    // unaligned segment edges of the tile, read directly (< VE elements each)
+    if (m.first) {
+      const int64_t vb = m.c0;
+      const int nh = static_cast<int>(vb - m.tb);
+      if (tid < nh) elem<MODE, GT, RD>(p, g, d, m.tb + tid, a0);
+    }
+    if (m.last) {
+      const int64_t ve = m.c0 + m.n;
+      const int nt = static_cast<int>(m.te - ve);
+      if (tid >= 128 && tid - 128 < nt) elem<MODE, GT, RD>(p, g, d, ve + (tid - 128), a1);
+    }
+    __syncwarp();
+    if (lane == 0) tma_arrive(&empty[s]);
+    if (MODE == kEndDelta && m.last) {
+      const double w = warp_sum((a0 + a1) + (a2 + a3));
+      a0 = a1 = a2 = a3 = 0.0;
+      if (lane == 0) s_red[warp] = w;
+      __syncthreads();
+      if (tid == 0) {
+        double sum = 0.0;
+#pragma unroll
+        for (int q = 0; q < kNormBlock / 32; ++q) sum += s_red[q];
+        p.partials[m.tile] = sum;
+      }
+      __syncthreads();
+    }
+  }
+  pdl_launch_dependents();
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int dn = atomicAdd(&p.sched->done, 1u);
+    s_last = (dn == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) {
+    p.sched->next = 0;
+    p.sched->done = 0;
+  }
+  if (MODE == kAccum) return;
+  last_cta_tail<kEndDelta>(p, first_tile, s_red);
+}
+
+template <int MODE, typename GT, bool RD>
+int launch_tma(const NormParams &p, int grid, void *stream) {
+  constexpr int smem = tma_smem_bytes<GT>();
+  static int attr_set = 0;  // once per process and instantiation (not a stream operation)
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(norms_tma_kernel<MODE, GT, RD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    attr_set = 1;
+  }
+  return static_cast<int>(launch_pdl(norms_tma_kernel<MODE, GT, RD>, dim3(grid), dim3(kNormBlock),
+                                     static_cast<size_t>(smem), static_cast<cudaStream_t>(stream), p));
+}
+
 template <int MODE, typename GT, bool RD>
 int launch_one(const NormParams &p, int grid, void *stream) {
   return static_cast<int>(
@@ -489,8 +732,13 @@ int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
   const bool rd = !p.first;
   switch (mode) {
     case kAccum:
+      if (AF_TMA >= 2)
+        return rd ? launch_tma<kAccum, GT, true>(p, grid, stream) : launch_tma<kAccum, GT, false>(p, grid, stream);
       return rd ? launch_one<kAccum, GT, true>(p, grid, stream) : launch_one<kAccum, GT, false>(p, grid, stream);
     case kEndDelta:
+      if (AF_TMA >= 1)
+        return rd ? launch_tma<kEndDelta, GT, true>(p, grid, stream)
+                  : launch_tma<kEndDelta, GT, false>(p, grid, stream);
       return rd ? launch_one<kEndDelta, GT, true>(p, grid, stream)
                 : launch_one<kEndDelta, GT, false>(p, grid, stream);
     case kStepSq:
@@ -534,6 +782,10 @@ static int occ_dt(int mode, int *blocks) {
 }
 
 int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks) {
+  if ((mode == kEndDelta && AF_TMA >= 1) || (mode == kAccum && AF_TMA >= 2)) {
+    *blocks = 1;  // the TMA-staged kernels run one CTA per SM
+    return 0;
+  }
   return grad_dtype == AF_DT_BF16 ? occ_dt<uint16_t>(mode, blocks) : occ_dt<float>(mode, blocks);
 }
 
