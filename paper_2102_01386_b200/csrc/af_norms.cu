@@ -332,7 +332,7 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
   }
   // each segment's active tiles' partials in tile order: one warp per segment,
   // lane-strided with 8 loads in flight, then the xor tree (deterministic)
-  for (int l = warp; l < p.L; l += kNormBlock / 32) {
+  for (int l = warp; l < p.L && warp < kNormBlock / 32; l += kNormBlock / 32) {
     int tb = p.seg_tile_begin[l];
     tb = tb < first_tile ? first_tile : tb;
     const int te = p.seg_tile_begin[l + 1];
@@ -357,7 +357,7 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
     __syncthreads();
     const unsigned long long e = s_epoch;
     const size_t off = (e & 1ull) * p.xworld * p.L + static_cast<size_t>(p.xrank) * p.L;
-    for (int i = tid; i < p.xworld * p.L; i += kNormBlock) {
+    for (int i = tid; i < p.xworld * p.L && tid < kNormBlock; i += kNormBlock) {
       const int r = i / p.L, l = i % p.L;
       p.peer_rows[r][off + l] = ss_row[l];
     }
@@ -540,8 +540,12 @@ __host__ __device__ constexpr int tma_smem_bytes() {
   return 1024 + kTmaStages * tma_stage_bytes<GT>();
 }
 
+constexpr int kTmaThreads = kNormBlock + 32;  // 8 consumer warps + 1 producer warp
+
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNormBlock) : "memory"); }
+
 template <int MODE, typename GT, bool RD>
-__global__ void __launch_bounds__(kNormBlock, 1) norms_tma_kernel(const NormParams p) {
+__global__ void __launch_bounds__(kTmaThreads, 1) norms_tma_kernel(const NormParams p) {
   static_assert(MODE == kAccum || MODE == kEndDelta, "TMA variant: accumulate and interval end");
   extern __shared__ __align__(1024) unsigned char tsm[];
   constexpr int VE = VT<GT>::VE;
@@ -570,123 +574,128 @@ __global__ void __launch_bounds__(kNormBlock, 1) norms_tma_kernel(const NormPara
   const GT *__restrict__ g = static_cast<const GT *>(p.grad);
   float *__restrict__ d = p.delta - p.shard_begin;
 
-  // producer state (thread 0)
-  uint32_t issued = 0;
-  int p_tile = -1, p_chunk = 0, p_nch = 0;
-  int64_t p_vb = 0, p_ve = 0, p_tb = 0, p_te = 0;
-  bool p_done = false;
-  auto produce = [&]() {
-    const int s = static_cast<int>(issued % kTmaStages);
-    if (issued >= static_cast<uint32_t>(kTmaStages)) tma_wait(&empty[s], ((issued / kTmaStages) - 1u) & 1u);
-    if (!p_done && p_chunk == p_nch) {
-      const int t = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
-      if (t >= p.n_tiles) {
-        p_done = true;
-      } else {
-        const Tile tt = p.tiles[t];
-        p_tile = t;
-        p_tb = tt.begin;
-        p_te = tt.end;
-        p_vb = ((tt.begin + VE - 1) / VE) * VE;
-        p_ve = (tt.end / VE) * VE;
-        if (p_vb > p_ve) p_vb = p_ve = tt.end;
-        p_nch = static_cast<int>((p_ve - p_vb + kTmaChunk - 1) / kTmaChunk);
-        if (p_nch < 1) p_nch = 1;
-        p_chunk = 0;
-      }
-    }
-    StageMeta &m = meta[s];
-    if (p_done) {
-      m.tile = -1;
-      tma_arrive(&full[s]);
-    } else {
-      const int64_t c0 = p_vb + static_cast<int64_t>(p_chunk) * kTmaChunk;
-      const int64_t rem = p_ve - c0;
-      const int n = static_cast<int>(rem < kTmaChunk ? (rem > 0 ? rem : 0) : kTmaChunk);
-      m.c0 = c0;
-      m.tb = p_tb;
-      m.te = p_te;
-      m.tile = p_tile;
-      m.n = n;
-      m.first = (p_chunk == 0);
-      m.last = (p_chunk == p_nch - 1);
-      const uint32_t gbytes = static_cast<uint32_t>(n) * sizeof(GT), dbytes = RD ? static_cast<uint32_t>(n) * 4u : 0u;
-      tma_expect_tx(&full[s], gbytes + dbytes);
-      if (n > 0) {
-        unsigned char *st = bufs + static_cast<size_t>(s) * SB;
-        tma_g2s(st, g + c0, gbytes, &full[s]);
-        if (RD) tma_g2s(st + GB, d + c0, dbytes, &full[s]);
-      }
-      ++p_chunk;
-    }
-    ++issued;
-  };
-  if (tid == 0)
-    for (int i = 0; i < kTmaStages - 1; ++i) produce();
-
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  for (uint32_t k = 0;; ++k) {
-    if (tid == 0) produce();  // chunk k + stages - 1
-    const int s = static_cast<int>(k % kTmaStages);
-    tma_wait(&full[s], (k / kTmaStages) & 1u);
-    const StageMeta m = meta[s];
-    if (m.tile < 0) break;
-    const unsigned char *st = bufs + static_cast<size_t>(s) * SB;
-    const uint4 *gs = reinterpret_cast<const uint4 *>(st);
-    const float4 *ds = reinterpret_cast<const float4 *>(st + GB);
-    const int nv = m.n / VE;
-    for (int v = tid; v < nv; v += kNormBlock) {
-      float x[VE];
-      unpack<VE>(gs[v], x);
-      if (RD) {
-#pragma unroll
-        for (int q = 0; q < DV; ++q) {
-          const float4 dv = ds[v * DV + q];
-          x[4 * q + 0] = __fadd_rn(dv.x, x[4 * q + 0]);
-          x[4 * q + 1] = __fadd_rn(dv.y, x[4 * q + 1]);
-          x[4 * q + 2] = __fadd_rn(dv.z, x[4 * q + 2]);
-          x[4 * q + 3] = __fadd_rn(dv.w, x[4 * q + 3]);
+  if (warp == kNormBlock / 32) {
+    // ---------------- producer warp: lane 0 fetches tiles (one ahead) and issues bulk copies
+    if (lane == 0) {
+      int nxt = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+      Tile nxt_t{0, 0, 0, 0, 0, 0};
+      if (nxt < p.n_tiles) nxt_t = p.tiles[nxt];
+      uint32_t issued = 0;
+      for (;;) {
+        const int tile = nxt;
+        const Tile tt = nxt_t;
+        if (tile < p.n_tiles) {  // prefetch the next tile while this one streams
+          nxt = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+          if (nxt < p.n_tiles) nxt_t = p.tiles[nxt];
         }
-      }
-      if (MODE == kAccum) {
-        float4 *dst = reinterpret_cast<float4 *>(d + m.c0) + static_cast<int64_t>(v) * DV;
-#pragma unroll
-        for (int q = 0; q < DV; ++q) __stcs(dst + q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
-      } else {
-#pragma unroll
-        for (int k2 = 0; k2 < VE; k2 += 4) {
-          a0 = sq_acc(x[k2 + 0], a0);
-          a1 = sq_acc(x[k2 + 1], a1);
-          a2 = sq_acc(x[k2 + 2], a2);
-          a3 = sq_acc(x[k2 + 3], a3);
+        const bool done = tile >= p.n_tiles;
+        int64_t vb = 0, ve = 0;
+        int nch = 1;
+        if (!done) {
+          vb = ((tt.begin + VE - 1) / VE) * VE;
+          ve = (tt.end / VE) * VE;
+          if (vb > ve) vb = ve = tt.end;
+          nch = static_cast<int>((ve - vb + kTmaChunk - 1) / kTmaChunk);
+          if (nch < 1) nch = 1;
         }
+        for (int ch = 0; ch < nch; ++ch) {
+          const int s = static_cast<int>(issued % kTmaStages);
+          if (issued >= static_cast<uint32_t>(kTmaStages)) tma_wait(&empty[s], ((issued / kTmaStages) - 1u) & 1u);
+          StageMeta &m = meta[s];
+          if (done) {
+            m.tile = -1;
+            tma_arrive(&full[s]);
+          } else {
+            const int64_t c0 = vb + static_cast<int64_t>(ch) * kTmaChunk;
+            const int64_t rem = ve - c0;
+            const int n = static_cast<int>(rem < kTmaChunk ? (rem > 0 ? rem : 0) : kTmaChunk);
+            m.c0 = c0;
+            m.tb = tt.begin;
+            m.te = tt.end;
+            m.tile = tile;
+            m.n = n;
+            m.first = (ch == 0);
+            m.last = (ch == nch - 1);
+            const uint32_t gbytes = static_cast<uint32_t>(n) * sizeof(GT);
+            const uint32_t dbytes = RD ? static_cast<uint32_t>(n) * 4u : 0u;
+            tma_expect_tx(&full[s], gbytes + dbytes);
+            if (n > 0) {
+              unsigned char *st = bufs + static_cast<size_t>(s) * SB;
+              tma_g2s(st, g + c0, gbytes, &full[s]);
+              if (RD) tma_g2s(st + GB, d + c0, dbytes, &full[s]);
+            }
+          }
+          ++issued;
+        }
+        if (done) break;
       }
-    }
-    // unaligned segment edges of the tile, read directly (< VE elements each)
-    if (m.first) {
-      const int64_t vb = m.c0;
-      const int nh = static_cast<int>(vb - m.tb);
-      if (tid < nh) elem<MODE, GT, RD>(p, g, d, m.tb + tid, a0);
-    }
-    if (m.last) {
-      const int64_t ve = m.c0 + m.n;
-      const int nt = static_cast<int>(m.te - ve);
-      if (tid >= 128 && tid - 128 < nt) elem<MODE, GT, RD>(p, g, d, ve + (tid - 128), a1);
     }
     __syncwarp();
-    if (lane == 0) tma_arrive(&empty[s]);
-    if (MODE == kEndDelta && m.last) {
-      const double w = warp_sum((a0 + a1) + (a2 + a3));
-      a0 = a1 = a2 = a3 = 0.0;
-      if (lane == 0) s_red[warp] = w;
-      __syncthreads();
-      if (tid == 0) {
-        double sum = 0.0;
+  } else {
+    // ---------------- consumer warps
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (uint32_t k = 0;; ++k) {
+      const int s = static_cast<int>(k % kTmaStages);
+      tma_wait(&full[s], (k / kTmaStages) & 1u);
+      const StageMeta m = meta[s];
+      if (m.tile < 0) break;
+      const unsigned char *st = bufs + static_cast<size_t>(s) * SB;
+      const uint4 *gs = reinterpret_cast<const uint4 *>(st);
+      const float4 *ds = reinterpret_cast<const float4 *>(st + GB);
+      const int nv = m.n / VE;
+      for (int v = tid; v < nv; v += kNormBlock) {
+        float x[VE];
+        unpack<VE>(gs[v], x);
+        if (RD) {
 #pragma unroll
-        for (int q = 0; q < kNormBlock / 32; ++q) sum += s_red[q];
-        p.partials[m.tile] = sum;
+          for (int q = 0; q < DV; ++q) {
+            const float4 dv = ds[v * DV + q];
+            x[4 * q + 0] = __fadd_rn(dv.x, x[4 * q + 0]);
+            x[4 * q + 1] = __fadd_rn(dv.y, x[4 * q + 1]);
+            x[4 * q + 2] = __fadd_rn(dv.z, x[4 * q + 2]);
+            x[4 * q + 3] = __fadd_rn(dv.w, x[4 * q + 3]);
+          }
+        }
+        if (MODE == kAccum) {
+          float4 *dst = reinterpret_cast<float4 *>(d + m.c0) + static_cast<int64_t>(v) * DV;
+#pragma unroll
+          for (int q = 0; q < DV; ++q)
+            __stcs(dst + q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
+        } else {
+#pragma unroll
+          for (int k2 = 0; k2 < VE; k2 += 4) {
+            a0 = sq_acc(x[k2 + 0], a0);
+            a1 = sq_acc(x[k2 + 1], a1);
+            a2 = sq_acc(x[k2 + 2], a2);
+            a3 = sq_acc(x[k2 + 3], a3);
+          }
+        }
       }
-      __syncthreads();
+      // unaligned segment edges of the tile, read directly (< VE elements each)
+      if (m.first) {
+        const int nh = static_cast<int>(m.c0 - m.tb);
+        if (tid < nh) elem<MODE, GT, RD>(p, g, d, m.tb + tid, a0);
+      }
+      if (m.last) {
+        const int64_t ve = m.c0 + m.n;
+        const int nt = static_cast<int>(m.te - ve);
+        if (tid >= 128 && tid - 128 < nt) elem<MODE, GT, RD>(p, g, d, ve + (tid - 128), a1);
+      }
+      __syncwarp();
+      if (lane == 0) tma_arrive(&empty[s]);
+      if (MODE == kEndDelta && m.last) {
+        const double w = warp_sum((a0 + a1) + (a2 + a3));
+        a0 = a1 = a2 = a3 = 0.0;
+        if (lane == 0) s_red[warp] = w;
+        consumers_sync();
+        if (tid == 0) {
+          double sum = 0.0;
+#pragma unroll
+          for (int q = 0; q < kNormBlock / 32; ++q) sum += s_red[q];
+          p.partials[m.tile] = sum;
+        }
+        consumers_sync();
+      }
     }
   }
   pdl_launch_dependents();
@@ -717,7 +726,7 @@ int launch_tma(const NormParams &p, int grid, void *stream) {
     if (e != cudaSuccess) return static_cast<int>(e);
     attr_set = 1;
   }
-  return static_cast<int>(launch_pdl(norms_tma_kernel<MODE, GT, RD>, dim3(grid), dim3(kNormBlock),
+  return static_cast<int>(launch_pdl(norms_tma_kernel<MODE, GT, RD>, dim3(grid), dim3(kTmaThreads),
                                      static_cast<size_t>(smem), static_cast<cudaStream_t>(stream), p));
 }
 
