@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
 // bytes in flight no longer depend on registers.  Unaligned segment edges are
 // read directly (as in norms_kernel).  kAccum writes Delta back with st.global.
 #ifndef AF_TMA
-#define AF_TMA 1  // 0: LDG kernels only; 1: TMA for the interval end; 2: also for the accumulate
+#define AF_TMA 0  // 0: LDG kernels only (measured faster, profiles/r01_v8_*); 1: TMA for the interval end; 2: also the accumulate
 #endif
 constexpr int kTmaStages = 4;
 constexpr int kTmaChunk = 4096;

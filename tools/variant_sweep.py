@@ -15,7 +15,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
-    "tma0": "-DAF_TMA=0",
+    "tma1": "-DAF_TMA=1",
     "tma2": "-DAF_TMA=2",
     "minb3": "-DAF_MINB_END=3",
     "u2": "-DAF_U_END=2",
