@@ -580,3 +580,74 @@ def test_global_cache_get_put_across_ranks():
                 oc.put(miss, rows, depth)
         assert sum(c.status()[1] for c in cs) == len(oc.store)
         assert all(c.status()[0] == 0 for c in cs)
+
+
+# ---------------------------------------------------------------- more edge cases
+
+def _inject(fm, oz, ss_list, lay):
+    """Drive both sides through intervals with injected per-segment sums."""
+    g = torch.zeros(lay.n, device="cuda")
+    rows = fm.exchange_rows()
+    out = []
+    for ss in ss_list:
+        fm.layer_norms(g, interval_end=True)
+        rows.copy_(torch.from_numpy(np.asarray(ss, dtype=np.float64)).view(1, -1))
+        fm.update_and_decide()
+        oz.pending = np.asarray(ss, dtype=np.float64).copy()
+        out.append((fm.decision(), oz.update_and_decide()))
+    return out
+
+
+def test_near_tie_is_flagged_on_both_sides():
+    """A scanned eta within 1e-5 * thr of the threshold sets NEAR_TIE with the
+    same segment on both sides (Q16)."""
+    lay = uniform_layout(4 * 16, 4)
+    fm, oz = _fm(lay, "f32"), _oracle(lay, "f32")
+    prev = np.array([1.0, 1.0, 1.0, 1.0])
+    # norms 1 - eta: etas (0.1, 0.2 * (1 + 2e-6), 0.3, 0.4); N = 50 -> thr = 0.25 ...
+    # use eta_1 just below thr: thr = (0.2 + 0.3) / 2 = 0.25; eta_0 = 0.25 * (1 - 5e-6)
+    cur = 1.0 - np.array([0.25 * (1 - 5e-6), 0.2, 0.3, 0.4])
+    recs = _inject(fm, oz, [prev ** 2, cur ** 2], lay)
+    g, o = recs[1]
+    assert o["flags"] & O.FLAG_NEAR_TIE and g["flags"] & O.FLAG_NEAR_TIE
+    assert g["near_tie_seg"] == o["near_tie_seg"] == 0
+
+
+def test_min_active_and_percentile_100():
+    lay = uniform_layout(5 * 16, 5)
+    fm = _fm(lay, "f32", min_active=6, percentile=100.0)
+    oz = _oracle(lay, "f32", min_active=6, percentile=100.0)
+    recs = _inject(fm, oz, [np.ones(5), np.full(5, 0.5)], lay)
+    assert recs[1][0]["flags"] & O.FLAG_SKIPPED_FEW and recs[1][1]["flags"] & O.FLAG_SKIPPED_FEW
+    fm = _fm(lay, "f32", percentile=100.0)
+    oz = _oracle(lay, "f32", percentile=100.0)
+    for g, o in _inject(fm, oz, [np.ones(5), np.array([0.9, 0.8, 0.5, 0.7, 0.6]) ** 2], lay):
+        assert g["boundary_after"] == o["boundary_after"]
+        assert (math.isnan(o["threshold"]) and math.isnan(g["threshold"])) or g["threshold"] == o["threshold"]
+
+
+def test_cuda_graph_replay_matches_eager():
+    """The bench replays steps as CUDA graphs: a captured accumulate + interval
+    end gives the same records as the same calls launched eagerly."""
+    lay = _ragged_layout()
+    step = _decaying_step(lay, "bf16", 17)
+    g0, g1 = to_device_grad(step(1, 0), "bf16"), to_device_grad(step(1, 1), "bf16")
+    eager, graphed = _fm(lay, "bf16"), _fm(lay, "bf16")
+    for fm in (eager, graphed):
+        fm.layer_norms(g0)
+        fm.interval_end(g1)
+        fm.layer_norms(g0)
+    torch.cuda.synchronize()
+    gph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gph):
+        graphed.layer_norms(g1, dry_run=True)
+        graphed.interval_end(g0, dry_run=True)
+    recs = []
+    for _ in range(3):
+        gph.replay()
+        torch.cuda.synchronize()
+        recs.append(canon(graphed.decision()))
+    eager.layer_norms(g1, dry_run=True)
+    eager.interval_end(g0, dry_run=True)
+    want = canon(eager.decision())
+    assert all(r == want for r in recs)
