@@ -22,8 +22,17 @@
 namespace af {
 namespace {
 
-constexpr int kStages = 6;
-constexpr int kChunk = 32 * 1024;
+#ifndef AF_CACHE_STAGES
+#define AF_CACHE_STAGES 6
+#endif
+#ifndef AF_CACHE_CHUNK
+#define AF_CACHE_CHUNK (32 * 1024)
+#endif
+#ifndef AF_CACHE_CTAS_PER_SM
+#define AF_CACHE_CTAS_PER_SM 1
+#endif
+constexpr int kStages = AF_CACHE_STAGES;
+constexpr int kChunk = AF_CACHE_CHUNK;
 constexpr int kMaxDesc = 512;
 
 struct Desc {
@@ -339,19 +348,18 @@ static int launch_cache(const CacheParams &p0, int grid, void *stream) {
   if (items < grid) grid = static_cast<int>(items);
   if (grid < 1) grid = 1;
   const int smem = cache_smem_bytes();
-  // once per process and kernel (not a stream operation: keep it out of CUDA-graph captures)
-  static int attr_set = 0;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(cache_kernel<PUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return static_cast<int>(e);
-    attr_set = 1;
-  }
+  const cudaError_t e = ensure_smem_attr<cache_kernel<PUT>>(smem);
+  if (e != cudaSuccess) return static_cast<int>(e);
   return static_cast<int>(launch_pdl(cache_kernel<PUT>, dim3(grid), dim3(32), static_cast<size_t>(smem),
                                      static_cast<cudaStream_t>(stream), p));
 }
 
-int launch_cache_put(const CacheParams &p, int grid, void *stream) { return launch_cache<true>(p, grid, stream); }
-int launch_cache_get(const CacheParams &p, int grid, void *stream) { return launch_cache<false>(p, grid, stream); }
+int launch_cache_put(const CacheParams &p, int grid, void *stream) {
+  return launch_cache<true>(p, grid * AF_CACHE_CTAS_PER_SM, stream);
+}
+int launch_cache_get(const CacheParams &p, int grid, void *stream) {
+  return launch_cache<false>(p, grid * AF_CACHE_CTAS_PER_SM, stream);
+}
 
 }  // namespace af
 

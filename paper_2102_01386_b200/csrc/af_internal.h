@@ -202,6 +202,22 @@ inline cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, cuda
 }
 #endif
 
+#ifdef __CUDACC__
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device --
+// not a stream operation, so it stays out of CUDA-graph captures.
+template <auto Kernel>
+inline cudaError_t ensure_smem_attr(int smem) {
+  static unsigned long long done = 0;  // one bit per device ordinal
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && ((done >> dev) & 1ull)) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess && dev < 64) done |= 1ull << dev;
+  return e;
+}
+#endif
+
 // Launchers (defined in the .cu files).  Return cudaError_t as int.
 int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *stream);
 int launch_decide(const DecideParams &p, void *stream);

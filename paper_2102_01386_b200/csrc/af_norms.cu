@@ -719,13 +719,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) norms_tma_kernel(const NormPar
 template <int MODE, typename GT, bool RD>
 int launch_tma(const NormParams &p, int grid, void *stream) {
   constexpr int smem = tma_smem_bytes<GT>();
-  static int attr_set = 0;  // once per process and instantiation (not a stream operation)
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(norms_tma_kernel<MODE, GT, RD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem);
-    if (e != cudaSuccess) return static_cast<int>(e);
-    attr_set = 1;
-  }
+  const cudaError_t e = ensure_smem_attr<norms_tma_kernel<MODE, GT, RD>>(smem);
+  if (e != cudaSuccess) return static_cast<int>(e);
   return static_cast<int>(launch_pdl(norms_tma_kernel<MODE, GT, RD>, dim3(grid), dim3(kTmaThreads),
                                      static_cast<size_t>(smem), static_cast<cudaStream_t>(stream), p));
 }

@@ -15,6 +15,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
+    "c_s3_2cta": "-DAF_CACHE_STAGES=3 -DAF_CACHE_CTAS_PER_SM=2",
+    "c_16k_s12": "-DAF_CACHE_CHUNK=16384 -DAF_CACHE_STAGES=12",
+    "c_16k_s6_2cta": "-DAF_CACHE_CHUNK=16384 -DAF_CACHE_STAGES=6 -DAF_CACHE_CTAS_PER_SM=2",
+    "c_64k_s3": "-DAF_CACHE_CHUNK=65536 -DAF_CACHE_STAGES=3",
     "tma1": "-DAF_TMA=1",
     "tma2": "-DAF_TMA=2",
     "minb3": "-DAF_MINB_END=3",
@@ -45,6 +49,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--only", nargs="*")
+    ap.add_argument("--cache", action="store_true", help="run tools/cache_probe.py instead of bench.py")
     a = ap.parse_args()
     sys.path.insert(0, ROOT)
     for name, extra in VARIANTS.items():
@@ -53,6 +58,12 @@ def main():
         env = dict(os.environ, AF_NVCC_EXTRA=extra)
         subprocess.run([sys.executable, os.path.join(ROOT, "paper_2102_01386_b200", "_build.py"), "--force"], cwd=ROOT, env=env,
                        check=True)
+        if a.cache:
+            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "cache_probe.py")], cwd=ROOT,
+                               capture_output=True, text=True)
+            print(json.dumps({"variant": name, "flags": extra, "cache": r.stdout.strip()[-2000:],
+                              "err": r.stderr[-500:] if r.returncode else ""}), flush=True)
+            continue
         for wl in ("bert-large-f32", "bert-base-bf16"):
             r = subprocess.run([sys.executable, "bench.py", "--workload", wl, "--steps", str(a.steps), "--warmup", "10",
                                 "--no-e2e", "--no-cpu-baseline", "--no-cache-sweep"], cwd=ROOT,
