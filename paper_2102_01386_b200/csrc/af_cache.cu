@@ -10,9 +10,10 @@
 // Each CTA drives a TMA bulk-copy ring (cp.async.bulk global->shared with an
 // mbarrier transaction count, then cp.async.bulk shared->global in bulk groups),
 // STAGES x 32 KiB of shared memory, one elected lane issuing, so up to
-// STAGES-1 chunk loads and the matching stores are in flight per SM without
+// STAGES-1 chunk loads and the matching stores are in flight per CTA without
 // register staging.  Work items are (row, 32 KiB chunk) pairs dealt round-robin
-// to a persistent grid of one CTA per SM.  A get evicts a record only after
+// to a persistent grid of two CTAs (3 stages each) per SM -- the best of the
+// profiles/r01_v9_variants_cache.jsonl sweep.  A get evicts a record only after
 // every chunk of its row has read the meta word (a per-record reader count,
 // fenced), so all chunks of a row agree on hit/miss.
 #include <cuda_runtime.h>
@@ -23,13 +24,13 @@ namespace af {
 namespace {
 
 #ifndef AF_CACHE_STAGES
-#define AF_CACHE_STAGES 6
+#define AF_CACHE_STAGES 3
 #endif
 #ifndef AF_CACHE_CHUNK
 #define AF_CACHE_CHUNK (32 * 1024)
 #endif
 #ifndef AF_CACHE_CTAS_PER_SM
-#define AF_CACHE_CTAS_PER_SM 1
+#define AF_CACHE_CTAS_PER_SM 2
 #endif
 constexpr int kStages = AF_CACHE_STAGES;
 constexpr int kChunk = AF_CACHE_CHUNK;
