@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cache-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly (no CUDA graphs)")
     ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-row probes (fused AdamW)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="N = 1: skip the short run of the other BERT workload reported under 'secondary'")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: per-layer partial exchange (in-kernel NVLink P2P, or NCCL all-gather)")
     ap.add_argument("--unfused", action="store_true",
@@ -357,11 +359,30 @@ def run_ours(args, rank, world, local):
         result["e2e"] = run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(lay, dt, s_g, B, budget_s=12.0)
+    if world == 1 and not args.no_secondary:
+        result["secondary"] = secondary_workload(args)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def secondary_workload(args):
+    """N = 1: the other BASELINE config (bert-base-bf16, configs[1], when the main
+    line is bert-large-f32) timed the same way, in a subprocess, summarised."""
+    import subprocess
+    other = "bert-base-bf16" if args.workload == "bert-large-f32" else "bert-large-f32"
+    cmd = [sys.executable, os.path.abspath(__file__), "--workload", other, "--steps", str(args.steps), "--warmup",
+           str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-cache-sweep", "--no-extras", "--no-secondary"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=dict(os.environ, WORLD_SIZE="1", RANK="0"))
+    try:
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception:  # noqa: BLE001
+        return {"workload": other, "error": r.stderr[-500:]}
+    keep = ("value", "unit", "ms_per_step", "grad_norm_decide_gbs", "grad_norm_decide_frac_of_hbm_peak", "dtype",
+            "config", "phases", "roofline", "clocks")
+    return {"workload": other, **{k: d[k] for k in keep if k in d}}
 
 
 def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(32, 256, 1024, 4096), reps=20):
