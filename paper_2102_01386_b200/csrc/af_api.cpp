@@ -731,6 +731,10 @@ af_status af_set_state(af_ctx *c, const void *buf, size_t len) {
   if (b.f < 0 || b.f > c->n_pool || b.T < 0) return fail(AF_EINVAL, "state blob out of range");
   AF_CUDA(cudaDeviceSynchronize(), "set_state sync");
   DevState st{};
+  // keep the peer-exchange epoch: it counts interval ends on every rank and the
+  // peers' flag words already hold it
+  AF_CUDA(cudaMemcpy(&st, c->scratch + c->o_state, sizeof(st), cudaMemcpyDeviceToHost), "cudaMemcpy(state)");
+  st.sticky = 0;
   st.T = b.T;
   st.f = b.f;
   std::memcpy(st.prev, b.prev, sizeof(st.prev));

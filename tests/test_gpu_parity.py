@@ -649,3 +649,35 @@ def test_cuda_graph_replay_matches_eager():
     eager.interval_end(g1, dry_run=True)
     want = canon(eager.decision())
     assert all(r == want for r in recs)
+
+
+def test_peer_exchange_survives_state_restore():
+    """Checkpoint / resume with the one-shot exchange: restoring T, f, prev keeps
+    the exchange epoch, so a replayed interval gives the same decision (no stale
+    rows, no timeout)."""
+    lay = _ragged_layout()
+    step = _decaying_step(lay, "f32", 51)
+    P = 2
+    fms = [_fm(lay, "f32", rank=r, world=P) for r in range(P)]
+    for fm in fms:
+        fm.set_peers_local(fms)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+
+    def interval(T):
+        g0, g1 = to_device_grad(step(T, 0), "f32"), to_device_grad(step(T, 1), "f32")
+        torch.cuda.synchronize()
+        for fm, s in zip(fms, streams):
+            with torch.cuda.stream(s):
+                fm.layer_norms(g0, stream=s)
+                fm.interval_end(g1, stream=s)
+        torch.cuda.synchronize()
+        return [canon(fm.decision()) for fm in fms]
+
+    for T in range(3):
+        interval(T)
+    blobs = [fm.get_state() for fm in fms]
+    first = interval(3)
+    for fm, b in zip(fms, blobs):
+        fm.set_state(b)
+    again = interval(3)
+    assert first == again and not any(d["flags"] & 32 for d in again)
