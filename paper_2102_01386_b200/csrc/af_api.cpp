@@ -203,14 +203,22 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   const bool bf16 = (c->dtype == AF_DT_BF16);
   c->ts[0].tile_elems = bf16 ? AF_TILE_ACC_BF16 : AF_TILE_ACC_F32;
   c->ts[1].tile_elems = bf16 ? AF_TILE_ELEMS_BF16 : AF_TILE_ELEMS_F32;
-  for (auto &T : c->ts) {
+  // interval-end table: "tapered" tiles -- AF_TILE_BIG_MULT x larger in the first
+  // AF_TILE_BIG_FRAC_PCT % of the shard (fewer fp64 partials for the last CTA to
+  // sum), nominal size in the tail (balanced finish).  Fixed at create, so the
+  // partials and their summation order stay deterministic.
+  const int64_t big_until = c->sb + (c->se - c->sb) / 100 * AF_TILE_BIG_FRAC_PCT;
+  for (int k = 0; k < 2; ++k) {
+    auto &T = c->ts[k];
     const int64_t TE = T.tile_elems;
+    const int64_t TB = (k == 1) ? TE * AF_TILE_BIG_MULT : TE;
     T.seg_tile_begin.assign(L + 1, 0);
     for (int l = 0; l < L; ++l) {
       T.seg_tile_begin[l] = static_cast<int32_t>(T.tiles.size());
       const int64_t lo = std::max(c->offs[l], c->sb), hi = std::min(c->offs[l + 1], c->se);
       for (int64_t pos = lo; pos < hi;) {
-        const int64_t nxt = std::min(hi, (pos / TE + 1) * TE);
+        const int64_t te = (pos < big_until) ? TB : TE;
+        const int64_t nxt = std::min(hi, (pos / te + 1) * te);
         T.tiles.push_back(Tile{pos, nxt, l, 0, 0, 0});
         pos = nxt;
       }

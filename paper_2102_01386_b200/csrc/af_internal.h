@@ -19,6 +19,12 @@ constexpr int kNormBlock = 256;          // threads per CTA of the streaming ker
 #ifndef AF_TILE_ELEMS_BF16
 #define AF_TILE_ELEMS_BF16 16384
 #endif
+#ifndef AF_TILE_BIG_MULT  // interval-end tiles are this much larger in the bulk of the shard
+#define AF_TILE_BIG_MULT 8
+#endif
+#ifndef AF_TILE_BIG_FRAC_PCT
+#define AF_TILE_BIG_FRAC_PCT 85
+#endif
 #ifndef AF_TILE_ACC_F32  // the accumulate kernel keeps no partials: finer tiles balance better
 #define AF_TILE_ACC_F32 8192
 #endif

@@ -105,13 +105,17 @@ def test_null_arguments():
     assert L.lib.af_cache_create(10, 64, 0, 1, None) == L.AF_EINVAL
 
 
-def _expected_tiles(lay, sb, se, tile_elems):
+def _expected_tiles(lay, sb, se, tile_elems, big_mult=1, big_frac_pct=0, upto_seg=None):
+    """Independent re-count of the segment-aligned tiles (tapered for the
+    interval-end table: big_mult x tiles in the first big_frac_pct % of the shard)."""
     n = 0
-    for l in range(lay.n_segments):
+    big_until = sb + (se - sb) // 100 * big_frac_pct
+    for l in range(lay.n_segments if upto_seg is None else upto_seg):
         lo, hi = max(lay.offsets[l], sb), min(lay.offsets[l + 1], se)
         pos = lo
         while pos < hi:
-            pos = min(hi, (pos // tile_elems + 1) * tile_elems)
+            te = tile_elems * big_mult if pos < big_until else tile_elems
+            pos = min(hi, (pos // te + 1) * te)
             n += 1
     return n
 
@@ -129,7 +133,7 @@ def test_shards_cover_buffer_and_tiles_are_segment_aligned(which, dt, world):
         assert i["shard_begin"] % 8 == 0
         prev_end = i["shard_end"]
         assert i["tile_elems"] % 8 == 0 and i["tile_elems"] >= 4096
-        assert i["n_tiles"] == _expected_tiles(lay, i["shard_begin"], i["shard_end"], i["tile_elems"])
+        assert i["n_tiles"] == _expected_tiles(lay, i["shard_begin"], i["shard_end"], i["tile_elems"], 8, 85)
         assert i["n_tiles_acc"] == _expected_tiles(lay, i["shard_begin"], i["shard_end"], i["tile_elems_acc"])
         assert fm.accum_bytes == 4 * (i["shard_end"] - i["shard_begin"])
         ft = i["first_tile_of_pool"]
@@ -146,9 +150,9 @@ def test_first_tile_skips_embedding_with_first_block():
     fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="bf16", bind=False)
     i = fm.info()
     te = i["tile_elems"]
-    pre_tiles = -(-lay.seg_len(0) // te)
-    blk_tiles = _expected_tiles(bert_layout("base"), lay.offsets[1], lay.offsets[2], te)
-    assert i["first_tile_of_pool"][1] == pre_tiles + blk_tiles
+    # f = 1 frozen: PRE and POOL[0] skipped
+    assert i["first_tile_of_pool"][1] == _expected_tiles(lay, 0, lay.n, te, 8, 85, upto_seg=2)
+    assert i["first_tile_of_pool"][2] == _expected_tiles(lay, 0, lay.n, te, 8, 85, upto_seg=3)
     assert i["first_tile_of_pool"][0] == 0
 
 

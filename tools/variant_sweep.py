@@ -15,6 +15,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
+    "taper_off": "-DAF_TILE_BIG_MULT=1",
+    "taper4": "-DAF_TILE_BIG_MULT=4",
+    "taper8_90": "-DAF_TILE_BIG_FRAC_PCT=90",
+    "taper16": "-DAF_TILE_BIG_MULT=16",
     "c_s3_2cta": "-DAF_CACHE_STAGES=3 -DAF_CACHE_CTAS_PER_SM=2",
     "c_16k_s12": "-DAF_CACHE_CHUNK=16384 -DAF_CACHE_STAGES=12",
     "c_16k_s6_2cta": "-DAF_CACHE_CHUNK=16384 -DAF_CACHE_STAGES=6 -DAF_CACHE_CTAS_PER_SM=2",
