@@ -20,7 +20,7 @@ constexpr int kNormBlock = 256;          // threads per CTA of the streaming ker
 #define AF_TILE_ELEMS_BF16 16384
 #endif
 #ifndef AF_TILE_BIG_MULT  // interval-end tiles are this much larger in the bulk of the shard
-#define AF_TILE_BIG_MULT 8
+#define AF_TILE_BIG_MULT 1  // tapering measured slower (profiles/r01_v10_variants_taper.jsonl): off
 #endif
 #ifndef AF_TILE_BIG_FRAC_PCT
 #define AF_TILE_BIG_FRAC_PCT 85

@@ -133,7 +133,7 @@ def test_shards_cover_buffer_and_tiles_are_segment_aligned(which, dt, world):
         assert i["shard_begin"] % 8 == 0
         prev_end = i["shard_end"]
         assert i["tile_elems"] % 8 == 0 and i["tile_elems"] >= 4096
-        assert i["n_tiles"] == _expected_tiles(lay, i["shard_begin"], i["shard_end"], i["tile_elems"], 8, 85)
+        assert i["n_tiles"] == _expected_tiles(lay, i["shard_begin"], i["shard_end"], i["tile_elems"], 1, 85)
         assert i["n_tiles_acc"] == _expected_tiles(lay, i["shard_begin"], i["shard_end"], i["tile_elems_acc"])
         assert fm.accum_bytes == 4 * (i["shard_end"] - i["shard_begin"])
         ft = i["first_tile_of_pool"]
@@ -151,8 +151,8 @@ def test_first_tile_skips_embedding_with_first_block():
     i = fm.info()
     te = i["tile_elems"]
     # f = 1 frozen: PRE and POOL[0] skipped
-    assert i["first_tile_of_pool"][1] == _expected_tiles(lay, 0, lay.n, te, 8, 85, upto_seg=2)
-    assert i["first_tile_of_pool"][2] == _expected_tiles(lay, 0, lay.n, te, 8, 85, upto_seg=3)
+    assert i["first_tile_of_pool"][1] == _expected_tiles(lay, 0, lay.n, te, 1, 85, upto_seg=2)
+    assert i["first_tile_of_pool"][2] == _expected_tiles(lay, 0, lay.n, te, 1, 85, upto_seg=3)
     assert i["first_tile_of_pool"][0] == 0
 
 
