@@ -330,76 +330,24 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
     __syncthreads();
     ss_row = p.xrows + (s_epoch & 1ull) * p.xworld * p.L + static_cast<size_t>(p.xrank) * p.L;
   }
-  // Per-segment sums of the active tiles' partials, balanced over the 8 warps and
-  // deterministic: the active tiles [first_tile, n_tiles) are split into 8
-  // contiguous warp ranges; a warp walks its range in rounds of 32 tiles (one per
-  // lane, kFinU rounds of loads in flight), reduces each round per segment with a
-  // masked xor tree and adds it to its running per-segment sums; the 8 warps'
-  // sums are then added in warp order.  The order depends only on the tile range.
-  constexpr int kFinU = 8;
-  __shared__ double s_wseg[kNormBlock / 32][AF_MAX_SEGMENTS];
-  __shared__ int s_stb[AF_MAX_SEGMENTS + 1];
-  for (int i = tid; i <= p.L && tid < kNormBlock; i += kNormBlock) s_stb[i] = p.seg_tile_begin[i];
-  if (warp < kNormBlock / 32)
-    for (int l = lane; l < p.L; l += 32) s_wseg[warp][l] = 0.0;
-  __syncthreads();
-  if (warp < kNormBlock / 32) {
-    const int64_t n_act = p.n_tiles - first_tile;
-    const int r0 = first_tile + static_cast<int>(n_act * warp / (kNormBlock / 32));
-    const int r1 = first_tile + static_cast<int>(n_act * (warp + 1) / (kNormBlock / 32));
-    // segment of this lane's first tile (binary search), then tracked incrementally
-    int cur = 0;
-    {
-      int lo = 0, hi = p.L - 1;
-      const int k0 = r0 + lane;
-      while (lo < hi) {  // last l with s_stb[l] <= k0
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_stb[mid] <= k0) lo = mid;
-        else hi = mid - 1;
+  // each segment's active tiles' partials in tile order: one warp per segment,
+  // lane-strided with 8 loads in flight, then the xor tree (deterministic)
+  for (int l = warp; l < p.L && warp < kNormBlock / 32; l += kNormBlock / 32) {
+    int tb = p.seg_tile_begin[l];
+    tb = tb < first_tile ? first_tile : tb;
+    const int te = p.seg_tile_begin[l + 1];
+    double s = 0.0;
+#pragma unroll 8
+    for (int k = tb + lane; k < te; k += 32) s += __ldcg(p.partials + k);
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (MODE == kEndDelta) {
+        ss_row[l] = s;
+      } else {
+        const double acc = p.first ? s : p.ss_acc[l] + s;
+        if (p.commit) p.ss_acc[l] = acc;
+        if (p.end) ss_row[l] = acc;
       }
-      cur = lo;
-    }
-    for (int base = r0; base < r1; base += 32 * kFinU) {
-      double v[kFinU];
-      int sg[kFinU];
-#pragma unroll
-      for (int u = 0; u < kFinU; ++u) {
-        const int k = base + u * 32 + lane;
-        v[u] = (k < r1) ? __ldcg(p.partials + k) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kFinU; ++u) {
-        const int k = base + u * 32 + lane;
-        if (k < r1) {
-          while (k >= s_stb[cur + 1]) ++cur;
-          sg[u] = cur;
-        } else {
-          sg[u] = -1;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kFinU; ++u) {
-        if (base + u * 32 >= r1) break;  // warp-uniform
-        const int sa = __shfl_sync(0xFFFFFFFFu, sg[u], 0);
-        const int sb = __reduce_max_sync(0xFFFFFFFFu, sg[u]);
-        for (int sgi = sa; sgi <= sb; ++sgi) {
-          const double t = warp_sum(sg[u] == sgi ? v[u] : 0.0);
-          if (lane == 0) s_wseg[warp][sgi] += t;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int l = tid; l < p.L && tid < kNormBlock; l += kNormBlock) {
-    double sum = 0.0;
-#pragma unroll
-    for (int w = 0; w < kNormBlock / 32; ++w) sum += s_wseg[w][l];
-    if (MODE == kEndDelta) {
-      ss_row[l] = sum;
-    } else {
-      const double acc = p.first ? sum : p.ss_acc[l] + sum;
-      if (p.commit) p.ss_acc[l] = acc;
-      if (p.end) ss_row[l] = acc;
     }
   }
   if (xchg) {
