@@ -26,3 +26,15 @@ def test_c_program_reproduces_closed_form_trace(tmp_path, golden):
     bounds = [int(ln.split()[3]) for ln in lines if ln.startswith("T ")]
     assert bounds == golden("tiny_trace.json")["boundary_after"]
     assert lines[-1].startswith("cache roundtrip ok depths 2 2 2 valid_after_evict 0 err 0")
+
+
+def test_training_loop_example_runs_and_freezes_monotonically():
+    """examples/autofreeze_loop.py (small): the frozen prefix only grows, some
+    layers freeze, and the cache serves hits from the epoch after a freeze."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("loop", os.path.join(ROOT, "examples", "autofreeze_loop.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    trace, hits = mod.run(epochs=3, small=True, verbose=False)
+    assert trace == sorted(trace) and trace[-1] >= 1
+    assert hits > 0
