@@ -213,12 +213,9 @@ def run_ours(args, rank, world, local):
     if world > 1:
         # NVLink one-shot exchange inside the interval-end kernel (CUDA IPC peer
         # mappings); NCCL all-gather as the fallback
-        try:
-            if args.exchange != "p2p":
-                raise RuntimeError("nccl requested")
-            fm.set_peers_ipc()
+        if args.exchange == "p2p" and fm.set_peers_ipc():   # collective; same answer on every rank
             exchange = "p2p"
-        except Exception:  # noqa: BLE001
+        else:
             fm.set_comm()
             exchange = "nccl"
     info = fm.info()

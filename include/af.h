@@ -197,6 +197,9 @@ AF_API af_status af_ctx_exchange_rows(af_ctx *ctx, double **ss_all_dev);
 AF_API af_status af_ctx_exchange_ipc_handle(af_ctx *ctx, void *handle_out);
 AF_API af_status af_ctx_set_peers_ipc(af_ctx *ctx, const void *handles);
 AF_API af_status af_ctx_set_peers_local(af_ctx *ctx, af_ctx *const *peers);
+/* Host only: stop using the registered peers (e.g. when another rank failed to
+ * map them and the ranks agree to fall back to NCCL). */
+AF_API af_status af_ctx_clear_peers(af_ctx *ctx);
 
 /* One training step.  grad_dev = the FULL flat gradient
  * buffer (n_total elements of grad_dtype, 16-byte aligned; only this rank's

@@ -73,6 +73,7 @@ SIGNATURES = {
     "af_ctx_exchange_ipc_handle": (c_int, [c_void_p, c_void_p]),
     "af_ctx_set_peers_ipc": (c_int, [c_void_p, c_void_p]),
     "af_ctx_set_peers_local": (c_int, [c_void_p, c_void_p]),
+    "af_ctx_clear_peers": (c_int, [c_void_p]),
     "af_layer_norms": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p]),
     "af_update_and_decide": (c_int, [c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_interval_end": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p, c_void_p]),

@@ -101,16 +101,28 @@ class FreezingModule:
 
     def set_peers_ipc(self, group=None):
         """Collective: exchange CUDA IPC handles of every rank's exchange buffers
-        through torch.distributed and register them (one-shot NVLink exchange)."""
+        through torch.distributed and register them (one-shot NVLink exchange).
+        Returns True on every rank, or False on every rank (no peers registered)
+        when any rank could not export or map a handle -- fall back to set_comm()."""
         import torch.distributed as dist
         h = (ctypes.c_uint8 * L.AF_IPC_HANDLE_BYTES)()
         with torch.cuda.device(self.device):
-            check(lib.af_ctx_exchange_ipc_handle(self._h, h), "af_ctx_exchange_ipc_handle")
+            mine = bytes(h) if lib.af_ctx_exchange_ipc_handle(self._h, h) == L.AF_OK else None
+        if mine is not None:
+            mine = bytes(h)
         allh = [None] * self.world
-        dist.all_gather_object(allh, bytes(h), group=group)
-        buf = (ctypes.c_uint8 * (L.AF_IPC_HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(allh))
-        with torch.cuda.device(self.device):
-            check(lib.af_ctx_set_peers_ipc(self._h, buf), "af_ctx_set_peers_ipc")
+        dist.all_gather_object(allh, mine, group=group)
+        ok = all(x is not None for x in allh)
+        if ok:
+            buf = (ctypes.c_uint8 * (L.AF_IPC_HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(allh))
+            with torch.cuda.device(self.device):
+                ok = lib.af_ctx_set_peers_ipc(self._h, buf) == L.AF_OK
+        oks = [None] * self.world
+        dist.all_gather_object(oks, ok, group=group)
+        if not all(oks):
+            lib.af_ctx_clear_peers(self._h)
+            return False
+        return True
 
     def exchange_rows(self):
         """float64 view [world, L] of the exchange matrix inside the scratch buffer."""

@@ -678,6 +678,12 @@ af_status af_ctx_set_peers_ipc(af_ctx *c, const void *handles) {
   return upload_peers(c, scratch_of);
 }
 
+af_status af_ctx_clear_peers(af_ctx *c) {
+  if (!c) return fail(AF_EINVAL, "NULL ctx");
+  c->peers = false;  // mappings stay open until af_ctx_destroy
+  return AF_OK;
+}
+
 af_status af_ctx_set_peers_local(af_ctx *c, af_ctx *const *peers) {
   if (!c || !peers) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");

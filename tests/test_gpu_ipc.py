@@ -33,7 +33,7 @@ def _worker(rank, world, port, q):
         # ragged layout: the two shards have different tile counts
         lay = uniform_layout(1_000_003, 7, pre=123_457, head=777)
         fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="bf16", rank=rank, world=world)
-        fm.set_peers_ipc()
+        assert fm.set_peers_ipc()
         oz = O.Freezer(lay.offsets, lay.kinds, O.DT_BF16)
         scale = np.random.default_rng(5).random(lay.n_segments) * 0.5 + 0.3
         out = []
