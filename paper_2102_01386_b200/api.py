@@ -108,8 +108,6 @@ class FreezingModule:
         h = (ctypes.c_uint8 * L.AF_IPC_HANDLE_BYTES)()
         with torch.cuda.device(self.device):
             mine = bytes(h) if lib.af_ctx_exchange_ipc_handle(self._h, h) == L.AF_OK else None
-        if mine is not None:
-            mine = bytes(h)
         allh = [None] * self.world
         dist.all_gather_object(allh, mine, group=group)
         ok = all(x is not None for x in allh)
