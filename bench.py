@@ -239,6 +239,9 @@ def run_ours(args, rank, world, local):
     # one committed interval so that T = 1 and every dry-run decide does the full test,
     # then one committed accumulate step so that Delta is armed: every dry-run
     # accumulate reads+writes Delta and every dry-run interval end reads it.
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()   # ranks enter the first exchange together (the in-kernel wait is bounded)
     fm.layer_norms(grads[0])
     fm.layer_norms(grads[1], interval_end=True)
     fm.update_and_decide()
