@@ -681,3 +681,51 @@ def test_peer_exchange_survives_state_restore():
         fm.set_state(b)
     again = interval(3)
     assert first == again and not any(d["flags"] & 32 for d in again)
+
+
+# ---------------------------------------------------------------- randomized differential test
+
+@pytest.mark.parametrize("seed", range(6))
+def test_randomized_layouts_and_configs(seed):
+    """Random layouts (up to AF_MAX_SEGMENTS segments, sub-vector segments,
+    with/without PRE and HEAD), dtypes, accumulation readings, percentiles and
+    interval lengths, optionally sharded over P fake ranks: every record matches
+    the oracle within the contract and Delta stays bit-exact."""
+    rng = np.random.default_rng(1000 + seed)
+    L = int(rng.choice([1, 2, 7, 64, 200, 254]))
+    pre = int(rng.integers(0, 2)) * int(rng.integers(1, 50_000))
+    head = int(rng.integers(0, 2)) * int(rng.integers(1, 3_000))
+    n = pre + head + L * int(rng.integers(3, 3_000))
+    lay = uniform_layout(n, L, pre=pre, head=head)
+    dt = str(rng.choice(["f32", "bf16"]))
+    acc = str(rng.choice(["delta", "delta", "step_sumsq"]))
+    N = float(rng.choice([25.0, 50.0, 75.0, rng.uniform(5, 95)]))
+    P = int(rng.choice([1, 1, 3]))
+    kw = dict(percentile=N, acc_mode=acc)
+    fms = [_fm(lay, dt, rank=r, world=P, **kw) for r in range(P)]
+    oz = _oracle(lay, dt, **kw)
+    step = _decaying_step(lay, dt, 2000 + seed)
+    for T in range(int(rng.integers(4, 8))):
+        S = int(rng.integers(1, 4))
+        for t in range(S):
+            gnp = step(T, t)
+            g = to_device_grad(gnp, dt)
+            end = t == S - 1
+            for fm in fms:
+                if end and P == 1:
+                    fm.interval_end(g)
+                else:
+                    fm.layer_norms(g, interval_end=end)
+            oz.layer_norms(gnp, end)
+            if not end and acc == "delta" and P == 1:
+                torch.cuda.synchronize()
+                assert np.array_equal(delta_host(fms[0], lay.n), oz.delta)
+        if P > 1:
+            rows = [fm.exchange_rows() for fm in fms]
+            gathered = torch.stack([rows[r][r].clone() for r in range(P)])
+            for fm, rw in zip(fms, rows):
+                rw.copy_(gathered)
+                fm.update_and_decide()
+        decs = [fm.decision() for fm in fms]
+        assert all(canon(d) == canon(decs[0]) for d in decs[1:])
+        compare_records(decs[0], oz.update_and_decide(), lay.n_segments, tag=f"seed={seed} T={T}")
