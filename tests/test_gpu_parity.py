@@ -685,7 +685,7 @@ def test_peer_exchange_survives_state_restore():
 
 # ---------------------------------------------------------------- randomized differential test
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(16))
 def test_randomized_layouts_and_configs(seed):
     """Random layouts (up to AF_MAX_SEGMENTS segments, sub-vector segments,
     with/without PRE and HEAD), dtypes, accumulation readings, percentiles and
