@@ -34,8 +34,9 @@ def _oracle(lay, dt, **kw):
     return O.Freezer(lay.offsets, lay.kinds, O.DT_BF16 if dt == "bf16" else O.DT_F32, **m)
 
 
-def run_both(lay, dt, step_fn, schedule, check_delta=True, **kw):
-    """schedule = list of steps-per-interval; step_fn(T, t) -> numpy gradient."""
+def run_both(lay, dt, step_fn, schedule, check_delta=True, fused=False, **kw):
+    """schedule = list of steps-per-interval; step_fn(T, t) -> numpy gradient.
+    fused=True ends each interval with af_interval_end (the bench's launch)."""
     fm, oz = _fm(lay, dt, **kw), _oracle(lay, dt, **kw)
     n_local = lay.n
     ties, recs = 0, []
@@ -43,12 +44,16 @@ def run_both(lay, dt, step_fn, schedule, check_delta=True, **kw):
         for t in range(S):
             g = step_fn(T, t)
             end = t == S - 1
-            fm.layer_norms(to_device_grad(g, dt), interval_end=end)
+            if end and fused:
+                fm.interval_end(to_device_grad(g, dt))
+            else:
+                fm.layer_norms(to_device_grad(g, dt), interval_end=end)
             oz.layer_norms(g, end)
             if check_delta and not end and oz.delta is not None:
                 torch.cuda.synchronize()
                 assert np.array_equal(delta_host(fm, n_local), oz.delta), f"Delta T={T} t={t}"
-        fm.update_and_decide()
+        if not fused:
+            fm.update_and_decide()
         gr, orr = fm.decision(), oz.update_and_decide()
         ties += compare_records(gr, orr, lay.n_segments, tag=f"T={T}")
         recs.append((gr, orr))
@@ -307,7 +312,7 @@ def test_bert_full_size_parity(which, dt):
     every per-layer norm vs the oracle on the same generated gradients."""
     lay = bert_layout(which)
     step = lambda T, t: bert_grad_step(lay, 0, T, t, dtype=dt)  # noqa: E731
-    recs, ties, fm, oz = run_both(lay, dt, step, [2, 2, 1], check_delta=False)
+    recs, ties, fm, oz = run_both(lay, dt, step, [2, 2, 1], check_delta=False, fused=True)
     # Delta after one accumulate step equals the oracle's bit for bit
     g0, g1 = step(5, 0), step(5, 1)
     fm.layer_norms(to_device_grad(g0, dt))
@@ -729,3 +734,24 @@ def test_randomized_layouts_and_configs(seed):
         decs = [fm.decision() for fm in fms]
         assert all(canon(d) == canon(decs[0]) for d in decs[1:])
         compare_records(decs[0], oz.update_and_decide(), lay.n_segments, tag=f"seed={seed} T={T}")
+
+
+def test_maximum_segment_count_and_zero_gradients():
+    """AF_MAX_SEGMENTS = 256 segments (PRE + 254 POOL + HEAD); then all-zero
+    gradients: norms 0, eta 0 (Q7), threshold 0, nothing freezes (strict <), no NaN."""
+    lay = uniform_layout(256 * 777 + 5, 254, pre=901, head=333)
+    assert lay.n_segments == 256
+    recs, _, fm, oz = run_both(lay, "bf16", _decaying_step(lay, "bf16", 77), [2, 2, 2], fused=True)
+    zero = lambda T, t: np.zeros(lay.n, np.uint16)  # noqa: E731
+    f0 = recs[-1][0]["boundary_after"]
+    lay2 = lay
+    fm2, oz2 = _fm(lay2, "bf16"), _oracle(lay2, "bf16")
+    for T in range(3):
+        g = to_device_grad(zero(T, 0), "bf16")
+        fm2.interval_end(g)
+        oz2.layer_norms(zero(T, 0), True)
+        gr, orr = fm2.decision(), oz2.update_and_decide()
+        compare_records(gr, orr, lay2.n_segments, tag=f"zero T={T}")
+        assert gr["boundary_after"] == 0 and all(v == 0.0 for v in gr["norm"])
+        assert not (gr["flags"] & O.FLAG_NONFINITE)
+    assert f0 >= 0
