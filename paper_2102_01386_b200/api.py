@@ -77,7 +77,8 @@ class FreezingModule:
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         with torch.cuda.device(dev):
-            self.accum = torch.empty(max(1, self.accum_bytes), dtype=torch.uint8, device=dev)
+            # zeroed so that never-accumulated (frozen-from-the-start) elements read as 0
+            self.accum = torch.zeros(max(1, self.accum_bytes), dtype=torch.uint8, device=dev)
             self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device=dev)
             check(lib.af_ctx_bind(self._h, c_void_p(self.accum.data_ptr() if self.accum_bytes else 0),
                                   c_void_p(self.scratch.data_ptr())), "af_ctx_bind")
