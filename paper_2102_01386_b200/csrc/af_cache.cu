@@ -29,6 +29,9 @@ namespace {
 #ifndef AF_CACHE_CHUNK
 #define AF_CACHE_CHUNK (32 * 1024)
 #endif
+#ifndef AF_CACHE_SMALL_FACTOR  // calls with <= factor x (TMA grid) items take the direct-copy path
+#define AF_CACHE_SMALL_FACTOR 1
+#endif
 #ifndef AF_CACHE_CTAS_PER_SM
 #define AF_CACHE_CTAS_PER_SM 2
 #endif
@@ -130,6 +133,79 @@ __device__ void pump(const Desc *descs, int m, unsigned char *stage_buf, uint64_
   seq = base + n_ok;
 }
 
+// Item j = (row j / n_chunks, chunk j % n_chunks): owner / range checks, the
+// record's address, meta update (put) or hit + evict-on-read bookkeeping (get).
+// Returns the copy to perform (ok = 0: nothing to copy).
+template <bool PUT>
+__device__ __forceinline__ Desc describe_item(const CacheParams &p, int64_t j) {
+  const int i = static_cast<int>(j / p.n_chunks);
+  const int c = static_cast<int>(j % p.n_chunks);
+  const int64_t id = p.ids[i];
+  Desc dsc{nullptr, nullptr, 0u, 0u};
+  bool ok = true;
+  char *payload = p.payload;
+  CacheMeta *meta = p.meta;
+  if (id < 0 || id >= p.num_examples) {
+    if (c == 0) atomicOr(p.err, AF_CACHE_ERR_RANGE);
+    ok = false;
+  } else if (p.peer_payload) {  // global: the owner's store, possibly a peer's
+    const int owner = static_cast<int>(id % p.world);
+    payload = p.peer_payload[owner];
+    meta = p.peer_meta[owner];
+  } else if (id % p.world != p.rank) {
+    if (c == 0) atomicOr(p.err, AF_CACHE_ERR_OWNER);
+    ok = false;
+  }
+  const int64_t off = static_cast<int64_t>(c) * p.chunk_bytes;
+  const int64_t rem = p.row_bytes - off;
+  dsc.bytes = static_cast<uint32_t>(rem < p.chunk_bytes ? rem : p.chunk_bytes);
+  if (ok && p.rowslot) {
+    // tiered: the plan kernel resolved the row's slot (and its meta / eviction)
+    const int32_t slot = p.rowslot[i];
+    if (slot >= 0) {
+      char *rec = (slot < p.hbm_rows ? p.payload + static_cast<int64_t>(slot) * p.row_bytes
+                                     : p.host + (static_cast<int64_t>(slot) - p.hbm_rows) * p.row_bytes) +
+                  off;
+      if (PUT) {
+        dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+        dsc.dst = rec;
+      } else {
+        dsc.src = rec;
+        dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+      }
+      dsc.ok = 1u;
+    }
+  } else if (ok) {
+    const int64_t slot = id / p.world;
+    char *rec = payload + slot * p.row_bytes + off;
+    if (PUT) {
+      dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+      dsc.dst = rec;
+      dsc.ok = 1u;
+      if (c == 0) *reinterpret_cast<int2 *>(meta + slot) = make_int2(p.depth, 1);  // {depth, valid}
+    } else {
+      const int4 mv = __ldcg(reinterpret_cast<const int4 *>(meta) + slot);  // {depth, valid, readers, -}
+      const bool hit = mv.y != 0;
+      if (c == 0) p.depth_out[i] = hit ? mv.x : -1;
+      if (hit) {
+        dsc.src = rec;
+        dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+        dsc.ok = 1u;
+        // evict on read once every chunk of the row has read the record
+        __threadfence();
+        const unsigned int seen = atomicAdd(&meta[slot].readers, 1u);
+        if (seen == static_cast<unsigned int>(p.n_chunks) - 1u) {
+          if (mv.x < p.cur_boundary) meta[slot].valid = 0;
+          meta[slot].readers = 0u;
+        }
+      }
+    }
+  } else if (!PUT && c == 0 && !p.rowslot) {
+    p.depth_out[i] = -1;  // (tiered: the plan kernel wrote depth_out)
+  }
+  return dsc;
+}
+
 template <bool PUT>
 __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -152,71 +228,7 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
     const int m = static_cast<int>((my_items - kb) < kMaxDesc ? (my_items - kb) : kMaxDesc);
     for (int q = lane; q < m; q += 32) {
       const int64_t j = blockIdx.x + (kb + q) * G;
-      const int i = static_cast<int>(j / p.n_chunks);
-      const int c = static_cast<int>(j % p.n_chunks);
-      const int64_t id = p.ids[i];
-      Desc dsc{nullptr, nullptr, 0u, 0u};
-      bool ok = true;
-      char *payload = p.payload;
-      CacheMeta *meta = p.meta;
-      if (id < 0 || id >= p.num_examples) {
-        if (c == 0) atomicOr(p.err, AF_CACHE_ERR_RANGE);
-        ok = false;
-      } else if (p.peer_payload) {  // global: the owner's store, possibly a peer's
-        const int owner = static_cast<int>(id % p.world);
-        payload = p.peer_payload[owner];
-        meta = p.peer_meta[owner];
-      } else if (id % p.world != p.rank) {
-        if (c == 0) atomicOr(p.err, AF_CACHE_ERR_OWNER);
-        ok = false;
-      }
-      const int64_t off = static_cast<int64_t>(c) * p.chunk_bytes;
-      const int64_t rem = p.row_bytes - off;
-      dsc.bytes = static_cast<uint32_t>(rem < p.chunk_bytes ? rem : p.chunk_bytes);
-      if (ok && p.rowslot) {
-        // tiered: the plan kernel resolved the row's slot (and its meta / eviction)
-        const int32_t slot = p.rowslot[i];
-        if (slot >= 0) {
-          char *rec = (slot < p.hbm_rows ? p.payload + static_cast<int64_t>(slot) * p.row_bytes
-                                         : p.host + (static_cast<int64_t>(slot) - p.hbm_rows) * p.row_bytes) +
-                      off;
-          if (PUT) {
-            dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
-            dsc.dst = rec;
-          } else {
-            dsc.src = rec;
-            dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
-          }
-          dsc.ok = 1u;
-        }
-      } else if (ok) {
-        const int64_t slot = id / p.world;
-        char *rec = payload + slot * p.row_bytes + off;
-        if (PUT) {
-          dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
-          dsc.dst = rec;
-          dsc.ok = 1u;
-          if (c == 0) *reinterpret_cast<int2 *>(meta + slot) = make_int2(p.depth, 1);  // {depth, valid}
-        } else {
-          const int4 mv = __ldcg(reinterpret_cast<const int4 *>(meta) + slot);  // {depth, valid, readers, -}
-          const bool hit = mv.y != 0;
-          if (c == 0) p.depth_out[i] = hit ? mv.x : -1;
-          if (hit) {
-            dsc.src = rec;
-            dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
-            dsc.ok = 1u;
-            // evict on read once every chunk of the row has read the record
-            __threadfence();
-            const unsigned int seen = atomicAdd(&meta[slot].readers, 1u);
-            if (seen == static_cast<unsigned int>(p.n_chunks) - 1u) {
-              if (mv.x < p.cur_boundary) meta[slot].valid = 0;
-              meta[slot].readers = 0u;
-            }
-          }
-        }
-      } else if (!PUT && c == 0 && !p.rowslot) {
-        p.depth_out[i] = -1;  // (tiered: the plan kernel wrote depth_out)
-      }
+      const Desc dsc = describe_item<PUT>(p, j);
       descs[q] = dsc;
     }
     __syncwarp();
@@ -227,6 +239,44 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
   if (lane == 0) bulk_wait_all();  // all stores complete before the CTA retires its shared memory
 }
 
+
+// Small calls (no more items than 2 CTAs per SM): one 256-thread CTA per item
+// copies its <= 32 KiB chunk with 16-byte loads, all in flight at once -- no
+// shared-memory ring to fill, so the call costs about one load round trip.
+// The paper's batches are small (6 examples per GPU), so this is the
+// latency path.
+constexpr int kSmallThreads = 256;
+
+template <bool PUT>
+__global__ void __launch_bounds__(kSmallThreads) cache_small_kernel(const CacheParams p) {
+  __shared__ Desc s_d;
+  pdl_wait();
+  const int64_t n_items = static_cast<int64_t>(p.n) * p.n_chunks;
+  for (int64_t j = blockIdx.x; j < n_items; j += gridDim.x) {
+    if (threadIdx.x == 0) s_d = describe_item<PUT>(p, j);
+    __syncthreads();
+    const Desc d = s_d;
+    if (d.ok) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(d.src);
+      uint4 *dst = reinterpret_cast<uint4 *>(d.dst);
+      const int nv = static_cast<int>(d.bytes / 16);
+      constexpr int V = (kChunk / 16 + kSmallThreads - 1) / kSmallThreads;
+      uint4 v[V];
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const int k = threadIdx.x + u * kSmallThreads;
+        if (k < nv) v[u] = __ldcs(src + k);
+      }
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const int k = threadIdx.x + u * kSmallThreads;
+        if (k < nv) __stcs(dst + k, v[u]);
+      }
+    }
+    __syncthreads();
+  }
+  pdl_launch_dependents();
+}
 
 // Tiered-mode plan (one CTA, 1024 threads): resolves every row of the call in call
 // order with block-wide exclusive scans, so slot allocation and freeing are
@@ -346,6 +396,10 @@ static int launch_cache(const CacheParams &p0, int grid, void *stream) {
   p.chunk_bytes = kChunk;
   p.n_chunks = static_cast<int32_t>((p.row_bytes + kChunk - 1) / kChunk);
   const int64_t items = static_cast<int64_t>(p.n) * p.n_chunks;
+  if (items <= static_cast<int64_t>(grid) * AF_CACHE_SMALL_FACTOR) {
+    return static_cast<int>(launch_pdl(cache_small_kernel<PUT>, dim3(static_cast<unsigned>(items)),
+                                       dim3(kSmallThreads), 0, static_cast<cudaStream_t>(stream), p));
+  }
   if (items < grid) grid = static_cast<int>(items);
   if (grid < 1) grid = 1;
   const int smem = cache_smem_bytes();

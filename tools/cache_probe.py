@@ -18,7 +18,7 @@ def main():
     c = af.ActivationCache(num, rb)
     src_all = torch.randint(0, 256, (4096, rb), dtype=torch.uint8, device="cuda")
     out = {}
-    for B in (32, 256, 1024, 4096):
+    for B in (6, 32, 48, 256, 1024, 4096):
         ids = torch.randperm(num, device="cuda")[:B].contiguous()
         src = src_all[:B]
         dst = torch.empty_like(src)
