@@ -29,9 +29,6 @@ namespace {
 #ifndef AF_CACHE_CHUNK
 #define AF_CACHE_CHUNK (32 * 1024)
 #endif
-#ifndef AF_CACHE_SMALL_FACTOR  // calls with <= factor x (TMA grid) items take the direct-copy path
-#define AF_CACHE_SMALL_FACTOR 1
-#endif
 #ifndef AF_CACHE_CTAS_PER_SM
 #define AF_CACHE_CTAS_PER_SM 2
 #endif
@@ -240,44 +237,6 @@ __global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
 }
 
 
-// Small calls (no more items than 2 CTAs per SM): one 256-thread CTA per item
-// copies its <= 32 KiB chunk with 16-byte loads, all in flight at once -- no
-// shared-memory ring to fill, so the call costs about one load round trip.
-// The paper's batches are small (6 examples per GPU), so this is the
-// latency path.
-constexpr int kSmallThreads = 256;
-
-template <bool PUT>
-__global__ void __launch_bounds__(kSmallThreads) cache_small_kernel(const CacheParams p) {
-  __shared__ Desc s_d;
-  pdl_wait();
-  const int64_t n_items = static_cast<int64_t>(p.n) * p.n_chunks;
-  for (int64_t j = blockIdx.x; j < n_items; j += gridDim.x) {
-    if (threadIdx.x == 0) s_d = describe_item<PUT>(p, j);
-    __syncthreads();
-    const Desc d = s_d;
-    if (d.ok) {
-      const uint4 *src = reinterpret_cast<const uint4 *>(d.src);
-      uint4 *dst = reinterpret_cast<uint4 *>(d.dst);
-      const int nv = static_cast<int>(d.bytes / 16);
-      constexpr int V = (kChunk / 16 + kSmallThreads - 1) / kSmallThreads;
-      uint4 v[V];
-#pragma unroll
-      for (int u = 0; u < V; ++u) {
-        const int k = threadIdx.x + u * kSmallThreads;
-        if (k < nv) v[u] = __ldcs(src + k);
-      }
-#pragma unroll
-      for (int u = 0; u < V; ++u) {
-        const int k = threadIdx.x + u * kSmallThreads;
-        if (k < nv) __stcs(dst + k, v[u]);
-      }
-    }
-    __syncthreads();
-  }
-  pdl_launch_dependents();
-}
-
 // Tiered-mode plan (one CTA, 1024 threads): resolves every row of the call in call
 // order with block-wide exclusive scans, so slot allocation and freeing are
 // deterministic.  put: existing record -> its slot (re-cache deeper); new id ->
@@ -396,10 +355,6 @@ static int launch_cache(const CacheParams &p0, int grid, void *stream) {
   p.chunk_bytes = kChunk;
   p.n_chunks = static_cast<int32_t>((p.row_bytes + kChunk - 1) / kChunk);
   const int64_t items = static_cast<int64_t>(p.n) * p.n_chunks;
-  if (items <= static_cast<int64_t>(grid) * AF_CACHE_SMALL_FACTOR) {
-    return static_cast<int>(launch_pdl(cache_small_kernel<PUT>, dim3(static_cast<unsigned>(items)),
-                                       dim3(kSmallThreads), 0, static_cast<cudaStream_t>(stream), p));
-  }
   if (items < grid) grid = static_cast<int>(items);
   if (grid < 1) grid = 1;
   const int smem = cache_smem_bytes();

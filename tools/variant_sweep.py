@@ -15,8 +15,6 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
-    "nosmall": "-DAF_CACHE_SMALL_FACTOR=0",
-    "small2": "-DAF_CACHE_SMALL_FACTOR=2",
     "taper_off": "-DAF_TILE_BIG_MULT=1",
     "taper4": "-DAF_TILE_BIG_MULT=4",
     "taper8_90": "-DAF_TILE_BIG_FRAC_PCT=90",
