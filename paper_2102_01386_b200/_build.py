@@ -11,8 +11,8 @@ import sysconfig
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = ["af_api.cpp", "af_norms.cu", "af_decide.cu", "af_cache.cu"]
-HEADERS = ["af_internal.h"]
+SOURCES = ["af_host.cpp", "af_ctx.cpp", "af_cache_api.cpp", "af_norms.cu", "af_decide.cu", "af_cache.cu"]
+HEADERS = ["af_internal.h", "af_host.h", "af_decide.cuh"]
 LIB = os.path.join(PKG, "libautofreeze.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

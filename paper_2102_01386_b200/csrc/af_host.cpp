@@ -1,0 +1,83 @@
+// af_host.cpp -- shared host helpers and the stateless entry points of the C ABI.
+#include "af_host.h"
+
+#include <cstring>
+
+namespace af {
+namespace {
+thread_local std::string g_last_error;
+}  // namespace
+
+void set_last_error(const std::string &msg) { g_last_error = msg; }
+const char *g_last_error_cstr() { return g_last_error.c_str(); }
+
+af_status fail(af_status s, const char *what) {
+  g_last_error = what;
+  return s;
+}
+
+af_status cuda_fail(cudaError_t e, const char *where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return AF_ECUDA;
+}
+
+int device_sm_count(int *sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  return static_cast<int>(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
+}
+
+af_status ipc_export(const void *ptr, IpcRef *out) {
+  typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  AF_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(AF_ECUDA, "cuMemGetAddressRange entry point not found");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<GetRange>(fn)(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0)
+    return fail(AF_ECUDA, "cuMemGetAddressRange failed");
+  AF_CUDA(cudaIpcGetMemHandle(&out->h, reinterpret_cast<void *>(base)), "cudaIpcGetMemHandle");
+  out->offset = reinterpret_cast<unsigned long long>(ptr) - base;
+  return AF_OK;
+}
+
+af_status ipc_import(const IpcRef &r, std::vector<void *> &opened, char **out) {
+  void *p = nullptr;
+  AF_CUDA(cudaIpcOpenMemHandle(&p, r.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  opened.push_back(p);
+  *out = static_cast<char *>(p) + r.offset;
+  return AF_OK;
+}
+
+}  // namespace af
+
+using namespace af;
+
+extern "C" {
+
+const char *af_status_str(af_status s) {
+  switch (s) {
+    case AF_OK: return "AF_OK";
+    case AF_EINVAL: return "AF_EINVAL";
+    case AF_ESTATE: return "AF_ESTATE";
+    case AF_EWORKSPACE: return "AF_EWORKSPACE";
+    case AF_ECUDA: return "AF_ECUDA";
+    case AF_ENCCL: return "AF_ENCCL";
+    case AF_ENONFINITE: return "AF_ENONFINITE";
+    case AF_EOWNER: return "AF_EOWNER";
+    case AF_ERANGE: return "AF_ERANGE";
+  }
+  return "AF_UNKNOWN";
+}
+
+const char *af_last_error(void) { return af::g_last_error_cstr(); }
+const char *af_version(void) { return "0.1.0"; }
+
+int af_should_cache(int32_t frozen_layers, double t_layer_fwd_s, double t_batch_read_s) {
+  if (frozen_layers <= 0 || !(t_layer_fwd_s >= 0.0) || !(t_batch_read_s >= 0.0)) return 0;
+  return static_cast<double>(frozen_layers) * t_layer_fwd_s > t_batch_read_s ? 1 : 0;
+}
+
+}  // extern "C"
