@@ -50,6 +50,17 @@ def _type7_exact(values, N):
     return x[lo] + (h - lo) * (x[lo + 1] - x[lo])
 
 
+def _type7_bound(values, N):
+    """Rounding bound of the float evaluation: a few ulps of the result plus the
+    error of h = (n-1)*(N/100) (~2 ulp(h)) carried by the gap it interpolates."""
+    x = sorted(values)
+    h = (len(x) - 1) * (N / 100.0)
+    lo = min(int(math.floor(h)), len(x) - 1)
+    gap = (x[lo + 1] - x[lo]) if lo + 1 < len(x) else 0.0
+    want = float(_type7_exact(values, N))
+    return Fraction(4 * math.ulp(want) + 4 * math.ulp(h) * gap + 1e-300)
+
+
 @pytest.mark.parametrize("seed", range(20))
 def test_linear_percentile_matches_exact_definition(seed):
     rng = np.random.default_rng(seed)
@@ -58,8 +69,8 @@ def test_linear_percentile_matches_exact_definition(seed):
     for N in (25.0, 50.0, 75.0, 33.3, 90.0, 100.0, 1.0):
         got = O.percentile_threshold(vals, N)
         want = _type7_exact(vals, N)
-        # the float computation rounds a handful of times: a few ulps of the value
-        assert abs(Fraction(got) - want) <= 4 * math.ulp(float(want)) + 1e-300
+        # the float computation rounds a handful of times
+        assert abs(Fraction(got) - want) <= _type7_bound(vals, N)
 
 
 def test_linear_percentile_dyadic_exact():
