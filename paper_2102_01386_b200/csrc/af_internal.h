@@ -55,6 +55,7 @@ struct DevState {
   uint32_t sticky;   // reserved
   int32_t pad;
   unsigned long long epoch;      // peer-exchange epoch: interval ends seen (identical on all ranks)
+  unsigned long long tmark[4];   // AF_TIMING builds: %globaltimer at kernel start / tail start / after sums / end
   double prev[AF_MAX_SEGMENTS];  // ||Delta_{T-1,l}||
 };
 

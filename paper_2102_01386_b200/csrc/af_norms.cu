@@ -31,6 +31,14 @@
 // Tunables (compile-time; defaults chosen from the B200 variant sweep in
 // profiles/r01_v3_variants.jsonl): vectors in flight per thread
 // and load cache hints.
+#ifndef AF_TIMING
+#define AF_TIMING 0
+#endif
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 #ifndef AF_U_END
 #define AF_U_END 4
 #endif
@@ -317,6 +325,7 @@ template <int MODE>
 __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, double *s_red_unused) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   (void)s_red_unused;
+  if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
   // peer exchange: this interval end's epoch selects the exchange buffer
   const bool xchg = p.xworld > 1 && p.end;
   __shared__ unsigned long long s_epoch;
@@ -386,9 +395,17 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
     __syncthreads();
     if (s_timeout && tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 1u);
   }
+  if (AF_TIMING) {
+    __syncthreads();
+    if (tid == 0) const_cast<DevState *>(p.state)->tmark[2] = gtimer();
+  }
   if (p.fuse_decide) {
     __syncthreads();
     decide_block(p.dec);
+  }
+  if (AF_TIMING) {
+    __syncthreads();
+    if (tid == 0) const_cast<DevState *>(p.state)->tmark[3] = gtimer();
   }
 }
 
@@ -401,6 +418,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_wait();  // f, Delta and the counters are written by the preceding kernels
+  if (AF_TIMING && blockIdx.x == 0 && threadIdx.x == 0) const_cast<DevState *>(p.state)->tmark[0] = gtimer();
   int f = p.state->f;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int first_tile = p.first_tile_of_f[f];
