@@ -48,7 +48,7 @@ __all__ = [
     "FLAG_DRY_RUN", "CACHE_ERR_RANGE", "CACHE_ERR_OWNER", "MISS",
     "widen", "accumulate", "segment_sumsq", "layer_norm", "eta", "percentile_threshold",
     "prefix_scan", "should_cache", "active_segments", "Freezer", "Cache", "OracleStateError",
-    "adamw_constants", "adamw_step",
+    "adamw_constants", "adamw_step", "reduce_gradients",
 ]
 
 SEG_PRE, SEG_POOL, SEG_HEAD = 0, 1, 2
@@ -182,6 +182,21 @@ def adamw_step(p, m, v, g32, c):
     v[...] = v * c["beta2"] + (g32 * g32) * c["omb2"]
     den = np.sqrt(v) / c["sqrt_bc2"] + c["eps"]
     p -= c["step_size"] * (m / den)
+
+
+# ---------------------------------------------------------------- gradient sync (NEXT 1, ZeRO form)
+
+def reduce_gradients(grads, grad_dtype, scale):
+    """The data-parallel gradient the freezing test runs on (the decision
+    is taken on DDP-synchronised gradients; DDP all-reduces the
+    gradient every iteration): gs = fl(sum_r g_r) * scale, every rank's gradient
+    widened to fp32 and added in rank order 0..P-1 with one fp32 rounding per
+    add, then ONE fp32 multiply by fp32(scale) (scale = 1/P: DDP's average).
+    Reading Q27 (the paper fixes neither order nor precision of the sum)."""
+    s = widen(grads[0], grad_dtype).copy()
+    for g in grads[1:]:
+        s = s + widen(g, grad_dtype)            # fp32 + fp32 -> fp32, RNE
+    return s * np.float32(scale)
 
 
 # ---------------------------------------------------------------- freezing module

@@ -428,3 +428,36 @@ def test_adamw_first_step_closed_form():
     O.adamw_step(p, m, v, g, O.adamw_constants(1e-3, 0.9, 0.999, 1e-8, 0.0, 1))
     want = -1e-3 * g.astype(np.float64) / (np.abs(g.astype(np.float64)) + 1e-8)
     np.testing.assert_allclose(p, want, rtol=1e-6)
+
+
+# ------------------------------------------------------------------ gradient sync (NEXT 1, ZeRO form)
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_reduce_gradients_dyadic_exact(P):
+    # k/1024 with |k| < 2^20: every partial sum of <= 8 terms is exact in fp32,
+    # and scale = 1/8 is a power of two -- the result is the exact rational
+    rng = np.random.default_rng(P)
+    ks = rng.integers(-(1 << 20) + 1, 1 << 20, size=(P, 257))
+    grads = [(k / 1024.0).astype(np.float32) for k in ks]
+    got = O.reduce_gradients(grads, O.DT_F32, 0.125)
+    want = [Fraction(int(sum(int(x) for x in col)), 1024 * 8) for col in ks.T]
+    assert all(Fraction(float(g)) == w for g, w in zip(got, want))
+
+
+def test_reduce_gradients_rank_order_rounding():
+    # 1 + 2^-24 rounds (ties-to-even) back to 1 in fp32: the rank-order sum
+    # 1 + 2^-24 + 2^-24 is 1, whereas any other association (or an fp64 sum)
+    # gives 1 + 2^-23 -- pins the order and the per-add fp32 rounding (Q27)
+    e = np.float32(2.0 ** -24)
+    grads = [np.array([1.0], np.float32), np.array([e], np.float32), np.array([e], np.float32)]
+    assert O.reduce_gradients(grads, O.DT_F32, 1.0)[0] == np.float32(1.0)
+    assert O.reduce_gradients(grads[::-1], O.DT_F32, 1.0)[0] == np.float32(1.0 + 2.0 ** -23)
+
+
+def test_reduce_gradients_bf16_and_scale_rounding():
+    # bf16 bit patterns widen exactly; the scale is applied once, rounded to fp32
+    bits = [np.array([0x3F80, 0x4000, 0xBF80], np.uint16), np.array([0x3F80, 0x3F80, 0x3F80], np.uint16)]
+    got = O.reduce_gradients(bits, O.DT_BF16, 1.0 / 3.0)
+    s = np.array([2.0, 3.0, 0.0], np.float32)             # 1+1, 2+1, -1+1
+    assert np.array_equal(got, s * np.float32(1.0 / 3.0))
+    assert got[1] == np.float32(1.0)                      # fl(3 * fl(1/3)) = 1 in fp32
