@@ -347,7 +347,10 @@ def run_ours(args, rank, world, local):
                      "frac": round(ach / peak, 4), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_rank[dom],
                      **ncu_traffic(args.workload if world == 1 else None, dom)},
-        "gpu_launches": (4 if (world == 1 or exchange == "p2p") else 5) * args.steps,
+        # accumulate + interval end (+ wide finalize) (+ decide kernel, NCCL all-gather) + cache get + put
+        "gpu_launches": (4 + (1 if info["n_fin_ctas"] else 0)
+                         + (1 if (args.unfused or (world > 1 and exchange != "p2p")) else 0)
+                         + (1 if (world > 1 and exchange != "p2p") else 0)) * args.steps,
         "clocks": clk.summary(),
     }
     if not args.no_cache_sweep:

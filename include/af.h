@@ -142,6 +142,8 @@ typedef struct {
   int32_t first_tile_of_pool[AF_MAX_SEGMENTS + 1]; /* first active tile when f = j frozen */
   int32_t n_tiles_acc;              /* tiles of the accumulate kernel (finer, no partials) */
   int32_t tile_elems_acc;
+  int32_t n_fin_ctas;               /* > 0: interval ends launch a second, wide finalize
+                                       kernel of this many CTAs after the streaming kernel */
 } af_info;
 
 typedef struct af_ctx af_ctx;
@@ -220,11 +222,11 @@ AF_API af_status af_update_and_decide(af_ctx *ctx, uint32_t flags, af_decision *
 
 /* Fused interval end: exactly af_layer_norms(AF_INTERVAL_END |
  * flags) followed by af_update_and_decide(flags), same results and state.  With
- * world == 1 it is ONE kernel launch: the CTA that completes a segment's last
- * tile sums that segment, and the grid's last CTA runs the decision (no second
- * launch, no host involvement).  With world > 1: kernel, NCCL all-gather (when a
- * communicator is set; otherwise the caller must use the two-call form to fill
- * the exchange rows), decide kernel.  flags: AF_DRY_RUN only. */
+ * world == 1 or peers registered, no host involvement: the streaming kernel, then
+ * (af_info.n_fin_ctas > 0) a wide finalize kernel chained by programmatic
+ * dependent launch; the last CTA sums the segments, exchanges rows with the peers
+ * and runs the decision.  With world > 1 and only a communicator: kernel, NCCL
+ * all-gather, decide kernel.  flags: AF_DRY_RUN only. */
 AF_API af_status af_interval_end(af_ctx *ctx, const void *grad_dev, uint32_t flags, af_decision *out_host,
                                  void *stream);
 
@@ -248,6 +250,42 @@ typedef struct {
 AF_API af_status af_adamw_step(af_ctx *ctx, float *params_dev, float *exp_avg_dev, float *exp_avg_sq_dev,
                                const void *grad_dev, const af_adamw *hp, uint32_t flags, af_decision *out_host,
                                void *stream);
+
+/* Host only: cap the CTAs of the streaming kernels (0 = the persistent grid of
+ * occupancy x SMs).  For sharing the GPU with concurrent work, e.g. the ranks of
+ * a fused reduce-scatter tested on one GPU, whose kernels must be co-resident. */
+AF_API af_status af_ctx_set_max_ctas(af_ctx *ctx, int32_t max_ctas);
+
+/* SURVEY.md §8(f) NEXT 1, ZeRO form: the data-parallel gradient sync fused with
+ * the accumulate it feeds (PAPER.md P:44, P:288-290 -- DDP's gradient all-reduce,
+ * whose per-layer volume freezing removes; P:335 -- the test runs on the
+ * synchronised gradient).  Every rank registers its FULL flat gradient buffer
+ * (n_total elements of grad_dtype, 16-byte aligned, persistent: a DDP-style
+ * bucket); then one kernel per step and rank reads its shard [shard_begin,
+ * shard_end) of all `world` buffers over peer memory, and for each active
+ * element i
+ *     gs_i = fl( (..(g_0,i + g_1,i) + ..) + g_P-1,i ) * scale )   fp32, rank order
+ * writes gs_i to grad_shard_out_dev[i - shard_begin] (fp32, optional, 16-byte
+ * aligned; frozen segments untouched) and accumulates it exactly as af_layer_norms
+ * accumulates g (Delta += gs; AF_INTERVAL_END: the sums of squares of Delta + gs,
+ * peer exchange and decision as in af_interval_end).  scale = 1/world gives DDP's
+ * average.  The kernel opens with a cross-GPU epoch barrier (every rank's
+ * gradient is complete) and closes with another (no rank still reads this
+ * rank's buffer), so the caller may overwrite its gradient as soon as the stream
+ * passes the call.  A rank that never arrives (~seconds) sets a sticky flag: the
+ * next decision carries AF_DEC_EXCHANGE_TIMEOUT and is not committed.
+ * Requirements: acc_mode AF_ACC_DELTA, world <= 8, and with world > 1 the peers
+ * registered (af_ctx_set_peers_*: the barrier flags live in the scratch).
+ * Registration: af_ctx_grad_ipc_handle on every rank, all-gather the
+ * AF_IPC_HANDLE_BYTES handles, af_ctx_set_grad_peers_ipc (collective); or, for
+ * ranks in one process, af_ctx_set_grad_peers_local(grads_dev[world]).  Errors:
+ * AF_ESTATE (nothing registered / no peers / STEP_SUMSQ), AF_EINVAL (bad
+ * handle, alignment, non-finite scale, unknown flags). */
+AF_API af_status af_ctx_grad_ipc_handle(af_ctx *ctx, const void *grad_dev, void *handle_out);
+AF_API af_status af_ctx_set_grad_peers_ipc(af_ctx *ctx, const void *handles);
+AF_API af_status af_ctx_set_grad_peers_local(af_ctx *ctx, const void *const *grads_dev);
+AF_API af_status af_reduce_scatter_step(af_ctx *ctx, float scale, float *grad_shard_out_dev, uint32_t flags,
+                                        af_decision *out_host, void *stream);
 
 /* Synchronous.  Serialise / restore {T, f, prev norms, Delta-armed flag}
  * (checkpoint at interval boundaries is exact).  With buf == NULL, get_state

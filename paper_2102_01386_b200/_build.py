@@ -35,8 +35,18 @@ def nccl_dirs():
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
+STAMP = LIB + ".flags"   # the AF_NVCC_EXTRA the library was built with (git-ignored)
+
+
+def _extra():
+    return os.environ.get("AF_NVCC_EXTRA", "").strip()
+
+
 def _stale():
     if not os.path.exists(LIB):
+        return True
+    built = open(STAMP).read() if os.path.exists(STAMP) else ""
+    if built != _extra():
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "af.h"),
@@ -57,7 +67,7 @@ def build(force=False, verbose=False, ptxas_verbose=False):
            "-cudart", "static"]
     if ptxas_verbose:
         cmd += ["-Xptxas", "-v"]
-    cmd += os.environ.get("AF_NVCC_EXTRA", "").split()
+    cmd += _extra().split()
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
@@ -67,6 +77,8 @@ def build(force=False, verbose=False, ptxas_verbose=False):
     if r.returncode != 0:
         raise RuntimeError("nvcc failed building libautofreeze.so")
     os.replace(LIB + ".tmp", LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(_extra())
     return LIB
 
 

@@ -47,7 +47,8 @@ class AfInfo(ctypes.Structure):
                 ("n_total", c_int64), ("shard_begin", c_int64), ("shard_end", c_int64),
                 ("n_tiles", c_int32), ("tile_elems", c_int32),
                 ("first_tile_of_pool", c_int32 * (AF_MAX_SEGMENTS + 1)),
-                ("n_tiles_acc", c_int32), ("tile_elems_acc", c_int32)]
+                ("n_tiles_acc", c_int32), ("tile_elems_acc", c_int32),
+                ("n_fin_ctas", c_int32)]
 
 
 class AfAdamW(ctypes.Structure):
@@ -79,6 +80,11 @@ SIGNATURES = {
     "af_interval_end": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_adamw_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(AfAdamW), c_uint32,
                               c_void_p, c_void_p]),
+    "af_ctx_set_max_ctas": (c_int, [c_void_p, c_int32]),
+    "af_ctx_grad_ipc_handle": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "af_ctx_set_grad_peers_ipc": (c_int, [c_void_p, c_void_p]),
+    "af_ctx_set_grad_peers_local": (c_int, [c_void_p, c_void_p]),
+    "af_reduce_scatter_step": (c_int, [c_void_p, ctypes.c_float, c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_get_state": (c_int, [c_void_p, c_void_p, POINTER(c_size_t)]),
     "af_set_state": (c_int, [c_void_p, c_void_p, c_size_t]),
     "af_ctx_destroy": (c_int, [c_void_p]),

@@ -70,7 +70,7 @@ class FreezingModule:
         return dict(n_segments=i.n_segments, n_pool=i.n_pool, rank=i.rank, world=i.world,
                     n_total=i.n_total, shard_begin=i.shard_begin, shard_end=i.shard_end,
                     n_tiles=i.n_tiles, tile_elems=i.tile_elems, n_tiles_acc=i.n_tiles_acc,
-                    tile_elems_acc=i.tile_elems_acc,
+                    tile_elems_acc=i.tile_elems_acc, n_fin_ctas=i.n_fin_ctas,
                     first_tile_of_pool=list(i.first_tile_of_pool[:i.n_pool + 1]))
 
     def bind(self, device=None):
@@ -122,6 +122,46 @@ class FreezingModule:
             lib.af_ctx_clear_peers(self._h)
             return False
         return True
+
+    def set_max_ctas(self, n):
+        """Cap the streaming kernels' CTAs (0: the full persistent grid)."""
+        check(lib.af_ctx_set_max_ctas(self._h, int(n)), "af_ctx_set_max_ctas")
+
+    def set_grad_peers_local(self, grads):
+        """NEXT 1 (ZeRO form): register every rank's full gradient buffer, for ranks
+        living in this process; grads[r] is rank r's tensor."""
+        self._rs_grads = list(grads)                 # keep the buffers alive
+        arr = (c_void_p * len(grads))(*[g.data_ptr() for g in grads])
+        check(lib.af_ctx_set_grad_peers_local(self._h, arr), "af_ctx_set_grad_peers_local")
+
+    def set_grad_peers_ipc(self, grad, group=None):
+        """NEXT 1 (ZeRO form), collective: export this rank's persistent gradient
+        buffer, all-gather the CUDA IPC handles and map every rank's buffer."""
+        import torch.distributed as dist
+        self._rs_grads = [grad]
+        h = (ctypes.c_uint8 * L.AF_IPC_HANDLE_BYTES)()
+        with torch.cuda.device(self.device):
+            check(lib.af_ctx_grad_ipc_handle(self._h, c_void_p(grad.data_ptr()), h), "af_ctx_grad_ipc_handle")
+        allh = [None] * self.world
+        dist.all_gather_object(allh, bytes(h), group=group)
+        buf = (ctypes.c_uint8 * (L.AF_IPC_HANDLE_BYTES * self.world)).from_buffer_copy(b"".join(allh))
+        with torch.cuda.device(self.device):
+            check(lib.af_ctx_set_grad_peers_ipc(self._h, buf), "af_ctx_set_grad_peers_ipc")
+
+    def reduce_scatter_step(self, out=None, scale=None, interval_end=False, dry_run=False, stream=None,
+                            copy_record=True):
+        """af_reduce_scatter_step: this rank's shard of (sum over ranks of the
+        registered gradients) * scale (default 1/world) into `out` (fp32, indexed
+        from shard_begin; None: not written), accumulated into Delta -- or, with
+        interval_end=True, the whole interval end and decision."""
+        sc = (1.0 / self.world) if scale is None else float(scale)
+        flags = (L.AF_INTERVAL_END if interval_end else 0) | (L.AF_DRY_RUN if dry_run else 0)
+        rec = c_void_p(self._rec_host.data_ptr()) if (copy_record and interval_end) else c_void_p(0)
+        check(lib.af_reduce_scatter_step(self._h, ctypes.c_float(sc), c_void_p(out.data_ptr() if out is not None else 0),
+                                         flags, rec, _stream_handle(stream)), "af_reduce_scatter_step")
+        if interval_end and copy_record and not torch.cuda.is_current_stream_capturing():
+            self._event.record(stream if stream is not None else torch.cuda.current_stream())
+        return out
 
     def exchange_rows(self):
         """float64 view [world, L] of the exchange matrix inside the scratch buffer."""

@@ -374,6 +374,17 @@ int launch_cache_get(const CacheParams &p, int grid, void *stream) {
 }  // namespace af
 
 namespace af {
+int preload_cache_kernels() {  // see preload_norm_kernels: no lazy load while peers spin
+  cudaFuncAttributes a;
+  for (const void *k : {reinterpret_cast<const void *>(cache_kernel<true>),
+                        reinterpret_cast<const void *>(cache_kernel<false>),
+                        reinterpret_cast<const void *>(cache_plan_kernel)}) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, k);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  return 0;
+}
+
 int launch_cache_plan(const CachePlanParams &p, void *stream) {
   return static_cast<int>(launch_pdl(cache_plan_kernel, dim3(1), dim3(kPlanThreads), 0,
                                      static_cast<cudaStream_t>(stream), p));

@@ -110,6 +110,8 @@ af_status af_cache_bind(af_cache *c, void *payload_dev, void *meta_dev) {
   cudaError_t e = static_cast<cudaError_t>(device_sm_count(&sms));
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
   c->grid = std::max(1, sms);
+  e = static_cast<cudaError_t>(preload_cache_kernels());
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes (kernel preload)");
   c->payload = static_cast<char *>(payload_dev);
   c->meta = static_cast<char *>(meta_dev);
   AF_CUDA(cudaMemset(c->meta, 0, c->meta_bytes()), "cudaMemset(meta)");

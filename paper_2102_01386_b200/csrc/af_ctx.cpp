@@ -41,13 +41,14 @@ struct af_ctx {
   } ts[2];
   // workspace
   size_t accum_bytes = 0, scratch_bytes = 0;
-  size_t o_state = 0, o_sched = 0, o_pool = 0, o_part = 0, o_ssall = 0,
+  size_t o_state = 0, o_sched = 0, o_pool = 0, o_part = 0, o_part2 = 0, o_ssall = 0,
          o_ssacc = 0, o_last = 0, o_ring = 0, o_xrows = 0,
-         o_xflags = 0, o_peer_rows = 0, o_peer_flags = 0;
+         o_xflags = 0, o_peer_rows = 0, o_peer_flags = 0, o_rsflags = 0, o_peer_rsflags = 0, o_rs_grads = 0;
   float *accum = nullptr;
   char *scratch = nullptr;
   bool bound = false;
-  int grid[kNumModes] = {0, 0, 0, 0, 0};  // persistent grid per streaming-kernel mode (occupancy x SMs)
+  int grid[kNumModes] = {};  // persistent grid per streaming-kernel mode (occupancy x SMs)
+  int max_ctas = 0;          // af_ctx_set_max_ctas: cap on the streaming grids (0: none)
   // host flags
   bool armed = false;    // Delta / ss_acc hold this interval's partial sum
   bool pending = false;  // an interval end awaits af_update_and_decide
@@ -56,6 +57,8 @@ struct af_ctx {
   af_decision *rec_host_dev = nullptr;
   bool peers = false;               // NVLink one-shot exchange registered
   std::vector<void *> ipc_opened;   // peer allocations opened with cudaIpcOpenMemHandle
+  bool grad_peers = false;          // fused reduce-scatter: every rank's gradient buffer registered
+  const void *own_grad = nullptr;   // this rank's buffer (af_ctx_grad_ipc_handle)
 
   template <typename T>
   T *at(size_t o) const {
@@ -174,6 +177,9 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   c->o_xflags = take(static_cast<size_t>(cfg->world) * sizeof(unsigned long long));
   c->o_peer_rows = take(static_cast<size_t>(cfg->world) * sizeof(void *));
   c->o_peer_flags = take(static_cast<size_t>(cfg->world) * sizeof(void *));
+  c->o_rsflags = take(2 * static_cast<size_t>(cfg->world) * sizeof(unsigned long long));
+  c->o_peer_rsflags = take(static_cast<size_t>(cfg->world) * sizeof(void *));
+  c->o_rs_grads = take(static_cast<size_t>(cfg->world) * sizeof(void *));
   c->o_ssall = take(static_cast<size_t>(cfg->world) * L * sizeof(double));
   c->o_ssacc = take(L * sizeof(double));
   c->o_last = take(sizeof(af_decision));
@@ -185,6 +191,7 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
     T.o_tiles = take(T.tiles.size() * sizeof(Tile));
   }
   c->o_part = take(c->ts[1].tiles.size() * sizeof(double));
+  c->o_part2 = take((c->ts[1].tiles.size() / kFinChunk + L + 2) * sizeof(double));
   c->scratch_bytes = o;
   *out = c;
   return AF_OK;
@@ -211,6 +218,8 @@ af_status af_ctx_info(const af_ctx *c, af_info *info) {
   info->tile_elems = c->ts[1].tile_elems;
   info->n_tiles_acc = static_cast<int32_t>(c->ts[0].tiles.size());
   info->tile_elems_acc = c->ts[0].tile_elems;
+  info->n_fin_ctas = af::fin_ctas(c->cfg.acc_mode == AF_ACC_DELTA ? kEndDelta : kStepSq,
+                                  static_cast<int>(c->ts[1].tiles.size()));
   for (int j = 0; j <= c->n_pool; ++j) info->first_tile_of_pool[j] = c->ts[1].first_tile_of_f[j];
   return AF_OK;
 }
@@ -223,6 +232,9 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
   int sms = 0;
   cudaError_t e = static_cast<cudaError_t>(device_sm_count(&sms));
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  e = static_cast<cudaError_t>(preload_norm_kernels(c->dtype));
+  if (e == cudaSuccess) e = static_cast<cudaError_t>(preload_decide_kernel());
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes (kernel preload)");
   for (int m = 0; m < kNumModes; ++m) {
     int bps = 0;
     e = static_cast<cudaError_t>(norms_max_blocks_per_sm(m, c->dtype, &bps));
@@ -286,6 +298,12 @@ af_status af_ctx_exchange_rows(af_ctx *c, double **ss_all_dev) {
 
 namespace {
 
+int grid_for(const af_ctx *c, int mode, int n_tiles) {
+  int g = std::min<int>(c->grid[mode], std::max<int>(1, n_tiles));
+  if (c->max_ctas > 0) g = std::min(g, c->max_ctas);
+  return std::max(1, g);
+}
+
 NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   NormParams p{};
   const int k = (c->cfg.acc_mode == AF_ACC_DELTA && !end) ? 0 : 1;  // which tile table
@@ -301,6 +319,8 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   p.state = c->at<DevState>(c->o_state);
   p.sched = c->at<Sched>(c->o_sched) + k;
   p.partials = c->at<double>(c->o_part);
+  p.part2 = c->at<double>(c->o_part2);
+  p.fin_sched = c->at<Sched>(c->o_sched) + 2;
   p.ss_out = c->at<double>(c->o_ssall) + static_cast<size_t>(c->cfg.rank) * c->L;
   p.ss_acc = c->at<double>(c->o_ssacc);
   p.n_pool = c->n_pool;
@@ -389,7 +409,7 @@ af_status af_layer_norms(af_ctx *c, const void *grad_dev, uint32_t flags, void *
   const bool end = flags & AF_INTERVAL_END, dry = flags & AF_DRY_RUN;
   const int mode = norm_mode(c, end);
   NormParams p = norm_params(c, grad_dev, end, dry);
-  const int grid = std::max(1, std::min<int>(c->grid[mode], std::max<int>(1, p.n_tiles)));
+  const int grid = grid_for(c, mode, p.n_tiles);
   const int e = launch_norms(p, mode, c->dtype, grid, stream);
   if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "norms kernel launch");
   if (end) {
@@ -437,7 +457,7 @@ af_status af_adamw_step(af_ctx *c, float *params_dev, float *exp_avg_dev, float 
     p.fuse_decide = 1;
     p.dec = decide_params(c, dry, out_host);
   }
-  const int grid = std::max(1, std::min<int>(c->grid[mode], std::max<int>(1, p.n_tiles)));
+  const int grid = grid_for(c, mode, p.n_tiles);
   const int e = launch_norms(p, mode, c->dtype, grid, stream);
   if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "fused AdamW kernel launch");
   if (fuse) {
@@ -488,7 +508,7 @@ af_status af_interval_end(af_ctx *c, const void *grad_dev, uint32_t flags, af_de
   NormParams p = norm_params(c, grad_dev, true, dry);
   p.fuse_decide = 1;
   p.dec = decide_params(c, dry, out_host);
-  const int grid = std::max(1, std::min<int>(c->grid[mode], std::max<int>(1, p.n_tiles)));
+  const int grid = grid_for(c, mode, p.n_tiles);
   const int e = launch_norms(p, mode, c->dtype, grid, stream);
   if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "fused interval-end kernel launch");
   st = copy_record_if_unmapped(c, p.dec, out_host, stream);
@@ -506,17 +526,22 @@ struct IpcHandle {  // AF_IPC_HANDLE_BYTES
   cudaIpcMemHandle_t h;
   uint64_t offset;                 // scratch offset inside the exported allocation
   uint64_t xrows_off, xflags_off;  // exchange-area offsets inside the scratch
+  uint64_t rsflags_off;            // fused reduce-scatter flags inside the scratch
   int32_t rank, world, L, pad;
 };
 static_assert(sizeof(IpcHandle) <= AF_IPC_HANDLE_BYTES, "ipc handle size");
 
 static af_status upload_peers(af_ctx *c, const std::vector<char *> &scratch_of) {
   std::vector<double *> rows(c->cfg.world);
-  std::vector<unsigned long long *> flags(c->cfg.world);
+  std::vector<unsigned long long *> flags(c->cfg.world), rsflags(c->cfg.world);
   for (int r = 0; r < c->cfg.world; ++r) {
     rows[r] = reinterpret_cast<double *>(scratch_of[r] + c->o_xrows);
     flags[r] = reinterpret_cast<unsigned long long *>(scratch_of[r] + c->o_xflags);
+    rsflags[r] = reinterpret_cast<unsigned long long *>(scratch_of[r] + c->o_rsflags);
   }
+  AF_CUDA(cudaMemcpy(c->scratch + c->o_peer_rsflags, rsflags.data(), rsflags.size() * sizeof(void *),
+                     cudaMemcpyHostToDevice),
+          "cudaMemcpy(peer rs flags)");
   AF_CUDA(cudaMemcpy(c->scratch + c->o_peer_rows, rows.data(), rows.size() * sizeof(void *), cudaMemcpyHostToDevice),
           "cudaMemcpy(peer rows)");
   AF_CUDA(cudaMemcpy(c->scratch + c->o_peer_flags, flags.data(), flags.size() * sizeof(void *),
@@ -538,6 +563,7 @@ af_status af_ctx_exchange_ipc_handle(af_ctx *c, void *handle_out) {
   h.offset = r.offset;
   h.xrows_off = c->o_xrows;
   h.xflags_off = c->o_xflags;
+  h.rsflags_off = c->o_rsflags;
   h.rank = c->cfg.rank;
   h.world = c->cfg.world;
   h.L = c->L;
@@ -555,7 +581,7 @@ af_status af_ctx_set_peers_ipc(af_ctx *c, const void *handles) {
     IpcHandle h;
     std::memcpy(&h, static_cast<const char *>(handles) + static_cast<size_t>(r) * AF_IPC_HANDLE_BYTES, sizeof(h));
     if (h.rank != r || h.world != c->cfg.world || h.L != c->L || h.xrows_off != c->o_xrows ||
-        h.xflags_off != c->o_xflags)
+        h.xflags_off != c->o_xflags || h.rsflags_off != c->o_rsflags)
       return fail(AF_EINVAL, "peer handle mismatch");
     if (r == c->cfg.rank) {
       scratch_of[r] = c->scratch;
@@ -581,11 +607,130 @@ af_status af_ctx_set_peers_local(af_ctx *c, af_ctx *const *peers) {
   for (int r = 0; r < c->cfg.world; ++r) {
     const af_ctx *q = peers[r];
     if (!q || !q->bound || q->cfg.rank != r || q->cfg.world != c->cfg.world || q->L != c->L ||
-        q->o_xrows != c->o_xrows || q->o_xflags != c->o_xflags)
+        q->o_xrows != c->o_xrows || q->o_xflags != c->o_xflags || q->o_rsflags != c->o_rsflags)
       return fail(AF_EINVAL, "peer context mismatch");
     scratch_of[r] = q->scratch;
   }
   return upload_peers(c, scratch_of);
+}
+
+af_status af_ctx_set_max_ctas(af_ctx *c, int32_t max_ctas) {
+  if (!c) return fail(AF_EINVAL, "NULL ctx");
+  if (max_ctas < 0) return fail(AF_EINVAL, "max_ctas < 0");
+  c->max_ctas = max_ctas;
+  return AF_OK;
+}
+
+// ---------------------------------------------------------------- fused reduce-scatter
+
+struct GradHandle {  // AF_IPC_HANDLE_BYTES
+  cudaIpcMemHandle_t h;
+  uint64_t offset;
+  int64_t n;
+  int32_t rank, world, dtype, pad;
+};
+static_assert(sizeof(GradHandle) <= AF_IPC_HANDLE_BYTES, "grad handle size");
+
+static af_status upload_grads(af_ctx *c, const std::vector<const void *> &g) {
+  AF_CUDA(cudaMemcpy(c->scratch + c->o_rs_grads, g.data(), g.size() * sizeof(void *), cudaMemcpyHostToDevice),
+          "cudaMemcpy(rs grads)");
+  AF_CUDA(cudaDeviceSynchronize(), "set grad peers");
+  c->grad_peers = true;
+  return AF_OK;
+}
+
+af_status af_ctx_grad_ipc_handle(af_ctx *c, const void *grad_dev, void *handle_out) {
+  if (!c || !grad_dev || !handle_out) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (!aligned(grad_dev, 16)) return fail(AF_EINVAL, "gradient buffer must be 16-byte aligned");
+  IpcRef r{};
+  af_status st = ipc_export(grad_dev, &r);
+  if (st != AF_OK) return st;
+  GradHandle h{};
+  h.h = r.h;
+  h.offset = r.offset;
+  h.n = c->n;
+  h.rank = c->cfg.rank;
+  h.world = c->cfg.world;
+  h.dtype = c->dtype;
+  std::memset(handle_out, 0, AF_IPC_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  c->own_grad = grad_dev;
+  return AF_OK;
+}
+
+af_status af_ctx_set_grad_peers_ipc(af_ctx *c, const void *handles) {
+  if (!c || !handles) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (c->cfg.world > kMaxRsWorld) return fail(AF_EINVAL, "fused reduce-scatter supports world <= 8");
+  if (!c->own_grad) return fail(AF_ESTATE, "call af_ctx_grad_ipc_handle on this rank first");
+  std::vector<const void *> g(c->cfg.world, nullptr);
+  for (int r = 0; r < c->cfg.world; ++r) {
+    GradHandle h;
+    std::memcpy(&h, static_cast<const char *>(handles) + static_cast<size_t>(r) * AF_IPC_HANDLE_BYTES, sizeof(h));
+    if (h.rank != r || h.world != c->cfg.world || h.n != c->n || h.dtype != c->dtype)
+      return fail(AF_EINVAL, "gradient handle mismatch");
+    if (r == c->cfg.rank) {
+      g[r] = c->own_grad;
+      continue;
+    }
+    char *ptr = nullptr;
+    af_status st = ipc_import(IpcRef{h.h, h.offset}, c->ipc_opened, &ptr);
+    if (st != AF_OK) return st;
+    g[r] = ptr;
+  }
+  return upload_grads(c, g);
+}
+
+af_status af_ctx_set_grad_peers_local(af_ctx *c, const void *const *grads_dev) {
+  if (!c || !grads_dev) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (c->cfg.world > kMaxRsWorld) return fail(AF_EINVAL, "fused reduce-scatter supports world <= 8");
+  std::vector<const void *> g(c->cfg.world);
+  for (int r = 0; r < c->cfg.world; ++r) {
+    if (!grads_dev[r] || !aligned(grads_dev[r], 16)) return fail(AF_EINVAL, "gradient buffers must be 16-byte aligned");
+    g[r] = grads_dev[r];
+  }
+  c->own_grad = g[c->cfg.rank];
+  return upload_grads(c, g);
+}
+
+af_status af_reduce_scatter_step(af_ctx *c, float scale, float *grad_shard_out_dev, uint32_t flags,
+                                 af_decision *out_host, void *stream) {
+  if (!c) return fail(AF_EINVAL, "NULL ctx");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (!c->grad_peers) return fail(AF_ESTATE, "no gradient buffers registered (af_ctx_set_grad_peers_*)");
+  if (c->cfg.acc_mode != AF_ACC_DELTA) return fail(AF_ESTATE, "af_reduce_scatter_step needs acc_mode AF_ACC_DELTA");
+  if (flags & ~(AF_INTERVAL_END | AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
+  if (grad_shard_out_dev && !aligned(grad_shard_out_dev, 16)) return fail(AF_EINVAL, "output must be 16-byte aligned");
+  if (!std::isfinite(scale)) return fail(AF_EINVAL, "scale must be finite");
+  if (c->cfg.world > 1 && !c->peers)
+    return fail(AF_ESTATE, "world > 1 needs peers (af_ctx_set_peers_*) for the reduce-scatter flags");
+  const bool end = flags & AF_INTERVAL_END, dry = flags & AF_DRY_RUN;
+  const int mode = end ? kRsEnd : kRsAccum;
+  NormParams p = norm_params(c, c->own_grad, end, dry);
+  p.rs_world = c->cfg.world;
+  p.rs_rank = c->cfg.rank;
+  p.rs_grads = c->at<const void *const>(c->o_rs_grads);
+  p.rs_scale = scale;
+  p.rs_out = grad_shard_out_dev;
+  p.rs_flags = c->at<unsigned long long>(c->o_rsflags);
+  p.peer_rs_flags = c->at<unsigned long long *const>(c->o_peer_rsflags);
+  if (end) {
+    p.fuse_decide = 1;
+    p.dec = decide_params(c, dry, out_host);
+  }
+  const int e = launch_norms(p, mode, c->dtype, grid_for(c, mode, p.n_tiles), stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "fused reduce-scatter kernel launch");
+  if (end) {
+    af_status st = copy_record_if_unmapped(c, p.dec, out_host, stream);
+    if (st != AF_OK) return st;
+  }
+  if (!dry) {
+    c->armed = !end;
+    c->pending = false;
+  }
+  return AF_OK;
 }
 
 struct StateBlob {

@@ -15,6 +15,11 @@ __global__ void __launch_bounds__(kDecideThreads) decide_kernel(const DecidePara
 
 }  // namespace
 
+int preload_decide_kernel() {
+  cudaFuncAttributes a;
+  return static_cast<int>(cudaFuncGetAttributes(&a, decide_kernel));
+}
+
 int launch_decide(const DecideParams &p, void *stream) {
   return static_cast<int>(launch_pdl(decide_kernel, dim3(1), dim3(kDecideThreads), 0, static_cast<cudaStream_t>(stream), p));
 }

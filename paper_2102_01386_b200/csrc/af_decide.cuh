@@ -56,7 +56,8 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
   if (t < n_act) s_act[t] = s_eta[p.pool_seg[f + t]];
   __syncthreads();
 
-  const bool xfail = p.xparity && (p.state->sticky & 1u);  // a peer never arrived
+  // a peer never arrived: at the exchange (bit 0) or at a fused reduce-scatter barrier (bit 1)
+  const bool xfail = (p.xparity && (p.state->sticky & 1u)) || (p.state->sticky & 2u);
   const bool nonfinite = s_nonfinite != 0 || xfail;
   unsigned int flags = p.commit ? 0u : AF_DEC_DRY_RUN;
   if (xfail) flags |= AF_DEC_EXCHANGE_TIMEOUT;

@@ -56,11 +56,18 @@ struct DevState {
   int32_t pad;
   unsigned long long epoch;      // peer-exchange epoch: interval ends seen (identical on all ranks)
   unsigned long long tmark[4];   // AF_TIMING builds: %globaltimer at kernel start / tail start / after sums / end
+  unsigned long long rs_epoch;   // fused reduce-scatter steps completed (identical on all ranks)
   double prev[AF_MAX_SEGMENTS];  // ||Delta_{T-1,l}||
 };
 
-enum Mode : int { kAccum = 0, kEndDelta = 1, kStepSq = 2, kAdamAccum = 3, kAdamEnd = 4 };
-constexpr int kNumModes = 5;
+#ifndef AF_FIN_WIDE  // 0: always finalize in the streaming kernel's last CTA
+#define AF_FIN_WIDE 1
+#endif
+constexpr int kFinChunk = 2048;  // partials per fin_kernel CTA (8 per thread)
+
+enum Mode : int { kAccum = 0, kEndDelta = 1, kStepSq = 2, kAdamAccum = 3, kAdamEnd = 4, kRsAccum = 5, kRsEnd = 6 };
+constexpr int kNumModes = 7;
+constexpr int kMaxRsWorld = 8;  // ranks of one fused reduce-scatter (one NVLink domain's GPUs per node)
 
 // AdamW constants of one step, rounded once to fp32 on the host (NEXT 1 fusion).
 struct AdamConst {
@@ -102,6 +109,12 @@ struct NormParams {
   const DevState *state;           // reads f
   Sched *sched;
   double *partials;                // [n_tiles]
+  // wide finalize (n_tiles > kFinChunk): the streaming kernel only writes the
+  // partials; fin_kernel's CTAs reduce chunks of kFinChunk partials into
+  // part2[chunk + segment] and its last CTA combines them in chunk order
+  int32_t wide_fin;
+  double *part2;                   // [n_tiles / kFinChunk + L + 2]
+  Sched *fin_sched;                // done counter of fin_kernel
   double *ss_out;                  // [L] this rank's row of the exchange matrix
   double *ss_acc;                  // [L] STEP_SUMSQ accumulator
   int32_t n_pool;
@@ -120,6 +133,15 @@ struct NormParams {
   double *const *peer_rows;        // [world] device pointers to each rank's xrows
   unsigned long long *xflags;      // local flags [world]: epoch reached by each rank
   unsigned long long *const *peer_flags;  // [world] pointers to each rank's xflags
+  // kRsAccum / kRsEnd (NEXT 1, ZeRO form): the gradient is the rank-order sum of
+  // the world's full gradient buffers (read over peer memory) times rs_scale;
+  // this rank's shard of it is written to rs_out (optional) and accumulated.
+  int32_t rs_world, rs_rank;
+  const void *const *rs_grads;     // [rs_world] device pointers (peer-mapped)
+  float rs_scale;
+  float *rs_out;                   // shard output, element i at rs_out[i - shard_begin]; may be null
+  unsigned long long *rs_flags;    // local [2][world]: ready / done epoch reached by each rank
+  unsigned long long *const *peer_rs_flags;  // [world] each rank's rs_flags
   DecideParams dec;
 };
 
@@ -227,11 +249,18 @@ inline cudaError_t ensure_smem_attr(int smem) {
 
 // Launchers (defined in the .cu files).  Return cudaError_t as int.
 int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *stream);
+// CTAs of the wide finalize launch that follows the streaming kernel of `mode`
+// (0: the streaming kernel's last CTA finalizes)
+int fin_ctas(int mode, int n_tiles);
 int launch_decide(const DecideParams &p, void *stream);
 int launch_cache_put(const CacheParams &p, int grid, void *stream);
 int launch_cache_get(const CacheParams &p, int grid, void *stream);
 int launch_cache_plan(const CachePlanParams &p, void *stream);
 int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks);
+// force-load the kernels (lazy module loading must not happen while peers spin)
+int preload_norm_kernels(int grad_dtype);
+int preload_decide_kernel();
+int preload_cache_kernels();
 int cache_smem_bytes();
 
 }  // namespace af

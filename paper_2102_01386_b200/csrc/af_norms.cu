@@ -54,6 +54,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef AF_MINB_END
 #define AF_MINB_END 1
 #endif
+#ifndef AF_U_RS  // fused reduce-scatter: vectors in flight per thread and rank
+#define AF_U_RS 2
+#endif
 
 namespace af {
 namespace {
@@ -312,6 +315,146 @@ __device__ __forceinline__ double process_tile_adam(const NormParams &p, const T
   return (a0 + a1) + (a2 + a3);
 }
 
+// NEXT 1, ZeRO form: the data-parallel gradient sync fused
+// with the accumulate.  Each rank reads its shard of every rank's full gradient
+// buffer over peer memory (pull: the loads of all ranks are in flight together),
+// sums them in rank order 0..P-1 in fp32 (one rounding per add), scales once
+// (gs = fl(sum * scale), the DDP average with scale = 1/P), writes gs to the
+// optimizer's shard buffer and accumulates it into Delta exactly like kAccum /
+// kEndDelta accumulate g.  The reduced gradient never makes an HBM round trip
+// before the accumulate reads it.
+template <bool END, typename GT, bool RD>
+__device__ __forceinline__ double process_tile_rs(const NormParams &p, const Tile &t,
+                                                  const GT *const (&gr)[kMaxRsWorld]) {
+  constexpr int VE = VT<GT>::VE;
+  constexpr int DV = VE / 4;
+  constexpr int U = AF_U_RS;
+  const int P = p.rs_world;
+  const float sc = p.rs_scale;
+  float *__restrict__ d = p.delta - p.shard_begin;
+  float *__restrict__ o = p.rs_out ? p.rs_out - p.shard_begin : nullptr;
+  const int64_t b = t.begin, e = t.end;
+  int64_t vb = ((b + VE - 1) / VE) * VE;
+  int64_t ve = (e / VE) * VE;
+  if (vb > ve) vb = ve = e;
+  const int tid = threadIdx.x;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  auto scalar = [&](int64_t i, double &acc) {
+    float gs = g_scalar(gr[0], i);
+    for (int r = 1; r < P; ++r) gs = __fadd_rn(gs, g_scalar(gr[r], i));
+    gs = __fmul_rn(gs, sc);
+    if (o) o[i] = gs;
+    const float x = RD ? __fadd_rn(d[i], gs) : gs;
+    if (END)
+      acc = sq_acc(x, acc);
+    else
+      d[i] = x;
+  };
+  const int nh = static_cast<int>(vb - b), nt = static_cast<int>(e - ve);
+  if (tid < nh) scalar(b + tid, a0);
+  if (tid >= 128 && tid - 128 < nt) scalar(ve + (tid - 128), a1);
+  const int64_t nch = (ve - vb) / VE;
+  float4 *db = reinterpret_cast<float4 *>(d + vb);
+  float4 *ob = o ? reinterpret_cast<float4 *>(o + vb) : nullptr;
+  for (int64_t c0 = tid; c0 < nch; c0 += U * kNormBlock) {
+    uint4 gv[U][kMaxRsWorld];
+    float4 dv[U][DV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = c0 + static_cast<int64_t>(u) * kNormBlock;
+      if (c < nch) {
+#pragma unroll
+        for (int r = 0; r < kMaxRsWorld; ++r)
+          if (r < P) gv[u][r] = __ldcs(reinterpret_cast<const uint4 *>(gr[r] + vb) + c);
+        if (RD) {
+#pragma unroll
+          for (int q = 0; q < DV; ++q) dv[u][q] = __ldcs(db + c * DV + q);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t c = c0 + static_cast<int64_t>(u) * kNormBlock;
+      if (c < nch) {
+        float x[VE];
+        unpack<VE>(gv[u][0], x);
+#pragma unroll
+        for (int r = 1; r < kMaxRsWorld; ++r) {
+          if (r < P) {
+            float y[VE];
+            unpack<VE>(gv[u][r], y);
+#pragma unroll
+            for (int k = 0; k < VE; ++k) x[k] = __fadd_rn(x[k], y[k]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < VE; ++k) x[k] = __fmul_rn(x[k], sc);
+        if (ob) {
+#pragma unroll
+          for (int q = 0; q < DV; ++q) ob[c * DV + q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+        }
+        if (RD) {
+#pragma unroll
+          for (int q = 0; q < DV; ++q) {
+            x[4 * q + 0] = __fadd_rn(dv[u][q].x, x[4 * q + 0]);
+            x[4 * q + 1] = __fadd_rn(dv[u][q].y, x[4 * q + 1]);
+            x[4 * q + 2] = __fadd_rn(dv[u][q].z, x[4 * q + 2]);
+            x[4 * q + 3] = __fadd_rn(dv[u][q].w, x[4 * q + 3]);
+          }
+        }
+        if (!END) {
+#pragma unroll
+          for (int q = 0; q < DV; ++q)
+            __stcs(db + c * DV + q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
+        } else {
+#pragma unroll
+          for (int k = 0; k < VE; k += 4) {
+            a0 = sq_acc(x[k + 0], a0);
+            a1 = sq_acc(x[k + 1], a1);
+            a2 = sq_acc(x[k + 2], a2);
+            a3 = sq_acc(x[k + 3], a3);
+          }
+        }
+      }
+    }
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+// Cross-GPU epoch barrier of the fused reduce-scatter: threads r < P store the
+// epoch into rank r's flag word for this rank (st.release.sys over peer memory),
+// then wait until every rank's word in the local array reached it (ld.acquire.sys,
+// bounded: a rank that never arrives sets sticky bit 2 -- the next decision is
+// flagged EXCHANGE_TIMEOUT and not committed -- instead of hanging the GPU).
+// which = 0: "my gradient is ready to be read" (every CTA, before its first
+// load), which = 1: "I have finished reading" (the last CTA, before the kernel
+// may complete and the caller's next backward overwrite the buffers).
+__device__ __noinline__ void rs_barrier(const NormParams &p, int which, unsigned long long e) {
+  const int tid = threadIdx.x, P = p.rs_world;
+  __shared__ int s_to;
+  if (tid == 0) s_to = 0;
+  if (tid < P) {
+    unsigned long long *flag = p.peer_rs_flags[tid] + which * P + p.rs_rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
+  }
+  __syncthreads();
+  if (tid < P) {
+    const unsigned long long *flag = p.rs_flags + which * P + tid;
+    unsigned long long v = 0;
+    for (long long spin = 0;; ++spin) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      if (v >= e) break;
+      if (spin > (1ll << 22)) {
+        s_to = 1;
+        break;
+      }
+      __nanosleep(128);
+    }
+  }
+  __syncthreads();
+  if (s_to && tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 2u);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
@@ -321,11 +464,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 // The last CTA's work after the grid has drained: per-segment sums, the optional
 // NVLink one-shot exchange and the fused decision.  Not inlined, so its
 // registers do not raise the streaming loop's (occupancy) budget.
-template <int MODE>
-__device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, double *s_red_unused) {
+template <int MODE, bool WIDE>
+__device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  (void)s_red_unused;
-  if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
+  if (AF_TIMING && !WIDE && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
   // peer exchange: this interval end's epoch selects the exchange buffer
   const bool xchg = p.xworld > 1 && p.end;
   __shared__ unsigned long long s_epoch;
@@ -341,22 +483,40 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
   }
   // each segment's active tiles' partials in tile order: one warp per segment,
   // lane-strided with 8 loads in flight, then the xor tree (deterministic)
-  for (int l = warp; l < p.L && warp < kNormBlock / 32; l += kNormBlock / 32) {
-    int tb = p.seg_tile_begin[l];
-    tb = tb < first_tile ? first_tile : tb;
-    const int te = p.seg_tile_begin[l + 1];
-    double s = 0.0;
-#pragma unroll 8
-    for (int k = tb + lane; k < te; k += 32) s += __ldcg(p.partials + k);
-    s = warp_sum(s);
-    if (lane == 0) {
-      if (MODE == kEndDelta) {
-        ss_row[l] = s;
-      } else {
-        const double acc = p.first ? s : p.ss_acc[l] + s;
-        if (p.commit) p.ss_acc[l] = acc;
-        if (p.end) ss_row[l] = acc;
+  auto publish = [&](int l, double s) {
+    if (MODE == kEndDelta) {
+      ss_row[l] = s;
+    } else {
+      const double acc = p.first ? s : p.ss_acc[l] + s;
+      if (p.commit) p.ss_acc[l] = acc;
+      if (p.end) ss_row[l] = acc;
+    }
+  };
+  if constexpr (WIDE) {
+    // fin_kernel's chunk sums: segment l's active tiles span chunks
+    // [c_lo, c_hi] (chunk c = tiles first_tile + [c*kFinChunk, (c+1)*kFinChunk)),
+    // whose pieces of l sit at part2[c + l]; summed in chunk order
+    for (int l = tid; l < p.L; l += kNormBlock) {
+      int tb = p.seg_tile_begin[l];
+      tb = tb < first_tile ? first_tile : tb;
+      const int te = p.seg_tile_begin[l + 1];
+      double s = 0.0;
+      if (te > tb) {
+        const int c_lo = (tb - first_tile) / kFinChunk, c_hi = (te - 1 - first_tile) / kFinChunk;
+        for (int c = c_lo; c <= c_hi; ++c) s += __ldcg(p.part2 + c + l);
       }
+      publish(l, s);
+    }
+  } else {
+    for (int l = warp; l < p.L && warp < kNormBlock / 32; l += kNormBlock / 32) {
+      int tb = p.seg_tile_begin[l];
+      tb = tb < first_tile ? first_tile : tb;
+      const int te = p.seg_tile_begin[l + 1];
+      double s = 0.0;
+#pragma unroll 8
+      for (int k = tb + lane; k < te; k += 32) s += __ldcg(p.partials + k);
+      s = warp_sum(s);
+      if (lane == 0) publish(l, s);
     }
   }
   if (xchg) {
@@ -412,16 +572,28 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
 template <int MODE, typename GT, bool RD>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAccum) ? 1 : AF_MINB_END)
     norms_kernel(const NormParams p) {
+  constexpr bool RS = MODE == kRsAccum || MODE == kRsEnd;
   __shared__ int s_tile[3];
   __shared__ Tile s_desc[3];
   __shared__ double s_red[kNormBlock / 32];
   __shared__ int s_last;
+  __shared__ unsigned long long s_rs_epoch;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_wait();  // f, Delta and the counters are written by the preceding kernels
   if (AF_TIMING && blockIdx.x == 0 && threadIdx.x == 0) const_cast<DevState *>(p.state)->tmark[0] = gtimer();
   int f = p.state->f;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int first_tile = p.first_tile_of_f[f];
+  const GT *rs_g[kMaxRsWorld];
+  if constexpr (RS) {
+#pragma unroll
+    for (int r = 0; r < kMaxRsWorld; ++r) rs_g[r] = r < p.rs_world ? static_cast<const GT *>(p.rs_grads[r]) : nullptr;
+    if (p.rs_world > 1) {
+      if (tid == 0) s_rs_epoch = p.state->rs_epoch + 1ull;  // advanced by the last CTA only
+      __syncthreads();
+      rs_barrier(p, 0, s_rs_epoch);  // every rank's gradient is complete before any peer load
+    }
+  }
 
   // Tile scheduler, two tiles of lookahead: while tile `it` is processed, thread 0
   // has the atomic for tile it+2 (one register) and an async copy (cp.async) of
@@ -456,13 +628,15 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
     double v;
     if constexpr (MODE == kAdamAccum || MODE == kAdamEnd)
       v = process_tile_adam<MODE == kAdamEnd, GT, RD>(p, t);
+    else if constexpr (RS)
+      v = process_tile_rs<MODE == kRsEnd, GT, RD>(p, t, rs_g);
     else
       v = process_tile<MODE, GT, RD>(p, t);
     if (tid == 0) {
       s_tile[slot2] = next2;
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    if (MODE != kAccum && MODE != kAdamAccum) {
+    if (MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum) {
       const double w = warp_sum(v);
       if (lane == 0) s_red[warp] = w;
       __syncthreads();
@@ -492,8 +666,71 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
     p.sched->next = 0;
     p.sched->done = 0;
   }
-  if (MODE == kAccum || MODE == kAdamAccum) return;
-  last_cta_tail<(MODE == kAdamEnd) ? kEndDelta : MODE>(p, first_tile, s_red);
+  if constexpr (RS) {
+    if (p.rs_world > 1) {
+      rs_barrier(p, 1, s_rs_epoch);  // no rank reads this rank's gradient any more
+      if (tid == 0) const_cast<DevState *>(p.state)->rs_epoch = s_rs_epoch;
+    }
+  }
+  if (MODE == kAccum || MODE == kAdamAccum || MODE == kRsAccum) return;
+  if (p.wide_fin) {  // fin_kernel sums the partials
+    if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
+    return;
+  }
+  last_cta_tail<(MODE == kAdamEnd || MODE == kRsEnd) ? kEndDelta : MODE, false>(p, first_tile);
+}
+
+// Wide finalize of the interval-end kernels (n_tiles > kFinChunk): CTA c stages
+// the fp64 partials of tiles first_tile + [c*kFinChunk, (c+1)*kFinChunk) in
+// shared memory (8 coalesced loads per thread, one round trip), reduces each
+// segment's piece of them (one warp per segment, lane-strided, xor tree) into
+// part2[c + l] -- piece (c, l) is the (c + l)-th piece in tile order -- and the
+// grid's last CTA combines the pieces of each segment in chunk order, then
+// exchanges and decides as the streaming kernel's last CTA would.  Every sum has
+// a fixed order: the result is deterministic.
+template <int MODE>
+__global__ void __launch_bounds__(kNormBlock) fin_kernel(const NormParams p) {
+  __shared__ double s_p[kFinChunk];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  pdl_wait();  // the streaming kernel's partials
+  int f = p.state->f;
+  f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
+  const int first_tile = p.first_tile_of_f[f];
+  const int c = blockIdx.x;
+  const int c0 = first_tile + c * kFinChunk;
+  if (c0 < p.n_tiles) {
+    const int n = min(kFinChunk, p.n_tiles - c0);
+#pragma unroll
+    for (int u = 0; u < kFinChunk / kNormBlock; ++u) {
+      const int k = u * kNormBlock + tid;
+      if (k < n) s_p[k] = __ldcg(p.partials + c0 + k);
+    }
+    const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
+    __syncthreads();
+    for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {
+      int a = p.seg_tile_begin[l], b = p.seg_tile_begin[l + 1];
+      a = (a < c0 ? c0 : a) - c0;
+      b = (b > c0 + n ? c0 + n : b) - c0;
+      double s = 0.0;
+#pragma unroll 8
+      for (int k = a + lane; k < b; k += 32) s += s_p[k];
+      s = warp_sum(s);
+      if (lane == 0) p.part2[c + l] = s;
+    }
+  }
+  pdl_launch_dependents();
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int d = atomicAdd(&p.fin_sched->done, 1u);
+    s_last = (d == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) p.fin_sched->done = 0;
+  last_cta_tail<MODE, true>(p, first_tile);
 }
 
 
@@ -731,7 +968,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) norms_tma_kernel(const NormPar
     p.sched->done = 0;
   }
   if (MODE == kAccum) return;
-  last_cta_tail<kEndDelta>(p, first_tile, s_red);
+  last_cta_tail<kEndDelta, false>(p, first_tile);
 }
 
 template <int MODE, typename GT, bool RD>
@@ -770,15 +1007,32 @@ int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
                 : launch_one<kAdamAccum, GT, false>(p, grid, stream);
     case kAdamEnd:
       return rd ? launch_one<kAdamEnd, GT, true>(p, grid, stream) : launch_one<kAdamEnd, GT, false>(p, grid, stream);
+    case kRsAccum:
+      return rd ? launch_one<kRsAccum, GT, true>(p, grid, stream) : launch_one<kRsAccum, GT, false>(p, grid, stream);
+    case kRsEnd:
+      return rd ? launch_one<kRsEnd, GT, true>(p, grid, stream) : launch_one<kRsEnd, GT, false>(p, grid, stream);
   }
   return static_cast<int>(cudaErrorInvalidValue);
 }
 
 }  // namespace
 
-int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *stream) {
-  if (grad_dtype == AF_DT_BF16) return launch_dt<uint16_t>(p, mode, grid, stream);
-  return launch_dt<float>(p, mode, grid, stream);
+int fin_ctas(int mode, int n_tiles) {
+  const bool end_mode = mode == kEndDelta || mode == kStepSq || mode == kAdamEnd || mode == kRsEnd;
+  if (!AF_FIN_WIDE || !end_mode || n_tiles <= kFinChunk || (mode == kEndDelta && AF_TMA >= 1)) return 0;
+  return (n_tiles + kFinChunk - 1) / kFinChunk;
+}
+
+int launch_norms(const NormParams &p_in, int mode, int grad_dtype, int grid, void *stream) {
+  NormParams p = p_in;
+  const int nfin = fin_ctas(mode, p.n_tiles);
+  p.wide_fin = nfin > 0;
+  const int e = grad_dtype == AF_DT_BF16 ? launch_dt<uint16_t>(p, mode, grid, stream)
+                                         : launch_dt<float>(p, mode, grid, stream);
+  if (e != 0 || !nfin) return e;
+  auto *fk = mode == kStepSq ? fin_kernel<kStepSq> : fin_kernel<kEndDelta>;
+  return static_cast<int>(
+      launch_pdl(fk, dim3(nfin), dim3(kNormBlock), 0, static_cast<cudaStream_t>(stream), p));
 }
 
 template <typename GT>
@@ -797,10 +1051,57 @@ static int occ_dt(int mode, int *blocks) {
     case kAdamEnd:
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kAdamEnd, GT, true>, kNormBlock, 0);
       break;
+    case kRsAccum:
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kRsAccum, GT, true>, kNormBlock, 0);
+      break;
+    case kRsEnd:
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kRsEnd, GT, true>, kNormBlock, 0);
+      break;
     default:
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kStepSq, GT, false>, kNormBlock, 0);
   }
   return static_cast<int>(e);
+}
+
+// Load every kernel of this file now.  Under CUDA's lazy module loading the
+// first launch of a kernel loads it, and a load may wait for the kernels in
+// flight -- fatal when those are spinning on a peer rank (fused reduce-scatter
+// barriers, the exchange) whose own launch sits behind this host thread.
+template <typename GT>
+static cudaError_t preload_dt() {
+  const void *ks[] = {
+      reinterpret_cast<const void *>(norms_kernel<kAccum, GT, true>),
+      reinterpret_cast<const void *>(norms_kernel<kAccum, GT, false>),
+      reinterpret_cast<const void *>(norms_kernel<kEndDelta, GT, true>),
+      reinterpret_cast<const void *>(norms_kernel<kEndDelta, GT, false>),
+      reinterpret_cast<const void *>(norms_kernel<kStepSq, GT, false>),
+      reinterpret_cast<const void *>(norms_kernel<kAdamAccum, GT, true>),
+      reinterpret_cast<const void *>(norms_kernel<kAdamAccum, GT, false>),
+      reinterpret_cast<const void *>(norms_kernel<kAdamEnd, GT, true>),
+      reinterpret_cast<const void *>(norms_kernel<kAdamEnd, GT, false>),
+      reinterpret_cast<const void *>(norms_kernel<kRsAccum, GT, true>),
+      reinterpret_cast<const void *>(norms_kernel<kRsAccum, GT, false>),
+      reinterpret_cast<const void *>(norms_kernel<kRsEnd, GT, true>),
+      reinterpret_cast<const void *>(norms_kernel<kRsEnd, GT, false>),
+  };
+  cudaFuncAttributes a;
+  for (const void *k : ks) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, k);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int preload_norm_kernels(int grad_dtype) {
+  cudaError_t e = grad_dtype == AF_DT_BF16 ? preload_dt<uint16_t>() : preload_dt<float>();
+  if (e != cudaSuccess) return static_cast<int>(e);
+  cudaFuncAttributes a;
+  for (const void *k : {reinterpret_cast<const void *>(fin_kernel<kEndDelta>),
+                        reinterpret_cast<const void *>(fin_kernel<kStepSq>)}) {
+    e = cudaFuncGetAttributes(&a, k);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  return 0;
 }
 
 int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks) {

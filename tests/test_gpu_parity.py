@@ -304,6 +304,26 @@ def test_fake_sharded_parity(P):
         compare_records(decs[0], oz.update_and_decide(), lay.n_segments, tag=f"P={P} T={T}")
 
 
+# ---------------------------------------------------------------- wide finalize
+
+@pytest.mark.parametrize("n,L,pre,head,dt,acc,fused", [
+    (40_000_003, 150, 1_000_001, 3_333, "f32", "delta", True),    # chunks span ~120 segments
+    (40_000_003, 150, 1_000_001, 3_333, "bf16", "step_sumsq", False),
+    (36_000_001, 2, 17, 5, "f32", "delta", False),                # segments span many chunks
+])
+def test_wide_finalize_parity(n, L, pre, head, dt, acc, fused):
+    """More than kFinChunk interval-end tiles: the streaming kernel leaves the
+    partials to the second, wide finalize launch (chunk sums + chunk-order
+    combine).  Records match the oracle while the frozen prefix moves the first
+    active tile off the chunk grid."""
+    lay = uniform_layout(n, L, pre=pre, head=head)
+    recs, _, fm, oz = run_both(lay, dt, _decaying_step(lay, dt, 41), [2, 1, 2, 1, 2, 1], check_delta=False,
+                               fused=fused, acc_mode=acc)
+    assert fm.info()["n_fin_ctas"] > 1
+    if L > 2:
+        assert max(r[0]["boundary_after"] for r in recs) >= 1
+
+
 # ---------------------------------------------------------------- full BASELINE sizes
 
 @pytest.mark.parametrize("which,dt", [("base", "bf16"), ("large", "f32")])

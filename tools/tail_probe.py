@@ -35,7 +35,8 @@ def main():
             marks.append((t[1] - t[0], t[2] - t[1], t[3] - t[2]))
         m = np.median(np.array(marks), axis=0) / 1e3
         print(json.dumps({"case": name, "stream_us": round(float(m[0]), 2), "segment_sums_us": round(float(m[1]), 2),
-                          "decide_us": round(float(m[2]), 2), "n_tiles": fm.info()["n_tiles"]}), flush=True)
+                          "decide_us": round(float(m[2]), 2), "n_tiles": fm.info()["n_tiles"],
+                          "n_fin_ctas": fm.info()["n_fin_ctas"]}), flush=True)
         del fm, g
         torch.cuda.empty_cache()
 

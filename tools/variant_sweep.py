@@ -15,6 +15,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
+    "fin_narrow": "-DAF_FIN_WIDE=0",
+    "timing": "-DAF_TIMING=1",
+    "timing_fin_narrow": "-DAF_TIMING=1 -DAF_FIN_WIDE=0",
     "taper_off": "-DAF_TILE_BIG_MULT=1",
     "taper4": "-DAF_TILE_BIG_MULT=4",
     "taper8_90": "-DAF_TILE_BIG_FRAC_PCT=90",
@@ -54,6 +57,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--only", nargs="*")
     ap.add_argument("--cache", action="store_true", help="run tools/cache_probe.py instead of bench.py")
+    ap.add_argument("--probe", help="run tools/<PROBE>.py (e.g. latency_probe, tail_probe) instead of bench.py")
     a = ap.parse_args()
     sys.path.insert(0, ROOT)
     for name, extra in VARIANTS.items():
@@ -62,11 +66,17 @@ def main():
         env = dict(os.environ, AF_NVCC_EXTRA=extra)
         subprocess.run([sys.executable, os.path.join(ROOT, "paper_2102_01386_b200", "_build.py"), "--force"], cwd=ROOT, env=env,
                        check=True)
-        if a.cache:
-            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "cache_probe.py")], cwd=ROOT,
+        if a.cache or a.probe:
+            probe = "cache_probe" if a.cache else a.probe
+            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", probe + ".py")], cwd=ROOT,
                                capture_output=True, text=True)
-            print(json.dumps({"variant": name, "flags": extra, "cache": r.stdout.strip()[-2000:],
-                              "err": r.stderr[-500:] if r.returncode else ""}), flush=True)
+            for line in r.stdout.strip().splitlines():
+                try:
+                    print(json.dumps({"variant": name, "flags": extra, **json.loads(line)}), flush=True)
+                except Exception:  # noqa: BLE001
+                    print(json.dumps({"variant": name, "flags": extra, "out": line[-2000:]}), flush=True)
+            if r.returncode:
+                print(json.dumps({"variant": name, "err": r.stderr[-1500:]}), flush=True)
             continue
         for wl in ("bert-large-f32", "bert-base-bf16"):
             r = subprocess.run([sys.executable, "bench.py", "--workload", wl, "--steps", str(a.steps), "--warmup", "10",
