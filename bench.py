@@ -358,6 +358,8 @@ def run_ours(args, rank, world, local):
         result["cache_host_tier"] = host_tier_probe(rows, dev)
     if not args.no_extras:
         result["next1_fused_adamw"] = adamw_probe(fm, lay, dt, s_g, n_loc, grads, dev)
+        if world == 1:
+            result["next1_fused_reduce_scatter_p1"] = rs_probe(lay, dt, s_g, grads, dev)
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -474,6 +476,35 @@ def adamw_probe(fm, lay, dt, s_g, n_loc, grads, dev, reps=20):
     return {"us": round(ms * 1e3, 1), "bytes_per_elem": s_g + 32, "gbs": round(by / (ms * 1e-3) / 1e9, 1),
             "frac_of_peak": round(by / (ms * 1e-3) / 1e9 / peak, 4),
             "saved_vs_unfused_bytes_per_elem": s_g}
+
+
+def rs_probe(lay, dt, s_g, grads, dev, reps=20):
+    """NEXT 1 (ZeRO form) at P = 1 on this GPU: af_reduce_scatter_step reading the
+    registered gradient, writing the reduced shard (fp32) and accumulating Delta --
+    s_g + 4 + 8 bytes per element.  The P > 1 form pulls P-1 shards over NVLink
+    (not measurable on one GPU)."""
+    import torch
+
+    import paper_2102_01386_b200 as af
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, device=dev)
+    fm.set_grad_peers_local([grads[0]])
+    out = torch.empty(lay.n, device=dev)
+    fm.reduce_scatter_step(out)                       # committed: Delta armed, every rep reads it
+    for _ in range(2):
+        fm.reduce_scatter_step(out, dry_run=True)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fm.reduce_scatter_step(out, dry_run=True)
+    b.record()
+    b.synchronize()
+    ms = a.elapsed_time(b) / reps
+    peak, _ = measured_peaks()
+    by = lay.n * (s_g + 12)
+    del out, fm
+    return {"us": round(ms * 1e3, 1), "bytes_per_elem": s_g + 12, "gbs": round(by / (ms * 1e-3) / 1e9, 1),
+            "frac_of_peak": round(by / (ms * 1e-3) / 1e9 / peak, 4), "world": 1}
 
 
 def run_sweep(args, local):

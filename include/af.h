@@ -287,6 +287,18 @@ AF_API af_status af_ctx_set_grad_peers_local(af_ctx *ctx, const void *const *gra
 AF_API af_status af_reduce_scatter_step(af_ctx *ctx, float scale, float *grad_shard_out_dev, uint32_t flags,
                                         af_decision *out_host, void *stream);
 
+/* af_reduce_scatter_step with the optimizer of the same shard fused in (ZeRO:
+ * each rank owns its shard's AdamW state): for every active element i of the
+ * shard, gs_i as above, then AdamW with gs_i exactly as af_adamw_step (same
+ * constants, same fp32 operation order) on params/exp_avg/exp_avg_sq (FULL
+ * flat fp32 buffers indexed by i, 16-byte aligned; only the shard's active
+ * elements are touched), and the Delta accumulate / interval end with gs_i.
+ * grad_shard_out_dev may be NULL.  The caller all-gathers the updated
+ * parameter shards.  Errors as af_reduce_scatter_step and af_adamw_step. */
+AF_API af_status af_reduce_scatter_adamw_step(af_ctx *ctx, float scale, float *params_dev, float *exp_avg_dev,
+                                              float *exp_avg_sq_dev, const af_adamw *hp, float *grad_shard_out_dev,
+                                              uint32_t flags, af_decision *out_host, void *stream);
+
 /* Synchronous.  Serialise / restore {T, f, prev norms, Delta-armed flag}
  * (checkpoint at interval boundaries is exact).  With buf == NULL, get_state
  * stores the required size in *len. */

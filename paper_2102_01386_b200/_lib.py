@@ -85,6 +85,8 @@ SIGNATURES = {
     "af_ctx_set_grad_peers_ipc": (c_int, [c_void_p, c_void_p]),
     "af_ctx_set_grad_peers_local": (c_int, [c_void_p, c_void_p]),
     "af_reduce_scatter_step": (c_int, [c_void_p, ctypes.c_float, c_void_p, c_uint32, c_void_p, c_void_p]),
+    "af_reduce_scatter_adamw_step": (c_int, [c_void_p, ctypes.c_float, c_void_p, c_void_p, c_void_p, POINTER(AfAdamW),
+                                             c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_get_state": (c_int, [c_void_p, c_void_p, POINTER(c_size_t)]),
     "af_set_state": (c_int, [c_void_p, c_void_p, c_size_t]),
     "af_ctx_destroy": (c_int, [c_void_p]),

@@ -163,6 +163,23 @@ class FreezingModule:
             self._event.record(stream if stream is not None else torch.cuda.current_stream())
         return out
 
+    def reduce_scatter_adamw_step(self, params, exp_avg, exp_avg_sq, lr, step, beta1=0.9, beta2=0.999, eps=1e-8,
+                                  weight_decay=0.0, out=None, scale=None, interval_end=False, dry_run=False,
+                                  stream=None, copy_record=True):
+        """af_reduce_scatter_adamw_step: the fused reduce-scatter with AdamW on this
+        rank's shard of params / exp_avg / exp_avg_sq (full flat fp32 tensors)."""
+        sc = (1.0 / self.world) if scale is None else float(scale)
+        hp = L.AfAdamW(float(lr), float(beta1), float(beta2), float(eps), float(weight_decay), int(step))
+        flags = (L.AF_INTERVAL_END if interval_end else 0) | (L.AF_DRY_RUN if dry_run else 0)
+        rec = c_void_p(self._rec_host.data_ptr()) if (copy_record and interval_end) else c_void_p(0)
+        check(lib.af_reduce_scatter_adamw_step(
+            self._h, ctypes.c_float(sc), c_void_p(params.data_ptr()), c_void_p(exp_avg.data_ptr()),
+            c_void_p(exp_avg_sq.data_ptr()), byref(hp), c_void_p(out.data_ptr() if out is not None else 0), flags,
+            rec, _stream_handle(stream)), "af_reduce_scatter_adamw_step")
+        if interval_end and copy_record and not torch.cuda.is_current_stream_capturing():
+            self._event.record(stream if stream is not None else torch.cuda.current_stream())
+        return out
+
     def exchange_rows(self):
         """float64 view [world, L] of the exchange matrix inside the scratch buffer."""
         p = c_void_p()

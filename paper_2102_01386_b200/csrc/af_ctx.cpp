@@ -232,12 +232,12 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
   int sms = 0;
   cudaError_t e = static_cast<cudaError_t>(device_sm_count(&sms));
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
-  e = static_cast<cudaError_t>(preload_norm_kernels(c->dtype));
+  e = static_cast<cudaError_t>(preload_norm_kernels(c->dtype, c->cfg.world));
   if (e == cudaSuccess) e = static_cast<cudaError_t>(preload_decide_kernel());
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes (kernel preload)");
   for (int m = 0; m < kNumModes; ++m) {
     int bps = 0;
-    e = static_cast<cudaError_t>(norms_max_blocks_per_sm(m, c->dtype, &bps));
+    e = static_cast<cudaError_t>(norms_max_blocks_per_sm(m, c->dtype, c->cfg.world, &bps));
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     c->grid[m] = std::max(1, sms * std::max(1, bps));
   }
@@ -421,19 +421,49 @@ af_status af_layer_norms(af_ctx *c, const void *grad_dev, uint32_t flags, void *
   return AF_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// AdamW constants rounded once to fp32 (the oracle rounds the same fp64 values)
+AdamConst adam_const(const af_adamw &hp) {
+  AdamConst a{};
+  const double lr = hp.lr, b1 = hp.beta1, b2 = hp.beta2;
+  a.decay = static_cast<float>(1.0 - lr * static_cast<double>(hp.weight_decay));
+  a.beta1 = hp.beta1;
+  a.one_minus_beta1 = static_cast<float>(1.0 - b1);
+  a.beta2 = hp.beta2;
+  a.one_minus_beta2 = static_cast<float>(1.0 - b2);
+  a.step_size = static_cast<float>(lr / (1.0 - std::pow(b1, hp.step)));
+  a.sqrt_bc2 = static_cast<float>(std::sqrt(1.0 - std::pow(b2, hp.step)));
+  a.eps = hp.eps;
+  return a;
+}
+
+af_status check_adam(const af_adamw *hp, const float *params_dev, const float *exp_avg_dev,
+                     const float *exp_avg_sq_dev) {
+  if (!hp || !params_dev || !exp_avg_dev || !exp_avg_sq_dev) return fail(AF_EINVAL, "NULL argument");
+  if (!aligned(params_dev, 16) || !aligned(exp_avg_dev, 16) || !aligned(exp_avg_sq_dev, 16))
+    return fail(AF_EINVAL, "optimizer buffers must be 16-byte aligned");
+  if (hp->step < 1 || !(hp->beta1 >= 0.f && hp->beta1 < 1.f) || !(hp->beta2 >= 0.f && hp->beta2 < 1.f) ||
+      !(hp->eps > 0.f) || !(hp->lr >= 0.f) || !(hp->weight_decay >= 0.f))
+    return fail(AF_EINVAL, "bad AdamW hyper-parameters");
+  return AF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 af_status af_adamw_step(af_ctx *c, float *params_dev, float *exp_avg_dev, float *exp_avg_sq_dev,
                         const void *grad_dev, const af_adamw *hp, uint32_t flags, af_decision *out_host,
                         void *stream) {
   af_status st = check_norm_args(c, grad_dev);
   if (st != AF_OK) return st;
-  if (!hp || !params_dev || !exp_avg_dev || !exp_avg_sq_dev) return fail(AF_EINVAL, "NULL argument");
-  if (!aligned(params_dev, 16) || !aligned(exp_avg_dev, 16) || !aligned(exp_avg_sq_dev, 16))
-    return fail(AF_EINVAL, "optimizer buffers must be 16-byte aligned");
+  st = check_adam(hp, params_dev, exp_avg_dev, exp_avg_sq_dev);
+  if (st != AF_OK) return st;
   if (c->cfg.acc_mode != AF_ACC_DELTA) return fail(AF_ESTATE, "af_adamw_step needs acc_mode AF_ACC_DELTA");
   if (flags & ~(AF_INTERVAL_END | AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
-  if (hp->step < 1 || !(hp->beta1 >= 0.f && hp->beta1 < 1.f) || !(hp->beta2 >= 0.f && hp->beta2 < 1.f) ||
-      !(hp->eps > 0.f) || !(hp->lr >= 0.f) || !(hp->weight_decay >= 0.f))
-    return fail(AF_EINVAL, "bad AdamW hyper-parameters");
   const bool end = flags & AF_INTERVAL_END, dry = flags & AF_DRY_RUN;
   if (end && c->cfg.world > 1 && !c->peers && !c->comm)
     return fail(AF_ESTATE, "interval end with world > 1 needs peers or a communicator");
@@ -442,16 +472,7 @@ af_status af_adamw_step(af_ctx *c, float *params_dev, float *exp_avg_dev, float 
   p.params = params_dev;
   p.exp_avg = exp_avg_dev;
   p.exp_avg_sq = exp_avg_sq_dev;
-  // constants rounded once to fp32 (the oracle rounds the same fp64 values)
-  const double lr = hp->lr, b1 = hp->beta1, b2 = hp->beta2;
-  p.adam.decay = static_cast<float>(1.0 - lr * static_cast<double>(hp->weight_decay));
-  p.adam.beta1 = hp->beta1;
-  p.adam.one_minus_beta1 = static_cast<float>(1.0 - b1);
-  p.adam.beta2 = hp->beta2;
-  p.adam.one_minus_beta2 = static_cast<float>(1.0 - b2);
-  p.adam.step_size = static_cast<float>(lr / (1.0 - std::pow(b1, hp->step)));
-  p.adam.sqrt_bc2 = static_cast<float>(std::sqrt(1.0 - std::pow(b2, hp->step)));
-  p.adam.eps = hp->eps;
+  p.adam = adam_const(*hp);
   const bool fuse = end && (c->cfg.world == 1 || c->peers);
   if (fuse) {
     p.fuse_decide = 1;
@@ -695,8 +716,11 @@ af_status af_ctx_set_grad_peers_local(af_ctx *c, const void *const *grads_dev) {
   return upload_grads(c, g);
 }
 
-af_status af_reduce_scatter_step(af_ctx *c, float scale, float *grad_shard_out_dev, uint32_t flags,
-                                 af_decision *out_host, void *stream) {
+}  // extern "C"
+
+static af_status rs_step(af_ctx *c, float scale, float *grad_shard_out_dev, const af_adamw *hp, float *params_dev,
+                         float *exp_avg_dev, float *exp_avg_sq_dev, uint32_t flags, af_decision *out_host,
+                         void *stream) {
   if (!c) return fail(AF_EINVAL, "NULL ctx");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   if (!c->grad_peers) return fail(AF_ESTATE, "no gradient buffers registered (af_ctx_set_grad_peers_*)");
@@ -707,8 +731,15 @@ af_status af_reduce_scatter_step(af_ctx *c, float scale, float *grad_shard_out_d
   if (c->cfg.world > 1 && !c->peers)
     return fail(AF_ESTATE, "world > 1 needs peers (af_ctx_set_peers_*) for the reduce-scatter flags");
   const bool end = flags & AF_INTERVAL_END, dry = flags & AF_DRY_RUN;
-  const int mode = end ? kRsEnd : kRsAccum;
+  const bool adam = hp != nullptr;
+  const int mode = adam ? (end ? kRsAdamEnd : kRsAdamAccum) : (end ? kRsEnd : kRsAccum);
   NormParams p = norm_params(c, c->own_grad, end, dry);
+  if (adam) {
+    p.params = params_dev;
+    p.exp_avg = exp_avg_dev;
+    p.exp_avg_sq = exp_avg_sq_dev;
+    p.adam = adam_const(*hp);
+  }
   p.rs_world = c->cfg.world;
   p.rs_rank = c->cfg.rank;
   p.rs_grads = c->at<const void *const>(c->o_rs_grads);
@@ -731,6 +762,21 @@ af_status af_reduce_scatter_step(af_ctx *c, float scale, float *grad_shard_out_d
     c->pending = false;
   }
   return AF_OK;
+}
+
+extern "C" {
+
+af_status af_reduce_scatter_step(af_ctx *c, float scale, float *grad_shard_out_dev, uint32_t flags,
+                                 af_decision *out_host, void *stream) {
+  return rs_step(c, scale, grad_shard_out_dev, nullptr, nullptr, nullptr, nullptr, flags, out_host, stream);
+}
+
+af_status af_reduce_scatter_adamw_step(af_ctx *c, float scale, float *params_dev, float *exp_avg_dev,
+                                       float *exp_avg_sq_dev, const af_adamw *hp, float *grad_shard_out_dev,
+                                       uint32_t flags, af_decision *out_host, void *stream) {
+  const af_status st = check_adam(hp, params_dev, exp_avg_dev, exp_avg_sq_dev);
+  if (st != AF_OK) return st;
+  return rs_step(c, scale, grad_shard_out_dev, hp, params_dev, exp_avg_dev, exp_avg_sq_dev, flags, out_host, stream);
 }
 
 struct StateBlob {

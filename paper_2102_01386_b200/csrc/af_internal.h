@@ -65,8 +65,11 @@ struct DevState {
 #endif
 constexpr int kFinChunk = 2048;  // partials per fin_kernel CTA (8 per thread)
 
-enum Mode : int { kAccum = 0, kEndDelta = 1, kStepSq = 2, kAdamAccum = 3, kAdamEnd = 4, kRsAccum = 5, kRsEnd = 6 };
-constexpr int kNumModes = 7;
+enum Mode : int {
+  kAccum = 0, kEndDelta = 1, kStepSq = 2, kAdamAccum = 3, kAdamEnd = 4,
+  kRsAccum = 5, kRsEnd = 6, kRsAdamAccum = 7, kRsAdamEnd = 8
+};
+constexpr int kNumModes = 9;
 constexpr int kMaxRsWorld = 8;  // ranks of one fused reduce-scatter (one NVLink domain's GPUs per node)
 
 // AdamW constants of one step, rounded once to fp32 on the host (NEXT 1 fusion).
@@ -256,9 +259,9 @@ int launch_decide(const DecideParams &p, void *stream);
 int launch_cache_put(const CacheParams &p, int grid, void *stream);
 int launch_cache_get(const CacheParams &p, int grid, void *stream);
 int launch_cache_plan(const CachePlanParams &p, void *stream);
-int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks);
+int norms_max_blocks_per_sm(int mode, int grad_dtype, int world, int *blocks);
 // force-load the kernels (lazy module loading must not happen while peers spin)
-int preload_norm_kernels(int grad_dtype);
+int preload_norm_kernels(int grad_dtype, int world);
 int preload_decide_kernel();
 int preload_cache_kernels();
 int cache_smem_bytes();

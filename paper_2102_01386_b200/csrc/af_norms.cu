@@ -54,8 +54,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef AF_MINB_END
 #define AF_MINB_END 1
 #endif
-#ifndef AF_U_RS  // fused reduce-scatter: vectors in flight per thread and rank
-#define AF_U_RS 2
+#ifndef AF_U_RS_VEC  // fused reduce-scatter: gradient vectors in flight per thread (over all ranks)
+#define AF_U_RS_VEC 8
 #endif
 
 namespace af {
@@ -323,12 +323,16 @@ __device__ __forceinline__ double process_tile_adam(const NormParams &p, const T
 // optimizer's shard buffer and accumulates it into Delta exactly like kAccum /
 // kEndDelta accumulate g.  The reduced gradient never makes an HBM round trip
 // before the accumulate reads it.
-template <bool END, typename GT, bool RD>
-__device__ __forceinline__ double process_tile_rs(const NormParams &p, const Tile &t,
-                                                  const GT *const (&gr)[kMaxRsWorld]) {
+template <bool END, bool ADAM, typename GT, bool RD, int PM>
+__device__ __forceinline__ double process_tile_rs(const NormParams &p, const Tile &t, const GT *const (&gr)[PM]) {
   constexpr int VE = VT<GT>::VE;
   constexpr int DV = VE / 4;
-  constexpr int U = AF_U_RS;
+  // PM = compile-time bound on the ranks (1, 2, 4, 8; P <= PM at run time): the
+  // vectors in flight per thread stay U x PM = AF_U_RS_BYTES / 16 whatever P is
+  constexpr int U = ADAM ? 1 : (AF_U_RS_VEC / PM > 0 ? AF_U_RS_VEC / PM : 1);
+  float *__restrict__ pw = p.params;
+  float *__restrict__ mm = p.exp_avg;
+  float *__restrict__ vv = p.exp_avg_sq;
   const int P = p.rs_world;
   const float sc = p.rs_scale;
   float *__restrict__ d = p.delta - p.shard_begin;
@@ -349,6 +353,13 @@ __device__ __forceinline__ double process_tile_rs(const NormParams &p, const Til
       acc = sq_acc(x, acc);
     else
       d[i] = x;
+    if (ADAM) {
+      float pv = pw[i], mv = mm[i], v2 = vv[i];
+      adamw_elem(p.adam, gs, pv, mv, v2);
+      pw[i] = pv;
+      mm[i] = mv;
+      vv[i] = v2;
+    }
   };
   const int nh = static_cast<int>(vb - b), nt = static_cast<int>(e - ve);
   if (tid < nh) scalar(b + tid, a0);
@@ -357,18 +368,27 @@ __device__ __forceinline__ double process_tile_rs(const NormParams &p, const Til
   float4 *db = reinterpret_cast<float4 *>(d + vb);
   float4 *ob = o ? reinterpret_cast<float4 *>(o + vb) : nullptr;
   for (int64_t c0 = tid; c0 < nch; c0 += U * kNormBlock) {
-    uint4 gv[U][kMaxRsWorld];
+    uint4 gv[U][PM];
     float4 dv[U][DV];
+    float4 pa[ADAM ? U : 1][DV], ma[ADAM ? U : 1][DV], va[ADAM ? U : 1][DV];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t c = c0 + static_cast<int64_t>(u) * kNormBlock;
       if (c < nch) {
 #pragma unroll
-        for (int r = 0; r < kMaxRsWorld; ++r)
+        for (int r = 0; r < PM; ++r)
           if (r < P) gv[u][r] = __ldcs(reinterpret_cast<const uint4 *>(gr[r] + vb) + c);
         if (RD) {
 #pragma unroll
           for (int q = 0; q < DV; ++q) dv[u][q] = __ldcs(db + c * DV + q);
+        }
+        if (ADAM) {
+#pragma unroll
+          for (int q = 0; q < DV; ++q) {
+            pa[u][q] = __ldcs(reinterpret_cast<const float4 *>(pw + vb) + c * DV + q);
+            ma[u][q] = __ldcs(reinterpret_cast<const float4 *>(mm + vb) + c * DV + q);
+            va[u][q] = __ldcs(reinterpret_cast<const float4 *>(vv + vb) + c * DV + q);
+          }
         }
       }
     }
@@ -379,7 +399,7 @@ __device__ __forceinline__ double process_tile_rs(const NormParams &p, const Til
         float x[VE];
         unpack<VE>(gv[u][0], x);
 #pragma unroll
-        for (int r = 1; r < kMaxRsWorld; ++r) {
+        for (int r = 1; r < PM; ++r) {
           if (r < P) {
             float y[VE];
             unpack<VE>(gv[u][r], y);
@@ -392,6 +412,18 @@ __device__ __forceinline__ double process_tile_rs(const NormParams &p, const Til
         if (ob) {
 #pragma unroll
           for (int q = 0; q < DV; ++q) ob[c * DV + q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+        }
+        if (ADAM) {
+#pragma unroll
+          for (int q = 0; q < DV; ++q) {
+            adamw_elem(p.adam, x[4 * q + 0], pa[u][q].x, ma[u][q].x, va[u][q].x);
+            adamw_elem(p.adam, x[4 * q + 1], pa[u][q].y, ma[u][q].y, va[u][q].y);
+            adamw_elem(p.adam, x[4 * q + 2], pa[u][q].z, ma[u][q].z, va[u][q].z);
+            adamw_elem(p.adam, x[4 * q + 3], pa[u][q].w, ma[u][q].w, va[u][q].w);
+            __stcs(reinterpret_cast<float4 *>(pw + vb) + c * DV + q, pa[u][q]);
+            __stcs(reinterpret_cast<float4 *>(mm + vb) + c * DV + q, ma[u][q]);
+            __stcs(reinterpret_cast<float4 *>(vv + vb) + c * DV + q, va[u][q]);
+          }
         }
         if (RD) {
 #pragma unroll
@@ -569,10 +601,10 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) 
   }
 }
 
-template <int MODE, typename GT, bool RD>
+template <int MODE, typename GT, bool RD, int PM = 1>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAccum) ? 1 : AF_MINB_END)
     norms_kernel(const NormParams p) {
-  constexpr bool RS = MODE == kRsAccum || MODE == kRsEnd;
+  constexpr bool RS = MODE == kRsAccum || MODE == kRsEnd || MODE == kRsAdamAccum || MODE == kRsAdamEnd;
   __shared__ int s_tile[3];
   __shared__ Tile s_desc[3];
   __shared__ double s_red[kNormBlock / 32];
@@ -584,10 +616,10 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
   int f = p.state->f;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int first_tile = p.first_tile_of_f[f];
-  const GT *rs_g[kMaxRsWorld];
+  const GT *rs_g[PM];
   if constexpr (RS) {
 #pragma unroll
-    for (int r = 0; r < kMaxRsWorld; ++r) rs_g[r] = r < p.rs_world ? static_cast<const GT *>(p.rs_grads[r]) : nullptr;
+    for (int r = 0; r < PM; ++r) rs_g[r] = r < p.rs_world ? static_cast<const GT *>(p.rs_grads[r]) : nullptr;
     if (p.rs_world > 1) {
       if (tid == 0) s_rs_epoch = p.state->rs_epoch + 1ull;  // advanced by the last CTA only
       __syncthreads();
@@ -629,14 +661,15 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
     if constexpr (MODE == kAdamAccum || MODE == kAdamEnd)
       v = process_tile_adam<MODE == kAdamEnd, GT, RD>(p, t);
     else if constexpr (RS)
-      v = process_tile_rs<MODE == kRsEnd, GT, RD>(p, t, rs_g);
+      v = process_tile_rs<MODE == kRsEnd || MODE == kRsAdamEnd, MODE == kRsAdamAccum || MODE == kRsAdamEnd, GT, RD,
+                          PM>(p, t, rs_g);
     else
       v = process_tile<MODE, GT, RD>(p, t);
     if (tid == 0) {
       s_tile[slot2] = next2;
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    if (MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum) {
+    if (MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum && MODE != kRsAdamAccum) {
       const double w = warp_sum(v);
       if (lane == 0) s_red[warp] = w;
       __syncthreads();
@@ -672,12 +705,12 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
       if (tid == 0) const_cast<DevState *>(p.state)->rs_epoch = s_rs_epoch;
     }
   }
-  if (MODE == kAccum || MODE == kAdamAccum || MODE == kRsAccum) return;
+  if (MODE == kAccum || MODE == kAdamAccum || MODE == kRsAccum || MODE == kRsAdamAccum) return;
   if (p.wide_fin) {  // fin_kernel sums the partials
     if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
     return;
   }
-  last_cta_tail<(MODE == kAdamEnd || MODE == kRsEnd) ? kEndDelta : MODE, false>(p, first_tile);
+  last_cta_tail<(MODE == kAdamEnd || MODE == kRsEnd || MODE == kRsAdamEnd) ? kEndDelta : MODE, false>(p, first_tile);
 }
 
 // Wide finalize of the interval-end kernels (n_tiles > kFinChunk): CTA c stages
@@ -980,45 +1013,60 @@ int launch_tma(const NormParams &p, int grid, void *stream) {
                                      static_cast<size_t>(smem), static_cast<cudaStream_t>(stream), p));
 }
 
-template <int MODE, typename GT, bool RD>
-int launch_one(const NormParams &p, int grid, void *stream) {
-  return static_cast<int>(
-      launch_pdl(norms_kernel<MODE, GT, RD>, dim3(grid), dim3(kNormBlock), 0, static_cast<cudaStream_t>(stream), p));
+using NormKernel = void (*)(const NormParams);
+
+template <int MODE, typename GT, int PM>
+NormKernel rd_pick(bool rd) {
+  return rd ? norms_kernel<MODE, GT, true, PM> : norms_kernel<MODE, GT, false, PM>;
+}
+
+template <typename GT, int PM>
+NormKernel rs_kernel(int mode, bool rd) {
+  switch (mode) {
+    case kRsAccum: return rd_pick<kRsAccum, GT, PM>(rd);
+    case kRsEnd: return rd_pick<kRsEnd, GT, PM>(rd);
+    case kRsAdamAccum: return rd_pick<kRsAdamAccum, GT, PM>(rd);
+    default: return rd_pick<kRsAdamEnd, GT, PM>(rd);
+  }
+}
+
+int pm_of(int world) { return world <= 1 ? 1 : (world == 2 ? 2 : (world <= 4 ? 4 : 8)); }
+
+// The streaming kernel instantiation of (mode, Delta read, world).
+template <typename GT>
+NormKernel kernel_for(int mode, bool rd, int world) {
+  switch (mode) {
+    case kAccum: return rd_pick<kAccum, GT, 1>(rd);
+    case kEndDelta: return rd_pick<kEndDelta, GT, 1>(rd);
+    case kStepSq: return norms_kernel<kStepSq, GT, false>;
+    case kAdamAccum: return rd_pick<kAdamAccum, GT, 1>(rd);
+    case kAdamEnd: return rd_pick<kAdamEnd, GT, 1>(rd);
+    default:
+      switch (pm_of(world)) {
+        case 1: return rs_kernel<GT, 1>(mode, rd);
+        case 2: return rs_kernel<GT, 2>(mode, rd);
+        case 4: return rs_kernel<GT, 4>(mode, rd);
+        default: return rs_kernel<GT, 8>(mode, rd);
+      }
+  }
 }
 
 template <typename GT>
 int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
   const bool rd = !p.first;
-  switch (mode) {
-    case kAccum:
-      if (AF_TMA >= 2)
-        return rd ? launch_tma<kAccum, GT, true>(p, grid, stream) : launch_tma<kAccum, GT, false>(p, grid, stream);
-      return rd ? launch_one<kAccum, GT, true>(p, grid, stream) : launch_one<kAccum, GT, false>(p, grid, stream);
-    case kEndDelta:
-      if (AF_TMA >= 1)
-        return rd ? launch_tma<kEndDelta, GT, true>(p, grid, stream)
-                  : launch_tma<kEndDelta, GT, false>(p, grid, stream);
-      return rd ? launch_one<kEndDelta, GT, true>(p, grid, stream)
-                : launch_one<kEndDelta, GT, false>(p, grid, stream);
-    case kStepSq:
-      return launch_one<kStepSq, GT, false>(p, grid, stream);
-    case kAdamAccum:
-      return rd ? launch_one<kAdamAccum, GT, true>(p, grid, stream)
-                : launch_one<kAdamAccum, GT, false>(p, grid, stream);
-    case kAdamEnd:
-      return rd ? launch_one<kAdamEnd, GT, true>(p, grid, stream) : launch_one<kAdamEnd, GT, false>(p, grid, stream);
-    case kRsAccum:
-      return rd ? launch_one<kRsAccum, GT, true>(p, grid, stream) : launch_one<kRsAccum, GT, false>(p, grid, stream);
-    case kRsEnd:
-      return rd ? launch_one<kRsEnd, GT, true>(p, grid, stream) : launch_one<kRsEnd, GT, false>(p, grid, stream);
-  }
-  return static_cast<int>(cudaErrorInvalidValue);
+  if (mode == kAccum && AF_TMA >= 2)
+    return rd ? launch_tma<kAccum, GT, true>(p, grid, stream) : launch_tma<kAccum, GT, false>(p, grid, stream);
+  if (mode == kEndDelta && AF_TMA >= 1)
+    return rd ? launch_tma<kEndDelta, GT, true>(p, grid, stream) : launch_tma<kEndDelta, GT, false>(p, grid, stream);
+  if (mode < 0 || mode >= kNumModes) return static_cast<int>(cudaErrorInvalidValue);
+  return static_cast<int>(launch_pdl(kernel_for<GT>(mode, rd, p.rs_world), dim3(grid), dim3(kNormBlock), 0,
+                                     static_cast<cudaStream_t>(stream), p));
 }
 
 }  // namespace
 
 int fin_ctas(int mode, int n_tiles) {
-  const bool end_mode = mode == kEndDelta || mode == kStepSq || mode == kAdamEnd || mode == kRsEnd;
+  const bool end_mode = mode == kEndDelta || mode == kStepSq || mode == kAdamEnd || mode == kRsEnd || mode == kRsAdamEnd;
   if (!AF_FIN_WIDE || !end_mode || n_tiles <= kFinChunk || (mode == kEndDelta && AF_TMA >= 1)) return 0;
   return (n_tiles + kFinChunk - 1) / kFinChunk;
 }
@@ -1035,65 +1083,24 @@ int launch_norms(const NormParams &p_in, int mode, int grad_dtype, int grid, voi
       launch_pdl(fk, dim3(nfin), dim3(kNormBlock), 0, static_cast<cudaStream_t>(stream), p));
 }
 
+// Load every kernel this context can launch now.  Under CUDA's lazy module
+// loading the first launch of a kernel loads it, and a load may wait for the
+// kernels in flight -- fatal when those are spinning on a peer rank (fused
+// reduce-scatter barriers, the exchange) whose own launch sits behind this host
+// thread.
 template <typename GT>
-static int occ_dt(int mode, int *blocks) {
-  cudaError_t e;
-  switch (mode) {
-    case kAccum:
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kAccum, GT, true>, kNormBlock, 0);
-      break;
-    case kEndDelta:
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kEndDelta, GT, true>, kNormBlock, 0);
-      break;
-    case kAdamAccum:
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kAdamAccum, GT, true>, kNormBlock, 0);
-      break;
-    case kAdamEnd:
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kAdamEnd, GT, true>, kNormBlock, 0);
-      break;
-    case kRsAccum:
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kRsAccum, GT, true>, kNormBlock, 0);
-      break;
-    case kRsEnd:
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kRsEnd, GT, true>, kNormBlock, 0);
-      break;
-    default:
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, norms_kernel<kStepSq, GT, false>, kNormBlock, 0);
-  }
-  return static_cast<int>(e);
-}
-
-// Load every kernel of this file now.  Under CUDA's lazy module loading the
-// first launch of a kernel loads it, and a load may wait for the kernels in
-// flight -- fatal when those are spinning on a peer rank (fused reduce-scatter
-// barriers, the exchange) whose own launch sits behind this host thread.
-template <typename GT>
-static cudaError_t preload_dt() {
-  const void *ks[] = {
-      reinterpret_cast<const void *>(norms_kernel<kAccum, GT, true>),
-      reinterpret_cast<const void *>(norms_kernel<kAccum, GT, false>),
-      reinterpret_cast<const void *>(norms_kernel<kEndDelta, GT, true>),
-      reinterpret_cast<const void *>(norms_kernel<kEndDelta, GT, false>),
-      reinterpret_cast<const void *>(norms_kernel<kStepSq, GT, false>),
-      reinterpret_cast<const void *>(norms_kernel<kAdamAccum, GT, true>),
-      reinterpret_cast<const void *>(norms_kernel<kAdamAccum, GT, false>),
-      reinterpret_cast<const void *>(norms_kernel<kAdamEnd, GT, true>),
-      reinterpret_cast<const void *>(norms_kernel<kAdamEnd, GT, false>),
-      reinterpret_cast<const void *>(norms_kernel<kRsAccum, GT, true>),
-      reinterpret_cast<const void *>(norms_kernel<kRsAccum, GT, false>),
-      reinterpret_cast<const void *>(norms_kernel<kRsEnd, GT, true>),
-      reinterpret_cast<const void *>(norms_kernel<kRsEnd, GT, false>),
-  };
+static cudaError_t preload_dt(int world) {
   cudaFuncAttributes a;
-  for (const void *k : ks) {
-    const cudaError_t e = cudaFuncGetAttributes(&a, k);
-    if (e != cudaSuccess) return e;
-  }
+  for (int m = 0; m < kNumModes; ++m)
+    for (int rd = 0; rd < 2; ++rd) {
+      const cudaError_t e = cudaFuncGetAttributes(&a, kernel_for<GT>(m, rd != 0, world));
+      if (e != cudaSuccess) return e;
+    }
   return cudaSuccess;
 }
 
-int preload_norm_kernels(int grad_dtype) {
-  cudaError_t e = grad_dtype == AF_DT_BF16 ? preload_dt<uint16_t>() : preload_dt<float>();
+int preload_norm_kernels(int grad_dtype, int world) {
+  cudaError_t e = grad_dtype == AF_DT_BF16 ? preload_dt<uint16_t>(world) : preload_dt<float>(world);
   if (e != cudaSuccess) return static_cast<int>(e);
   cudaFuncAttributes a;
   for (const void *k : {reinterpret_cast<const void *>(fin_kernel<kEndDelta>),
@@ -1104,12 +1111,15 @@ int preload_norm_kernels(int grad_dtype) {
   return 0;
 }
 
-int norms_max_blocks_per_sm(int mode, int grad_dtype, int *blocks) {
+int norms_max_blocks_per_sm(int mode, int grad_dtype, int world, int *blocks) {
   if ((mode == kEndDelta && AF_TMA >= 1) || (mode == kAccum && AF_TMA >= 2)) {
     *blocks = 1;  // the TMA-staged kernels run one CTA per SM
     return 0;
   }
-  return grad_dtype == AF_DT_BF16 ? occ_dt<uint16_t>(mode, blocks) : occ_dt<float>(mode, blocks);
+  NormKernel k = grad_dtype == AF_DT_BF16 ? kernel_for<uint16_t>(mode, true, world) : kernel_for<float>(mode, true, world);
+  if (mode == kStepSq) k = grad_dtype == AF_DT_BF16 ? kernel_for<uint16_t>(mode, false, world)
+                                                   : kernel_for<float>(mode, false, world);
+  return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, kNormBlock, 0));
 }
 
 }  // namespace af

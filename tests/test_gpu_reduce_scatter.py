@@ -144,3 +144,48 @@ def test_reduce_scatter_argument_errors():
     st.set_grad_peers_local([torch.zeros(lay.n, device="cuda")])
     with pytest.raises(af.AfError):                             # STEP_SUMSQ reading
         st.reduce_scatter_step(None)
+
+
+@pytest.mark.parametrize("P,dt,seed", [(2, "bf16", 52), (3, "f32", 53)])
+def test_fused_reduce_scatter_adamw_parity(P, dt, seed):
+    """af_reduce_scatter_adamw_step: every rank's shard of params / moments
+    bit-exact vs the oracle's AdamW on the reduced gradient (its other elements
+    untouched), Delta and records as the oracle's."""
+    lay = uniform_layout(600_011, 9, pre=20_001, head=777)
+    fms, grads = _ranks(lay, dt, P, max(1, 120 // P))
+    infos = [fm.info() for fm in fms]
+    rng = np.random.default_rng(seed)
+    p0 = rng.standard_normal(lay.n).astype(np.float32)
+    Pm, M, V = p0.copy(), np.zeros(lay.n, np.float32), np.zeros(lay.n, np.float32)
+    dev = [[torch.from_numpy(x.copy()).cuda() for x in (p0, M, V)] for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    oz = O.Freezer(lay.offsets, lay.kinds, O.DT_F32)
+    code = O.DT_BF16 if dt == "bf16" else O.DT_F32
+    step = _rank_step(lay, dt, seed, P)
+    k = 0
+    for T, S in enumerate([2, 1, 3, 2, 2]):
+        for t in range(S):
+            k += 1
+            gnp = step(T, t)
+            for g, x in zip(grads, gnp):
+                g.copy_(to_device_grad(x, dt))
+            torch.cuda.synchronize()
+            end = t == S - 1
+            for fm, s, (tp, tm, tv) in zip(fms, streams, dev):
+                with torch.cuda.stream(s):
+                    fm.reduce_scatter_adamw_step(tp, tm, tv, lr=1e-3, step=k, weight_decay=0.01,
+                                                 interval_end=end, stream=s)
+            torch.cuda.synchronize()
+            gs = O.reduce_gradients(gnp, code, 1.0 / P)
+            oz.adamw_active(Pm, M, V, gs, O.adamw_constants(1e-3, 0.9, 0.999, 1e-8, 0.01, k))
+            oz.layer_norms(gs, end)
+        decs = [fm.decision() for fm in fms]
+        compare_records(decs[0], oz.update_and_decide(), lay.n_segments, tag=f"T={T}")
+        for i, (tp, tm, tv) in zip(infos, dev):
+            sb, se = i["shard_begin"], i["shard_end"]
+            for got, want, init in ((tp, Pm, p0), (tm, M, 0.0), (tv, V, 0.0)):
+                g = got.cpu().numpy()
+                assert np.array_equal(g[sb:se], want[sb:se]), f"T={T} rank shard [{sb},{se})"
+                assert np.all(g[:sb] == (init[:sb] if isinstance(init, np.ndarray) else init))
+                assert np.all(g[se:] == (init[se:] if isinstance(init, np.ndarray) else init))
+    assert oz.f >= 1
