@@ -28,32 +28,47 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
   __shared__ double s_eta[AF_MAX_SEGMENTS];
   __shared__ double s_act[AF_MAX_SEGMENTS];
   __shared__ double s_sorted[AF_MAX_SEGMENTS];
+  __shared__ int s_pool[AF_MAX_SEGMENTS];
   __shared__ double s_thr;
   __shared__ int s_k, s_near, s_nonfinite;
   __shared__ unsigned int s_flags;
 
+  // Latency-bound: every global load below is independent of the others, so
+  // they are in flight together (one L2 round trip) -- the state words, this
+  // segment's previous norm, the POOL map, and the exchange rows of BOTH
+  // buffers when they are double-buffered (the epoch's parity picks one after
+  // the loads; each is summed in rank order, the other discarded).
   const int t = threadIdx.x;
   const int L = p.L;
   const int T = p.state->T;
-  const double *ss_all = p.ss_all + (p.xparity ? (p.state->epoch & 1ull) * p.world * p.L : 0);
   int f = p.state->f;
+  const unsigned long long epoch = p.xparity ? p.state->epoch : 0ull;
+  const double pv = (t < L) ? p.state->prev[t] : 0.0;
+  if (t < p.n_pool) s_pool[t] = p.pool_seg[t];
+  double ss = 0.0, ss_odd = 0.0;
+  if (t < L) {
+    const size_t stride = static_cast<size_t>(p.world) * L;
+    for (int r = 0; r < p.world; ++r) {
+      ss = __dadd_rn(ss, __ldcg(p.ss_all + r * L + t));
+      if (p.xparity) ss_odd = __dadd_rn(ss_odd, __ldcg(p.ss_all + stride + r * L + t));
+    }
+  }
+  if (epoch & 1ull) ss = ss_odd;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int n_act = p.n_pool - f;
 
   if (t == 0) s_nonfinite = 0;
   __syncthreads();
 
-  double ss = 0.0, nrm = 0.0, et = 0.0;
+  double nrm = 0.0, et = 0.0;
   if (t < L) {
-    for (int r = 0; r < p.world; ++r) ss = __dadd_rn(ss, __ldcg(ss_all + r * L + t));
     nrm = __dsqrt_rn(ss);
-    const double pv = p.state->prev[t];
     et = (pv == 0.0) ? 0.0 : __ddiv_rn(fabs(__dsub_rn(pv, nrm)), pv);
     s_eta[t] = et;
     if (!isfinite(ss)) s_nonfinite = 1;  // benign race: every writer stores 1
   }
   __syncthreads();
-  if (t < n_act) s_act[t] = s_eta[p.pool_seg[f + t]];
+  if (t < n_act) s_act[t] = s_eta[s_pool[f + t]];
   __syncthreads();
 
   // a peer never arrived: at the exchange (bit 0) or at a fused reduce-scatter barrier (bit 1)
@@ -115,7 +130,7 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
         const double dd = fabs(__dsub_rn(e, thr));
         if (dd > 0.0 && dd <= win) {
           fl2 |= AF_DEC_NEAR_TIE;
-          if (near < 0) near = p.pool_seg[f + i];
+          if (near < 0) near = s_pool[f + i];
         }
         if (e < thr)
           ++k;
