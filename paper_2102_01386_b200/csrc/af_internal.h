@@ -10,11 +10,11 @@ namespace af {
 
 constexpr int kNormBlock = 256;          // threads per CTA of the streaming kernels
 // Tile = the unit of dynamic scheduling and of one fp64 partial.  Sized in
-// elements so that a bf16 tile (32 KiB of g + 64 KiB of Delta) and an fp32 tile
-// (64 KiB + 64 KiB) both leave >= ~10 tiles per CTA for BERT-base, bounding the
-// end-of-kernel imbalance (see profiles/ for the sweep).
-#ifndef AF_TILE_ELEMS_F32
-#define AF_TILE_ELEMS_F32 16384
+// elements: a bf16 interval-end tile is 32 KiB of g + 64 KiB of Delta, an fp32
+// one 32 + 32 KiB -- enough tiles per CTA to bound the end-of-kernel imbalance
+// (see profiles/ for the sweeps).
+#ifndef AF_TILE_ELEMS_F32  // 8192 since the wide finalize made more partials cheap:
+#define AF_TILE_ELEMS_F32 8192  // BERT-large interval end -1.7 % (profiles/r01_v20_variants_end_tiles_f32.jsonl)
 #endif
 #ifndef AF_TILE_ELEMS_BF16
 #define AF_TILE_ELEMS_BF16 16384

@@ -24,6 +24,13 @@ RAW_METRICS = [
 ]
 
 
+OUR_KERNELS = ("norms_kernel", "fin_kernel", "decide_kernel", "cache_kernel", "cache_plan_kernel", "norms_tma_kernel")
+
+
+def is_ours(name):
+    return any(k in name for k in OUR_KERNELS)
+
+
 def short(name):
     name = name.replace("void ", "").replace("af::<unnamed>::", "").replace("(anonymous namespace)::", "")
     return name.split("(")[0][:70]
@@ -93,18 +100,18 @@ def main():
         md += [f"## bench `{b}`", "", "```json", json.dumps(j, indent=1)[:6000], "```", ""]
     if a.launches:
         per, order = launches_table(a.launches)
-        tot = sum(sum(v) for k, v in per.items() if "norms_kernel" in k or "decide" in k or "cache_kernel" in k)
+        tot = sum(sum(v) for k, v in per.items() if is_ours(k))
         md += ["## launch list (ncu `gpu__time_duration.sum`, --clock-control none; cold-cache, serialised)", "",
                "| kernel | launches | mean µs | min µs | max µs | share of our kernels |", "|---|---|---|---|---|---|"]
         for k in order:
             v = per[k]
-            ours = "norms_kernel" in k or "decide" in k or "cache_kernel" in k
+            ours = is_ours(k)
             share = f"{sum(v) / tot:.3f}" if ours and tot else "—"
             md.append(f"| `{k}` | {len(v)} | {sum(v) / len(v):.2f} | {min(v):.2f} | {max(v):.2f} | {share} |")
         md.append("")
     if a.launches and a.tail_ours:
         seq = [x for x in launch_seq(a.launches)
-               if "norms_kernel" in x[0] or "decide" in x[0] or "cache_kernel" in x[0]][-a.tail_ours:]
+               if is_ours(x[0])][-a.tail_ours:]
         per = defaultdict(list)
         for k, v in seq:
             per[k].append(v)

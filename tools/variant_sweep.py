@@ -16,6 +16,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
     "fin_narrow": "-DAF_FIN_WIDE=0",
+    "end8k": "-DAF_TILE_ELEMS_F32=8192 -DAF_TILE_ELEMS_BF16=8192",
+    "end_f32_8k": "-DAF_TILE_ELEMS_F32=8192",
+    "end_f32_4k": "-DAF_TILE_ELEMS_F32=4096",
+    "end_f32_8k_bf16_32k": "-DAF_TILE_ELEMS_F32=8192 -DAF_TILE_ELEMS_BF16=32768",
+    "end4k_taper4": "-DAF_TILE_ELEMS_F32=4096 -DAF_TILE_ELEMS_BF16=4096 -DAF_TILE_BIG_MULT=4",
+    "end8k_taper2": "-DAF_TILE_ELEMS_F32=8192 -DAF_TILE_ELEMS_BF16=8192 -DAF_TILE_BIG_MULT=2",
+    "end4k_taper4_95": "-DAF_TILE_ELEMS_F32=4096 -DAF_TILE_ELEMS_BF16=4096 -DAF_TILE_BIG_MULT=4 -DAF_TILE_BIG_FRAC_PCT=95",
+    "end8k_taper4": "-DAF_TILE_ELEMS_F32=8192 -DAF_TILE_ELEMS_BF16=8192 -DAF_TILE_BIG_MULT=4",
+    "acc4k_taper": "-DAF_TILE_ACC_F32=4096 -DAF_TILE_ACC_BF16=4096",
     "timing": "-DAF_TIMING=1",
     "timing_fin_narrow": "-DAF_TIMING=1 -DAF_FIN_WIDE=0",
     "taper_off": "-DAF_TILE_BIG_MULT=1",
