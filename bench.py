@@ -412,7 +412,8 @@ def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(32, 256, 1024, 4
         for name, fn in (("put", lambda: cache.put(ids, src, 4)), ("get", lambda: cache.get(ids, 4, dst, dep))):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
             torch.cuda.synchronize()
-            for r in range(reps):
+            torch.cuda._sleep(5_000_000)     # ~2.5 ms: the host queues every rep before the GPU reaches
+            for r in range(reps):            # them, so the events time the device, not Python launch latency
                 ev[2 * r].record()
                 fn()
                 ev[2 * r + 1].record()

@@ -26,15 +26,17 @@ def main():
         c.put(ids, src, 4)
         res = {}
         for name, fn in (("put", lambda: c.put(ids, src, 4)), ("get", lambda: c.get(ids, 4, dst, dep))):
-            ts = []
-            for _ in range(20):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # queue every rep behind a ~2.5 ms sleep kernel: the events then time the
+            # device, not the host's launch latency (which dominates tiny batches)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+            torch.cuda.synchronize()
+            torch.cuda._sleep(5_000_000)
+            for a, b in ev:
                 a.record()
                 fn()
                 b.record()
-                b.synchronize()
-                ts.append(a.elapsed_time(b))
-            ms = statistics.median(ts)
+            torch.cuda.synchronize()
+            ms = statistics.median(a.elapsed_time(b) for a, b in ev)
             res[name] = round(2 * B * rb / (ms * 1e-3) / 1e9, 1)
         out[B] = res
     print(json.dumps(out), flush=True)

@@ -47,6 +47,41 @@ def main():
         with torch.cuda.stream(s):
             f.interval_end(g, stream=s)
     torch.cuda.synchronize()
+    # wide finalize (> 2048 interval-end tiles)
+    big = uniform_layout(2100 * 8192 + 77, 7, pre=4099, head=33)
+    fw = af.FreezingModule(big.offsets, big.kinds, grad_dtype="f32")
+    assert fw.info()["n_fin_ctas"] > 1
+    gb = torch.randn(big.n, device="cuda") * 1e-3
+    fw.layer_norms(gb)
+    fw.interval_end(gb)
+    fw.layer_norms(gb)
+    fw.interval_end(gb)
+    # fused reduce-scatter: P = 1 (plain and with AdamW), then P = 2 ranks in this process
+    r1 = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="bf16")
+    gr = (torch.randn(lay.n, device="cuda") * 1e-3).to(torch.bfloat16)
+    r1.set_grad_peers_local([gr])
+    out = torch.empty(lay.n, device="cuda")
+    r1.reduce_scatter_step(out)
+    r1.reduce_scatter_step(out, interval_end=True)
+    p1 = torch.zeros(lay.n, device="cuda")
+    m1, v1 = torch.zeros_like(p1), torch.zeros_like(p1)
+    r1.reduce_scatter_adamw_step(p1, m1, v1, lr=1e-3, step=1, out=out)
+    r1.reduce_scatter_adamw_step(p1, m1, v1, lr=1e-3, step=2, interval_end=True)
+    rs = [af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="f32", rank=r, world=2) for r in range(2)]
+    gg = [torch.randn(lay.n, device="cuda") * 1e-3 for _ in range(2)]
+    for f in rs:
+        f.set_peers_local(rs)
+        f.set_grad_peers_local(gg)
+        f.set_max_ctas(8)
+    outs = [torch.empty(lay.n, device="cuda") for _ in range(2)]
+    torch.cuda.synchronize()
+    for end in (False, True):
+        for f, s, o in zip(rs, ss, outs):
+            with torch.cuda.stream(s):
+                f.reduce_scatter_step(o, interval_end=end, stream=s)
+        torch.cuda.synchronize()
+    # sticky bits: 0 unless the tool serialised the two ranks' kernels (barrier timeouts)
+    print("reduce-scatter sticky", [int(f.scratch[8:12].view(torch.int32).item()) for f in rs], flush=True)
     # caches: direct and tiered
     for kw in ({}, {"hbm_rows": 30, "host_rows": 20}):
         c = af.ActivationCache(100, 4096 + 16, **kw)
