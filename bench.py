@@ -60,6 +60,9 @@ def parse():
                     help="N = 1: skip the short run of the other BERT workload reported under 'secondary'")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: per-layer partial exchange (in-kernel NVLink P2P, or NCCL all-gather)")
+    ap.add_argument("--zero", action="store_true",
+                    help="ZeRO form (NEXT 1): every rank holds its own full gradient; the step's accumulate and "
+                         "interval end are af_reduce_scatter_step (the gradient sync fused in, peer pulls)")
     ap.add_argument("--unfused", action="store_true",
                     help="interval end as af_layer_norms(END) + af_update_and_decide (two launches)")
     ap.add_argument("--sweep", action="store_true",
@@ -221,6 +224,19 @@ def run_ours(args, rank, world, local):
     info = fm.info()
     n_loc = info["shard_end"] - info["shard_begin"]
     grads = [device_grad(lay, dt, 1000 + k, dev) for k in range(2)]
+    rs_out = None
+    if args.zero:
+        # each rank's own gradient (seeded by rank), registered once; the step pulls
+        # this rank's shard of every rank's buffer and writes the reduced shard
+        if world > 1 and exchange != "p2p":
+            raise SystemExit("--zero needs the peer mappings (CUDA IPC) on every rank")
+        g_own = device_grad(lay, dt, 2000 + rank, dev)
+        grads = [g_own, g_own]
+        if world > 1:
+            fm.set_grad_peers_ipc(g_own)
+        else:
+            fm.set_grad_peers_local([g_own])
+        rs_out = torch.empty(n_loc, device=dev)
     # activation cache partition of this rank (id mod world)
     B = max(1, args.cache_batch // world)
     cache = af.ActivationCache(NUM_EXAMPLES, ROW_BYTES, rank=rank, world=world, device=dev)
@@ -242,10 +258,15 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()   # ranks enter the first exchange together (the in-kernel wait is bounded)
-    fm.layer_norms(grads[0])
-    fm.layer_norms(grads[1], interval_end=True)
-    fm.update_and_decide()
-    fm.layer_norms(grads[0])
+    if args.zero:
+        fm.reduce_scatter_step(rs_out)
+        fm.reduce_scatter_step(rs_out, interval_end=True)
+        fm.reduce_scatter_step(rs_out)
+    else:
+        fm.layer_norms(grads[0])
+        fm.layer_norms(grads[1], interval_end=True)
+        fm.update_and_decide()
+        fm.layer_norms(grads[0])
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     n_ev = 5
@@ -254,9 +275,14 @@ def run_ours(args, rank, world, local):
         g = grads[i & 1]
         ids = id_batches[i % len(id_batches)]
         if evs: evs[0].record(stream)
-        fm.layer_norms(g, dry_run=True)                               # a2
+        if args.zero:
+            fm.reduce_scatter_step(rs_out, dry_run=True)              # gradient sync + a2
+        else:
+            fm.layer_norms(g, dry_run=True)                           # a2
         if evs: evs[1].record(stream)
-        if args.unfused:
+        if args.zero:
+            fm.reduce_scatter_step(rs_out, interval_end=True, dry_run=True)   # sync + a3-a9
+        elif args.unfused:
             fm.layer_norms(grads[(i + 1) & 1], interval_end=True, dry_run=True)
             fm.update_and_decide(dry_run=True)
         else:
@@ -314,6 +340,9 @@ def run_ours(args, rank, world, local):
         ms = max_over_ranks(ms_local, dev)
     ms_per_step = ms / args.steps
     bytes_rank = algorithmic_bytes(n_loc, s_g, B, ROW_BYTES)
+    if args.zero:   # P gradient shards read (P-1 over NVLink) + the reduced shard written (fp32)
+        bytes_rank["accumulate"] = n_loc * (world * s_g + 8 + 4)
+        bytes_rank["grad_norm_decide"] = n_loc * (world * s_g + 4 + 4)
     step_bytes_all = sum(bytes_rank.values()) * world   # every rank moves ~the same bytes
     value = step_bytes_all / (ms_per_step * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
@@ -333,10 +362,11 @@ def run_ours(args, rank, world, local):
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": ("bf16" if dt == "bf16" else "f32") + "+f64",
         "data": "synthetic (seeded device RNG, BERT layer layout, DESIGN.md input recipe)",
-        "config": {"workload": f"{args.workload}" + ("-sharded" if world > 1 else ""),
+        "config": {"workload": f"{args.workload}" + ("-sharded" if world > 1 else "") + ("-zero" if args.zero else ""),
                    "n_elements": lay.n, "segments": lay.n_segments, "n_local": n_loc,
                    "cache": {"examples": NUM_EXAMPLES, "row_bytes": ROW_BYTES, "rows_per_rank_step": B},
-                   "boundary_f": 0, "parallelism": f"shard{world}", "exchange": exchange,
+                   "boundary_f": 0, "parallelism": (f"zero{world}" if args.zero else f"shard{world}"),
+                   "exchange": exchange,
                    "launch": "eager" if args.no_graph else "CUDA graph per step (8 graphs rotating id batches)",
                    "l2": "inputs larger than L2: each step streams >= 4 GB/rank through the 126 MB L2"},
         "grad_norm_decide_gbs": round(gn_dec, 1),
@@ -360,7 +390,7 @@ def run_ours(args, rank, world, local):
         result["next1_fused_adamw"] = adamw_probe(fm, lay, dt, s_g, n_loc, grads, dev)
         if world == 1:
             result["next1_fused_reduce_scatter_p1"] = rs_probe(lay, dt, s_g, grads, dev)
-    if not args.no_e2e:
+    if not args.no_e2e and not args.zero:
         result["e2e"] = run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(lay, dt, s_g, B, budget_s=12.0)
