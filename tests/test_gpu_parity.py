@@ -775,3 +775,36 @@ def test_maximum_segment_count_and_zero_gradients():
         assert gr["boundary_after"] == 0 and all(v == 0.0 for v in gr["norm"])
         assert not (gr["flags"] & O.FLAG_NONFINITE)
     assert f0 >= 0
+
+
+# ---------------------------------------------------------------- maximum sizes
+
+def test_more_than_2_31_elements_closed_form():
+    """A flat buffer of 2^31 + 4777 elements (int64 offsets; element indices past
+    2^31 in every kernel): per-segment constant dyadic gradients make every sum
+    exact, so the record's sums of squares must equal n_l * (2 c_l)^2 exactly and
+    Delta must read back c_l at the far end of the buffer."""
+    import paper_2102_01386_b200 as af
+    n_pre, n_a, n_b, n_head = 1000, 1 << 30, (1 << 30) + 777, 3000
+    offs = np.cumsum([0, n_pre, n_a, n_b, n_head]).tolist()
+    kinds = [O.SEG_PRE, O.SEG_POOL, O.SEG_POOL, O.SEG_HEAD]
+    n = offs[-1]
+    assert n > (1 << 31)
+    cs = [2.0 ** -10, 2.0 ** -9, 2.0 ** -8, 2.0 ** -11]
+    g = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    for l, c in enumerate(cs):
+        g[offs[l]:offs[l + 1]].fill_(c)
+    fm = af.FreezingModule(offs, kinds, grad_dtype="bf16")
+    fm.layer_norms(g)
+    torch.cuda.synchronize()
+    d = fm.accum.view(torch.float32)
+    for i in (0, n_pre - 1, n_pre, (1 << 31) - 1, 1 << 31, (1 << 31) + 1, n - n_head - 1, n - 1):
+        l = int(np.searchsorted(offs, i, side="right") - 1)
+        assert float(d[i].item()) == cs[l], i
+    fm.interval_end(g)
+    rec = fm.decision()
+    for l, c in enumerate(cs):
+        want = (offs[l + 1] - offs[l]) * (2 * c) ** 2       # exact in fp64
+        assert rec["sumsq"][l] == want, (l, rec["sumsq"][l], want)
+    del g, fm
+    torch.cuda.empty_cache()

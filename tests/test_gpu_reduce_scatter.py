@@ -189,3 +189,22 @@ def test_fused_reduce_scatter_adamw_parity(P, dt, seed):
                 assert np.all(g[:sb] == (init[:sb] if isinstance(init, np.ndarray) else init))
                 assert np.all(g[se:] == (init[se:] if isinstance(init, np.ndarray) else init))
     assert oz.f >= 1
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fused_reduce_scatter_randomized(seed):
+    """Random layouts (sub-vector segments, with/without PRE and HEAD), dtypes,
+    world sizes 1..8 (every PM instantiation, P < PM included), scales and
+    interval lengths: the reduced shards and Delta bit-exact, records as the
+    oracle's, identical on every rank."""
+    rng = np.random.default_rng(3000 + seed)
+    L = int(rng.choice([1, 2, 5, 33, 120]))
+    pre = int(rng.integers(0, 2)) * int(rng.integers(1, 20_000))
+    head = int(rng.integers(0, 2)) * int(rng.integers(1, 2_000))
+    n = pre + head + L * int(rng.integers(3, 2_500))
+    lay = uniform_layout(n, L, pre=pre, head=head)
+    dt = str(rng.choice(["f32", "bf16"]))
+    P = int(rng.integers(1, 9))
+    scale = float(rng.choice([1.0 / P, 0.375, 1.0]))
+    sched = [int(rng.integers(1, 4)) for _ in range(int(rng.integers(3, 6)))]
+    _run(lay, dt, P, sched, seed=4000 + seed, scale=scale)
