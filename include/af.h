@@ -144,6 +144,8 @@ typedef struct {
   int32_t tile_elems_acc;
   int32_t n_fin_ctas;               /* > 0: interval ends launch a second, wide finalize
                                        kernel of this many CTAs after the streaming kernel */
+  int32_t n_fin_chunks;             /* > 0: the interval end's partials are reduced in chunks
+                                       of 2048 tiles (wide finalize, in-kernel or launched) */
 } af_info;
 
 typedef struct af_ctx af_ctx;

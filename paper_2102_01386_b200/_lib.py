@@ -48,7 +48,7 @@ class AfInfo(ctypes.Structure):
                 ("n_tiles", c_int32), ("tile_elems", c_int32),
                 ("first_tile_of_pool", c_int32 * (AF_MAX_SEGMENTS + 1)),
                 ("n_tiles_acc", c_int32), ("tile_elems_acc", c_int32),
-                ("n_fin_ctas", c_int32)]
+                ("n_fin_ctas", c_int32), ("n_fin_chunks", c_int32)]
 
 
 class AfAdamW(ctypes.Structure):

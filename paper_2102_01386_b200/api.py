@@ -70,7 +70,7 @@ class FreezingModule:
         return dict(n_segments=i.n_segments, n_pool=i.n_pool, rank=i.rank, world=i.world,
                     n_total=i.n_total, shard_begin=i.shard_begin, shard_end=i.shard_end,
                     n_tiles=i.n_tiles, tile_elems=i.tile_elems, n_tiles_acc=i.n_tiles_acc,
-                    tile_elems_acc=i.tile_elems_acc, n_fin_ctas=i.n_fin_ctas,
+                    tile_elems_acc=i.tile_elems_acc, n_fin_ctas=i.n_fin_ctas, n_fin_chunks=i.n_fin_chunks,
                     first_tile_of_pool=list(i.first_tile_of_pool[:i.n_pool + 1]))
 
     def bind(self, device=None):

@@ -41,7 +41,7 @@ struct af_ctx {
   } ts[2];
   // workspace
   size_t accum_bytes = 0, scratch_bytes = 0;
-  size_t o_state = 0, o_sched = 0, o_pool = 0, o_part = 0, o_part2 = 0, o_ssall = 0,
+  size_t o_state = 0, o_sched = 0, o_pool = 0, o_part = 0, o_part2 = 0, o_chunk = 0, o_ssall = 0,
          o_ssacc = 0, o_last = 0, o_ring = 0, o_xrows = 0,
          o_xflags = 0, o_peer_rows = 0, o_peer_flags = 0, o_rsflags = 0, o_peer_rsflags = 0, o_rs_grads = 0;
   float *accum = nullptr;
@@ -192,6 +192,7 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   }
   c->o_part = take(c->ts[1].tiles.size() * sizeof(double));
   c->o_part2 = take((c->ts[1].tiles.size() / kFinChunk + L + 2) * sizeof(double));
+  c->o_chunk = take((c->ts[1].tiles.size() / kFinChunk + 2) * sizeof(unsigned int));
   c->scratch_bytes = o;
   *out = c;
   return AF_OK;
@@ -218,8 +219,9 @@ af_status af_ctx_info(const af_ctx *c, af_info *info) {
   info->tile_elems = c->ts[1].tile_elems;
   info->n_tiles_acc = static_cast<int32_t>(c->ts[0].tiles.size());
   info->tile_elems_acc = c->ts[0].tile_elems;
-  info->n_fin_ctas = af::fin_ctas(c->cfg.acc_mode == AF_ACC_DELTA ? kEndDelta : kStepSq,
-                                  static_cast<int>(c->ts[1].tiles.size()));
+  info->n_fin_chunks = af::fin_ctas(c->cfg.acc_mode == AF_ACC_DELTA ? kEndDelta : kStepSq,
+                                    static_cast<int>(c->ts[1].tiles.size()));
+  info->n_fin_ctas = AF_FIN_WIDE == 1 ? info->n_fin_chunks : 0;
   for (int j = 0; j <= c->n_pool; ++j) info->first_tile_of_pool[j] = c->ts[1].first_tile_of_f[j];
   return AF_OK;
 }
@@ -321,6 +323,7 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   p.partials = c->at<double>(c->o_part);
   p.part2 = c->at<double>(c->o_part2);
   p.fin_sched = c->at<Sched>(c->o_sched) + 2;
+  p.chunk_cnt = c->at<unsigned int>(c->o_chunk);
   p.ss_out = c->at<double>(c->o_ssall) + static_cast<size_t>(c->cfg.rank) * c->L;
   p.ss_acc = c->at<double>(c->o_ssacc);
   p.n_pool = c->n_pool;

@@ -60,8 +60,8 @@ struct DevState {
   double prev[AF_MAX_SEGMENTS];  // ||Delta_{T-1,l}||
 };
 
-#ifndef AF_FIN_WIDE  // 0: always finalize in the streaming kernel's last CTA
-#define AF_FIN_WIDE 1
+#ifndef AF_FIN_WIDE  // 0: the streaming kernel's last CTA sums all partials; 1: a second, wide
+#define AF_FIN_WIDE 1   // finalize launch; 2: chunks reduced inside the streaming kernel
 #endif
 constexpr int kFinChunk = 2048;  // partials per fin_kernel CTA (8 per thread)
 
@@ -115,9 +115,10 @@ struct NormParams {
   // wide finalize (n_tiles > kFinChunk): the streaming kernel only writes the
   // partials; fin_kernel's CTAs reduce chunks of kFinChunk partials into
   // part2[chunk + segment] and its last CTA combines them in chunk order
-  int32_t wide_fin;
+  int32_t wide_fin;                // 0: narrow; 1: fin_kernel launch; 2: chunks reduced in-kernel
   double *part2;                   // [n_tiles / kFinChunk + L + 2]
   Sched *fin_sched;                // done counter of fin_kernel
+  unsigned int *chunk_cnt;         // [n_tiles / kFinChunk + 1] finished tiles per chunk (in-kernel form)
   double *ss_out;                  // [L] this rank's row of the exchange matrix
   double *ss_acc;                  // [L] STEP_SUMSQ accumulator
   int32_t n_pool;

@@ -601,16 +601,24 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) 
   }
 }
 
+__device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int c, double *s_p);
+
 template <int MODE, typename GT, bool RD, int PM = 1>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAccum) ? 1 : AF_MINB_END)
     norms_kernel(const NormParams p) {
   constexpr bool RS = MODE == kRsAccum || MODE == kRsEnd || MODE == kRsAdamAccum || MODE == kRsAdamEnd;
+  constexpr bool PARTIALS = MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum && MODE != kRsAdamAccum;
+  // in-kernel wide finalize (AF_FIN_WIDE == 2): the CTA that completes a chunk of
+  // kFinChunk tiles reduces it (staging buffer below) between its own tiles
+  __shared__ double s_fin[(PARTIALS && AF_FIN_WIDE == 2) ? kFinChunk : 1];
+  __shared__ int s_chunk;
   __shared__ int s_tile[3];
   __shared__ Tile s_desc[3];
   __shared__ double s_red[kNormBlock / 32];
   __shared__ int s_last;
   __shared__ unsigned long long s_rs_epoch;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_chunk = -1;
   pdl_wait();  // f, Delta and the counters are written by the preceding kernels
   if (AF_TIMING && blockIdx.x == 0 && threadIdx.x == 0) const_cast<DevState *>(p.state)->tmark[0] = gtimer();
   int f = p.state->f;
@@ -669,7 +677,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
       s_tile[slot2] = next2;
       asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    if (MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum && MODE != kRsAdamAccum) {
+    if constexpr (PARTIALS) {
       const double w = warp_sum(v);
       if (lane == 0) s_red[warp] = w;
       __syncthreads();
@@ -678,9 +686,25 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
 #pragma unroll
         for (int k = 0; k < kNormBlock / 32; ++k) s += s_red[k];
         p.partials[tile] = s;
+        if (AF_FIN_WIDE == 2 && p.wide_fin == 2) {
+          // count the chunk's finished tiles; the CTA finishing its last one reduces it
+          __threadfence();
+          const int c = (tile - first_tile) / kFinChunk;
+          const int nc = min(kFinChunk, p.n_tiles - first_tile - c * kFinChunk);
+          s_chunk = (atomicAdd(p.chunk_cnt + c, 1u) == static_cast<unsigned>(nc - 1)) ? c : -1;
+        }
       }
     }
     __syncthreads();
+    if constexpr (PARTIALS && AF_FIN_WIDE == 2) {
+      if (p.wide_fin == 2) {
+        const int c = s_chunk;
+        if (c >= 0) {
+          chunk_reduce(p, first_tile, c, s_fin);
+          if (tid == 0) p.chunk_cnt[c] = 0u;  // every tile of the chunk has counted: reset for the next launch
+        }
+      }
+    }
   }
   pdl_launch_dependents();
 
@@ -705,55 +729,68 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
       if (tid == 0) const_cast<DevState *>(p.state)->rs_epoch = s_rs_epoch;
     }
   }
-  if (MODE == kAccum || MODE == kAdamAccum || MODE == kRsAccum || MODE == kRsAdamAccum) return;
-  if (p.wide_fin) {  // fin_kernel sums the partials
+  if constexpr (!PARTIALS) return;
+  constexpr int TM = (MODE == kAdamEnd || MODE == kRsEnd || MODE == kRsAdamEnd) ? kEndDelta : MODE;
+  if (p.wide_fin == 1) {  // fin_kernel sums the partials
     if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
     return;
   }
-  last_cta_tail<(MODE == kAdamEnd || MODE == kRsEnd || MODE == kRsAdamEnd) ? kEndDelta : MODE, false>(p, first_tile);
+  if (p.wide_fin == 2) {  // every chunk already reduced: combine the pieces
+    if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
+    last_cta_tail<TM, true>(p, first_tile);
+    return;
+  }
+  last_cta_tail<TM, false>(p, first_tile);
 }
 
-// Wide finalize of the interval-end kernels (n_tiles > kFinChunk): CTA c stages
-// the fp64 partials of tiles first_tile + [c*kFinChunk, (c+1)*kFinChunk) in
-// shared memory (8 coalesced loads per thread, one round trip), reduces each
-// segment's piece of them (one warp per segment, lane-strided, xor tree) into
-// part2[c + l] -- piece (c, l) is the (c + l)-th piece in tile order -- and the
-// grid's last CTA combines the pieces of each segment in chunk order, then
-// exchanges and decides as the streaming kernel's last CTA would.  Every sum has
-// a fixed order: the result is deterministic.
+// Chunk c of the wide finalize (n_tiles > kFinChunk): the fp64 partials of tiles
+// first_tile + [c*kFinChunk, (c+1)*kFinChunk) are staged in shared memory (8
+// coalesced loads per thread, one round trip); each segment's piece of them is
+// reduced by one warp (lane-strided, xor tree) into part2[c + l] -- piece (c, l)
+// is the (c + l)-th piece in tile order, so the index needs no search.  Every
+// thread of the CTA calls it.  Fixed order: deterministic.
+__device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int c, double *s_p) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c0 = first_tile + c * kFinChunk;
+  if (c0 >= p.n_tiles) return;  // uniform over the CTA
+  const int n = min(kFinChunk, p.n_tiles - c0);
+#pragma unroll
+  for (int u = 0; u < kFinChunk / kNormBlock; ++u) {
+    const int k = u * kNormBlock + tid;
+    if (k < n) s_p[k] = __ldcg(p.partials + c0 + k);
+  }
+  const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
+  __syncthreads();
+  for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {
+    int a = p.seg_tile_begin[l], b = p.seg_tile_begin[l + 1];
+    a = (a < c0 ? c0 : a) - c0;
+    b = (b > c0 + n ? c0 + n : b) - c0;
+    double s = 0.0;
+#pragma unroll 8
+    for (int k = a + lane; k < b; k += 32) s += s_p[k];
+    s = warp_sum(s);
+    if (lane == 0) {
+      p.part2[c + l] = s;
+      __threadfence();  // before the CTA reports completion (done counters)
+    }
+  }
+  __syncthreads();  // s_p is free again
+}
+
+// Wide finalize as a second launch (AF_FIN_WIDE == 1): CTA c reduces chunk c and
+// the grid's last CTA combines the pieces of each segment in chunk order, then
+// exchanges and decides as the streaming kernel's last CTA would.
 template <int MODE>
 __global__ void __launch_bounds__(kNormBlock) fin_kernel(const NormParams p) {
   __shared__ double s_p[kFinChunk];
   __shared__ int s_last;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   pdl_wait();  // the streaming kernel's partials
   int f = p.state->f;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int first_tile = p.first_tile_of_f[f];
-  const int c = blockIdx.x;
-  const int c0 = first_tile + c * kFinChunk;
-  if (c0 < p.n_tiles) {
-    const int n = min(kFinChunk, p.n_tiles - c0);
-#pragma unroll
-    for (int u = 0; u < kFinChunk / kNormBlock; ++u) {
-      const int k = u * kNormBlock + tid;
-      if (k < n) s_p[k] = __ldcg(p.partials + c0 + k);
-    }
-    const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
-    __syncthreads();
-    for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {
-      int a = p.seg_tile_begin[l], b = p.seg_tile_begin[l + 1];
-      a = (a < c0 ? c0 : a) - c0;
-      b = (b > c0 + n ? c0 + n : b) - c0;
-      double s = 0.0;
-#pragma unroll 8
-      for (int k = a + lane; k < b; k += 32) s += s_p[k];
-      s = warp_sum(s);
-      if (lane == 0) p.part2[c + l] = s;
-    }
-  }
+  chunk_reduce(p, first_tile, blockIdx.x, s_p);
   pdl_launch_dependents();
-  __syncthreads();
   if (tid == 0) {
     __threadfence();
     const unsigned int d = atomicAdd(&p.fin_sched->done, 1u);
@@ -1074,10 +1111,10 @@ int fin_ctas(int mode, int n_tiles) {
 int launch_norms(const NormParams &p_in, int mode, int grad_dtype, int grid, void *stream) {
   NormParams p = p_in;
   const int nfin = fin_ctas(mode, p.n_tiles);
-  p.wide_fin = nfin > 0;
+  p.wide_fin = nfin > 0 ? AF_FIN_WIDE : 0;
   const int e = grad_dtype == AF_DT_BF16 ? launch_dt<uint16_t>(p, mode, grid, stream)
                                          : launch_dt<float>(p, mode, grid, stream);
-  if (e != 0 || !nfin) return e;
+  if (e != 0 || !nfin || AF_FIN_WIDE != 1) return e;
   auto *fk = mode == kStepSq ? fin_kernel<kStepSq> : fin_kernel<kEndDelta>;
   return static_cast<int>(
       launch_pdl(fk, dim3(nfin), dim3(kNormBlock), 0, static_cast<cudaStream_t>(stream), p));

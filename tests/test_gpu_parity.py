@@ -319,7 +319,7 @@ def test_wide_finalize_parity(n, L, pre, head, dt, acc, fused):
     lay = uniform_layout(n, L, pre=pre, head=head)
     recs, _, fm, oz = run_both(lay, dt, _decaying_step(lay, dt, 41), [2, 1, 2, 1, 2, 1], check_delta=False,
                                fused=fused, acc_mode=acc)
-    assert fm.info()["n_fin_ctas"] > 1
+    assert fm.info()["n_fin_chunks"] > 1
     if L > 2:
         assert max(r[0]["boundary_after"] for r in recs) >= 1
 

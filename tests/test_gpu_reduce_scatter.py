@@ -114,7 +114,7 @@ def test_fused_reduce_scatter_wide_finalize_and_scale():
     # > kFinChunk interval-end tiles per rank (the second, wide finalize launch)
     lay = uniform_layout(2 * 36_000_003, 40, pre=1_000_001, head=3_333)
     recs, fms = _run(lay, "bf16", 2, [2, 1, 2], seed=7, scale=1.0)
-    assert fms[0].info()["n_fin_ctas"] > 1
+    assert fms[0].info()["n_fin_chunks"] > 1
 
 
 def test_fused_reduce_scatter_missing_peer_times_out():

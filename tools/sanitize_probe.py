@@ -50,7 +50,7 @@ def main():
     # wide finalize (> 2048 interval-end tiles)
     big = uniform_layout(2100 * 8192 + 77, 7, pre=4099, head=33)
     fw = af.FreezingModule(big.offsets, big.kinds, grad_dtype="f32")
-    assert fw.info()["n_fin_ctas"] > 1
+    assert fw.info()["n_fin_chunks"] > 1
     gb = torch.randn(big.n, device="cuda") * 1e-3
     fw.layer_norms(gb)
     fw.interval_end(gb)

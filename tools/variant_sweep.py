@@ -16,6 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
     "fin_narrow": "-DAF_FIN_WIDE=0",
+    "fin_inkernel": "-DAF_FIN_WIDE=2",
+    "timing_fin_inkernel": "-DAF_TIMING=1 -DAF_FIN_WIDE=2",
     "end8k": "-DAF_TILE_ELEMS_F32=8192 -DAF_TILE_ELEMS_BF16=8192",
     "end_f32_8k": "-DAF_TILE_ELEMS_F32=8192",
     "end_f32_4k": "-DAF_TILE_ELEMS_F32=4096",
