@@ -170,6 +170,24 @@ def test_unbound_calls_report_workspace():
     assert L.lib.af_update_and_decide(fm._h, 0, None, None) == L.AF_EWORKSPACE
 
 
+def test_reduce_scatter_host_checks():
+    # NEXT 1 (ZeRO form): argument / state errors are synchronous host checks
+    lay = uniform_layout(1 << 12, 4)
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="f32", rank=0, world=2, bind=False)
+    assert L.lib.af_reduce_scatter_step(None, 1.0, None, 0, None, None) == L.AF_EINVAL
+    assert L.lib.af_reduce_scatter_step(fm._h, 0.5, None, 0, None, None) == L.AF_EWORKSPACE
+    assert L.lib.af_ctx_set_grad_peers_local(fm._h, None) == L.AF_EINVAL
+    assert L.lib.af_ctx_grad_ipc_handle(fm._h, None, None) == L.AF_EINVAL
+    assert L.lib.af_ctx_set_max_ctas(fm._h, -1) == L.AF_EINVAL
+    assert L.lib.af_ctx_set_max_ctas(fm._h, 0) == L.AF_OK
+    hp = L.AfAdamW(1e-3, 0.9, 0.999, 1e-8, 0.0, 0)           # step 0: invalid
+    buf = (ctypes.c_float * 16)()
+    a = ctypes.addressof(buf) // 16 * 16 + 16
+    assert L.lib.af_reduce_scatter_adamw_step(fm._h, 1.0, a, a, a, ctypes.byref(hp), None, 0, None,
+                                              None) == L.AF_EINVAL
+    fm.close()
+
+
 def test_cache_create_validation_and_sizes():
     h = ctypes.c_void_p()
     assert L.lib.af_cache_create(100, 100, 0, 1, ctypes.byref(h)) == L.AF_EINVAL   # not a multiple of 16

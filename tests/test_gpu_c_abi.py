@@ -38,3 +38,14 @@ def test_training_loop_example_runs_and_freezes_monotonically():
     trace, hits = mod.run(epochs=3, small=True, verbose=False)
     assert trace == sorted(trace) and trace[-1] >= 1
     assert hits > 0
+
+
+def test_zero_example_runs_and_freezes_monotonically():
+    """examples/zero_loop.py at world 1 (the fused reduce-scatter + AdamW path):
+    the frozen prefix only grows and some layers freeze."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("zero", os.path.join(ROOT, "examples", "zero_loop.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    trace = mod.run(intervals=8, verbose=False)
+    assert trace == sorted(trace) and trace[-1] >= 1, trace
