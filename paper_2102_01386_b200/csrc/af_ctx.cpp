@@ -122,7 +122,8 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   // segment-aligned tile tables of the shard (tile edges on a global grid of tile_elems)
   const bool bf16 = (c->dtype == AF_DT_BF16);
   c->ts[0].tile_elems = bf16 ? AF_TILE_ACC_BF16 : AF_TILE_ACC_F32;
-  c->ts[1].tile_elems = bf16 ? AF_TILE_ELEMS_BF16 : AF_TILE_ELEMS_F32;
+  c->ts[1].tile_elems = (cfg->acc_mode == AF_ACC_STEP_SUMSQ) ? (bf16 ? AF_TILE_SSQ_BF16 : AF_TILE_SSQ_F32)
+                                                              : (bf16 ? AF_TILE_ELEMS_BF16 : AF_TILE_ELEMS_F32);
   // interval-end table: "tapered" tiles -- AF_TILE_BIG_MULT x larger in the first
   // AF_TILE_BIG_FRAC_PCT % of the shard (fewer fp64 partials for the last CTA to
   // sum), nominal size in the tail (balanced finish).  Fixed at create, so the

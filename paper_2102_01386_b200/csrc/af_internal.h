@@ -25,6 +25,12 @@ constexpr int kNormBlock = 256;          // threads per CTA of the streaming ker
 #ifndef AF_TILE_BIG_FRAC_PCT
 #define AF_TILE_BIG_FRAC_PCT 85
 #endif
+#ifndef AF_TILE_SSQ_F32  // STEP_SUMSQ reads only g (s_g bytes per element): larger tiles in
+#define AF_TILE_SSQ_F32 32768  // elements keep the per-tile fixed costs small
+#endif                          // (profiles/r01_v26_variants_stepsq.jsonl)
+#ifndef AF_TILE_SSQ_BF16
+#define AF_TILE_SSQ_BF16 32768
+#endif
 #ifndef AF_TILE_ACC_F32  // the accumulate kernel keeps no partials: finer tiles balance better
 #define AF_TILE_ACC_F32 8192
 #endif

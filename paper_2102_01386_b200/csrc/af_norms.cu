@@ -45,6 +45,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef AF_U_ACC
 #define AF_U_ACC 8
 #endif
+#ifndef AF_U_SSQ_F32  // STEP_SUMSQ (profiles/r01_v26_variants_stepsq.jsonl)
+#define AF_U_SSQ_F32 4
+#endif
+#ifndef AF_U_SSQ_BF16
+#define AF_U_SSQ_BF16 8
+#endif
 #ifndef AF_G_HINT  // 0: ld.global.cs   1: ld.global.nc.L1::no_allocate.L2::256B
 #define AF_G_HINT 1
 #endif
@@ -140,7 +146,8 @@ __device__ __forceinline__ void elem(const NormParams &p, const GT *g, float *d,
 template <int MODE, typename GT, bool RD>
 __device__ __forceinline__ double process_tile(const NormParams &p, const Tile &t) {
   constexpr int VE = VT<GT>::VE;
-  constexpr int U = (MODE == kAccum) ? AF_U_ACC : AF_U_END;  // vectors in flight per thread
+  constexpr int U_SSQ = sizeof(GT) == 2 ? AF_U_SSQ_BF16 : AF_U_SSQ_F32;
+  constexpr int U = (MODE == kAccum) ? AF_U_ACC : (MODE == kStepSq ? U_SSQ : AF_U_END);  // vectors in flight
   constexpr int DH = (MODE == kAccum) ? 0 : AF_D_HINT_END;     // Delta is rewritten by kAccum
   const GT *__restrict__ g = static_cast<const GT *>(p.grad);
   // Delta is indexed by global element i at d[i]; the shard base offset is applied

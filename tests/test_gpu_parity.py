@@ -308,7 +308,7 @@ def test_fake_sharded_parity(P):
 
 @pytest.mark.parametrize("n,L,pre,head,dt,acc,fused", [
     (40_000_003, 150, 1_000_001, 3_333, "f32", "delta", True),    # chunks span ~120 segments
-    (40_000_003, 150, 1_000_001, 3_333, "bf16", "step_sumsq", False),
+    (80_000_003, 150, 1_000_001, 3_333, "bf16", "step_sumsq", False),   # STEP_SUMSQ tiles are 32768
     (36_000_001, 2, 17, 5, "f32", "delta", False),                # segments span many chunks
 ])
 def test_wide_finalize_parity(n, L, pre, head, dt, acc, fused):

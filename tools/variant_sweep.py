@@ -17,6 +17,9 @@ VARIANTS = {
     "default": "",
     "fin_narrow": "-DAF_FIN_WIDE=0",
     "fin_inkernel": "-DAF_FIN_WIDE=2",
+    "ssq_old": "-DAF_TILE_SSQ_F32=8192 -DAF_TILE_SSQ_BF16=16384 -DAF_U_SSQ_F32=4 -DAF_U_SSQ_BF16=4",
+    "ssq_64k_bf16": "-DAF_TILE_SSQ_BF16=65536",
+    "ssq_f32_16k": "-DAF_TILE_SSQ_F32=16384",
     "timing_fin_inkernel": "-DAF_TIMING=1 -DAF_FIN_WIDE=2",
     "end8k": "-DAF_TILE_ELEMS_F32=8192 -DAF_TILE_ELEMS_BF16=8192",
     "end_f32_8k": "-DAF_TILE_ELEMS_F32=8192",
