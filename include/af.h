@@ -192,7 +192,8 @@ AF_API af_status af_ctx_exchange_rows(af_ctx *ctx, double **ss_all_dev);
  * every peer's memory over NVLink (P2P stores), publishes its epoch in every
  * peer's flag slot (st.release.sys) and waits for all ranks' epochs
  * (ld.acquire.sys, bounded spin: a missing peer sets AF_DEC_EXCHANGE_TIMEOUT
- * instead of hanging) -- af_interval_end is ONE kernel at any world size.
+ * instead of hanging) -- af_interval_end needs no collective launch at any
+ * world size (the streaming kernel, plus the wide finalize when n_fin_ctas > 0).
  * _ipc: synchronous, collective; `handles` = world x AF_IPC_HANDLE_BYTES in rank
  * order, each from af_ctx_exchange_ipc_handle on that rank (exchanged by the
  * caller, e.g. torch.distributed.all_gather_object).  _local: every rank's ctx
