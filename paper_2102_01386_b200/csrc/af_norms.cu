@@ -57,6 +57,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef AF_D_HINT_END
 #define AF_D_HINT_END 0
 #endif
+#ifndef AF_D_HINT_ACC  // Delta loads of the accumulate: 0 ld.global.cs, 1 ld.global.nc.L1::no_allocate.L2::256B
+#define AF_D_HINT_ACC 0
+#endif
+#ifndef AF_D_STORE  // Delta stores: 0 st.global.cs, 1 st.global (write-back), 2 .L2::cache_hint evict_first
+#define AF_D_STORE 1   // write-back: -0.8 % BERT-large step (profiles/r01_v28_variants_stores.jsonl)
+#endif
+#ifndef AF_P_STORE  // AdamW p / m / v stores (same encoding)
+#define AF_P_STORE 0
+#endif
+#ifndef AF_D_STORE_ADAM  // Delta stores of the AdamW-fused kernels: streaming like p / m / v
+#define AF_D_STORE_ADAM 0  // (write-back there: -4 % fp32, -14 % bf16, profiles/r01_v29_*)
+#endif
 #ifndef AF_MINB_END
 #define AF_MINB_END 1
 #endif
@@ -82,6 +94,21 @@ __device__ __forceinline__ float4 ld_stream(const float4 *p) {
   if (HINT == 0) return __ldcs(p);
   const uint4 u = ld_stream<HINT>(reinterpret_cast<const uint4 *>(p));
   return make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w));
+}
+
+template <int HINT>
+__device__ __forceinline__ void st_delta(float4 *p, float4 v) {
+  if (HINT == 0) {
+    __stcs(p, v);
+  } else if (HINT == 1) {
+    *p = v;
+  } else {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w), "l"(pol)
+                 : "memory");
+  }
 }
 
 template <typename GT>
@@ -148,7 +175,9 @@ __device__ __forceinline__ double process_tile(const NormParams &p, const Tile &
   constexpr int VE = VT<GT>::VE;
   constexpr int U_SSQ = sizeof(GT) == 2 ? AF_U_SSQ_BF16 : AF_U_SSQ_F32;
   constexpr int U = (MODE == kAccum) ? AF_U_ACC : (MODE == kStepSq ? U_SSQ : AF_U_END);  // vectors in flight
-  constexpr int DH = (MODE == kAccum) ? 0 : AF_D_HINT_END;     // Delta is rewritten by kAccum
+  // Delta is rewritten by kAccum, but each element is read once, before its own
+  // write, by the same thread: the non-coherent path is safe there too
+  constexpr int DH = (MODE == kAccum) ? AF_D_HINT_ACC : AF_D_HINT_END;
   const GT *__restrict__ g = static_cast<const GT *>(p.grad);
   // Delta is indexed by global element i at d[i]; the shard base offset is applied
   // through the pointer (shard_begin is a multiple of 8, keeping 16 B alignment).
@@ -211,7 +240,7 @@ __device__ __forceinline__ double process_tile(const NormParams &p, const Tile &
         if (MODE == kAccum) {
 #pragma unroll
           for (int q = 0; q < DV; ++q)
-            __stcs(db + c * DV + q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
+            st_delta<AF_D_STORE>(db + c * DV + q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
         } else {
 #pragma unroll
           for (int k = 0; k < VE; k += 4) {
@@ -308,15 +337,15 @@ __device__ __forceinline__ double process_tile_adam(const NormParams &p, const T
         a2 = sq_acc(dq[2], a2);
         a3 = sq_acc(dq[3], a3);
       } else {
-        __stcs(db + c * DV + q, make_float4(dq[0], dq[1], dq[2], dq[3]));
+        st_delta<AF_D_STORE_ADAM>(db + c * DV + q, make_float4(dq[0], dq[1], dq[2], dq[3]));
       }
       adamw_elem(p.adam, gq[0], pv[q].x, mv[q].x, v2[q].x);
       adamw_elem(p.adam, gq[1], pv[q].y, mv[q].y, v2[q].y);
       adamw_elem(p.adam, gq[2], pv[q].z, mv[q].z, v2[q].z);
       adamw_elem(p.adam, gq[3], pv[q].w, mv[q].w, v2[q].w);
-      __stcs(pb + c * DV + q, pv[q]);
-      __stcs(mb + c * DV + q, mv[q]);
-      __stcs(vb4 + c * DV + q, v2[q]);
+      st_delta<AF_P_STORE>(pb + c * DV + q, pv[q]);
+      st_delta<AF_P_STORE>(mb + c * DV + q, mv[q]);
+      st_delta<AF_P_STORE>(vb4 + c * DV + q, v2[q]);
     }
   }
   return (a0 + a1) + (a2 + a3);
@@ -427,9 +456,9 @@ __device__ __forceinline__ double process_tile_rs(const NormParams &p, const Til
             adamw_elem(p.adam, x[4 * q + 1], pa[u][q].y, ma[u][q].y, va[u][q].y);
             adamw_elem(p.adam, x[4 * q + 2], pa[u][q].z, ma[u][q].z, va[u][q].z);
             adamw_elem(p.adam, x[4 * q + 3], pa[u][q].w, ma[u][q].w, va[u][q].w);
-            __stcs(reinterpret_cast<float4 *>(pw + vb) + c * DV + q, pa[u][q]);
-            __stcs(reinterpret_cast<float4 *>(mm + vb) + c * DV + q, ma[u][q]);
-            __stcs(reinterpret_cast<float4 *>(vv + vb) + c * DV + q, va[u][q]);
+            st_delta<AF_P_STORE>(reinterpret_cast<float4 *>(pw + vb) + c * DV + q, pa[u][q]);
+            st_delta<AF_P_STORE>(reinterpret_cast<float4 *>(mm + vb) + c * DV + q, ma[u][q]);
+            st_delta<AF_P_STORE>(reinterpret_cast<float4 *>(vv + vb) + c * DV + q, va[u][q]);
           }
         }
         if (RD) {
@@ -444,7 +473,8 @@ __device__ __forceinline__ double process_tile_rs(const NormParams &p, const Til
         if (!END) {
 #pragma unroll
           for (int q = 0; q < DV; ++q)
-            __stcs(db + c * DV + q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
+            st_delta<ADAM ? AF_D_STORE_ADAM : AF_D_STORE>(db + c * DV + q,
+                                                          make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
         } else {
 #pragma unroll
           for (int k = 0; k < VE; k += 4) {

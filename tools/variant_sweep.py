@@ -17,6 +17,14 @@ VARIANTS = {
     "default": "",
     "fin_narrow": "-DAF_FIN_WIDE=0",
     "fin_inkernel": "-DAF_FIN_WIDE=2",
+    "acc_dnc": "-DAF_D_HINT_ACC=1",
+    "st_cs": "-DAF_D_STORE=0",
+    "p_st_wb": "-DAF_P_STORE=1",
+    "acc_st_wb": "-DAF_D_STORE=1",
+    "acc_st_ef": "-DAF_D_STORE=2",
+    "acc_dnc_st_ef": "-DAF_D_HINT_ACC=1 -DAF_D_STORE=2",
+    "acc_u4": "-DAF_U_ACC=4",
+    "acc_16k": "-DAF_TILE_ACC_F32=16384 -DAF_TILE_ACC_BF16=16384",
     "ssq_old": "-DAF_TILE_SSQ_F32=8192 -DAF_TILE_SSQ_BF16=16384 -DAF_U_SSQ_F32=4 -DAF_U_SSQ_BF16=4",
     "ssq_64k_bf16": "-DAF_TILE_SSQ_BF16=65536",
     "ssq_f32_16k": "-DAF_TILE_SSQ_F32=16384",
@@ -106,6 +114,8 @@ def main():
                               "ms_per_step": d["ms_per_step"],
                               "accumulate_gbs": ph["accumulate"]["gbs"], "grad_norm_gbs": ph["grad_norm_decide"]["gbs"],
                               "accumulate_ms": ph["accumulate"]["ms"], "grad_norm_ms": ph["grad_norm_decide"]["ms"],
+                              "adamw_gbs": (d.get("next1_fused_adamw") or {}).get("gbs"),
+                              "rs_p1_gbs": (d.get("next1_fused_reduce_scatter_p1") or {}).get("gbs"),
                               "clocks": d.get("clocks")}), flush=True)
     subprocess.run([sys.executable, os.path.join(ROOT, "paper_2102_01386_b200", "_build.py"), "--force"], cwd=ROOT, check=True)
 
