@@ -49,6 +49,7 @@ struct af_ctx {
   bool bound = false;
   int grid[kNumModes] = {};  // persistent grid per streaming-kernel mode (occupancy x SMs)
   int max_ctas = 0;          // af_ctx_set_max_ctas: cap on the streaming grids (0: none)
+  bool reverse = false;      // tile order of the next streaming launch (alternates)
   // host flags
   bool armed = false;    // Delta / ss_acc hold this interval's partial sum
   bool pending = false;  // an interval end awaits af_update_and_decide
@@ -328,6 +329,8 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   p.ss_out = c->at<double>(c->o_ssall) + static_cast<size_t>(c->cfg.rank) * c->L;
   p.ss_acc = c->at<double>(c->o_ssacc);
   p.n_pool = c->n_pool;
+  p.reverse = (AF_ALTERNATE_ORDER && c->reverse) ? 1 : 0;
+  c->reverse = !c->reverse;
   p.first = c->armed ? 0 : 1;
   p.end = end ? 1 : 0;
   p.commit = dry ? 0 : 1;

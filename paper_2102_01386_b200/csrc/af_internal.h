@@ -69,6 +69,9 @@ struct DevState {
 #ifndef AF_FIN_WIDE  // 0: the streaming kernel's last CTA sums all partials; 1: a second, wide
 #define AF_FIN_WIDE 1   // finalize launch; 2: chunks reduced inside the streaming kernel
 #endif
+#ifndef AF_ALTERNATE_ORDER  // alternate the streaming kernels' tile order per launch (L2 reuse)
+#define AF_ALTERNATE_ORDER 1
+#endif
 constexpr int kFinChunk = 2048;  // partials per fin_kernel CTA (8 per thread)
 
 enum Mode : int {
@@ -132,6 +135,7 @@ struct NormParams {
   int32_t end;                     // interval end (STEP_SUMSQ: publish ss_acc)
   int32_t commit;                  // STEP_SUMSQ: store ss_acc
   int32_t fuse_decide;             // fused interval end: the last CTA decides
+  int32_t reverse;                 // process the active tiles last to first (alternates per launch)
   // kAdamAccum / kAdamEnd: AdamW update of the same elements (full flat fp32 buffers)
   float *params, *exp_avg, *exp_avg_sq;
   AdamConst adam;

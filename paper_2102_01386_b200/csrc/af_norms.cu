@@ -641,7 +641,7 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) 
 __device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int c, double *s_p);
 
 template <int MODE, typename GT, bool RD, int PM = 1>
-__global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAccum) ? 1 : AF_MINB_END)
+__global__ void __launch_bounds__(kNormBlock, MODE == kAccum ? 2 : ((MODE >= kAdamAccum) ? 1 : AF_MINB_END))
     norms_kernel(const NormParams p) {
   constexpr bool RS = MODE == kRsAccum || MODE == kRsEnd || MODE == kRsAdamAccum || MODE == kRsAdamEnd;
   constexpr bool PARTIALS = MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum && MODE != kRsAdamAccum;
@@ -676,11 +676,22 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
   // has the atomic for tile it+2 (one register) and an async copy (cp.async) of
   // tile it+1's descriptor into shared memory in flight; both land before the
   // end-of-tile barrier, so no warp waits on them and no registers hold them.
+  // Tile order alternates between launches (p.reverse, toggled by the host): each
+  // kernel starts where the previous one ended, so its first tiles find the
+  // previous kernel's last ~100 MB (Delta written back, g just read) in the
+  // 126 MB L2.  The order never changes a result: every tile's partial has a fixed
+  // reduction tree and the segments are summed in tile-index order.
+  const int n_act_tiles = p.n_tiles - first_tile;
+  auto tile_of = [&](unsigned int k) -> int {
+    const int kk = static_cast<int>(k);
+    if (kk >= n_act_tiles) return p.n_tiles;  // past the end: the loop's stop value
+    return p.reverse ? p.n_tiles - 1 - kk : first_tile + kk;
+  };
   if (tid == 0) {
-    const int t0 = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+    const int t0 = tile_of(atomicAdd(&p.sched->next, 1u));
     s_tile[0] = t0;
     if (t0 < p.n_tiles) s_desc[0] = p.tiles[t0];
-    s_tile[1] = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+    s_tile[1] = tile_of(atomicAdd(&p.sched->next, 1u));
   }
   __syncthreads();
   for (int it = 0;; ++it) {
@@ -690,7 +701,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE >= kAdamAc
     const Tile t = s_desc[slot];
     int next2 = 0;
     if (tid == 0) {
-      next2 = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
+      next2 = tile_of(atomicAdd(&p.sched->next, 1u));
       const int n1 = s_tile[slot1];
       if (n1 < p.n_tiles) {
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_desc[slot1]));

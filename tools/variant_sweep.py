@@ -19,6 +19,7 @@ VARIANTS = {
     "fin_inkernel": "-DAF_FIN_WIDE=2",
     "acc_dnc": "-DAF_D_HINT_ACC=1",
     "st_cs": "-DAF_D_STORE=0",
+    "fwd_only": "-DAF_ALTERNATE_ORDER=0",
     "p_st_wb": "-DAF_P_STORE=1",
     "acc_st_wb": "-DAF_D_STORE=1",
     "acc_st_ef": "-DAF_D_STORE=2",
