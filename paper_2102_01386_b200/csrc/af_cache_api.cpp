@@ -390,7 +390,7 @@ af_status af_cache_get_global(af_cache *c, const int64_t *ids_dev, int32_t n, in
 
 af_status af_cache_destroy(af_cache *c) {
   if (!c) return fail(AF_EINVAL, "NULL cache");
-  for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  ipc_release(c->ipc_opened);
   delete c;
   return AF_OK;
 }

@@ -851,7 +851,7 @@ af_status af_set_state(af_ctx *c, const void *buf, size_t len) {
 af_status af_ctx_destroy(af_ctx *c) {
   if (!c) return fail(AF_EINVAL, "NULL ctx");
   if (c->comm) ncclCommDestroy(c->comm);
-  for (void *p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  ipc_release(c->ipc_opened);
   delete c;
   return AF_OK;
 }

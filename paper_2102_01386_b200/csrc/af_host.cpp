@@ -2,6 +2,9 @@
 #include "af_host.h"
 
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
 
 namespace af {
 namespace {
@@ -43,12 +46,44 @@ af_status ipc_export(const void *ptr, IpcRef *out) {
   return AF_OK;
 }
 
+// A process may map a given peer allocation only once, but several objects can
+// need it (a context's scratch and gradient, a cache's payload and meta, when
+// the peer's allocator placed them in one segment): mappings are shared through
+// a process-wide table keyed by the handle bytes and reference-counted.
+namespace {
+std::mutex g_ipc_mu;
+std::map<std::string, std::pair<void *, int>> g_ipc_maps;  // handle bytes -> (base, refs)
+}  // namespace
+
 af_status ipc_import(const IpcRef &r, std::vector<void *> &opened, char **out) {
+  const std::string key(reinterpret_cast<const char *>(&r.h), sizeof(r.h));
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  auto it = g_ipc_maps.find(key);
   void *p = nullptr;
-  AF_CUDA(cudaIpcOpenMemHandle(&p, r.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  if (it != g_ipc_maps.end()) {
+    p = it->second.first;
+    ++it->second.second;
+  } else {
+    AF_CUDA(cudaIpcOpenMemHandle(&p, r.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    g_ipc_maps.emplace(key, std::make_pair(p, 1));
+  }
   opened.push_back(p);
   *out = static_cast<char *>(p) + r.offset;
   return AF_OK;
+}
+
+void ipc_release(const std::vector<void *> &opened) {
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (void *p : opened) {
+    for (auto it = g_ipc_maps.begin(); it != g_ipc_maps.end(); ++it) {
+      if (it->second.first != p) continue;
+      if (--it->second.second == 0) {
+        cudaIpcCloseMemHandle(p);
+        g_ipc_maps.erase(it);
+      }
+      break;
+    }
+  }
 }
 
 }  // namespace af

@@ -34,5 +34,6 @@ struct IpcRef {
 };
 af_status ipc_export(const void *ptr, IpcRef *out);
 af_status ipc_import(const IpcRef &r, std::vector<void *> &opened, char **out);
+void ipc_release(const std::vector<void *> &opened);  // drop the references ipc_import took
 
 }  // namespace af

@@ -100,6 +100,7 @@ def _rs_worker(rank, world, port, q):
         assert fm.set_peers_ipc()
         grad = torch.zeros(lay.n, dtype=torch.bfloat16, device="cuda")
         fm.set_grad_peers_ipc(grad)
+        fm.set_grad_peers_ipc(grad)    # re-registration maps each peer allocation once (shared mapping)
         fm.set_max_ctas(32)
         info = fm.info()
         sb, se = info["shard_begin"], info["shard_end"]
