@@ -271,16 +271,20 @@ def run_ours(args, rank, world, local):
     stream = torch.cuda.current_stream()
     n_ev = 5
 
-    def step(i, evs=None):
+    def step(i, evs=None, skip=()):
         g = grads[i & 1]
         ids = id_batches[i % len(id_batches)]
         if evs: evs[0].record(stream)
-        if args.zero:
+        if "accumulate" in skip:
+            pass
+        elif args.zero:
             fm.reduce_scatter_step(rs_out, dry_run=True)              # gradient sync + a2
         else:
             fm.layer_norms(g, dry_run=True)                           # a2
         if evs: evs[1].record(stream)
-        if args.zero:
+        if "grad_norm_decide" in skip:
+            pass
+        elif args.zero:
             fm.reduce_scatter_step(rs_out, interval_end=True, dry_run=True)   # sync + a3-a9
         elif args.unfused:
             fm.layer_norms(grads[(i + 1) & 1], interval_end=True, dry_run=True)
@@ -288,6 +292,8 @@ def run_ours(args, rank, world, local):
         else:
             fm.interval_end(grads[(i + 1) & 1], dry_run=True)         # a3-a9 (fused at N=1)
         if evs: evs[2].record(stream)
+        if "cache" in skip:
+            return
         cache.get(ids, 4, out_rows, depth_out)                        # a11
         if evs: evs[3].record(stream)
         cache.put(ids, rows, 4)                                       # a10
@@ -327,6 +333,8 @@ def run_ours(args, rank, world, local):
         if world > 1:
             dist.barrier()
     ms_local = t0.elapsed_time(t1)
+    marg = step_marginals(args, graphs, step, stream, world, dist) if graphs else None
+    cache_marg = marg["cache"] if marg else None
     # per-phase breakdown: a second, eagerly launched pass with CUDA events between calls
     n_ph = max(1, min(args.steps, 100))
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(n_ph)]
@@ -357,6 +365,14 @@ def run_ours(args, rank, world, local):
     gn_dec = bytes_rank["grad_norm_decide"] / (gn_dec_ms * 1e-3) / 1e9
     cache_gbs = (bytes_rank["cache_get"] + bytes_rank["cache_put"]) / (
         (ph_ms["cache_get"] + ph_ms["cache_put"]) * 1e-3) / 1e9
+    if cache_marg is not None:   # in-step device time of get + put (step_marginals)
+        cache_marg_gbs = (bytes_rank["cache_get"] + bytes_rank["cache_put"]) / (cache_marg * 1e-3) / 1e9
+        cache_in_step = {"us": round(cache_marg * 1e3, 2), "gbs": round(cache_marg_gbs, 1),
+                         "frac_of_peak": round(cache_marg_gbs / peak, 4),
+                         "method": "marginal: graph-replayed steps minus the same steps without the cache calls "
+                                   "(no events between kernels); phases.cache_* are eager event pairs, which add "
+                                   "a ~6 us floor per call"}
+        cache_gbs = cache_marg_gbs
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
@@ -372,6 +388,15 @@ def run_ours(args, rank, world, local):
         "grad_norm_decide_gbs": round(gn_dec, 1),
         "grad_norm_decide_frac_of_hbm_peak": round(gn_dec / peak, 4),
         "cache_gbs": round(cache_gbs, 1),
+        **({"cache_in_step": cache_in_step} if cache_marg is not None else {}),
+        **({"phases_in_step": {
+            "method": "marginal device time: the step's CUDA graphs replayed with and without the phase, K steps "
+                      "each, alternating, difference of medians (max over ranks); includes what the phase adds "
+                      "through overlap (PDL) and L2 state",
+            **{k: {"ms": round(v, 5),
+                   **({"gbs": round(phase_bytes(bytes_rank, k) / (v * 1e-3) / 1e9, 1),
+                       "frac_of_peak": round(phase_bytes(bytes_rank, k) / (v * 1e-3) / 1e9 / peak, 4)} if v > 0 else {})}
+               for k, v in marg.items() if k != "full"}}} if marg else {}),
         "phases": phase_report,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(ach / peak, 4), "peak_source": peak_src,
@@ -403,6 +428,51 @@ def run_ours(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def phase_bytes(bytes_rank, phase):
+    return bytes_rank["cache_get"] + bytes_rank["cache_put"] if phase == "cache" else bytes_rank[phase]
+
+
+def step_marginals(args, graphs, step, stream, world, dist, rounds=3):
+    """In-step device time (ms) of each phase: the step's graphs replayed with and
+    without the phase (accumulate / interval end / cache get + put), alternating,
+    K steps each; a phase's cost is the difference of the medians (max over
+    ranks).  Dry-run calls commit nothing, so dropping one leaves the others' work
+    unchanged."""
+    import torch
+    sets = {"full": graphs}
+    for ph in ("accumulate", "grad_norm_decide", "cache"):
+        gl = []
+        for i in range(len(graphs)):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                step(i, skip=(ph,))
+            gl.append(gph)
+        sets[ph] = gl
+    torch.cuda.synchronize()
+    t = {k: [] for k in sets}
+    for _ in range(rounds):
+        for k, gl in sets.items():
+            for i in range(args.warmup):
+                gl[i % len(gl)].replay()
+            if world > 1:
+                dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(stream)
+            for i in range(args.steps):
+                gl[i % len(gl)].replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            t[k].append(a.elapsed_time(b) / args.steps)
+    full = statistics.median(t["full"])
+    out = {"full": full}
+    dev = torch.device("cuda", torch.cuda.current_device())
+    for k in ("accumulate", "grad_norm_decide", "cache"):
+        d = full - statistics.median(t[k])
+        out[k] = max_over_ranks(d, dev) if world > 1 else d
+    return out
+
+
 def secondary_workload(args):
     """N = 1: the other BASELINE config (bert-base-bf16, configs[1], when the main
     line is bert-large-f32) timed the same way, in a subprocess, summarised."""
@@ -416,42 +486,62 @@ def secondary_workload(args):
     except Exception:  # noqa: BLE001
         return {"workload": other, "error": r.stderr[-500:]}
     keep = ("value", "unit", "ms_per_step", "grad_norm_decide_gbs", "grad_norm_decide_frac_of_hbm_peak", "dtype",
-            "config", "phases", "roofline", "clocks")
+            "config", "phases", "phases_in_step", "cache_gbs", "cache_in_step", "roofline", "clocks")
     return {"workload": other, **{k: d[k] for k in keep if k in d}}
 
 
-def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(32, 256, 1024, 4096), reps=20):
+def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(6, 32, 256, 1024, 4096), reps=20, iters=5):
     """Cache get / put GB/s (2 x rows x row_bytes per call) per batch size on this
-    rank's partition (all hits, no eviction: boundary == depth)."""
+    rank's partition (all hits, no eviction: boundary == depth), with a COLD L2 as
+    inside the step: each call gets fresh ids and follows a 512 MB read.  A call's
+    cost is marginal device time: a CUDA graph of reps x [flush, call] minus one of
+    reps x [flush], divided by reps -- launches back to back, no event between calls
+    (an event pair around one call adds a ~6 us floor; tools/cache_cold_probe.py)."""
     import torch
-    out = {}
+    out = {"l2": "cold (512 MB read before each call, fresh ids per call)",
+           "timing": "marginal device time per call in CUDA graphs (graph with calls minus graph without)"}
     B0 = rows.shape[0]
     big = rows.repeat((max(batches) + B0 - 1) // B0, 1)[: max(batches)].contiguous()
+    flush = torch.ones(256 << 20, dtype=torch.float16, device=dev)
+    acc = torch.zeros((), dtype=torch.float32, device=dev)
     peak, _ = measured_peaks()
+
+    def marginal_us(fn):
+        gs = {}
+        for w in (True, False):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for r in range(reps):
+                    torch.sum(flush, dim=0, dtype=torch.float32, out=acc)
+                    if w:
+                        fn(r)
+            gs[w] = g
+        t = {True: [], False: []}
+        for _ in range(iters):
+            for w in (True, False):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                gs[w].replay()
+                b.record()
+                torch.cuda.synchronize()
+                t[w].append(a.elapsed_time(b))
+        return (statistics.median(t[True]) - statistics.median(t[False])) / reps * 1e3
+
     for B in batches:
         if B > my_ids.numel():
             continue
-        ids = my_ids[torch.randperm(my_ids.numel(), device=dev)[:B]].contiguous()
+        id_sets = [my_ids[torch.randperm(my_ids.numel(), device=dev)[:B]].contiguous() for _ in range(reps)]
         src = big[:B]
         dst = torch.empty_like(src)
         dep = torch.empty(B, dtype=torch.int32, device=dev)
-        for _ in range(3):
-            cache.put(ids, src, 4)
-            cache.get(ids, 4, dst, dep)
         res = {}
-        for name, fn in (("put", lambda: cache.put(ids, src, 4)), ("get", lambda: cache.get(ids, 4, dst, dep))):
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
-            torch.cuda.synchronize()
-            torch.cuda._sleep(5_000_000)     # ~2.5 ms: the host queues every rep before the GPU reaches
-            for r in range(reps):            # them, so the events time the device, not Python launch latency
-                ev[2 * r].record()
-                fn()
-                ev[2 * r + 1].record()
-            torch.cuda.synchronize()
-            ms = statistics.median(ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(reps))
-            gbs = 2 * B * ROW_BYTES / (ms * 1e-3) / 1e9
-            res[name] = {"us": round(ms * 1e3, 2), "gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4)}
+        for name, fn in (("put", lambda r: cache.put(id_sets[r], src, 4)),
+                         ("get", lambda r: cache.get(id_sets[r], 4, dst, dep))):
+            us = marginal_us(fn)
+            gbs = 2 * B * ROW_BYTES / (us * 1e-6) / 1e9
+            res[name] = {"us": round(us, 2), "gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4)}
         out[str(B)] = res
+    del flush
     return out
 
 

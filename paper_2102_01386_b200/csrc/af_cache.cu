@@ -13,9 +13,13 @@
 // STAGES-1 chunk loads and the matching stores are in flight per CTA without
 // register staging.  Work items are (row, 32 KiB chunk) pairs dealt round-robin
 // to a persistent grid of two CTAs (3 stages each) per SM -- the best of the
-// profiles/r01_v9_variants_cache.jsonl sweep.  A get evicts a record only after
-// every chunk of its row has read the meta word (a per-record reader count,
-// fenced), so all chunks of a row agree on hit/miss.
+// profiles/r01_v9_variants_cache.jsonl sweep, confirmed with a cold L2 and
+// graph-timed calls in profiles/r01_v34_cache_cold_graph.jsonl.  Each CTA has two
+// warps: warp 0 turns ids into addresses and streams the copies, warp 1 does the
+// meta side (see cache_kernel), so a get's record load does not wait for its
+// meta word.  A get evicts a record only after every chunk of its row has read
+// the meta word (a per-record reader count, fenced), so all chunks of a row
+// agree on hit/miss.
 #include <cuda_runtime.h>
 
 #include "af_internal.h"
@@ -32,6 +36,7 @@ namespace {
 #ifndef AF_CACHE_CTAS_PER_SM
 #define AF_CACHE_CTAS_PER_SM 2
 #endif
+
 constexpr int kStages = AF_CACHE_STAGES;
 constexpr int kChunk = AF_CACHE_CHUNK;
 constexpr int kMaxDesc = 512;
@@ -85,22 +90,121 @@ __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// Lane 0 streams the ok descriptors through the ring.  `seq` counts loads over
-// the whole launch so that stage s = seq % kStages and its mbarrier parity
-// (seq / kStages) & 1 stay consistent across descriptor batches.
-__device__ void pump(const Desc *descs, int m, unsigned char *stage_buf, uint64_t *bars, uint32_t &seq) {
-  // gather the ok items' indices on the fly
-  int load_i = 0;          // next descriptor to load
-  uint32_t base = seq;     // sequence number of the first ok item of this batch
+// Two warps per CTA.  Warp 0 resolves each item's addresses from its id alone
+// (direct-mapped: slot = id / world) and its lane 0 starts the TMA loads at
+// once; warp 1 reads the meta words in parallel (get: hit + depth_out; put:
+// {depth, valid}) and publishes the hit flags through an mbarrier that lane 0
+// waits on before its first store.  A get therefore loads the record
+// speculatively -- the meta round trip and the evict-on-read bookkeeping (fence
+// + reader count) are off the id -> load -> store chain; a miss discards the
+// loaded chunk and stores nothing.
+constexpr int kMiss = -2147483647 - 1;
+
+template <bool PUT>
+__device__ __forceinline__ bool item_owner(const CacheParams &p, int i, int c, bool report, char *&payload,
+                                           CacheMeta *&meta, int64_t &id) {
+  id = p.ids[i];
+  payload = p.payload;
+  meta = p.meta;
+  if (id < 0 || id >= p.num_examples) {
+    if (report && c == 0) atomicOr(p.err, AF_CACHE_ERR_RANGE);
+    return false;
+  }
+  if (p.peer_payload) {  // global: the owner's store, possibly a peer's
+    const int owner = static_cast<int>(id % p.world);
+    payload = p.peer_payload[owner];
+    meta = p.peer_meta[owner];
+  } else if (id % p.world != p.rank) {
+    if (report && c == 0) atomicOr(p.err, AF_CACHE_ERR_OWNER);
+    return false;
+  }
+  return true;
+}
+
+template <bool PUT>
+__device__ __forceinline__ Desc item_addr(const CacheParams &p, int64_t j) {
+  const int i = static_cast<int>(j / p.n_chunks);
+  const int c = static_cast<int>(j % p.n_chunks);
+  Desc dsc{nullptr, nullptr, 0u, 0u};
+  const int64_t off = static_cast<int64_t>(c) * p.chunk_bytes;
+  const int64_t rem = p.row_bytes - off;
+  dsc.bytes = static_cast<uint32_t>(rem < p.chunk_bytes ? rem : p.chunk_bytes);
+  char *payload;
+  CacheMeta *meta;
+  int64_t id;
+  if (!item_owner<PUT>(p, i, c, true, payload, meta, id)) return dsc;
+  char *rec;
+  if (p.rowslot) {  // tiered: the plan kernel resolved the row's slot (and its meta / eviction)
+    const int32_t slot = p.rowslot[i];
+    if (slot < 0) return dsc;
+    rec = (slot < p.hbm_rows ? p.payload + static_cast<int64_t>(slot) * p.row_bytes
+                             : p.host + (static_cast<int64_t>(slot) - p.hbm_rows) * p.row_bytes) +
+          off;
+  } else {
+    rec = payload + (id / p.world) * p.row_bytes + off;
+  }
+  if (PUT) {
+    dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+    dsc.dst = rec;
+  } else {
+    dsc.src = rec;
+    dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
+  }
+  dsc.ok = 1u;
+  return dsc;
+}
+
+// warp 1: the meta side of item j.  Returns the record's depth on a get hit
+// (kMiss otherwise; tiered and put: 0 = store).
+template <bool PUT>
+__device__ __forceinline__ int item_meta(const CacheParams &p, int64_t j) {
+  const int i = static_cast<int>(j / p.n_chunks);
+  const int c = static_cast<int>(j % p.n_chunks);
+  char *payload;
+  CacheMeta *meta;
+  int64_t id;
+  const bool ok = item_owner<PUT>(p, i, c, false, payload, meta, id);
+  if (p.rowslot) return 0;  // tiered: the plan kernel did the meta work
+  if (!ok) {
+    if (!PUT && c == 0) p.depth_out[i] = -1;
+    return kMiss;
+  }
+  const int64_t slot = id / p.world;
+  if (PUT) {
+    if (c == 0) *reinterpret_cast<int2 *>(meta + slot) = make_int2(p.depth, 1);  // {depth, valid}
+    return 0;
+  }
+  const int4 mv = __ldcg(reinterpret_cast<const int4 *>(meta) + slot);  // {depth, valid, readers, -}
+  const bool hit = mv.y != 0;
+  if (c == 0) p.depth_out[i] = hit ? mv.x : -1;
+  return hit ? mv.x : kMiss;
+}
+
+// evict on read once every chunk of the row has read the record
+__device__ __forceinline__ void item_evict(const CacheParams &p, int64_t j, int depth) {
+  const int i = static_cast<int>(j / p.n_chunks);
+  const int64_t id = p.ids[i];
+  CacheMeta *meta = p.peer_meta ? p.peer_meta[id % p.world] : p.meta;
+  const int64_t slot = id / p.world;
+  __threadfence();
+  const unsigned int seen = atomicAdd(&meta[slot].readers, 1u);
+  if (seen == static_cast<unsigned int>(p.n_chunks) - 1u) {
+    if (depth < p.cur_boundary) meta[slot].valid = 0;
+    meta[slot].readers = 0u;
+  }
+}
+
+__device__ void pump_spec(const Desc *descs, const int *hitdep, int m, unsigned char *stage_buf, uint64_t *bars,
+                          uint32_t &seq, uint64_t *hbar, uint32_t hpar, bool gate) {
   uint32_t n_ok = 0;
   for (int i = 0; i < m; ++i) n_ok += descs[i].ok;
   auto next_ok = [&](int i) {
     while (i < m && !descs[i].ok) ++i;
     return i;
   };
-  // prologue: up to kStages-1 loads ahead
+  const uint32_t base = seq;
   uint32_t loaded = 0;
-  load_i = next_ok(0);
+  int load_i = next_ok(0);
   while (loaded < n_ok && loaded < kStages - 1) {
     const uint32_t u = base + loaded;
     const int s = u % kStages;
@@ -109,15 +213,18 @@ __device__ void pump(const Desc *descs, int m, unsigned char *stage_buf, uint64_
     ++loaded;
     load_i = next_ok(load_i + 1);
   }
+  if (gate && n_ok) mbar_wait(hbar, hpar);  // warp 1's hit flags for this batch
   int store_i = next_ok(0);
   for (uint32_t q = 0; q < n_ok; ++q) {
     const uint32_t u = base + q;
     const int s = u % kStages;
     mbar_wait(&bars[s], (u / kStages) & 1u);
-    bulk_s2g(descs[store_i].dst, stage_buf + static_cast<size_t>(s) * kChunk, descs[store_i].bytes);
+    const bool st = hitdep[store_i] != kMiss;
+    if (st) bulk_s2g(descs[store_i].dst, stage_buf + static_cast<size_t>(s) * kChunk, descs[store_i].bytes);
     store_i = next_ok(store_i + 1);
     if (loaded < n_ok) {
-      bulk_wait_read1();  // the store that last used the stage we refill has read its bytes
+      if (st) bulk_wait_read1();  // the store that last used the stage we refill has read its bytes
+      else bulk_wait_read0();
       const uint32_t v = base + loaded;
       const int sv = v % kStages;
       mbar_expect_tx(&bars[sv], descs[load_i].bytes);
@@ -130,112 +237,50 @@ __device__ void pump(const Desc *descs, int m, unsigned char *stage_buf, uint64_
   seq = base + n_ok;
 }
 
-// Item j = (row j / n_chunks, chunk j % n_chunks): owner / range checks, the
-// record's address, meta update (put) or hit + evict-on-read bookkeeping (get).
-// Returns the copy to perform (ok = 0: nothing to copy).
-template <bool PUT>
-__device__ __forceinline__ Desc describe_item(const CacheParams &p, int64_t j) {
-  const int i = static_cast<int>(j / p.n_chunks);
-  const int c = static_cast<int>(j % p.n_chunks);
-  const int64_t id = p.ids[i];
-  Desc dsc{nullptr, nullptr, 0u, 0u};
-  bool ok = true;
-  char *payload = p.payload;
-  CacheMeta *meta = p.meta;
-  if (id < 0 || id >= p.num_examples) {
-    if (c == 0) atomicOr(p.err, AF_CACHE_ERR_RANGE);
-    ok = false;
-  } else if (p.peer_payload) {  // global: the owner's store, possibly a peer's
-    const int owner = static_cast<int>(id % p.world);
-    payload = p.peer_payload[owner];
-    meta = p.peer_meta[owner];
-  } else if (id % p.world != p.rank) {
-    if (c == 0) atomicOr(p.err, AF_CACHE_ERR_OWNER);
-    ok = false;
-  }
-  const int64_t off = static_cast<int64_t>(c) * p.chunk_bytes;
-  const int64_t rem = p.row_bytes - off;
-  dsc.bytes = static_cast<uint32_t>(rem < p.chunk_bytes ? rem : p.chunk_bytes);
-  if (ok && p.rowslot) {
-    // tiered: the plan kernel resolved the row's slot (and its meta / eviction)
-    const int32_t slot = p.rowslot[i];
-    if (slot >= 0) {
-      char *rec = (slot < p.hbm_rows ? p.payload + static_cast<int64_t>(slot) * p.row_bytes
-                                     : p.host + (static_cast<int64_t>(slot) - p.hbm_rows) * p.row_bytes) +
-                  off;
-      if (PUT) {
-        dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
-        dsc.dst = rec;
-      } else {
-        dsc.src = rec;
-        dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
-      }
-      dsc.ok = 1u;
-    }
-  } else if (ok) {
-    const int64_t slot = id / p.world;
-    char *rec = payload + slot * p.row_bytes + off;
-    if (PUT) {
-      dsc.src = p.src_rows + static_cast<int64_t>(i) * p.row_bytes + off;
-      dsc.dst = rec;
-      dsc.ok = 1u;
-      if (c == 0) *reinterpret_cast<int2 *>(meta + slot) = make_int2(p.depth, 1);  // {depth, valid}
-    } else {
-      const int4 mv = __ldcg(reinterpret_cast<const int4 *>(meta) + slot);  // {depth, valid, readers, -}
-      const bool hit = mv.y != 0;
-      if (c == 0) p.depth_out[i] = hit ? mv.x : -1;
-      if (hit) {
-        dsc.src = rec;
-        dsc.dst = p.dst_rows + static_cast<int64_t>(i) * p.row_bytes + off;
-        dsc.ok = 1u;
-        // evict on read once every chunk of the row has read the record
-        __threadfence();
-        const unsigned int seen = atomicAdd(&meta[slot].readers, 1u);
-        if (seen == static_cast<unsigned int>(p.n_chunks) - 1u) {
-          if (mv.x < p.cur_boundary) meta[slot].valid = 0;
-          meta[slot].readers = 0u;
-        }
-      }
-    }
-  } else if (!PUT && c == 0 && !p.rowslot) {
-    p.depth_out[i] = -1;  // (tiered: the plan kernel wrote depth_out)
-  }
-  return dsc;
-}
+constexpr int kCacheThreads = 64;
 
 template <bool PUT>
-__global__ void __launch_bounds__(32) cache_kernel(const CacheParams p) {
+__global__ void __launch_bounds__(kCacheThreads) cache_kernel(const CacheParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
+  uint64_t *hbar = bars + kStages;
   unsigned char *stage_buf = smem + 128;
   Desc *descs = reinterpret_cast<Desc *>(stage_buf + static_cast<size_t>(kStages) * kChunk);
-  const int lane = threadIdx.x;
-  if (lane == 0) {
+  int *hitdep = reinterpret_cast<int *>(descs + kMaxDesc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    mbar_init(hbar, 1);
     fence_mbar_init();
   }
-  __syncwarp();
+  __syncthreads();
   pdl_wait();  // ids, rows and the meta words may come from the preceding kernels
 
   const int64_t n_items = static_cast<int64_t>(p.n) * p.n_chunks;
   const int64_t G = gridDim.x;
   const int64_t my_items = (n_items > blockIdx.x) ? (n_items - blockIdx.x + G - 1) / G : 0;
-  uint32_t seq = 0;
-  for (int64_t kb = 0; kb < my_items; kb += kMaxDesc) {
+  uint32_t seq = 0, batch = 0;
+  for (int64_t kb = 0; kb < my_items; kb += kMaxDesc, ++batch) {
     const int m = static_cast<int>((my_items - kb) < kMaxDesc ? (my_items - kb) : kMaxDesc);
-    for (int q = lane; q < m; q += 32) {
-      const int64_t j = blockIdx.x + (kb + q) * G;
-      const Desc dsc = describe_item<PUT>(p, j);
-      descs[q] = dsc;
+    if (warp == 0) {
+      for (int q = lane; q < m; q += 32) descs[q] = item_addr<PUT>(p, blockIdx.x + (kb + q) * G);
+      __syncwarp();
+      if (lane == 0) pump_spec(descs, hitdep, m, stage_buf, bars, seq, hbar, batch & 1u, !PUT);
+      __syncwarp();
+    } else {
+      for (int q = lane; q < m; q += 32) hitdep[q] = item_meta<PUT>(p, blockIdx.x + (kb + q) * G);
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(hbar)) : "memory");
+      if (!PUT && !p.rowslot) {
+        for (int q = lane; q < m; q += 32)
+          if (hitdep[q] != kMiss) item_evict(p, blockIdx.x + (kb + q) * G, hitdep[q]);
+      }
     }
-    __syncwarp();
-    if (lane == 0) pump(descs, m, stage_buf, bars, seq);
-    __syncwarp();
+    __syncthreads();  // descs / hitdep of this batch are consumed
   }
   pdl_launch_dependents();
-  if (lane == 0) bulk_wait_all();  // all stores complete before the CTA retires its shared memory
+  if (threadIdx.x == 0) bulk_wait_all();  // all stores complete before the CTA retires its shared memory
 }
-
 
 // Tiered-mode plan (one CTA, 1024 threads): resolves every row of the call in call
 // order with block-wide exclusive scans, so slot allocation and freeing are
@@ -347,7 +392,7 @@ __global__ void __launch_bounds__(kPlanThreads) cache_plan_kernel(const CachePla
 
 }  // namespace
 
-int cache_smem_bytes() { return 128 + kStages * kChunk + kMaxDesc * static_cast<int>(sizeof(Desc)); }
+int cache_smem_bytes() { return 128 + kStages * kChunk + kMaxDesc * static_cast<int>(sizeof(Desc) + sizeof(int)); }
 
 template <bool PUT>
 static int launch_cache(const CacheParams &p0, int grid, void *stream) {
@@ -360,7 +405,7 @@ static int launch_cache(const CacheParams &p0, int grid, void *stream) {
   const int smem = cache_smem_bytes();
   const cudaError_t e = ensure_smem_attr<cache_kernel<PUT>>(smem);
   if (e != cudaSuccess) return static_cast<int>(e);
-  return static_cast<int>(launch_pdl(cache_kernel<PUT>, dim3(grid), dim3(32), static_cast<size_t>(smem),
+  return static_cast<int>(launch_pdl(cache_kernel<PUT>, dim3(grid), dim3(kCacheThreads), static_cast<size_t>(smem),
                                      static_cast<cudaStream_t>(stream), p));
 }
 

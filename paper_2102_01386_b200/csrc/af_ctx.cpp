@@ -193,7 +193,7 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
     T.o_tiles = take(T.tiles.size() * sizeof(Tile));
   }
   c->o_part = take(c->ts[1].tiles.size() * sizeof(double));
-  c->o_part2 = take((c->ts[1].tiles.size() / kFinChunk + L + 2) * sizeof(double));
+  c->o_part2 = take((c->ts[1].tiles.size() / kFinChunkMin + L + 2) * sizeof(double));
   c->o_chunk = take((c->ts[1].tiles.size() / kFinChunk + 2) * sizeof(unsigned int));
   c->scratch_bytes = o;
   *out = c;

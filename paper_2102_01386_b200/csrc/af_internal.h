@@ -67,12 +67,20 @@ struct DevState {
 };
 
 #ifndef AF_FIN_WIDE  // 0: the streaming kernel's last CTA sums all partials; 1: a second, wide
-#define AF_FIN_WIDE 1   // finalize launch; 2: chunks reduced inside the streaming kernel
+#define AF_FIN_WIDE 1   // finalize launch; 2: chunks reduced inside the streaming kernel as they
+#endif              // complete; 3: the streaming kernel's last-retiring CTAs reduce the chunks
+#ifndef AF_FIN3_CHUNK  // AF_FIN_WIDE == 3: partials per chunk (one load per thread at 256)
+#define AF_FIN3_CHUNK 256
+#endif
+#ifndef AF_FIN3_MIN_TILES  // AF_FIN_WIDE == 3 above this many tiles (the last CTA alone below)
+#define AF_FIN3_MIN_TILES 2048
 #endif
 #ifndef AF_ALTERNATE_ORDER  // alternate the streaming kernels' tile order per launch (L2 reuse)
 #define AF_ALTERNATE_ORDER 1
 #endif
 constexpr int kFinChunk = 2048;  // partials per fin_kernel CTA (8 per thread)
+constexpr int kFin3Chunk = AF_FIN3_CHUNK;
+constexpr int kFinChunkMin = kFin3Chunk < kFinChunk ? kFin3Chunk : kFinChunk;  // sizes part2
 
 enum Mode : int {
   kAccum = 0, kEndDelta = 1, kStepSq = 2, kAdamAccum = 3, kAdamEnd = 4,
@@ -124,8 +132,10 @@ struct NormParams {
   // wide finalize (n_tiles > kFinChunk): the streaming kernel only writes the
   // partials; fin_kernel's CTAs reduce chunks of kFinChunk partials into
   // part2[chunk + segment] and its last CTA combines them in chunk order
-  int32_t wide_fin;                // 0: narrow; 1: fin_kernel launch; 2: chunks reduced in-kernel
-  double *part2;                   // [n_tiles / kFinChunk + L + 2]
+  int32_t wide_fin;                // 0: narrow; 1: fin_kernel launch; 2: chunks reduced in-kernel;
+                                   // 3: chunks reduced by the last-retiring CTAs
+  int32_t fin_chunk;               // tiles per chunk (kFinChunk; kFin3Chunk when wide_fin == 3)
+  double *part2;                   // [n_tiles / fin_chunk + L + 2]
   Sched *fin_sched;                // done counter of fin_kernel
   unsigned int *chunk_cnt;         // [n_tiles / kFinChunk + 1] finished tiles per chunk (in-kernel form)
   double *ss_out;                  // [L] this rank's row of the exchange matrix

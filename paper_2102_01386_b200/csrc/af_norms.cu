@@ -562,16 +562,18 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) 
     }
   };
   if constexpr (WIDE) {
-    // fin_kernel's chunk sums: segment l's active tiles span chunks
-    // [c_lo, c_hi] (chunk c = tiles first_tile + [c*kFinChunk, (c+1)*kFinChunk)),
-    // whose pieces of l sit at part2[c + l]; summed in chunk order
+    // the chunk sums: segment l's active tiles span chunks [c_lo, c_hi]
+    // (chunk c = tiles first_tile + [c*CH, (c+1)*CH), CH = p.fin_chunk), whose
+    // pieces of l sit at part2[c + l]; summed in chunk order
+    const int CH = p.fin_chunk;
     for (int l = tid; l < p.L; l += kNormBlock) {
       int tb = p.seg_tile_begin[l];
       tb = tb < first_tile ? first_tile : tb;
       const int te = p.seg_tile_begin[l + 1];
       double s = 0.0;
       if (te > tb) {
-        const int c_lo = (tb - first_tile) / kFinChunk, c_hi = (te - 1 - first_tile) / kFinChunk;
+        const int c_lo = (tb - first_tile) / CH, c_hi = (te - 1 - first_tile) / CH;
+#pragma unroll 8
         for (int c = c_lo; c <= c_hi; ++c) s += __ldcg(p.part2 + c + l);
       }
       publish(l, s);
@@ -638,7 +640,49 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) 
   }
 }
 
+template <int CH>
 __device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int c, double *s_p);
+
+// AF_FIN_WIDE == 3.  `ticket` = this CTA's place in the grid's retirement order.
+// The last W = min(chunks, grid) CTAs to retire become workers: each waits until
+// the whole grid has retired (every partial published), reduces chunks w, w+W, ...
+// of kFin3Chunk partials as fin_kernel's CTAs would (chunk_reduce, fixed order),
+// and the last worker to finish returns true and carries on as the grid's last
+// CTA (segment sums from the pieces, exchange, decision) -- no second launch and
+// no kernel boundary between the streaming and the finalize.  The wait cannot
+// deadlock: the scheduler is drained, so every CTA not yet retired is resident
+// or starts, finds no tile and retires, in a slot a retired non-worker freed (or
+// its own: the grid is sized to the device's co-resident limit).
+__device__ __noinline__ bool retire_finalize(const NormParams &p, int first_tile, int ticket, double *s_p) {
+  const int tid = threadIdx.x;
+  const int G = static_cast<int>(gridDim.x);
+  const int nch = (p.n_tiles - first_tile + kFin3Chunk - 1) / kFin3Chunk;
+  const int W = nch < G ? nch : G;
+  const int w = ticket - (G - W);
+  if (nch <= 0) return ticket == G - 1;  // no active tile: the last CTA carries on
+  if (w < 0) return false;
+  __shared__ int s_fin_last;
+  if (tid == 0) {
+    for (;;) {
+      unsigned int v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&p.sched->done) : "memory");
+      if (v >= static_cast<unsigned int>(G)) break;
+      __nanosleep(20);
+    }
+    if (AF_TIMING && ticket == G - 1) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
+  }
+  __syncthreads();
+  for (int c = w; c < nch; c += W) chunk_reduce<kFin3Chunk>(p, first_tile, c, s_p);
+  if (tid == 0) {
+    __threadfence();
+    s_fin_last = atomicAdd(&p.fin_sched->done, 1u) == static_cast<unsigned int>(W - 1);
+  }
+  __syncthreads();
+  if (!s_fin_last) return false;
+  __threadfence();
+  if (tid == 0) p.fin_sched->done = 0u;
+  return true;
+}
 
 template <int MODE, typename GT, bool RD, int PM = 1>
 __global__ void __launch_bounds__(kNormBlock, MODE == kAccum ? 2 : ((MODE >= kAdamAccum) ? 1 : AF_MINB_END))
@@ -647,7 +691,7 @@ __global__ void __launch_bounds__(kNormBlock, MODE == kAccum ? 2 : ((MODE >= kAd
   constexpr bool PARTIALS = MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum && MODE != kRsAdamAccum;
   // in-kernel wide finalize (AF_FIN_WIDE == 2): the CTA that completes a chunk of
   // kFinChunk tiles reduces it (staging buffer below) between its own tiles
-  __shared__ double s_fin[(PARTIALS && AF_FIN_WIDE == 2) ? kFinChunk : 1];
+  __shared__ double s_fin[(PARTIALS && AF_FIN_WIDE == 2) ? kFinChunk : ((PARTIALS && AF_FIN_WIDE == 3) ? kFin3Chunk : 1)];
   __shared__ int s_chunk;
   __shared__ int s_tile[3];
   __shared__ Tile s_desc[3];
@@ -748,7 +792,7 @@ __global__ void __launch_bounds__(kNormBlock, MODE == kAccum ? 2 : ((MODE >= kAd
       if (p.wide_fin == 2) {
         const int c = s_chunk;
         if (c >= 0) {
-          chunk_reduce(p, first_tile, c, s_fin);
+          chunk_reduce<kFinChunk>(p, first_tile, c, s_fin);
           if (tid == 0) p.chunk_cnt[c] = 0u;  // every tile of the chunk has counted: reset for the next launch
         }
       }
@@ -763,8 +807,17 @@ __global__ void __launch_bounds__(kNormBlock, MODE == kAccum ? 2 : ((MODE >= kAd
     __threadfence();
     const unsigned int d = atomicAdd(&p.sched->done, 1u);
     s_last = (d == gridDim.x - 1);
+    s_chunk = static_cast<int>(d);  // retirement ticket (wide_fin == 3)
   }
   __syncthreads();
+  if constexpr (PARTIALS && AF_FIN_WIDE == 3) {
+    // the last W CTAs to retire wait for the grid to drain, reduce the chunks of
+    // partials in parallel, and the last of them continues as "the last CTA"
+    if (p.wide_fin == 3) {
+      if (!retire_finalize(p, first_tile, s_chunk, s_fin)) return;
+      s_last = 1;  // (uniform: every thread of this CTA took the same branch)
+    }
+  }
   if (!s_last) return;
   __threadfence();
   if (tid == 0) {
@@ -783,7 +836,7 @@ __global__ void __launch_bounds__(kNormBlock, MODE == kAccum ? 2 : ((MODE >= kAd
     if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
     return;
   }
-  if (p.wide_fin == 2) {  // every chunk already reduced: combine the pieces
+  if (p.wide_fin >= 2) {  // every chunk already reduced: combine the pieces
     if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
     last_cta_tail<TM, true>(p, first_tile);
     return;
@@ -797,13 +850,15 @@ __global__ void __launch_bounds__(kNormBlock, MODE == kAccum ? 2 : ((MODE >= kAd
 // reduced by one warp (lane-strided, xor tree) into part2[c + l] -- piece (c, l)
 // is the (c + l)-th piece in tile order, so the index needs no search.  Every
 // thread of the CTA calls it.  Fixed order: deterministic.
+template <int CH>
 __device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int c, double *s_p) {
+  static_assert(CH % kNormBlock == 0, "chunk = whole loads per thread");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int c0 = first_tile + c * kFinChunk;
+  const int c0 = first_tile + c * CH;
   if (c0 >= p.n_tiles) return;  // uniform over the CTA
-  const int n = min(kFinChunk, p.n_tiles - c0);
+  const int n = min(CH, p.n_tiles - c0);
 #pragma unroll
-  for (int u = 0; u < kFinChunk / kNormBlock; ++u) {
+  for (int u = 0; u < CH / kNormBlock; ++u) {
     const int k = u * kNormBlock + tid;
     if (k < n) s_p[k] = __ldcg(p.partials + c0 + k);
   }
@@ -837,7 +892,7 @@ __global__ void __launch_bounds__(kNormBlock) fin_kernel(const NormParams p) {
   int f = p.state->f;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int first_tile = p.first_tile_of_f[f];
-  chunk_reduce(p, first_tile, blockIdx.x, s_p);
+  chunk_reduce<kFinChunk>(p, first_tile, blockIdx.x, s_p);
   pdl_launch_dependents();
   if (tid == 0) {
     __threadfence();
@@ -1152,7 +1207,9 @@ int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
 
 int fin_ctas(int mode, int n_tiles) {
   const bool end_mode = mode == kEndDelta || mode == kStepSq || mode == kAdamEnd || mode == kRsEnd || mode == kRsAdamEnd;
-  if (!AF_FIN_WIDE || !end_mode || n_tiles <= kFinChunk || (mode == kEndDelta && AF_TMA >= 1)) return 0;
+  if (!AF_FIN_WIDE || !end_mode || (mode == kEndDelta && AF_TMA >= 1)) return 0;
+  if (AF_FIN_WIDE == 3) return n_tiles <= AF_FIN3_MIN_TILES ? 0 : (n_tiles + kFin3Chunk - 1) / kFin3Chunk;
+  if (n_tiles <= kFinChunk) return 0;
   return (n_tiles + kFinChunk - 1) / kFinChunk;
 }
 
@@ -1160,6 +1217,7 @@ int launch_norms(const NormParams &p_in, int mode, int grad_dtype, int grid, voi
   NormParams p = p_in;
   const int nfin = fin_ctas(mode, p.n_tiles);
   p.wide_fin = nfin > 0 ? AF_FIN_WIDE : 0;
+  p.fin_chunk = AF_FIN_WIDE == 3 ? kFin3Chunk : kFinChunk;
   const int e = grad_dtype == AF_DT_BF16 ? launch_dt<uint16_t>(p, mode, grid, stream)
                                          : launch_dt<float>(p, mode, grid, stream);
   if (e != 0 || !nfin || AF_FIN_WIDE != 1) return e;

@@ -15,6 +15,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
+    "fin3": "-DAF_FIN_WIDE=3",
+    "fin3_512": "-DAF_FIN_WIDE=3 -DAF_FIN3_CHUNK=512",
+    "fin3_min512": "-DAF_FIN_WIDE=3 -DAF_FIN3_MIN_TILES=512",
+    "timing_fin3": "-DAF_TIMING=1 -DAF_FIN_WIDE=3",
     "fin_narrow": "-DAF_FIN_WIDE=0",
     "fin_inkernel": "-DAF_FIN_WIDE=2",
     "acc_dnc": "-DAF_D_HINT_ACC=1",
@@ -103,7 +107,7 @@ def main():
             continue
         for wl in ("bert-large-f32", "bert-base-bf16"):
             r = subprocess.run([sys.executable, "bench.py", "--workload", wl, "--steps", str(a.steps), "--warmup", "10",
-                                "--no-e2e", "--no-cpu-baseline", "--no-cache-sweep"], cwd=ROOT,
+                                "--no-e2e", "--no-cpu-baseline", "--no-cache-sweep", "--no-secondary"], cwd=ROOT,
                                capture_output=True, text=True)
             try:
                 d = json.loads(r.stdout.strip().splitlines()[-1])
@@ -115,6 +119,8 @@ def main():
                               "ms_per_step": d["ms_per_step"],
                               "accumulate_gbs": ph["accumulate"]["gbs"], "grad_norm_gbs": ph["grad_norm_decide"]["gbs"],
                               "accumulate_ms": ph["accumulate"]["ms"], "grad_norm_ms": ph["grad_norm_decide"]["ms"],
+                              "in_step_ms": {k: v["ms"] for k, v in (d.get("phases_in_step") or {}).items()
+                                             if isinstance(v, dict)},
                               "adamw_gbs": (d.get("next1_fused_adamw") or {}).get("gbs"),
                               "rs_p1_gbs": (d.get("next1_fused_reduce_scatter_p1") or {}).get("gbs"),
                               "clocks": d.get("clocks")}), flush=True)
