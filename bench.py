@@ -333,6 +333,8 @@ def run_ours(args, rank, world, local):
         if world > 1:
             dist.barrier()
     ms_local = t0.elapsed_time(t1)
+    dist_ms = step_distribution(args, run, stream, world, dist, dev)
+    frozen = None if args.zero else frozen_point(args, fm, lay, info, s_g, B, run, stream, world, dist, dev)
     marg = step_marginals(args, graphs, step, stream, world, dist) if graphs else None
     cache_marg = marg["cache"] if marg else None
     # per-phase breakdown: a second, eagerly launched pass with CUDA events between calls
@@ -397,6 +399,8 @@ def run_ours(args, rank, world, local):
                    **({"gbs": round(phase_bytes(bytes_rank, k) / (v * 1e-3) / 1e9, 1),
                        "frac_of_peak": round(phase_bytes(bytes_rank, k) / (v * 1e-3) / 1e9 / peak, 4)} if v > 0 else {})}
                for k, v in marg.items() if k != "full"}}} if marg else {}),
+        "step_ms_dist": dist_ms,
+        "frozen_half": frozen,
         "phases": phase_report,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(ach / peak, 4), "peak_source": peak_src,
@@ -426,6 +430,72 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def step_distribution(args, run, stream, world, dist, dev, n=100):
+    """p10 / p50 / p90 of single-step device times (SURVEY.md §8(d) timing
+    protocol): min(K, 100) replays, each bracketed by its own event pair (the
+    pair adds a little; the headline `ms_per_step` is the K-step block)."""
+    import torch
+    n = max(1, min(args.steps, n))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i, (a, b) in enumerate(evs):
+        a.record(stream)
+        run(i)
+        b.record(stream)
+    torch.cuda.synchronize()
+    t = sorted(a.elapsed_time(b) for a, b in evs)
+    q = {k: t[min(len(t) - 1, int(round(f * (len(t) - 1))))] for k, f in (("p10", 0.1), ("p50", 0.5), ("p90", 0.9))}
+    if world > 1:
+        q = {k: max_over_ranks(v, dev) for k, v in q.items()}
+    return {**{k: round(v, 5) for k, v in q.items()}, "samples": n}
+
+
+def frozen_point(args, fm, lay, info, s_g, B, run, stream, world, dist, dev):
+    """The same step with the boundary at f = B/2 POOL blocks frozen (SURVEY.md
+    §8(d): bytes scale with the active suffix; PRE is tied to the first POOL
+    block).  f is patched into a state blob (af_get_state layout: magic, version,
+    L, world, rank, T, f, ...); the step's graphs read f from device memory at
+    launch, so they replay unchanged.  The original state is restored after."""
+    import struct
+
+    import torch
+    blob = fm.get_state()
+    f = info["n_pool"] // 2
+    from afinputs.layouts import SEG_POOL
+    pool = [l for l, k in enumerate(lay.kinds) if k == SEG_POOL]
+    assert len(pool) == info["n_pool"]
+    act0 = lay.offsets[pool[f]]                       # segments before the (f+1)-th POOL block are frozen
+    sb, se = info["shard_begin"], info["shard_end"]
+    n_act = max(0, se - max(sb, act0))
+    patched = bytearray(blob)
+    struct.pack_into("<i", patched, 24, f)
+    fm.set_state(bytes(patched))
+    try:
+        for i in range(args.warmup):
+            run(i)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(args.steps):
+            run(i)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / args.steps
+        if world > 1:
+            ms = max_over_ranks(ms, dev)
+    finally:
+        fm.set_state(blob)
+    by = algorithmic_bytes(n_act, s_g, B, ROW_BYTES)
+    step_bytes = sum(by.values()) * world
+    return {"boundary_f": f, "active_elements_local": n_act, "ms_per_step": round(ms, 5),
+            "gbs": round(step_bytes / (ms * 1e-3) / 1e9, 1),
+            "note": "algorithmic bytes count active (unfrozen) elements only; GB/s on those bytes"}
 
 
 def phase_bytes(bytes_rank, phase):
@@ -479,14 +549,15 @@ def secondary_workload(args):
     import subprocess
     other = "bert-base-bf16" if args.workload == "bert-large-f32" else "bert-large-f32"
     cmd = [sys.executable, os.path.abspath(__file__), "--workload", other, "--steps", str(args.steps), "--warmup",
-           str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-cache-sweep", "--no-extras", "--no-secondary"]
+           str(args.warmup), "--no-e2e", "--no-cpu-baseline", "--no-cache-sweep", "--no-secondary"]
     r = subprocess.run(cmd, capture_output=True, text=True, env=dict(os.environ, WORLD_SIZE="1", RANK="0"))
     try:
         d = json.loads(r.stdout.strip().splitlines()[-1])
     except Exception:  # noqa: BLE001
         return {"workload": other, "error": r.stderr[-500:]}
     keep = ("value", "unit", "ms_per_step", "grad_norm_decide_gbs", "grad_norm_decide_frac_of_hbm_peak", "dtype",
-            "config", "phases", "phases_in_step", "cache_gbs", "cache_in_step", "roofline", "clocks")
+            "config", "phases", "phases_in_step", "cache_gbs", "cache_in_step", "roofline", "clocks", "step_ms_dist",
+            "frozen_half", "next1_fused_adamw", "next1_fused_reduce_scatter_p1")
     return {"workload": other, **{k: d[k] for k in keep if k in d}}
 
 
@@ -614,18 +685,23 @@ def rs_probe(lay, dt, s_g, grads, dev, reps=20):
     for _ in range(2):
         fm.reduce_scatter_step(out, dry_run=True)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(reps):
-        fm.reduce_scatter_step(out, dry_run=True)
-    b.record()
-    b.synchronize()
-    ms = a.elapsed_time(b) / reps
+    def timed(end):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fm.reduce_scatter_step(out, interval_end=end, dry_run=True)
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+    ms, ms_end = timed(False), timed(True)
     peak, _ = measured_peaks()
-    by = lay.n * (s_g + 12)
+    by, by_end = lay.n * (s_g + 12), lay.n * (s_g + 8)
     del out, fm
     return {"us": round(ms * 1e3, 1), "bytes_per_elem": s_g + 12, "gbs": round(by / (ms * 1e-3) / 1e9, 1),
-            "frac_of_peak": round(by / (ms * 1e-3) / 1e9 / peak, 4), "world": 1}
+            "frac_of_peak": round(by / (ms * 1e-3) / 1e9 / peak, 4), "world": 1,
+            "interval_end": {"us": round(ms_end * 1e3, 1), "bytes_per_elem": s_g + 8,
+                             "gbs": round(by_end / (ms_end * 1e-3) / 1e9, 1),
+                             "frac_of_peak": round(by_end / (ms_end * 1e-3) / 1e9 / peak, 4)}}
 
 
 def run_sweep(args, local):

@@ -75,6 +75,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef AF_U_RS_VEC  // fused reduce-scatter: gradient vectors in flight per thread (over all ranks)
 #define AF_U_RS_VEC 8
 #endif
+#ifndef AF_U_RS_VEC_BF16  // bf16: 4 (P = 1: 5.74 -> 6.29 TB/s; 16: 3.46, profiles/r01_v40_variants_rs.jsonl)
+#define AF_U_RS_VEC_BF16 4
+#endif
+#ifndef AF_U_RS_VEC_END  // the same at the interval end: fp32 keeps 8, bf16 4 (P = 1: fp32
+#define AF_U_RS_VEC_END 8   // 8 -> 4 is 6.76 -> 5.83 TB/s, bf16 5.81 -> 6.13 TB/s,
+#endif                     // profiles/r01_v39_variants_rs.jsonl; bf16 2: 5.79)
+#ifndef AF_U_RS_VEC_END_BF16
+#define AF_U_RS_VEC_END_BF16 4
+#endif
 
 namespace af {
 namespace {
@@ -365,7 +374,9 @@ __device__ __forceinline__ double process_tile_rs(const NormParams &p, const Til
   constexpr int DV = VE / 4;
   // PM = compile-time bound on the ranks (1, 2, 4, 8; P <= PM at run time): the
   // vectors in flight per thread stay U x PM = AF_U_RS_BYTES / 16 whatever P is
-  constexpr int U = ADAM ? 1 : (AF_U_RS_VEC / PM > 0 ? AF_U_RS_VEC / PM : 1);
+  constexpr bool BF = sizeof(GT) == 2;
+  constexpr int UV = END ? (BF ? AF_U_RS_VEC_END_BF16 : AF_U_RS_VEC_END) : (BF ? AF_U_RS_VEC_BF16 : AF_U_RS_VEC);
+  constexpr int U = ADAM ? 1 : (UV / PM > 0 ? UV / PM : 1);
   float *__restrict__ pw = p.params;
   float *__restrict__ mm = p.exp_avg;
   float *__restrict__ vv = p.exp_avg_sq;
@@ -685,7 +696,9 @@ __device__ __noinline__ bool retire_finalize(const NormParams &p, int first_tile
 }
 
 template <int MODE, typename GT, bool RD, int PM = 1>
-__global__ void __launch_bounds__(kNormBlock, MODE == kAccum ? 2 : ((MODE >= kAdamAccum) ? 1 : AF_MINB_END))
+__global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccum)
+                                  ? 2
+                                  : ((MODE >= kAdamAccum) ? 1 : AF_MINB_END))
     norms_kernel(const NormParams p) {
   constexpr bool RS = MODE == kRsAccum || MODE == kRsEnd || MODE == kRsAdamAccum || MODE == kRsAdamEnd;
   constexpr bool PARTIALS = MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum && MODE != kRsAdamAccum;

@@ -406,6 +406,34 @@ def test_cache_epoch_parity(rank, world):
     assert gc.status() == (0, len(oc.store))
 
 
+@pytest.mark.parametrize("rb", [16, 4096 + 16, 24_592, 196_608, 300_016])
+@pytest.mark.parametrize("n", [1, 7, 150, 256, 1100])
+def test_cache_chunk_choice_parity(rb, n):
+    """The per-call chunk size (balanced over the grid, af_cache.cu pick_chunks)
+    changes how rows split into items: bytes, depths and evict-on-read (every
+    chunk of a row must have read before the record goes) vs the oracle."""
+    from afinputs import cache_rows
+    num = 2 * n + 5
+    gc, oc = _cache_pair(num, rb)
+    ids = np.random.default_rng(n).permutation(num)[:n]
+    rows = cache_rows(1, n, n, rb)
+    half = n // 2
+    for part, depth in ((ids[:half], 2), (ids[half:], 5)):
+        if len(part):
+            gc.put(_ids(part), torch.from_numpy(rows[: len(part)]).cuda(), depth)
+            oc.put(part, rows[: len(part)], depth)
+    q = np.random.default_rng(n + 1).permutation(num)[:n]   # hits at depth 2 / 5 and misses
+    for _ in range(2):                                       # second pass: the depth-2 hits were evicted
+        out_g = torch.full((n, rb), 9, dtype=torch.uint8, device="cuda")
+        dep_g = torch.zeros(n, dtype=torch.int32, device="cuda")
+        gc.get(_ids(q), 3, out_g, dep_g)
+        out_o = np.full((n, rb), 9, np.uint8)
+        dep_o = oc.get(q, 3, out_o)
+        assert np.array_equal(dep_g.cpu().numpy(), dep_o)
+        assert np.array_equal(out_g.cpu().numpy(), out_o)
+        assert gc.status() == (0, len(oc.store))
+
+
 def test_cache_owner_and_range_errors():
     gc, oc = _cache_pair(10, 64, rank=1, world=4)
     rows = torch.zeros((4, 64), dtype=torch.uint8, device="cuda")

@@ -15,6 +15,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
+    "rs_bf16_u4": "-DAF_U_RS_VEC_BF16=4",
+    "rs_bf16_u16": "-DAF_U_RS_VEC_BF16=16",
+    "rs_end_bf16_u2": "-DAF_U_RS_VEC_END_BF16=2",
     "fin3": "-DAF_FIN_WIDE=3",
     "fin3_512": "-DAF_FIN_WIDE=3 -DAF_FIN3_CHUNK=512",
     "fin3_min512": "-DAF_FIN_WIDE=3 -DAF_FIN3_MIN_TILES=512",
@@ -123,6 +126,8 @@ def main():
                                              if isinstance(v, dict)},
                               "adamw_gbs": (d.get("next1_fused_adamw") or {}).get("gbs"),
                               "rs_p1_gbs": (d.get("next1_fused_reduce_scatter_p1") or {}).get("gbs"),
+                              "rs_p1_end_gbs": ((d.get("next1_fused_reduce_scatter_p1") or {}).get("interval_end")
+                                                or {}).get("gbs"),
                               "clocks": d.get("clocks")}), flush=True)
     subprocess.run([sys.executable, os.path.join(ROOT, "paper_2102_01386_b200", "_build.py"), "--force"], cwd=ROOT, check=True)
 
