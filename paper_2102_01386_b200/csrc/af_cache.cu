@@ -219,7 +219,7 @@ __device__ void pump_spec(const Desc *descs, const int *hitdep, int m, unsigned 
     const uint32_t u = base + q;
     const int s = u % kStages;
     mbar_wait(&bars[s], (u / kStages) & 1u);
-    const bool st = hitdep[store_i] != kMiss;
+    const bool st = !gate || hitdep[store_i] != kMiss;  // put: warp 1 publishes no flags (and never a miss for an ok item)
     if (st) bulk_s2g(descs[store_i].dst, stage_buf + static_cast<size_t>(s) * kChunk, descs[store_i].bytes);
     store_i = next_ok(store_i + 1);
     if (loaded < n_ok) {
