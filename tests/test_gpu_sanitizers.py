@@ -1,0 +1,31 @@
+"""compute-sanitizer over every kernel family (tools/sanitize_probe.py: the
+streaming kernels in every mode, the finalize and decide, the AdamW and
+reduce-scatter fusions, in-process peer ranks, the direct-mapped, tiered and
+global caches): memcheck and racecheck must report 0 errors."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _sanitizer():
+    for c in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if c and os.path.exists(c):
+            return c
+    pytest.fail("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_sanitizer_clean(tool):
+    r = subprocess.run([_sanitizer(), "--tool", tool, "--error-exitcode", "3", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_probe.py")], cwd=ROOT, capture_output=True, text=True,
+                       timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-3000:]
+    assert "sanitize probe done" in out
+    assert "0 errors" in out, out[-3000:]

@@ -93,6 +93,21 @@ def main():
         c.get(ids, 3, out, dep)
         c.put(ids, rows, 3)
         c.stats()
+    # global (NEXT 4): two ranks' stores in one process, any id from any rank;
+    # get_async on a side stream
+    cs = [af.ActivationCache(100, 2048 + 16, rank=r, world=2) for r in range(2)]
+    for c in cs:
+        c.set_peers_local(cs)
+    ids = torch.from_numpy(np.random.default_rng(1).permutation(100)[:40]).cuda()
+    rows = torch.randint(0, 256, (40, 2048 + 16), dtype=torch.uint8, device="cuda")
+    out = torch.empty_like(rows)
+    dep = torch.empty(40, dtype=torch.int32, device="cuda")
+    cs[0].put_global(ids, rows, 2)
+    cs[1].get_global(ids, 3, out, dep)
+    s = torch.cuda.Stream()
+    c = af.ActivationCache(100, 2048 + 16)
+    c.put(ids, rows, 2)
+    c.get_async(ids, 2, out, dep, s)
     torch.cuda.synchronize()
     print("sanitize probe done")
 
