@@ -211,7 +211,10 @@ def run_ours(args, rank, world, local):
     which, dt = WORKLOADS[args.workload]
     lay = bert_layout(which)
     s_g = 2 if dt == "bf16" else 4
-    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, rank=rank, world=world, device=dev)
+    # N > 1: shards of the active suffix, re-split per boundary f (the ZeRO form owns
+    # per-shard optimizer state and keeps static shards)
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, rank=rank, world=world, device=dev,
+                           shard_active=(world > 1 and not args.zero))
     exchange = "none"
     if world > 1:
         # NVLink one-shot exchange inside the interval-end kernel (CUDA IPC peer
@@ -334,7 +337,8 @@ def run_ours(args, rank, world, local):
             dist.barrier()
     ms_local = t0.elapsed_time(t1)
     dist_ms = step_distribution(args, run, stream, world, dist, dev)
-    frozen = None if args.zero else frozen_point(args, fm, lay, info, s_g, B, run, stream, world, dist, dev)
+    frozen = None if args.zero else frozen_point(args, fm, lay, info, s_g, B, run, stream, world, dist, dev,
+                                                 grads[0])
     marg = step_marginals(args, graphs, step, stream, world, dist) if graphs else None
     cache_marg = marg["cache"] if marg else None
     # per-phase breakdown: a second, eagerly launched pass with CUDA events between calls
@@ -385,6 +389,8 @@ def run_ours(args, rank, world, local):
                    "cache": {"examples": NUM_EXAMPLES, "row_bytes": ROW_BYTES, "rows_per_rank_step": B},
                    "boundary_f": 0, "parallelism": (f"zero{world}" if args.zero else f"shard{world}"),
                    "exchange": exchange,
+                   "shards": ("active-suffix (re-split per boundary f)" if (world > 1 and not args.zero)
+                              else "static"),
                    "launch": "eager" if args.no_graph else "CUDA graph per step (8 graphs rotating id batches)",
                    "l2": "inputs larger than L2: each step streams >= 4 GB/rank through the 126 MB L2"},
         "grad_norm_decide_gbs": round(gn_dec, 1),
@@ -454,12 +460,14 @@ def step_distribution(args, run, stream, world, dist, dev, n=100):
     return {**{k: round(v, 5) for k, v in q.items()}, "samples": n}
 
 
-def frozen_point(args, fm, lay, info, s_g, B, run, stream, world, dist, dev):
+def frozen_point(args, fm, lay, info, s_g, B, run, stream, world, dist, dev, g):
     """The same step with the boundary at f = B/2 POOL blocks frozen (SURVEY.md
     §8(d): bytes scale with the active suffix; PRE is tied to the first POOL
     block).  f is patched into a state blob (af_get_state layout: magic, version,
     L, world, rank, T, f, ...); the step's graphs read f from device memory at
-    launch, so they replay unchanged.  The original state is restored after."""
+    launch, so they replay unchanged.  The original state is restored after.  A
+    committed accumulate after each change re-arms Delta (active-suffix shards
+    start a fresh sum when f moves).  Bytes: the active elements of ALL ranks."""
     import struct
 
     import torch
@@ -469,11 +477,13 @@ def frozen_point(args, fm, lay, info, s_g, B, run, stream, world, dist, dev):
     pool = [l for l, k in enumerate(lay.kinds) if k == SEG_POOL]
     assert len(pool) == info["n_pool"]
     act0 = lay.offsets[pool[f]]                       # segments before the (f+1)-th POOL block are frozen
-    sb, se = info["shard_begin"], info["shard_end"]
-    n_act = max(0, se - max(sb, act0))
+    sb, se = fm.shard_of(f)
+    n_act_local = max(0, se - max(sb, act0))
+    n_act = lay.n - act0                              # the shards cover [0, n): all ranks' active elements
     patched = bytearray(blob)
     struct.pack_into("<i", patched, 24, f)
     fm.set_state(bytes(patched))
+    fm.layer_norms(g)
     try:
         for i in range(args.warmup):
             run(i)
@@ -491,9 +501,12 @@ def frozen_point(args, fm, lay, info, s_g, B, run, stream, world, dist, dev):
             ms = max_over_ranks(ms, dev)
     finally:
         fm.set_state(blob)
+        fm.layer_norms(g)
+        torch.cuda.synchronize()
     by = algorithmic_bytes(n_act, s_g, B, ROW_BYTES)
-    step_bytes = sum(by.values()) * world
-    return {"boundary_f": f, "active_elements_local": n_act, "ms_per_step": round(ms, 5),
+    step_bytes = by["accumulate"] + by["grad_norm_decide"] + (by["cache_get"] + by["cache_put"]) * world
+    return {"boundary_f": f, "active_elements": n_act, "active_elements_local": n_act_local,
+            "ms_per_step": round(ms, 5),
             "gbs": round(step_bytes / (ms * 1e-3) / 1e9, 1),
             "note": "algorithmic bytes count active (unfrozen) elements only; GB/s on those bytes"}
 

@@ -115,6 +115,13 @@ typedef struct {
   double tie_rel_eps;      /* near-tie window, e.g. 1e-5 (north_star)                 */
   int32_t min_active;      /* skip the test below this many active POOL layers; >= 1 (default 2) */
   int32_t rank, world;     /* this process's shard of the flat buffer; world in [1, AF_MAX_WORLD] */
+  int32_t shard_active;    /* 0: static contiguous shards of [0, n).  1 (world > 1): each boundary f
+                              gets its own balanced shards of the ACTIVE suffix [A_f, n) (A_f = start
+                              of the first unfrozen segment), so no rank idles as the prefix freezes
+                              (SURVEY.md §8(e)); Delta is then a full-size n-element buffer indexed
+                              by element.  Valid for af_layer_norms / af_update_and_decide /
+                              af_interval_end; the AdamW and reduce-scatter fusions (which own
+                              per-shard optimizer state) need static shards (AF_ESTATE). */
 } af_config;
 
 /* The decision record of one interval (Alg. 1 output + the quantities that
@@ -136,10 +143,13 @@ typedef struct {
 typedef struct {
   int32_t n_segments, n_pool, rank, world;
   int64_t n_total;                  /* elements of the full flat buffer                  */
-  int64_t shard_begin, shard_end;   /* this rank's element range (multiples of 8 except n) */
-  int32_t n_tiles;                  /* segment-aligned tiles of the shard (interval-end kernels) */
+  int64_t shard_begin, shard_end;   /* this rank's element range at f = 0 (multiples of 8 except n;
+                                       af_ctx_shard_of for other f)  */
+  int32_t n_tiles;                  /* segment-aligned tiles of the shard (interval-end kernels;
+                                       active-suffix shards: the largest per-f table) */
   int32_t tile_elems;               /* their nominal size in elements                    */
-  int32_t first_tile_of_pool[AF_MAX_SEGMENTS + 1]; /* first active tile when f = j frozen */
+  int32_t first_tile_of_pool[AF_MAX_SEGMENTS + 1]; /* first active tile when f = j frozen (index
+                                       into the concatenated per-f tables when shard_active) */
   int32_t n_tiles_acc;              /* tiles of the accumulate kernel (finer, no partials) */
   int32_t tile_elems_acc;
   int32_t n_fin_ctas;               /* > 0: interval ends launch a second, wide finalize
@@ -167,6 +177,11 @@ AF_API af_status af_ctx_workspace_bytes(const af_ctx *ctx, size_t *accum_bytes, 
 
 /* Host only.  Fills *info. */
 AF_API af_status af_ctx_info(const af_ctx *ctx, af_info *info);
+
+/* Host only.  This rank's element range [*begin, *end) when f POOL blocks are
+ * frozen (0 <= f <= n_pool): the static shard for every f, or the active-suffix
+ * shard (af_config.shard_active).  AF_EINVAL for f out of range. */
+AF_API af_status af_ctx_shard_of(const af_ctx *ctx, int32_t f, int64_t *begin, int64_t *end);
 
 /* Synchronous.  Binds caller-allocated device buffers (256-byte aligned, sizes
  * from af_ctx_workspace_bytes, on the current device) and initialises the

@@ -32,7 +32,8 @@ class AfLayout(ctypes.Structure):
 
 class AfConfig(ctypes.Structure):
     _fields_ = [("percentile", c_double), ("pct_method", c_int), ("acc_mode", c_int),
-                ("tie_rel_eps", c_double), ("min_active", c_int32), ("rank", c_int32), ("world", c_int32)]
+                ("tie_rel_eps", c_double), ("min_active", c_int32), ("rank", c_int32), ("world", c_int32),
+                ("shard_active", c_int32)]
 
 
 class AfDecision(ctypes.Structure):
@@ -67,6 +68,7 @@ SIGNATURES = {
     "af_ctx_create": (c_int, [POINTER(AfLayout), POINTER(AfConfig), POINTER(c_void_p)]),
     "af_ctx_workspace_bytes": (c_int, [c_void_p, POINTER(c_size_t), POINTER(c_size_t)]),
     "af_ctx_info": (c_int, [c_void_p, POINTER(AfInfo)]),
+    "af_ctx_shard_of": (c_int, [c_void_p, c_int32, POINTER(c_int64), POINTER(c_int64)]),
     "af_ctx_bind": (c_int, [c_void_p, c_void_p, c_void_p]),
     "af_nccl_unique_id": (c_int, [c_void_p]),
     "af_ctx_set_comm": (c_int, [c_void_p, c_void_p]),

@@ -39,7 +39,7 @@ class FreezingModule:
 
     def __init__(self, offsets, kinds, grad_dtype="bf16", percentile=50.0, pct_method="linear",
                  acc_mode="delta", tie_rel_eps=1e-5, min_active=2, rank=0, world=1, device=None,
-                 bind=True):
+                 bind=True, shard_active=False):
         self.offsets = [int(o) for o in offsets]
         self.kinds = [int(k) for k in kinds]
         self.n_segments = len(self.kinds)
@@ -47,7 +47,7 @@ class FreezingModule:
         self._kinds = (ctypes.c_int32 * max(1, len(self.kinds)))(*self.kinds)
         lay = L.AfLayout(len(self.kinds), self._offs, self._kinds, _DTYPES[grad_dtype])
         cfg = L.AfConfig(float(percentile), _PCT[pct_method], _ACC[acc_mode], float(tie_rel_eps),
-                         int(min_active), int(rank), int(world))
+                         int(min_active), int(rank), int(world), 1 if shard_active else 0)
         h = c_void_p()
         check(lib.af_ctx_create(byref(lay), byref(cfg), byref(h)), "af_ctx_create")
         self._h = h
@@ -64,6 +64,12 @@ class FreezingModule:
             self.bind(device)
 
     # -- setup -------------------------------------------------------------------
+    def shard_of(self, f):
+        """This rank's element range [begin, end) with f POOL blocks frozen."""
+        b, e = ctypes.c_int64(), ctypes.c_int64()
+        check(lib.af_ctx_shard_of(self._h, int(f), byref(b), byref(e)), "af_ctx_shard_of")
+        return b.value, e.value
+
     def info(self):
         i = L.AfInfo()
         check(lib.af_ctx_info(self._h, byref(i)), "af_ctx_info")

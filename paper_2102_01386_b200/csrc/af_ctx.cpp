@@ -35,10 +35,13 @@ struct af_ctx {
   // partial per tile)
   struct TileSet {
     int tile_elems = 0;
-    std::vector<Tile> tiles;
-    std::vector<int32_t> seg_tile_begin, first_tile_of_f;
-    size_t o_tiles = 0, o_ftf = 0, o_stb = 0;
+    std::vector<Tile> tiles;  // static: one table; active-suffix: the per-f tables concatenated
+    std::vector<int32_t> seg_tile_begin, first_tile_of_f, tile_end_of_f;
+    int32_t max_tiles = 0;    // largest single table
+    size_t o_tiles = 0, o_ftf = 0, o_stb = 0, o_tef = 0;
   } ts[2];
+  bool active = false;                  // active-suffix shards (cfg.shard_active && world > 1)
+  std::vector<int64_t> sb_of_f, se_of_f;  // this rank's shard per boundary f
   // workspace
   size_t accum_bytes = 0, scratch_bytes = 0;
   size_t o_state = 0, o_sched = 0, o_pool = 0, o_part = 0, o_part2 = 0, o_chunk = 0, o_ssall = 0,
@@ -111,16 +114,32 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   c->dtype = layout->grad_dtype;
   c->cfg = *cfg;
   c->n = n;
-  // contiguous shard, bounds rounded down to multiples of 8 elements
-  auto bound_of = [&](int r) -> int64_t {
-    if (r <= 0) return 0;
-    if (r >= cfg->world) return n;
-    const unsigned __int128 x = static_cast<unsigned __int128>(n) * static_cast<unsigned>(r) / cfg->world;
-    return static_cast<int64_t>(x) / kShardAlign * kShardAlign;
+  // contiguous shards, bounds rounded down to multiples of 8 elements:
+  // of [0, n) for every f (static), or of the active suffix [A_f, n) per boundary f
+  // (shard_active: A_f = start of the first segment not frozen at f -- PRE and
+  // POOL[0..f) are frozen, P:402 / Q11)
+  c->active = cfg->shard_active != 0 && cfg->world > 1;
+  auto first_seg_of = [&](int j) -> int {
+    if (j == 0) return 0;
+    return (j < n_pool) ? c->pool_seg[j] : c->pool_seg[n_pool - 1] + 1;
   };
-  c->sb = bound_of(cfg->rank);
-  c->se = bound_of(cfg->rank + 1);
-  // segment-aligned tile tables of the shard (tile edges on a global grid of tile_elems)
+  auto bound_in = [&](int64_t A, int r) -> int64_t {
+    if (r <= 0) return A;
+    if (r >= cfg->world) return n;
+    const unsigned __int128 x = static_cast<unsigned __int128>(n - A) * static_cast<unsigned>(r) / cfg->world;
+    const int64_t b = (A + static_cast<int64_t>(x)) / kShardAlign * kShardAlign;
+    return b < A ? A : b;
+  };
+  c->sb_of_f.assign(n_pool + 1, 0);
+  c->se_of_f.assign(n_pool + 1, n);
+  for (int j = 0; j <= n_pool; ++j) {
+    const int64_t A = c->active ? c->offs[first_seg_of(j)] : 0;
+    c->sb_of_f[j] = bound_in(A, cfg->rank);
+    c->se_of_f[j] = bound_in(A, cfg->rank + 1);
+  }
+  c->sb = c->sb_of_f[0];
+  c->se = c->se_of_f[0];
+  // segment-aligned tile tables (tile edges on a global grid of tile_elems)
   const bool bf16 = (c->dtype == AF_DT_BF16);
   c->ts[0].tile_elems = bf16 ? AF_TILE_ACC_BF16 : AF_TILE_ACC_F32;
   c->ts[1].tile_elems = (cfg->acc_mode == AF_ACC_STEP_SUMSQ) ? (bf16 ? AF_TILE_SSQ_BF16 : AF_TILE_SSQ_F32)
@@ -129,41 +148,53 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   // AF_TILE_BIG_FRAC_PCT % of the shard (fewer fp64 partials for the last CTA to
   // sum), nominal size in the tail (balanced finish).  Fixed at create, so the
   // partials and their summation order stay deterministic.
-  const int64_t big_until = c->sb + (c->se - c->sb) / 100 * AF_TILE_BIG_FRAC_PCT;
   for (int k = 0; k < 2; ++k) {
     auto &T = c->ts[k];
     const int64_t TE = T.tile_elems;
-    const int64_t TB = (k == 1) ? TE * AF_TILE_BIG_MULT : TE;
-    T.seg_tile_begin.assign(L + 1, 0);
-    for (int l = 0; l < L; ++l) {
-      T.seg_tile_begin[l] = static_cast<int32_t>(T.tiles.size());
-      const int64_t lo = std::max(c->offs[l], c->sb), hi = std::min(c->offs[l + 1], c->se);
-      for (int64_t pos = lo; pos < hi;) {
-        const int64_t te = (pos < big_until) ? TB : TE;
-        const int64_t nxt = std::min(hi, (pos / te + 1) * te);
-        T.tiles.push_back(Tile{pos, nxt, l, 0, 0, 0});
-        pos = nxt;
-      }
-      if (T.tiles.size() > static_cast<size_t>(1) << 30) {
-        delete c;
-        return fail(AF_ERANGE, "too many tiles");
-      }
-    }
-    T.seg_tile_begin[L] = static_cast<int32_t>(T.tiles.size());
-    for (auto &t : T.tiles) {
-      t.seg_first = T.seg_tile_begin[t.seg];
-      t.seg_end = T.seg_tile_begin[t.seg + 1];
-    }
-    // first active tile when j POOL layers are frozen: PRE and POOL[0..j) skipped (Q11)
+    const int n_tab = c->active ? n_pool + 1 : 1;
     T.first_tile_of_f.assign(n_pool + 1, 0);
-    for (int j = 0; j <= n_pool; ++j) {
-      int first_seg = 0;
-      if (j > 0) first_seg = (j < n_pool) ? c->pool_seg[j] : c->pool_seg[n_pool - 1] + 1;
-      T.first_tile_of_f[j] = T.seg_tile_begin[first_seg];
+    T.tile_end_of_f.assign(n_pool + 1, 0);
+    T.seg_tile_begin.assign(static_cast<size_t>(n_tab) * (L + 1), 0);
+    for (int q = 0; q < n_tab; ++q) {
+      const int64_t sb = c->sb_of_f[q], se = c->se_of_f[q];
+      const int64_t big_until = sb + (se - sb) / 100 * AF_TILE_BIG_FRAC_PCT;
+      const int64_t TB = (k == 1) ? TE * AF_TILE_BIG_MULT : TE;
+      int32_t *stb = T.seg_tile_begin.data() + static_cast<size_t>(q) * (L + 1);
+      const int32_t t0 = static_cast<int32_t>(T.tiles.size());
+      for (int l = 0; l < L; ++l) {
+        stb[l] = static_cast<int32_t>(T.tiles.size());
+        const int64_t lo = std::max(c->offs[l], sb), hi = std::min(c->offs[l + 1], se);
+        for (int64_t pos = lo; pos < hi;) {
+          const int64_t te = (pos < big_until) ? TB : TE;
+          const int64_t nxt = std::min(hi, (pos / te + 1) * te);
+          T.tiles.push_back(Tile{pos, nxt, l, stb[l], 0, 0});
+          pos = nxt;
+        }
+        if (T.tiles.size() > static_cast<size_t>(1) << 30) {
+          delete c;
+          return fail(AF_ERANGE, "too many tiles");
+        }
+      }
+      stb[L] = static_cast<int32_t>(T.tiles.size());
+      for (size_t t = static_cast<size_t>(t0); t < T.tiles.size(); ++t) T.tiles[t].seg_end = stb[T.tiles[t].seg + 1];
+      T.max_tiles = std::max(T.max_tiles, stb[L] - t0);
+      if (c->active) {
+        // table q holds exactly the tiles active at f = q
+        T.first_tile_of_f[q] = t0;
+        T.tile_end_of_f[q] = stb[L];
+      } else {
+        // first active tile when j POOL layers are frozen: PRE and POOL[0..j) skipped (Q11)
+        for (int j = 0; j <= n_pool; ++j) {
+          T.first_tile_of_f[j] = stb[first_seg_of(j)];
+          T.tile_end_of_f[j] = stb[L];
+        }
+      }
     }
   }
   // workspace layout
-  const int64_t n_local = c->se - c->sb;
+  // Delta: the shard (static), or the whole buffer indexed by element (active-suffix
+  // shards move with f; n x 4 B is small against 180 GB of HBM)
+  const int64_t n_local = c->active ? n : c->se - c->sb;
   c->accum_bytes = (cfg->acc_mode == AF_ACC_DELTA) ? static_cast<size_t>(n_local) * sizeof(float) : 0;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -189,12 +220,13 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   c->o_pool = take(n_pool * sizeof(int32_t));
   for (auto &T : c->ts) {
     T.o_ftf = take((n_pool + 1) * sizeof(int32_t));
-    T.o_stb = take((L + 1) * sizeof(int32_t));
+    T.o_tef = take((n_pool + 1) * sizeof(int32_t));
+    T.o_stb = take(T.seg_tile_begin.size() * sizeof(int32_t));
     T.o_tiles = take(T.tiles.size() * sizeof(Tile));
   }
   c->o_part = take(c->ts[1].tiles.size() * sizeof(double));
-  c->o_part2 = take((c->ts[1].tiles.size() / kFinChunkMin + L + 2) * sizeof(double));
-  c->o_chunk = take((c->ts[1].tiles.size() / kFinChunk + 2) * sizeof(unsigned int));
+  c->o_part2 = take((static_cast<size_t>(c->ts[1].max_tiles) / kFinChunkMin + L + 2) * sizeof(double));
+  c->o_chunk = take((static_cast<size_t>(c->ts[1].max_tiles) / kFinChunk + 2) * sizeof(unsigned int));
   c->scratch_bytes = o;
   *out = c;
   return AF_OK;
@@ -217,14 +249,21 @@ af_status af_ctx_info(const af_ctx *c, af_info *info) {
   info->n_total = c->n;
   info->shard_begin = c->sb;
   info->shard_end = c->se;
-  info->n_tiles = static_cast<int32_t>(c->ts[1].tiles.size());
+  info->n_tiles = c->ts[1].max_tiles;
   info->tile_elems = c->ts[1].tile_elems;
-  info->n_tiles_acc = static_cast<int32_t>(c->ts[0].tiles.size());
+  info->n_tiles_acc = c->ts[0].max_tiles;
   info->tile_elems_acc = c->ts[0].tile_elems;
-  info->n_fin_chunks = af::fin_ctas(c->cfg.acc_mode == AF_ACC_DELTA ? kEndDelta : kStepSq,
-                                    static_cast<int>(c->ts[1].tiles.size()));
+  info->n_fin_chunks = af::fin_ctas(c->cfg.acc_mode == AF_ACC_DELTA ? kEndDelta : kStepSq, c->ts[1].max_tiles);
   info->n_fin_ctas = AF_FIN_WIDE == 1 ? info->n_fin_chunks : 0;
   for (int j = 0; j <= c->n_pool; ++j) info->first_tile_of_pool[j] = c->ts[1].first_tile_of_f[j];
+  return AF_OK;
+}
+
+af_status af_ctx_shard_of(const af_ctx *c, int32_t f, int64_t *begin, int64_t *end) {
+  if (!c || !begin || !end) return fail(AF_EINVAL, "NULL argument");
+  if (f < 0 || f > c->n_pool) return fail(AF_EINVAL, "f out of [0, n_pool]");
+  *begin = c->sb_of_f[f];
+  *end = c->se_of_f[f];
   return AF_OK;
 }
 
@@ -241,7 +280,7 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes (kernel preload)");
   for (int m = 0; m < kNumModes; ++m) {
     int bps = 0;
-    e = static_cast<cudaError_t>(norms_max_blocks_per_sm(m, c->dtype, c->cfg.world, &bps));
+    e = static_cast<cudaError_t>(norms_max_blocks_per_sm(m, c->dtype, c->cfg.world, &bps, c->active));
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     c->grid[m] = std::max(1, sms * std::max(1, bps));
   }
@@ -256,6 +295,9 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
     AF_CUDA(cudaMemcpy(c->scratch + T.o_ftf, T.first_tile_of_f.data(), T.first_tile_of_f.size() * 4,
                        cudaMemcpyHostToDevice),
             "cudaMemcpy(first_tile_of_f)");
+    AF_CUDA(cudaMemcpy(c->scratch + T.o_tef, T.tile_end_of_f.data(), T.tile_end_of_f.size() * 4,
+                       cudaMemcpyHostToDevice),
+            "cudaMemcpy(tile_end_of_f)");
     AF_CUDA(cudaMemcpy(c->scratch + T.o_stb, T.seg_tile_begin.data(), T.seg_tile_begin.size() * 4,
                        cudaMemcpyHostToDevice),
             "cudaMemcpy(seg_tile_begin)");
@@ -314,12 +356,14 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   const auto &T = c->ts[k];
   p.grad = grad_dev;
   p.delta = c->accum;
-  p.shard_begin = c->sb;
+  p.shard_begin = c->active ? 0 : c->sb;  // active-suffix shards: Delta indexed by element
   p.tiles = c->at<Tile>(T.o_tiles);
-  p.n_tiles = static_cast<int32_t>(T.tiles.size());
+  p.n_tiles = T.max_tiles;
   p.L = c->L;
   p.first_tile_of_f = c->at<int32_t>(T.o_ftf);
+  p.tile_end_of_f = c->at<int32_t>(T.o_tef);
   p.seg_tile_begin = c->at<int32_t>(T.o_stb);
+  p.stb_stride = c->active ? c->L + 1 : 0;
   p.state = c->at<DevState>(c->o_state);
   p.sched = c->at<Sched>(c->o_sched) + k;
   p.partials = c->at<double>(c->o_part);
@@ -465,6 +509,7 @@ extern "C" {
 af_status af_adamw_step(af_ctx *c, float *params_dev, float *exp_avg_dev, float *exp_avg_sq_dev,
                         const void *grad_dev, const af_adamw *hp, uint32_t flags, af_decision *out_host,
                         void *stream) {
+  if (c && c->active) return fail(AF_ESTATE, "af_adamw_step needs static shards (shard_active = 0)");
   af_status st = check_norm_args(c, grad_dev);
   if (st != AF_OK) return st;
   st = check_adam(hp, params_dev, exp_avg_dev, exp_avg_sq_dev);
@@ -729,6 +774,7 @@ static af_status rs_step(af_ctx *c, float scale, float *grad_shard_out_dev, cons
                          float *exp_avg_dev, float *exp_avg_sq_dev, uint32_t flags, af_decision *out_host,
                          void *stream) {
   if (!c) return fail(AF_EINVAL, "NULL ctx");
+  if (c->active) return fail(AF_ESTATE, "af_reduce_scatter_step needs static shards (shard_active = 0)");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   if (!c->grad_peers) return fail(AF_ESTATE, "no gradient buffers registered (af_ctx_set_grad_peers_*)");
   if (c->cfg.acc_mode != AF_ACC_DELTA) return fail(AF_ESTATE, "af_reduce_scatter_step needs acc_mode AF_ACC_DELTA");
@@ -835,6 +881,9 @@ af_status af_set_state(af_ctx *c, const void *buf, size_t len) {
   // keep the peer-exchange epoch: it counts interval ends on every rank and the
   // peers' flag words already hold it
   AF_CUDA(cudaMemcpy(&st, c->scratch + c->o_state, sizeof(st), cudaMemcpyDeviceToHost), "cudaMemcpy(state)");
+  // active-suffix shards: Delta's elements belong to the shard of the f it was
+  // accumulated under; a different f starts a fresh interval sum
+  const bool moved = c->active && st.f != b.f;
   st.sticky = 0;
   st.T = b.T;
   st.f = b.f;
@@ -843,7 +892,7 @@ af_status af_set_state(af_ctx *c, const void *buf, size_t len) {
   AF_CUDA(cudaMemcpy(c->scratch + c->o_ssacc, b.ss_acc, c->L * sizeof(double), cudaMemcpyHostToDevice),
           "cudaMemcpy(ss_acc)");
   AF_CUDA(cudaDeviceSynchronize(), "set_state sync");
-  c->armed = b.armed != 0;
+  c->armed = b.armed != 0 && !moved;
   c->pending = false;
   return AF_OK;
 }

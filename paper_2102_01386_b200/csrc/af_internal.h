@@ -122,10 +122,12 @@ struct NormParams {
   float *delta;              // Delta shard base: element i lives at delta[i - shard_begin]
   int64_t shard_begin;
   const Tile *tiles;
-  int32_t n_tiles;
+  int32_t n_tiles;                 // host: the largest table (grid and finalize sizing)
   int32_t L;
-  const int32_t *first_tile_of_f;  // [n_pool + 1]
-  const int32_t *seg_tile_begin;   // [L + 1]
+  const int32_t *first_tile_of_f;  // [n_pool + 1] first active tile for boundary f
+  const int32_t *tile_end_of_f;    // [n_pool + 1] end of f's table (n_tiles for static shards)
+  const int32_t *seg_tile_begin;   // [L + 1] per table; table f's at + f * stb_stride
+  int32_t stb_stride;              // 0: one table (static shards); L + 1: one per f (active-suffix shards)
   const DevState *state;           // reads f
   Sched *sched;
   double *partials;                // [n_tiles]
@@ -280,7 +282,7 @@ int launch_decide(const DecideParams &p, void *stream);
 int launch_cache_put(const CacheParams &p, int grid, void *stream);
 int launch_cache_get(const CacheParams &p, int grid, void *stream);
 int launch_cache_plan(const CachePlanParams &p, void *stream);
-int norms_max_blocks_per_sm(int mode, int grad_dtype, int world, int *blocks);
+int norms_max_blocks_per_sm(int mode, int grad_dtype, int world, int *blocks, bool act = false);
 // force-load the kernels (lazy module loading must not happen while peers spin)
 int preload_norm_kernels(int grad_dtype, int world);
 int preload_decide_kernel();

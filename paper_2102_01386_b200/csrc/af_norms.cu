@@ -544,8 +544,22 @@ __device__ __forceinline__ double warp_sum(double v) {
 // The last CTA's work after the grid has drained: per-segment sums, the optional
 // NVLink one-shot exchange and the fused decision.  Not inlined, so its
 // registers do not raise the streaming loop's (occupancy) budget.
-template <int MODE, bool WIDE>
-__device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) {
+// ACT (active-suffix shards, af_config.shard_active): one tile table per boundary
+// f -- table f is tiles [first_tile_of_f[f], tile_end_of_f[f]) with its own
+// per-segment ranges at seg_tile_begin + f * (L + 1).  Static shards (ACT false)
+// compile to the single-table code: end = n_tiles, one segment-range array.
+template <bool ACT>
+__device__ __forceinline__ const int32_t *seg_ranges(const NormParams &p, int f) {
+  return ACT ? p.seg_tile_begin + static_cast<size_t>(f) * p.stb_stride : p.seg_tile_begin;
+}
+template <bool ACT>
+__device__ __forceinline__ int table_end(const NormParams &p, int f) {
+  return ACT ? p.tile_end_of_f[f] : p.n_tiles;
+}
+
+template <int MODE, bool WIDE, bool ACT>
+__device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, int f) {
+  const int32_t *stb = seg_ranges<ACT>(p, f);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (AF_TIMING && !WIDE && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
   // peer exchange: this interval end's epoch selects the exchange buffer
@@ -578,9 +592,9 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) 
     // pieces of l sit at part2[c + l]; summed in chunk order
     const int CH = p.fin_chunk;
     for (int l = tid; l < p.L; l += kNormBlock) {
-      int tb = p.seg_tile_begin[l];
+      int tb = stb[l];
       tb = tb < first_tile ? first_tile : tb;
-      const int te = p.seg_tile_begin[l + 1];
+      const int te = stb[l + 1];
       double s = 0.0;
       if (te > tb) {
         const int c_lo = (tb - first_tile) / CH, c_hi = (te - 1 - first_tile) / CH;
@@ -591,9 +605,9 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) 
     }
   } else {
     for (int l = warp; l < p.L && warp < kNormBlock / 32; l += kNormBlock / 32) {
-      int tb = p.seg_tile_begin[l];
+      int tb = stb[l];
       tb = tb < first_tile ? first_tile : tb;
-      const int te = p.seg_tile_begin[l + 1];
+      const int te = stb[l + 1];
       double s = 0.0;
 #pragma unroll 8
       for (int k = tb + lane; k < te; k += 32) s += __ldcg(p.partials + k);
@@ -651,8 +665,8 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile) 
   }
 }
 
-template <int CH>
-__device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int c, double *s_p);
+template <int CH, bool ACT>
+__device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int f, int c, double *s_p);
 
 // AF_FIN_WIDE == 3.  `ticket` = this CTA's place in the grid's retirement order.
 // The last W = min(chunks, grid) CTAs to retire become workers: each waits until
@@ -664,10 +678,11 @@ __device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, i
 // deadlock: the scheduler is drained, so every CTA not yet retired is resident
 // or starts, finds no tile and retires, in a slot a retired non-worker freed (or
 // its own: the grid is sized to the device's co-resident limit).
-__device__ __noinline__ bool retire_finalize(const NormParams &p, int first_tile, int ticket, double *s_p) {
+template <bool ACT>
+__device__ __noinline__ bool retire_finalize(const NormParams &p, int first_tile, int f, int ticket, double *s_p) {
   const int tid = threadIdx.x;
   const int G = static_cast<int>(gridDim.x);
-  const int nch = (p.n_tiles - first_tile + kFin3Chunk - 1) / kFin3Chunk;
+  const int nch = (table_end<ACT>(p, f) - first_tile + kFin3Chunk - 1) / kFin3Chunk;
   const int W = nch < G ? nch : G;
   const int w = ticket - (G - W);
   if (nch <= 0) return ticket == G - 1;  // no active tile: the last CTA carries on
@@ -683,7 +698,7 @@ __device__ __noinline__ bool retire_finalize(const NormParams &p, int first_tile
     if (AF_TIMING && ticket == G - 1) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
   }
   __syncthreads();
-  for (int c = w; c < nch; c += W) chunk_reduce<kFin3Chunk>(p, first_tile, c, s_p);
+  for (int c = w; c < nch; c += W) chunk_reduce<kFin3Chunk, ACT>(p, first_tile, f, c, s_p);
   if (tid == 0) {
     __threadfence();
     s_fin_last = atomicAdd(&p.fin_sched->done, 1u) == static_cast<unsigned int>(W - 1);
@@ -695,7 +710,7 @@ __device__ __noinline__ bool retire_finalize(const NormParams &p, int first_tile
   return true;
 }
 
-template <int MODE, typename GT, bool RD, int PM = 1>
+template <int MODE, typename GT, bool RD, int PM = 1, bool ACT = false>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccum)
                                   ? 2
                                   : ((MODE >= kAdamAccum) ? 1 : AF_MINB_END))
@@ -718,6 +733,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
   int f = p.state->f;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int first_tile = p.first_tile_of_f[f];
+  const int n_end = table_end<ACT>(p, f);  // static: the constant n_tiles
   const GT *rs_g[PM];
   if constexpr (RS) {
 #pragma unroll
@@ -738,29 +754,29 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
   // previous kernel's last ~100 MB (Delta written back, g just read) in the
   // 126 MB L2.  The order never changes a result: every tile's partial has a fixed
   // reduction tree and the segments are summed in tile-index order.
-  const int n_act_tiles = p.n_tiles - first_tile;
+  const int n_act_tiles = n_end - first_tile;
   auto tile_of = [&](unsigned int k) -> int {
     const int kk = static_cast<int>(k);
-    if (kk >= n_act_tiles) return p.n_tiles;  // past the end: the loop's stop value
-    return p.reverse ? p.n_tiles - 1 - kk : first_tile + kk;
+    if (kk >= n_act_tiles) return n_end;  // past the end: the loop's stop value
+    return p.reverse ? n_end - 1 - kk : first_tile + kk;
   };
   if (tid == 0) {
     const int t0 = tile_of(atomicAdd(&p.sched->next, 1u));
     s_tile[0] = t0;
-    if (t0 < p.n_tiles) s_desc[0] = p.tiles[t0];
+    if (t0 < n_end) s_desc[0] = p.tiles[t0];
     s_tile[1] = tile_of(atomicAdd(&p.sched->next, 1u));
   }
   __syncthreads();
   for (int it = 0;; ++it) {
     const int slot = it % 3, slot1 = (it + 1) % 3, slot2 = (it + 2) % 3;
     const int tile = s_tile[slot];
-    if (tile >= p.n_tiles) break;
+    if (tile >= n_end) break;
     const Tile t = s_desc[slot];
     int next2 = 0;
     if (tid == 0) {
       next2 = tile_of(atomicAdd(&p.sched->next, 1u));
       const int n1 = s_tile[slot1];
-      if (n1 < p.n_tiles) {
+      if (n1 < n_end) {
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_desc[slot1]));
         const Tile *src = p.tiles + n1;
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -795,7 +811,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
           // count the chunk's finished tiles; the CTA finishing its last one reduces it
           __threadfence();
           const int c = (tile - first_tile) / kFinChunk;
-          const int nc = min(kFinChunk, p.n_tiles - first_tile - c * kFinChunk);
+          const int nc = min(kFinChunk, n_end - first_tile - c * kFinChunk);
           s_chunk = (atomicAdd(p.chunk_cnt + c, 1u) == static_cast<unsigned>(nc - 1)) ? c : -1;
         }
       }
@@ -805,7 +821,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
       if (p.wide_fin == 2) {
         const int c = s_chunk;
         if (c >= 0) {
-          chunk_reduce<kFinChunk>(p, first_tile, c, s_fin);
+          chunk_reduce<kFinChunk, ACT>(p, first_tile, f, c, s_fin);
           if (tid == 0) p.chunk_cnt[c] = 0u;  // every tile of the chunk has counted: reset for the next launch
         }
       }
@@ -827,7 +843,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
     // the last W CTAs to retire wait for the grid to drain, reduce the chunks of
     // partials in parallel, and the last of them continues as "the last CTA"
     if (p.wide_fin == 3) {
-      if (!retire_finalize(p, first_tile, s_chunk, s_fin)) return;
+      if (!retire_finalize<ACT>(p, first_tile, f, s_chunk, s_fin)) return;
       s_last = 1;  // (uniform: every thread of this CTA took the same branch)
     }
   }
@@ -851,10 +867,10 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
   }
   if (p.wide_fin >= 2) {  // every chunk already reduced: combine the pieces
     if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
-    last_cta_tail<TM, true>(p, first_tile);
+    last_cta_tail<TM, true, ACT>(p, first_tile, ACT ? f : 0);
     return;
   }
-  last_cta_tail<TM, false>(p, first_tile);
+  last_cta_tail<TM, false, ACT>(p, first_tile, ACT ? f : 0);
 }
 
 // Chunk c of the wide finalize (n_tiles > kFinChunk): the fp64 partials of tiles
@@ -863,13 +879,15 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
 // reduced by one warp (lane-strided, xor tree) into part2[c + l] -- piece (c, l)
 // is the (c + l)-th piece in tile order, so the index needs no search.  Every
 // thread of the CTA calls it.  Fixed order: deterministic.
-template <int CH>
-__device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int c, double *s_p) {
+template <int CH, bool ACT>
+__device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int f, int c, double *s_p) {
+  const int32_t *stb = seg_ranges<ACT>(p, f);
+  const int tile_end = table_end<ACT>(p, f);
   static_assert(CH % kNormBlock == 0, "chunk = whole loads per thread");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c0 = first_tile + c * CH;
-  if (c0 >= p.n_tiles) return;  // uniform over the CTA
-  const int n = min(CH, p.n_tiles - c0);
+  if (c0 >= tile_end) return;  // uniform over the CTA
+  const int n = min(CH, tile_end - c0);
 #pragma unroll
   for (int u = 0; u < CH / kNormBlock; ++u) {
     const int k = u * kNormBlock + tid;
@@ -878,7 +896,7 @@ __device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, i
   const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
   __syncthreads();
   for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {
-    int a = p.seg_tile_begin[l], b = p.seg_tile_begin[l + 1];
+    int a = stb[l], b = stb[l + 1];
     a = (a < c0 ? c0 : a) - c0;
     b = (b > c0 + n ? c0 + n : b) - c0;
     double s = 0.0;
@@ -896,7 +914,7 @@ __device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, i
 // Wide finalize as a second launch (AF_FIN_WIDE == 1): CTA c reduces chunk c and
 // the grid's last CTA combines the pieces of each segment in chunk order, then
 // exchanges and decides as the streaming kernel's last CTA would.
-template <int MODE>
+template <int MODE, bool ACT>
 __global__ void __launch_bounds__(kNormBlock) fin_kernel(const NormParams p) {
   __shared__ double s_p[kFinChunk];
   __shared__ int s_last;
@@ -905,7 +923,7 @@ __global__ void __launch_bounds__(kNormBlock) fin_kernel(const NormParams p) {
   int f = p.state->f;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int first_tile = p.first_tile_of_f[f];
-  chunk_reduce<kFinChunk>(p, first_tile, blockIdx.x, s_p);
+  chunk_reduce<kFinChunk, ACT>(p, first_tile, f, blockIdx.x, s_p);
   pdl_launch_dependents();
   if (tid == 0) {
     __threadfence();
@@ -916,7 +934,7 @@ __global__ void __launch_bounds__(kNormBlock) fin_kernel(const NormParams p) {
   if (!s_last) return;
   __threadfence();
   if (tid == 0) p.fin_sched->done = 0;
-  last_cta_tail<MODE, true>(p, first_tile);
+  last_cta_tail<MODE, true, ACT>(p, first_tile, ACT ? f : 0);
 }
 
 
@@ -1154,7 +1172,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) norms_tma_kernel(const NormPar
     p.sched->done = 0;
   }
   if (MODE == kAccum) return;
-  last_cta_tail<kEndDelta, false>(p, first_tile);
+  last_cta_tail<kEndDelta, false, false>(p, first_tile, 0);
 }
 
 template <int MODE, typename GT, bool RD>
@@ -1185,9 +1203,22 @@ NormKernel rs_kernel(int mode, bool rd) {
 
 int pm_of(int world) { return world <= 1 ? 1 : (world == 2 ? 2 : (world <= 4 ? 4 : 8)); }
 
-// The streaming kernel instantiation of (mode, Delta read, world).
+// The streaming kernel instantiation of (mode, Delta read, world, active-suffix
+// tables).  Active-suffix tables exist for the replicated-gradient modes only.
 template <typename GT>
-NormKernel kernel_for(int mode, bool rd, int world) {
+NormKernel kernel_for(int mode, bool rd, int world, bool act = false) {
+#ifdef AF_NO_ACT  // diagnostic build: no active-suffix instantiations
+  act = false;
+#endif
+  if (act) {
+    switch (mode) {
+      case kAccum: return rd ? norms_kernel<kAccum, GT, true, 1, true> : norms_kernel<kAccum, GT, false, 1, true>;
+      case kEndDelta:
+        return rd ? norms_kernel<kEndDelta, GT, true, 1, true> : norms_kernel<kEndDelta, GT, false, 1, true>;
+      case kStepSq: return norms_kernel<kStepSq, GT, false, 1, true>;
+      default: break;  // refused by the host (static shards only)
+    }
+  }
   switch (mode) {
     case kAccum: return rd_pick<kAccum, GT, 1>(rd);
     case kEndDelta: return rd_pick<kEndDelta, GT, 1>(rd);
@@ -1207,12 +1238,13 @@ NormKernel kernel_for(int mode, bool rd, int world) {
 template <typename GT>
 int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
   const bool rd = !p.first;
-  if (mode == kAccum && AF_TMA >= 2)
+  if (mode == kAccum && AF_TMA >= 2 && p.stb_stride == 0)  // the TMA-staged variants: static tables only
     return rd ? launch_tma<kAccum, GT, true>(p, grid, stream) : launch_tma<kAccum, GT, false>(p, grid, stream);
-  if (mode == kEndDelta && AF_TMA >= 1)
+  if (mode == kEndDelta && AF_TMA >= 1 && p.stb_stride == 0)
     return rd ? launch_tma<kEndDelta, GT, true>(p, grid, stream) : launch_tma<kEndDelta, GT, false>(p, grid, stream);
   if (mode < 0 || mode >= kNumModes) return static_cast<int>(cudaErrorInvalidValue);
-  return static_cast<int>(launch_pdl(kernel_for<GT>(mode, rd, p.rs_world), dim3(grid), dim3(kNormBlock), 0,
+  return static_cast<int>(launch_pdl(kernel_for<GT>(mode, rd, p.rs_world, p.stb_stride != 0), dim3(grid),
+                                     dim3(kNormBlock), 0,
                                      static_cast<cudaStream_t>(stream), p));
 }
 
@@ -1234,7 +1266,14 @@ int launch_norms(const NormParams &p_in, int mode, int grad_dtype, int grid, voi
   const int e = grad_dtype == AF_DT_BF16 ? launch_dt<uint16_t>(p, mode, grid, stream)
                                          : launch_dt<float>(p, mode, grid, stream);
   if (e != 0 || !nfin || AF_FIN_WIDE != 1) return e;
-  auto *fk = mode == kStepSq ? fin_kernel<kStepSq> : fin_kernel<kEndDelta>;
+  const bool act = p.stb_stride != 0;
+#ifdef AF_NO_ACT
+  auto *fk = mode == kStepSq ? fin_kernel<kStepSq, false> : fin_kernel<kEndDelta, false>;
+  (void)act;
+#else
+  auto *fk = mode == kStepSq ? (act ? fin_kernel<kStepSq, true> : fin_kernel<kStepSq, false>)
+                             : (act ? fin_kernel<kEndDelta, true> : fin_kernel<kEndDelta, false>);
+#endif
   return static_cast<int>(
       launch_pdl(fk, dim3(nfin), dim3(kNormBlock), 0, static_cast<cudaStream_t>(stream), p));
 }
@@ -1249,8 +1288,10 @@ static cudaError_t preload_dt(int world) {
   cudaFuncAttributes a;
   for (int m = 0; m < kNumModes; ++m)
     for (int rd = 0; rd < 2; ++rd) {
-      const cudaError_t e = cudaFuncGetAttributes(&a, kernel_for<GT>(m, rd != 0, world));
-      if (e != cudaSuccess) return e;
+      for (int act = 0; act < 2; ++act) {
+        const cudaError_t e = cudaFuncGetAttributes(&a, kernel_for<GT>(m, rd != 0, world, act != 0));
+        if (e != cudaSuccess) return e;
+      }
     }
   return cudaSuccess;
 }
@@ -1259,22 +1300,30 @@ int preload_norm_kernels(int grad_dtype, int world) {
   cudaError_t e = grad_dtype == AF_DT_BF16 ? preload_dt<uint16_t>(world) : preload_dt<float>(world);
   if (e != cudaSuccess) return static_cast<int>(e);
   cudaFuncAttributes a;
-  for (const void *k : {reinterpret_cast<const void *>(fin_kernel<kEndDelta>),
-                        reinterpret_cast<const void *>(fin_kernel<kStepSq>)}) {
+  for (const void *k : {reinterpret_cast<const void *>(fin_kernel<kEndDelta, false>),
+                        reinterpret_cast<const void *>(fin_kernel<kStepSq, false>),
+#ifndef AF_NO_ACT
+                        reinterpret_cast<const void *>(fin_kernel<kEndDelta, true>),
+                        reinterpret_cast<const void *>(fin_kernel<kStepSq, true>)
+#else
+                        reinterpret_cast<const void *>(fin_kernel<kStepSq, false>)
+#endif
+                       }) {
     e = cudaFuncGetAttributes(&a, k);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   return 0;
 }
 
-int norms_max_blocks_per_sm(int mode, int grad_dtype, int world, int *blocks) {
+int norms_max_blocks_per_sm(int mode, int grad_dtype, int world, int *blocks, bool act) {
   if ((mode == kEndDelta && AF_TMA >= 1) || (mode == kAccum && AF_TMA >= 2)) {
     *blocks = 1;  // the TMA-staged kernels run one CTA per SM
     return 0;
   }
-  NormKernel k = grad_dtype == AF_DT_BF16 ? kernel_for<uint16_t>(mode, true, world) : kernel_for<float>(mode, true, world);
-  if (mode == kStepSq) k = grad_dtype == AF_DT_BF16 ? kernel_for<uint16_t>(mode, false, world)
-                                                   : kernel_for<float>(mode, false, world);
+  NormKernel k = grad_dtype == AF_DT_BF16 ? kernel_for<uint16_t>(mode, true, world, act)
+                                         : kernel_for<float>(mode, true, world, act);
+  if (mode == kStepSq) k = grad_dtype == AF_DT_BF16 ? kernel_for<uint16_t>(mode, false, world, act)
+                                                   : kernel_for<float>(mode, false, world, act);
   return static_cast<int>(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, kNormBlock, 0));
 }
 

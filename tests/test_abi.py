@@ -145,6 +145,52 @@ def test_shards_cover_buffer_and_tiles_are_segment_aligned(which, dt, world):
     assert prev_end == lay.n
 
 
+@pytest.mark.parametrize("which,dt", [("base", "bf16"), ("large", "f32")])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_active_suffix_shards_balance_every_boundary(which, dt, world):
+    """shard_active: for every boundary f the ranks' shards tile the active suffix
+    [A_f, n) (A_f = start of the first unfrozen segment; PRE goes with block 0)
+    contiguously, balanced within one alignment unit; Delta is full size; the
+    largest per-f table is reported; the fused AdamW / reduce-scatter refuse."""
+    lay = bert_layout(which)
+    pool = [l for l, k in enumerate(lay.kinds) if k == 1]
+    fms = [af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, rank=r, world=world, bind=False,
+                             shard_active=True) for r in range(world)]
+    te = fms[0].info()["tile_elems"]
+    for f in range(len(pool) + 1):
+        A = lay.offsets[pool[f]] if f < len(pool) else lay.offsets[pool[-1] + 1]
+        if f == 0:
+            A = 0
+        prev = A
+        for fm in fms:
+            b, e = fm.shard_of(f)
+            assert b == prev and (b == A or b % 8 == 0)
+            assert abs((e - b) - (lay.n - A) / world) <= 8
+            prev = e
+        assert prev == lay.n
+    for r, fm in enumerate(fms):
+        i = fm.info()
+        assert (i["shard_begin"], i["shard_end"]) == fm.shard_of(0)
+        assert fm.accum_bytes == 4 * lay.n
+        assert i["n_tiles"] == max(_expected_tiles(lay, *fm.shard_of(f), te, 1, 85) for f in range(len(pool) + 1))
+        # the static shards are unchanged by the option at world 1
+    one = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, bind=False, shard_active=True)
+    assert one.shard_of(5) == (0, lay.n) and one.accum_bytes == 4 * lay.n
+    for fm in fms:
+        fm.close()
+
+
+def test_active_suffix_shards_refuse_fused_optimizer_paths():
+    lay = tiny_layout()
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="f32", rank=0, world=2, bind=False,
+                           shard_active=True)
+    import ctypes as C
+    hp = L.AfAdamW(1e-3, 0.9, 0.999, 1e-8, 0.0, 1)
+    assert L.lib.af_adamw_step(fm._h, None, None, None, None, C.byref(hp), 0, None, None) == L.AF_ESTATE
+    assert L.lib.af_reduce_scatter_step(fm._h, C.c_float(1.0), None, 0, None, None) == L.AF_ESTATE
+    fm.close()
+
+
 def test_first_tile_skips_embedding_with_first_block():
     lay = bert_layout("base")
     fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="bf16", bind=False)

@@ -1,6 +1,7 @@
 """GPU parity: the sm_100a path (through the C ABI) vs the fp64 oracle on the
 same seeded inputs.  Run on a B200 with `pytest -m gpu`."""
 import math
+import struct
 
 import numpy as np
 import pytest
@@ -501,6 +502,63 @@ def test_peer_exchange_ranks_on_one_gpu(P, fused):
     each other's memory inside the interval-end kernel; identical decisions on all
     ranks, oracle parity."""
     _run_peer_ranks(P, fused)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("fused", [True, False])
+def test_active_suffix_shards_follow_the_boundary(P, dt, fused):
+    """shard_active: every interval the ranks re-split the ACTIVE suffix for the
+    boundary f read on the device, so no rank idles as the prefix freezes.  P
+    in-process ranks (concurrent streams, in-kernel peer exchange), several steps
+    per interval: each rank's Delta over its current shard is bit-exact vs the
+    oracle, decisions are identical on all ranks and match the oracle, and the
+    boundary moves (so the shards do)."""
+    lay = _ragged_layout()
+    step = _decaying_step(lay, dt, 77)
+    fms = [_fm(lay, dt, rank=r, world=P, shard_active=True) for r in range(P)]
+    for fm in fms:
+        fm.set_peers_local(fms)
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    oz = _oracle(lay, dt)
+    f_seen = set()
+    for T in range(9):
+        f = fms[0].decision()["boundary_after"] if T > 0 else 0
+        if T in (4, 6):
+            # jump the boundary (a checkpoint restore at an interval boundary): every
+            # rank's shard moves to f's table; the oracle follows
+            f = min(lay.n_segments - 3, f + 2)
+            for fm in fms:
+                blob = bytearray(fm.get_state())
+                struct.pack_into("<i", blob, 24, f)
+                fm.set_state(bytes(blob))
+            oz.f = f
+        f_seen.add(f)
+        for t in range(3):
+            gnp = step(T, t)
+            g = to_device_grad(gnp, dt)
+            torch.cuda.synchronize()
+            for fm, s in zip(fms, streams):
+                with torch.cuda.stream(s):
+                    if t == 2 and fused:
+                        fm.interval_end(g, stream=s)
+                    elif t == 2:
+                        fm.layer_norms(g, interval_end=True, stream=s)
+                        fm.update_and_decide(stream=s)
+                    else:
+                        fm.layer_norms(g, stream=s)
+            torch.cuda.synchronize()
+            oz.layer_norms(gnp, t == 2)
+            if t == 1:
+                for fm in fms:
+                    b, e = fm.shard_of(f)
+                    dh = delta_host(fm, lay.n)
+                    assert np.array_equal(dh[b:e], oz.delta[b:e]), f"Delta P={P} T={T} rank={fm.rank}"
+        decs = [fm.decision() for fm in fms]
+        assert not any(d["flags"] & 32 for d in decs), "exchange timeout"
+        assert all(canon(d) == canon(decs[0]) for d in decs[1:])
+        compare_records(decs[0], oz.update_and_decide(), lay.n_segments, tag=f"P={P} T={T}")
+    assert len(f_seen) >= 4, f_seen     # the boundary moved (decisions and restores)
 
 
 # ---------------------------------------------------------------- tiered cache with admission (NEXT 3)

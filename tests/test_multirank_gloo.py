@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, active=False):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -38,7 +38,8 @@ def _worker(rank, world, port, q):
         assert len(uid) == 128 and all(u == ids[0] for u in ids) and any(uid)
         # 2) shard bounds from the library (host-only create)
         lay = uniform_layout(1_000_003, 7, pre=123_457, head=777)
-        fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="bf16", rank=rank, world=world, bind=False)
+        fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="bf16", rank=rank, world=world, bind=False,
+                               shard_active=active)
         info = fm.info()
         sb, se = info["shard_begin"], info["shard_end"]
         bounds = [None] * world
@@ -50,6 +51,12 @@ def _worker(rank, world, port, q):
         local = O.Freezer(lay.offsets, lay.kinds, O.DT_BF16)
         decisions = []
         for T in range(6):
+            # active-suffix shards: this interval's shard is the library's split of the
+            # active suffix for the current boundary (static: the same every interval)
+            sb, se = fm.shard_of(full.f)
+            bnd = [None] * world
+            dist.all_gather_object(bnd, (sb, se))
+            assert all(bnd[r][1] == bnd[r + 1][0] for r in range(world - 1)) and bnd[-1][1] == lay.n
             for t in range(2):
                 g = bert_grad_step(lay, 3, T, t, dtype="bf16")
                 gl = g.copy()
@@ -80,11 +87,12 @@ def _worker(rank, world, port, q):
         q.put((rank, traceback.format_exc()))
 
 
-def test_two_rank_gloo_host_logic():
+@pytest.mark.parametrize("active", [False, True])
+def test_two_rank_gloo_host_logic(active):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, WORLD, port, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, WORLD, port, q, active)) for r in range(WORLD)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(WORLD))
