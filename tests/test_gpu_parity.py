@@ -561,6 +561,48 @@ def test_active_suffix_shards_follow_the_boundary(P, dt, fused, acc):
     assert len(f_seen) >= 4, f_seen     # the boundary moved (decisions and restores)
 
 
+@pytest.mark.parametrize("P", [3, 8])
+def test_active_suffix_shards_everything_frozen(P):
+    """The boundary at n_pool (only HEAD active, 777 elements): with P ranks the
+    active suffix is a few vectors per rank, some ranks own no tile at all; the
+    interval still exchanges and records HEAD's norm, the test skips (< 2 active
+    POOL), matching the oracle."""
+    lay = _ragged_layout()
+    n_pool = sum(1 for k in lay.kinds if k == 1)
+    step = _decaying_step(lay, "f32", 5)
+    fms = [_fm(lay, "f32", rank=r, world=P, shard_active=True) for r in range(P)]
+    for fm in fms:
+        fm.set_peers_local(fms)
+    spans = [fm.shard_of(n_pool) for fm in fms]
+    assert spans[0][0] == lay.offsets[-2] and spans[-1][1] == lay.n
+    oz = _oracle(lay, "f32")
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    for T in range(3):
+        if T == 1:
+            for fm in fms:
+                blob = bytearray(fm.get_state())
+                struct.pack_into("<i", blob, 24, n_pool)
+                fm.set_state(bytes(blob))
+            oz.f = n_pool
+        for t in range(2):
+            gnp = step(T, t)
+            g = to_device_grad(gnp, "f32")
+            torch.cuda.synchronize()
+            for fm, s in zip(fms, streams):
+                with torch.cuda.stream(s):
+                    if t == 1:
+                        fm.interval_end(g, stream=s)
+                    else:
+                        fm.layer_norms(g, stream=s)
+            torch.cuda.synchronize()
+            oz.layer_norms(gnp, t == 1)
+        decs = [fm.decision() for fm in fms]
+        assert not any(d["flags"] & 32 for d in decs)
+        assert all(canon(d) == canon(decs[0]) for d in decs[1:])
+        compare_records(decs[0], oz.update_and_decide(), lay.n_segments, tag=f"P={P} T={T}")
+    assert decs[0]["boundary_after"] == n_pool
+
+
 # ---------------------------------------------------------------- tiered cache with admission (NEXT 3)
 
 def test_cache_admission_printed_example_gpu():
