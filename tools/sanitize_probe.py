@@ -47,6 +47,23 @@ def main():
         with torch.cuda.stream(s):
             f.interval_end(g, stream=s)
     torch.cuda.synchronize()
+    # active-suffix shards (per-f tables): two ranks, bf16, boundary moved by a restore
+    fa = [af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="bf16", rank=r, world=2, shard_active=True)
+          for r in range(2)]
+    for f in fa:
+        f.set_peers_local(fa)
+    gh = g.to(torch.bfloat16)
+    for T in range(3):
+        if T == 1:
+            for f in fa:
+                blob = bytearray(f.get_state())
+                blob[24:28] = (2).to_bytes(4, "little")
+                f.set_state(bytes(blob))
+        for f, s in zip(fa, ss):
+            with torch.cuda.stream(s):
+                f.layer_norms(gh, stream=s)
+                f.interval_end(gh, stream=s)
+        torch.cuda.synchronize()
     # wide finalize (> 2048 interval-end tiles)
     big = uniform_layout(2100 * 8192 + 77, 7, pre=4099, head=33)
     fw = af.FreezingModule(big.offsets, big.kinds, grad_dtype="f32")
