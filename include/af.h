@@ -166,12 +166,15 @@ typedef struct af_cache af_cache;
 /* Host only (no device access).  Validates and copies the layout (offsets
  * strictly increasing from 0, kinds in the order PRE* POOL+ HEAD* with >= 1
  * POOL), the config, builds the segment-aligned tile table of this rank's
- * contiguous shard [floor(r*n/P) rounded down to 8, ...).
+ * contiguous shard [floor(r*n/P) rounded down to 8, ...) --
+ * or, with shard_active, one table per boundary f over this rank's slice of
+ * the active suffix [A_f, n) (A_f + floor(r*(n-A_f)/P), rounded down to 8).
  * AF_EINVAL on any violation; *out untouched on error. */
 AF_API af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **out);
 
 /* Host only.  Bytes of the two caller-owned device buffers:
- * accum = the fp32 Delta shard (n_local * 4 B; 0 in STEP_SUMSQ mode);
+ * accum = the fp32 Delta shard (n_local * 4 B; n * 4 B with shard_active, where
+ *         element i lives at accum[i]; 0 in STEP_SUMSQ mode);
  * scratch = device state, tile table, partials, exchange rows, decision ring. */
 AF_API af_status af_ctx_workspace_bytes(const af_ctx *ctx, size_t *accum_bytes, size_t *scratch_bytes);
 
