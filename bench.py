@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cache-sweep", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly (no CUDA graphs)")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="the step's cache get waits for the interval end to complete (no AF_CACHE_OVERLAP_PREV)")
     ap.add_argument("--no-extras", action="store_true", help="skip the NEXT-row probes (fused AdamW)")
     ap.add_argument("--no-secondary", action="store_true",
                     help="N = 1: skip the short run of the other BERT workload reported under 'secondary'")
@@ -297,7 +299,9 @@ def run_ours(args, rank, world, local):
         if evs: evs[2].record(stream)
         if "cache" in skip:
             return
-        cache.get(ids, 4, out_rows, depth_out)                        # a11
+        # a11; the get reads nothing the interval end writes: it may start during the
+        # interval end's last-CTA tail (AF_CACHE_OVERLAP_PREV)
+        cache.get(ids, 4, out_rows, depth_out, overlap_prev=not args.no_overlap)
         if evs: evs[3].record(stream)
         cache.put(ids, rows, 4)                                       # a10
         if evs: evs[4].record(stream)

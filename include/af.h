@@ -354,6 +354,18 @@ AF_API af_status af_cache_put(af_cache *c, const int64_t *ids_dev, int32_t n, co
 AF_API af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
                        void *rows_out_dev, int32_t *depth_out_dev, void *stream);
 
+/* af_cache_get with flags.  AF_CACHE_OVERLAP_PREV: the copy may start while the
+ * kernel just before it on `stream` is still finishing (programmatic dependent
+ * launch without the dependency wait) -- e.g. behind af_interval_end, whose last
+ * CTA sums and decides while the grid is otherwise idle.  The CALLER guarantees
+ * that this preceding kernel does not write ids, the store (no af_cache_put /
+ * get on the same cache) or rows_out / depth_out, and does not read rows_out /
+ * depth_out; every kernel before it has completed.  Direct-mapped stores only
+ * (AF_ESTATE for tiered or global).  Unknown flags: AF_EINVAL. */
+#define AF_CACHE_OVERLAP_PREV 0x1u
+AF_API af_status af_cache_get_ex(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
+                                 void *rows_out_dev, int32_t *depth_out_dev, uint32_t flags, void *stream);
+
 /* Storage-manager tiers and admission (§3.2).
  * Host only, before af_cache_storage_bytes / af_cache_bind: room for I =
  * hbm_rows + host_rows records (I may be < D = the rank's owned ids): hbm_rows in

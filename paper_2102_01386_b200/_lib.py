@@ -14,6 +14,7 @@ AF_MAX_SEGMENTS = 256
 AF_MAX_WORLD = 64
 AF_OK, AF_EINVAL, AF_ESTATE, AF_EWORKSPACE, AF_ECUDA, AF_ENCCL, AF_ENONFINITE, AF_EOWNER, AF_ERANGE = range(9)
 AF_DT_F32, AF_DT_BF16 = 0, 1
+AF_CACHE_OVERLAP_PREV = 0x1
 AF_SEG_PRE, AF_SEG_POOL, AF_SEG_HEAD = 0, 1, 2
 AF_ACC_DELTA, AF_ACC_STEP_SUMSQ = 0, 1
 AF_PCT_LINEAR, AF_PCT_NEAREST_RANK = 0, 1
@@ -97,6 +98,7 @@ SIGNATURES = {
     "af_cache_bind": (c_int, [c_void_p, c_void_p, c_void_p]),
     "af_cache_put": (c_int, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),
     "af_cache_get": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+    "af_cache_get_ex": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_uint32, c_void_p]),
     "af_cache_status": (c_int, [c_void_p, POINTER(c_uint32), POINTER(c_int64)]),
     "af_cache_set_capacity": (c_int, [c_void_p, c_int64, c_int64]),
     "af_cache_host_bytes": (c_int, [c_void_p, POINTER(c_size_t)]),

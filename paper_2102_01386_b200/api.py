@@ -303,11 +303,15 @@ class ActivationCache:
         check(lib.af_cache_put(self._h, c_void_p(ids.data_ptr()), n, c_void_p(rows.data_ptr()), int(depth),
                                _stream_handle(stream)), "af_cache_put")
 
-    def get(self, ids, cur_boundary, rows_out, depth_out, stream=None):
+    def get(self, ids, cur_boundary, rows_out, depth_out, stream=None, overlap_prev=False):
+        """overlap_prev: AF_CACHE_OVERLAP_PREV -- the copy may start while the kernel
+        before it on the stream finishes (the caller guarantees that kernel does not
+        touch ids, this store or the outputs; see include/af.h)."""
         n = int(ids.numel())
-        check(lib.af_cache_get(self._h, c_void_p(ids.data_ptr()), n, int(cur_boundary),
-                               c_void_p(rows_out.data_ptr()), c_void_p(depth_out.data_ptr()),
-                               _stream_handle(stream)), "af_cache_get")
+        check(lib.af_cache_get_ex(self._h, c_void_p(ids.data_ptr()), n, int(cur_boundary),
+                                  c_void_p(rows_out.data_ptr()), c_void_p(depth_out.data_ptr()),
+                                  L.AF_CACHE_OVERLAP_PREV if overlap_prev else 0, _stream_handle(stream)),
+              "af_cache_get_ex")
 
     def get_async(self, ids, cur_boundary, rows_out, depth_out, stream):
         """Prefetch (the paper's reader process, Fig. 8): enqueue the get on a side

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kCacheThreads) cache_kernel(const CacheParams 
     fence_mbar_init();
   }
   __syncthreads();
-  pdl_wait();  // ids, rows and the meta words may come from the preceding kernels
+  if (!p.no_wait) pdl_wait();  // ids, rows and the meta words may come from the preceding kernels
 
   const int64_t n_items = static_cast<int64_t>(p.n) * p.n_chunks;
   const int64_t G = gridDim.x;

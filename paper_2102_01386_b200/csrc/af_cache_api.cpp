@@ -203,6 +203,14 @@ af_status af_cache_put(af_cache *c, const int64_t *ids_dev, int32_t n, const voi
 
 af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary, void *rows_out_dev,
                        int32_t *depth_out_dev, void *stream) {
+  return af_cache_get_ex(c, ids_dev, n, cur_boundary, rows_out_dev, depth_out_dev, 0u, stream);
+}
+
+af_status af_cache_get_ex(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary, void *rows_out_dev,
+                          int32_t *depth_out_dev, uint32_t flags, void *stream) {
+  if (flags & ~AF_CACHE_OVERLAP_PREV) return fail(AF_EINVAL, "unknown flags");
+  if ((flags & AF_CACHE_OVERLAP_PREV) && c && c->tiered)
+    return fail(AF_ESTATE, "AF_CACHE_OVERLAP_PREV needs a direct-mapped store");
   CacheParams p;
   af_status s = cache_common(c, ids_dev, n, rows_out_dev, p);
   if (s != AF_OK) return s;
@@ -212,6 +220,7 @@ af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t c
   p.dst_rows = static_cast<char *>(rows_out_dev);
   p.depth_out = depth_out_dev;
   p.cur_boundary = cur_boundary;
+  p.no_wait = (flags & AF_CACHE_OVERLAP_PREV) ? 1 : 0;
   if (c->tiered) return cache_tiered(c, p, false, stream);
   const int e = launch_cache_get(p, c->grid, stream);
   if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache get launch");

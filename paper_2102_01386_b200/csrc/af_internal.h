@@ -207,6 +207,7 @@ struct CacheParams {
   int32_t *depth_out;       // get
   int32_t depth;            // put
   int32_t cur_boundary;     // get
+  int32_t no_wait;          // get: skip the PDL dependency wait (AF_CACHE_OVERLAP_PREV, caller-guaranteed)
   // tiered mode (rowslot != nullptr): the plan kernel already resolved each row's slot
   const int32_t *rowslot;   // [n] slot per row of the call, -1 = skip
   char *host;               // device alias of the page-locked host tier

@@ -435,6 +435,57 @@ def test_cache_chunk_choice_parity(rb, n):
         assert gc.status() == (0, len(oc.store))
 
 
+def test_cache_get_overlapping_the_interval_end():
+    """AF_CACHE_OVERLAP_PREV: a get launched right behind af_interval_end starts
+    during the interval end's tail (no dependency wait).  Bytes / depths equal
+    the oracle's, the decisions equal a run without the flag; the flag is
+    refused for tiered stores and unknown flags are rejected."""
+    import ctypes as C
+
+    import paper_2102_01386_b200 as af
+    from paper_2102_01386_b200 import _lib as L
+    from afinputs import cache_rows
+    lay = _ragged_layout()
+    step = _decaying_step(lay, "bf16", 9)
+    num, rb = 4000, 24_592
+    gc, oc = _cache_pair(num, rb)
+    ids_all = np.random.default_rng(4).permutation(num)[:3000]
+    rows = cache_rows(2, 2, len(ids_all), rb)
+    gc.put(_ids(ids_all), torch.from_numpy(rows).cuda(), 3)
+    oc.put(ids_all, rows, 3)
+    a, b = _fm(lay, "bf16"), _fm(lay, "bf16")
+    s = torch.cuda.current_stream()
+    for T in range(5):
+        q = np.random.default_rng(100 + T).permutation(num)[:700]
+        g0, g1 = to_device_grad(step(T, 0), "bf16"), to_device_grad(step(T, 1), "bf16")
+        out = torch.full((len(q), rb), 7, dtype=torch.uint8, device="cuda")
+        dep = torch.zeros(len(q), dtype=torch.int32, device="cuda")
+        qd = _ids(q)
+        torch.cuda.synchronize()
+        a.layer_norms(g0)
+        a.interval_end(g1)
+        gc.get(qd, 3 + (T % 2), out, dep, overlap_prev=True)      # behind the interval end's tail
+        b.layer_norms(g0)
+        b.interval_end(g1)
+        torch.cuda.synchronize()
+        out_o = np.full((len(q), rb), 7, np.uint8)
+        dep_o = oc.get(q, 3 + (T % 2), out_o)
+        assert np.array_equal(dep.cpu().numpy(), dep_o)
+        assert np.array_equal(out.cpu().numpy(), out_o)
+        assert canon(a.decision()) == canon(b.decision())
+    assert gc.status() == (0, len(oc.store))
+    t = af.ActivationCache(100, 4096, hbm_rows=10, host_rows=10)
+    ids = _ids([1, 2])
+    o = torch.empty((2, 4096), dtype=torch.uint8, device="cuda")
+    d = torch.empty(2, dtype=torch.int32, device="cuda")
+    st = L.lib.af_cache_get_ex(t._h, C.c_void_p(ids.data_ptr()), 2, 1, C.c_void_p(o.data_ptr()),
+                               C.c_void_p(d.data_ptr()), L.AF_CACHE_OVERLAP_PREV, None)
+    assert st == L.AF_ESTATE
+    st = L.lib.af_cache_get_ex(gc._h, C.c_void_p(ids.data_ptr()), 2, 1, C.c_void_p(o.data_ptr()),
+                               C.c_void_p(d.data_ptr()), 0x80, None)
+    assert st == L.AF_EINVAL
+
+
 def test_cache_owner_and_range_errors():
     gc, oc = _cache_pair(10, 64, rank=1, world=4)
     rows = torch.zeros((4, 64), dtype=torch.uint8, device="cuda")
