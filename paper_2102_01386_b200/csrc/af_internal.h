@@ -16,8 +16,8 @@ constexpr int kNormBlock = 256;          // threads per CTA of the streaming ker
 #ifndef AF_TILE_ELEMS_F32  // 8192 since the wide finalize made more partials cheap:
 #define AF_TILE_ELEMS_F32 8192  // BERT-large interval end -1.7 % (profiles/r01_v20_variants_end_tiles_f32.jsonl)
 #endif
-#ifndef AF_TILE_ELEMS_BF16
-#define AF_TILE_ELEMS_BF16 16384
+#ifndef AF_TILE_ELEMS_BF16  // 24576: BERT-base interval end -0.8 us in the step vs 16384, 12288 +9 us
+#define AF_TILE_ELEMS_BF16 24576  // (profiles/r01_v59_variants_end_tiles_bf16.jsonl)
 #endif
 #ifndef AF_TILE_BIG_MULT  // interval-end tiles are this much larger in the bulk of the shard
 #define AF_TILE_BIG_MULT 1  // tapering measured slower (profiles/r01_v10_variants_taper.jsonl): off

@@ -15,6 +15,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = {
     "default": "",
+    "end_bf16_12k": "-DAF_TILE_ELEMS_BF16=12288",
+    "end_bf16_24k": "-DAF_TILE_ELEMS_BF16=24576",
     "rs_bf16_u4": "-DAF_U_RS_VEC_BF16=4",
     "rs_bf16_u16": "-DAF_U_RS_VEC_BF16=16",
     "rs_end_bf16_u2": "-DAF_U_RS_VEC_END_BF16=2",
