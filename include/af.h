@@ -85,7 +85,12 @@ typedef enum { AF_PCT_LINEAR = 0, AF_PCT_NEAREST_RANK = 1 } af_pct_method;
 
 /* af_layer_norms / af_update_and_decide flags */
 #define AF_INTERVAL_END 0x1u /* this step ends the evaluation interval (every k/5 iterations) */
-#define AF_DRY_RUN 0x2u      /* do all the work but commit no state: Delta stays armed, f/prev/T unchanged */
+#define AF_DRY_RUN 0x2u      /* do all the work but commit no DECISION state: f, prev, T and the
+                                interval's armed/pending flags are unchanged (Delta stays armed, so
+                                the next step still reads it).  NOT a no-op on the buffers: a dry
+                                accumulate still writes Delta <- Delta + g, and dry AdamW / reduce-
+                                scatter variants still update params, moments and grad_shard_out
+                                (the bench's stationary reps; the oracle's dry_run matches) */
 
 /* af_decision.flags */
 #define AF_DEC_FIRST_INTERVAL 0x1u /* T == 0: norms recorded, no decision (Q9)            */
@@ -212,11 +217,19 @@ AF_API af_status af_ctx_exchange_rows(af_ctx *ctx, double **ss_all_dev);
  * (ld.acquire.sys, bounded spin: a missing peer sets AF_DEC_EXCHANGE_TIMEOUT
  * instead of hanging) -- af_interval_end needs no collective launch at any
  * world size (the streaming kernel, plus the wide finalize when n_fin_ctas > 0).
+ * A timeout is FATAL for the job: the rank that timed out poisons its flag slot
+ * in every peer, so a peer that arrives later flags EXCHANGE_TIMEOUT too instead
+ * of committing alone (best effort: a peer that had already read the rank's
+ * epoch before the poison commits), the flag is sticky (only af_set_state clears
+ * it) and every later streaming launch of the context skips its peer loads and
+ * stores.  The caller must stop on every rank and restore from a checkpoint.
  * _ipc: synchronous, collective; `handles` = world x AF_IPC_HANDLE_BYTES in rank
  * order, each from af_ctx_exchange_ipc_handle on that rank (exchanged by the
  * caller, e.g. torch.distributed.all_gather_object).  _local: every rank's ctx
- * lives in this process (single-process multi-GPU with peer access, or several
- * ranks sharing one GPU).  Takes precedence over an NCCL communicator. */
+ * lives in this process (several ranks sharing one GPU, or one process driving
+ * several GPUs: for a peer bound on another device, peer access from the current
+ * device is enabled here -- AF_EINVAL if cudaDeviceCanAccessPeer says no).
+ * Takes precedence over an NCCL communicator. */
 AF_API af_status af_ctx_exchange_ipc_handle(af_ctx *ctx, void *handle_out);
 AF_API af_status af_ctx_set_peers_ipc(af_ctx *ctx, const void *handles);
 AF_API af_status af_ctx_set_peers_local(af_ctx *ctx, af_ctx *const *peers);
@@ -326,6 +339,20 @@ AF_API af_status af_reduce_scatter_adamw_step(af_ctx *ctx, float scale, float *p
 AF_API af_status af_get_state(af_ctx *ctx, void *buf, size_t *len);
 AF_API af_status af_set_state(af_ctx *ctx, const void *buf, size_t len);
 
+/* Synchronous.  Copies the device ring's decision record of interval T (the
+ * ring keeps the last 16 intervals, T = af_decision.interval) into *out.
+ * AF_ERANGE when interval T is not in the ring (overwritten or not yet decided).
+ * For callers that enqueue several intervals without reading each record. */
+AF_API af_status af_ctx_read_record(af_ctx *ctx, int32_t interval, af_decision *out);
+
+/* Host only: test / diagnostic knobs (not for production).
+ * AF_DEBUG_TAIL_DELAY_NS: the last CTA of every later interval-end launch of
+ * this ctx busy-waits `value` ns (0 = off, <= 1e9) before summing and deciding,
+ * widening the window in which later kernels could observe an uncommitted
+ * decision (ordering tests). */
+#define AF_DEBUG_TAIL_DELAY_NS 1
+AF_API af_status af_ctx_set_debug(af_ctx *ctx, int32_t key, int64_t value);
+
 AF_API af_status af_ctx_destroy(af_ctx *ctx);
 
 /* ---- storage manager (activation cache) ----------------------------------- */
@@ -360,8 +387,12 @@ AF_API af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, in
  * CTA sums and decides while the grid is otherwise idle.  The CALLER guarantees
  * that this preceding kernel does not write ids, the store (no af_cache_put /
  * get on the same cache) or rows_out / depth_out, and does not read rows_out /
- * depth_out; every kernel before it has completed.  Direct-mapped stores only
- * (AF_ESTATE for tiered or global).  Unknown flags: AF_EINVAL. */
+ * depth_out; every kernel before it has completed.  Stream order is otherwise
+ * kept: the get does not COMPLETE before the preceding kernel has completed (it
+ * waits for it after its copies), so every later kernel on the stream still
+ * sees the preceding kernel's writes (e.g. the committed boundary f).
+ * Direct-mapped stores only (AF_ESTATE for tiered or global).  Unknown flags:
+ * AF_EINVAL. */
 #define AF_CACHE_OVERLAP_PREV 0x1u
 AF_API af_status af_cache_get_ex(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
                                  void *rows_out_dev, int32_t *depth_out_dev, uint32_t flags, void *stream);

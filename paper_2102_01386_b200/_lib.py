@@ -15,6 +15,7 @@ AF_MAX_WORLD = 64
 AF_OK, AF_EINVAL, AF_ESTATE, AF_EWORKSPACE, AF_ECUDA, AF_ENCCL, AF_ENONFINITE, AF_EOWNER, AF_ERANGE = range(9)
 AF_DT_F32, AF_DT_BF16 = 0, 1
 AF_CACHE_OVERLAP_PREV = 0x1
+AF_DEBUG_TAIL_DELAY_NS = 1
 AF_SEG_PRE, AF_SEG_POOL, AF_SEG_HEAD = 0, 1, 2
 AF_ACC_DELTA, AF_ACC_STEP_SUMSQ = 0, 1
 AF_PCT_LINEAR, AF_PCT_NEAREST_RANK = 0, 1
@@ -92,6 +93,8 @@ SIGNATURES = {
                                              c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_get_state": (c_int, [c_void_p, c_void_p, POINTER(c_size_t)]),
     "af_set_state": (c_int, [c_void_p, c_void_p, c_size_t]),
+    "af_ctx_read_record": (c_int, [c_void_p, c_int32, POINTER(AfDecision)]),
+    "af_ctx_set_debug": (c_int, [c_void_p, c_int32, c_int64]),
     "af_ctx_destroy": (c_int, [c_void_p]),
     "af_cache_create": (c_int, [c_int64, c_int64, c_int32, c_int32, POINTER(c_void_p)]),
     "af_cache_storage_bytes": (c_int, [c_void_p, POINTER(c_size_t), POINTER(c_size_t)]),

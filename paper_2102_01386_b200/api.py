@@ -23,6 +23,25 @@ def _stream_handle(stream):
     return c_void_p(s.cuda_stream)
 
 
+def _dev_tensor(t, name, device, min_bytes=0, dtypes=None, min_numel=0):
+    """Argument checks at the binding boundary (the C ABI takes raw pointers and
+    cannot see sizes): on `device`, contiguous, of an accepted dtype, large enough."""
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.device.type != "cuda" or (device is not None and t.device != torch.device(device)):
+        raise ValueError(f"{name} must live on {device} (got {t.device})")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtypes is not None and t.dtype not in dtypes:
+        raise TypeError(f"{name} must have dtype in {[str(d) for d in dtypes]} (got {t.dtype})")
+    if t.numel() * t.element_size() < min_bytes or t.numel() < min_numel:
+        raise ValueError(f"{name} is too small ({t.numel()} elements of {t.element_size()} B)")
+    return t
+
+
+_GRAD_TORCH = {L.AF_DT_F32: (torch.float32,), L.AF_DT_BF16: (torch.bfloat16, torch.int16)}
+
+
 def decision_to_dict(rec, n_segments):
     return dict(interval=rec.interval, boundary_before=rec.boundary_before,
                 boundary_after=rec.boundary_after, n_active=rec.n_active,
@@ -136,6 +155,8 @@ class FreezingModule:
     def set_grad_peers_local(self, grads):
         """NEXT 1 (ZeRO form): register every rank's full gradient buffer, for ranks
         living in this process; grads[r] is rank r's tensor."""
+        for r, g in enumerate(grads):
+            _dev_tensor(g, f"grads[{r}]", None, dtypes=_GRAD_TORCH[self.grad_dtype], min_numel=self.offsets[-1])
         self._rs_grads = list(grads)                 # keep the buffers alive
         arr = (c_void_p * len(grads))(*[g.data_ptr() for g in grads])
         check(lib.af_ctx_set_grad_peers_local(self._h, arr), "af_ctx_set_grad_peers_local")
@@ -144,6 +165,7 @@ class FreezingModule:
         """NEXT 1 (ZeRO form), collective: export this rank's persistent gradient
         buffer, all-gather the CUDA IPC handles and map every rank's buffer."""
         import torch.distributed as dist
+        self._grad(grad)
         self._rs_grads = [grad]
         h = (ctypes.c_uint8 * L.AF_IPC_HANDLE_BYTES)()
         with torch.cuda.device(self.device):
@@ -160,6 +182,8 @@ class FreezingModule:
         registered gradients) * scale (default 1/world) into `out` (fp32, indexed
         from shard_begin; None: not written), accumulated into Delta -- or, with
         interval_end=True, the whole interval end and decision."""
+        if out is not None:
+            _dev_tensor(out, "out", self.device, dtypes=(torch.float32,), min_numel=self._shard_len())
         sc = (1.0 / self.world) if scale is None else float(scale)
         flags = (L.AF_INTERVAL_END if interval_end else 0) | (L.AF_DRY_RUN if dry_run else 0)
         rec = c_void_p(self._rec_host.data_ptr()) if (copy_record and interval_end) else c_void_p(0)
@@ -174,6 +198,10 @@ class FreezingModule:
                                   stream=None, copy_record=True):
         """af_reduce_scatter_adamw_step: the fused reduce-scatter with AdamW on this
         rank's shard of params / exp_avg / exp_avg_sq (full flat fp32 tensors)."""
+        for t, nm in ((params, "params"), (exp_avg, "exp_avg"), (exp_avg_sq, "exp_avg_sq")):
+            self._f32_full(t, nm)
+        if out is not None:
+            _dev_tensor(out, "out", self.device, dtypes=(torch.float32,), min_numel=self._shard_len())
         sc = (1.0 / self.world) if scale is None else float(scale)
         hp = L.AfAdamW(float(lr), float(beta1), float(beta2), float(eps), float(weight_decay), int(step))
         flags = (L.AF_INTERVAL_END if interval_end else 0) | (L.AF_DRY_RUN if dry_run else 0)
@@ -186,6 +214,22 @@ class FreezingModule:
             self._event.record(stream if stream is not None else torch.cuda.current_stream())
         return out
 
+    def _shard_len(self):
+        b, e = self.shard_of(0)
+        return e - b
+
+    def read_record(self, interval):
+        """af_ctx_read_record (synchronous): the device ring's record of `interval`
+        (the last 16 intervals), for callers that enqueue several intervals
+        without reading each record."""
+        r = L.AfDecision()
+        check(lib.af_ctx_read_record(self._h, int(interval), byref(r)), "af_ctx_read_record")
+        return decision_to_dict(r, self.n_segments)
+
+    def set_debug(self, key, value):
+        """af_ctx_set_debug: test / diagnostic knobs (AF_DEBUG_TAIL_DELAY_NS)."""
+        check(lib.af_ctx_set_debug(self._h, int(key), int(value)), "af_ctx_set_debug")
+
     def exchange_rows(self):
         """float64 view [world, L] of the exchange matrix inside the scratch buffer."""
         p = c_void_p()
@@ -194,8 +238,16 @@ class FreezingModule:
         n = self.world * self.n_segments * 8
         return self.scratch[off:off + n].view(torch.float64).view(self.world, self.n_segments)
 
+    # -- argument checks -----------------------------------------------------------
+    def _grad(self, grad, name="grad"):
+        return _dev_tensor(grad, name, self.device, dtypes=_GRAD_TORCH[self.grad_dtype], min_numel=self.offsets[-1])
+
+    def _f32_full(self, t, name):
+        return _dev_tensor(t, name, self.device, dtypes=(torch.float32,), min_numel=self.offsets[-1])
+
     # -- the hot path --------------------------------------------------------------
     def layer_norms(self, grad, interval_end=False, dry_run=False, stream=None):
+        self._grad(grad)
         flags = (L.AF_INTERVAL_END if interval_end else 0) | (L.AF_DRY_RUN if dry_run else 0)
         check(lib.af_layer_norms(self._h, c_void_p(grad.data_ptr()), flags, _stream_handle(stream)),
               "af_layer_norms")
@@ -210,6 +262,7 @@ class FreezingModule:
     def interval_end(self, grad, dry_run=False, stream=None, copy_record=True):
         """af_interval_end: the interval-end step and the decision in one call
         (one kernel launch when world == 1)."""
+        self._grad(grad)
         flags = L.AF_DRY_RUN if dry_run else 0
         out = c_void_p(self._rec_host.data_ptr()) if copy_record else c_void_p(0)
         check(lib.af_interval_end(self._h, c_void_p(grad.data_ptr()), flags, out, _stream_handle(stream)),
@@ -221,6 +274,9 @@ class FreezingModule:
                    weight_decay=0.0, interval_end=False, dry_run=False, stream=None, copy_record=True):
         """af_adamw_step: AdamW on this rank's shard fused with the Delta accumulate
         (or, with interval_end=True, with the whole interval end and decision)."""
+        self._grad(grad)
+        for t, nm in ((params, "params"), (exp_avg, "exp_avg"), (exp_avg_sq, "exp_avg_sq")):
+            self._f32_full(t, nm)
         hp = L.AfAdamW(float(lr), float(beta1), float(beta2), float(eps), float(weight_decay), int(step))
         flags = (L.AF_INTERVAL_END if interval_end else 0) | (L.AF_DRY_RUN if dry_run else 0)
         out = c_void_p(self._rec_host.data_ptr()) if (copy_record and interval_end) else c_void_p(0)
@@ -283,6 +339,7 @@ class ActivationCache:
         check(lib.af_cache_host_bytes(h, byref(hb)), "af_cache_host_bytes")
         self.payload_bytes, self.meta_bytes, self.host_bytes = p.value, m.value, hb.value
         self.payload = self.meta = self.host_tier = None
+        self.device = None
         if bind:
             self.bind(device)
 
@@ -298,8 +355,18 @@ class ActivationCache:
                 self.host_tier = torch.empty(self.host_bytes, dtype=torch.uint8, pin_memory=True)
                 check(lib.af_cache_bind_host(self._h, c_void_p(self.host_tier.data_ptr())), "af_cache_bind_host")
 
+    def _ids(self, ids):
+        return _dev_tensor(ids, "ids", self.device, dtypes=(torch.int64,))
+
+    def _rows(self, rows, n, name):
+        return _dev_tensor(rows, name, self.device, min_bytes=n * self.row_bytes)
+
+    def _depth_out(self, d, n):
+        return _dev_tensor(d, "depth_out", self.device, dtypes=(torch.int32,), min_numel=n)
+
     def put(self, ids, rows, depth, stream=None):
-        n = int(ids.numel())
+        n = int(self._ids(ids).numel())
+        self._rows(rows, n, "rows")
         check(lib.af_cache_put(self._h, c_void_p(ids.data_ptr()), n, c_void_p(rows.data_ptr()), int(depth),
                                _stream_handle(stream)), "af_cache_put")
 
@@ -307,7 +374,9 @@ class ActivationCache:
         """overlap_prev: AF_CACHE_OVERLAP_PREV -- the copy may start while the kernel
         before it on the stream finishes (the caller guarantees that kernel does not
         touch ids, this store or the outputs; see include/af.h)."""
-        n = int(ids.numel())
+        n = int(self._ids(ids).numel())
+        self._rows(rows_out, n, "rows_out")
+        self._depth_out(depth_out, n)
         check(lib.af_cache_get_ex(self._h, c_void_p(ids.data_ptr()), n, int(cur_boundary),
                                   c_void_p(rows_out.data_ptr()), c_void_p(depth_out.data_ptr()),
                                   L.AF_CACHE_OVERLAP_PREV if overlap_prev else 0, _stream_handle(stream)),
@@ -339,11 +408,15 @@ class ActivationCache:
             check(lib.af_cache_set_peers_ipc(self._h, buf), "af_cache_set_peers_ipc")
 
     def put_global(self, ids, rows, depth, stream=None):
+        self._rows(rows, int(self._ids(ids).numel()), "rows")
         check(lib.af_cache_put_global(self._h, c_void_p(ids.data_ptr()), int(ids.numel()),
                                       c_void_p(rows.data_ptr()), int(depth), _stream_handle(stream)),
               "af_cache_put_global")
 
     def get_global(self, ids, cur_boundary, rows_out, depth_out, stream=None):
+        n = int(self._ids(ids).numel())
+        self._rows(rows_out, n, "rows_out")
+        self._depth_out(depth_out, n)
         check(lib.af_cache_get_global(self._h, c_void_p(ids.data_ptr()), int(ids.numel()), int(cur_boundary),
                                       c_void_p(rows_out.data_ptr()), c_void_p(depth_out.data_ptr()),
                                       _stream_handle(stream)), "af_cache_get_global")

@@ -278,6 +278,14 @@ __global__ void __launch_bounds__(kCacheThreads) cache_kernel(const CacheParams 
     }
     __syncthreads();  // descs / hitdep of this batch are consumed
   }
+  // AF_CACHE_OVERLAP_PREV: the copy above ran without waiting for the preceding
+  // kernel, but the get must not COMPLETE before it -- every later kernel waits
+  // only on the get, and the preceding interval end may still be committing f /
+  // prev / T in its last CTA (or spinning on peers there).  Waiting here keeps
+  // PDL's transitive order: get complete => predecessor complete.
+#ifndef AF_CACHE_OVERLAP_UNSAFE  // diagnostic build only: the round-1 behaviour the ordering test must catch
+  if (p.no_wait) pdl_wait();
+#endif
   pdl_launch_dependents();
   if (threadIdx.x == 0) bulk_wait_all();  // all stores complete before the CTA retires its shared memory
 }

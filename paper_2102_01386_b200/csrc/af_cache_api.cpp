@@ -41,6 +41,7 @@ extern "C" {
 
 
 af_status af_cache_create(int64_t num_examples, int64_t row_bytes, int32_t rank, int32_t world, af_cache **out) {
+  AF_NVTX();
   if (!out) return fail(AF_EINVAL, "NULL argument");
   if (num_examples < 0) return fail(AF_EINVAL, "num_examples < 0");
   if (row_bytes <= 0 || row_bytes % 16 != 0) return fail(AF_EINVAL, "row_bytes must be a positive multiple of 16");
@@ -62,6 +63,7 @@ af_status af_cache_create(int64_t num_examples, int64_t row_bytes, int32_t rank,
 }
 
 af_status af_cache_set_capacity(af_cache *c, int64_t hbm_rows, int64_t host_rows) {
+  AF_NVTX();
   if (!c) return fail(AF_EINVAL, "NULL cache");
   if (c->bound) return fail(AF_ESTATE, "set the capacity before binding storage");
   if (hbm_rows < 0 || host_rows < 0 || hbm_rows + host_rows < 1) return fail(AF_EINVAL, "bad capacity");
@@ -73,6 +75,7 @@ af_status af_cache_set_capacity(af_cache *c, int64_t hbm_rows, int64_t host_rows
 }
 
 af_status af_cache_storage_bytes(const af_cache *c, size_t *payload_bytes, size_t *meta_bytes) {
+  AF_NVTX();
   if (!c || !payload_bytes || !meta_bytes) return fail(AF_EINVAL, "NULL argument");
   const int64_t rows = c->tiered ? c->hbm_rows : c->capacity;
   *payload_bytes = static_cast<size_t>(rows) * static_cast<size_t>(c->row_bytes);
@@ -81,12 +84,14 @@ af_status af_cache_storage_bytes(const af_cache *c, size_t *payload_bytes, size_
 }
 
 af_status af_cache_host_bytes(const af_cache *c, size_t *host_bytes) {
+  AF_NVTX();
   if (!c || !host_bytes) return fail(AF_EINVAL, "NULL argument");
   *host_bytes = static_cast<size_t>(c->tiered ? c->host_rows : 0) * static_cast<size_t>(c->row_bytes);
   return AF_OK;
 }
 
 af_status af_cache_bind_host(af_cache *c, void *host_pinned) {
+  AF_NVTX();
   if (!c || !host_pinned) return fail(AF_EINVAL, "NULL argument");
   if (!c->tiered || c->host_rows == 0) return fail(AF_ESTATE, "no host tier configured");
   if (!aligned(host_pinned, 16)) return fail(AF_EINVAL, "host tier must be 16-byte aligned");
@@ -102,6 +107,7 @@ af_status af_cache_bind_host(af_cache *c, void *host_pinned) {
 }
 
 af_status af_cache_bind(af_cache *c, void *payload_dev, void *meta_dev) {
+  AF_NVTX();
   const int64_t rows = c ? (c->tiered ? c->hbm_rows : c->capacity) : 0;
   if (!c || !meta_dev || (rows > 0 && !payload_dev)) return fail(AF_EINVAL, "NULL argument");
   if ((payload_dev && !aligned(payload_dev, 16)) || !aligned(meta_dev, 256))
@@ -188,6 +194,7 @@ static af_status cache_tiered(af_cache *c, CacheParams &p, bool put, void *strea
 
 af_status af_cache_put(af_cache *c, const int64_t *ids_dev, int32_t n, const void *rows_dev, int32_t depth,
                        void *stream) {
+  AF_NVTX();
   CacheParams p;
   af_status s = cache_common(c, ids_dev, n, rows_dev, p);
   if (s != AF_OK) return s;
@@ -203,11 +210,13 @@ af_status af_cache_put(af_cache *c, const int64_t *ids_dev, int32_t n, const voi
 
 af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary, void *rows_out_dev,
                        int32_t *depth_out_dev, void *stream) {
+  AF_NVTX();
   return af_cache_get_ex(c, ids_dev, n, cur_boundary, rows_out_dev, depth_out_dev, 0u, stream);
 }
 
 af_status af_cache_get_ex(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary, void *rows_out_dev,
                           int32_t *depth_out_dev, uint32_t flags, void *stream) {
+  AF_NVTX();
   if (flags & ~AF_CACHE_OVERLAP_PREV) return fail(AF_EINVAL, "unknown flags");
   if ((flags & AF_CACHE_OVERLAP_PREV) && c && c->tiered)
     return fail(AF_ESTATE, "AF_CACHE_OVERLAP_PREV needs a direct-mapped store");
@@ -228,6 +237,7 @@ af_status af_cache_get_ex(af_cache *c, const int64_t *ids_dev, int32_t n, int32_
 }
 
 af_status af_cache_stats(af_cache *c, af_cache_info *out) {
+  AF_NVTX();
   if (!c || !out) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
   AF_CUDA(cudaDeviceSynchronize(), "cache stats sync");
@@ -255,6 +265,7 @@ af_status af_cache_stats(af_cache *c, af_cache_info *out) {
 }
 
 af_status af_cache_status(af_cache *c, uint32_t *device_error_flags, int64_t *n_valid) {
+  AF_NVTX();
   if (!c || !device_error_flags) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
   AF_CUDA(cudaDeviceSynchronize(), "cache status sync");
@@ -294,6 +305,7 @@ static af_status cache_upload_peers(af_cache *c, const std::vector<char *> &pay,
 }
 
 af_status af_cache_exchange_ipc_handle(af_cache *c, void *handle_out) {
+  AF_NVTX();
   if (!c || !handle_out) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
   if (c->tiered) return fail(AF_ESTATE, "global get/put needs the direct-mapped cache");
@@ -312,6 +324,7 @@ af_status af_cache_exchange_ipc_handle(af_cache *c, void *handle_out) {
 }
 
 af_status af_cache_set_peers_ipc(af_cache *c, const void *handles) {
+  AF_NVTX();
   if (!c || !handles) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
   if (c->tiered) return fail(AF_ESTATE, "global get/put needs the direct-mapped cache");
@@ -337,6 +350,7 @@ af_status af_cache_set_peers_ipc(af_cache *c, const void *handles) {
 }
 
 af_status af_cache_set_peers_local(af_cache *c, af_cache *const *peers) {
+  AF_NVTX();
   if (!c || !peers) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
   if (c->tiered) return fail(AF_ESTATE, "global get/put needs the direct-mapped cache");
@@ -347,6 +361,8 @@ af_status af_cache_set_peers_local(af_cache *c, af_cache *const *peers) {
     if (!q || !q->bound || q->tiered || q->rank != r || q->world != c->world || q->num_examples != c->num_examples ||
         q->row_bytes != c->row_bytes)
       return fail(AF_EINVAL, "peer cache mismatch");
+    const af_status st = enable_peer_access_to(q->payload);  // a store on another device: over NVLink
+    if (st != AF_OK) return st;
     pay[r] = q->payload;
     met[r] = q->meta + kMetaHeader;
   }
@@ -361,6 +377,7 @@ static af_status cache_global_common(af_cache *c) {
 
 af_status af_cache_put_global(af_cache *c, const int64_t *ids_dev, int32_t n, const void *rows_dev, int32_t depth,
                               void *stream) {
+  AF_NVTX();
   af_status s = cache_global_common(c);
   if (s != AF_OK) return s;
   CacheParams p;
@@ -379,6 +396,7 @@ af_status af_cache_put_global(af_cache *c, const int64_t *ids_dev, int32_t n, co
 
 af_status af_cache_get_global(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
                               void *rows_out_dev, int32_t *depth_out_dev, void *stream) {
+  AF_NVTX();
   af_status s = cache_global_common(c);
   if (s != AF_OK) return s;
   CacheParams p;
@@ -398,6 +416,7 @@ af_status af_cache_get_global(af_cache *c, const int64_t *ids_dev, int32_t n, in
 }
 
 af_status af_cache_destroy(af_cache *c) {
+  AF_NVTX();
   if (!c) return fail(AF_EINVAL, "NULL cache");
   ipc_release(c->ipc_opened);
   delete c;

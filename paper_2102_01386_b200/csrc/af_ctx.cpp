@@ -63,6 +63,8 @@ struct af_ctx {
   std::vector<void *> ipc_opened;   // peer allocations opened with cudaIpcOpenMemHandle
   bool grad_peers = false;          // fused reduce-scatter: every rank's gradient buffer registered
   const void *own_grad = nullptr;   // this rank's buffer (af_ctx_grad_ipc_handle)
+  int device = -1;                  // the device the workspace was bound on
+  uint32_t dbg_tail_delay_ns = 0;   // AF_DEBUG_TAIL_DELAY_NS
 
   template <typename T>
   T *at(size_t o) const {
@@ -73,6 +75,7 @@ struct af_ctx {
 extern "C" {
 
 af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **out) {
+  AF_NVTX();
   if (!layout || !cfg || !out) return fail(AF_EINVAL, "NULL argument");
   const int L = layout->n_segments;
   if (L < 1 || L > AF_MAX_SEGMENTS) return fail(AF_EINVAL, "n_segments out of [1, AF_MAX_SEGMENTS]");
@@ -233,6 +236,7 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
 }
 
 af_status af_ctx_workspace_bytes(const af_ctx *c, size_t *accum_bytes, size_t *scratch_bytes) {
+  AF_NVTX();
   if (!c || !accum_bytes || !scratch_bytes) return fail(AF_EINVAL, "NULL argument");
   *accum_bytes = c->accum_bytes;
   *scratch_bytes = c->scratch_bytes;
@@ -240,6 +244,7 @@ af_status af_ctx_workspace_bytes(const af_ctx *c, size_t *accum_bytes, size_t *s
 }
 
 af_status af_ctx_info(const af_ctx *c, af_info *info) {
+  AF_NVTX();
   if (!c || !info) return fail(AF_EINVAL, "NULL argument");
   std::memset(info, 0, sizeof(*info));
   info->n_segments = c->L;
@@ -260,6 +265,7 @@ af_status af_ctx_info(const af_ctx *c, af_info *info) {
 }
 
 af_status af_ctx_shard_of(const af_ctx *c, int32_t f, int64_t *begin, int64_t *end) {
+  AF_NVTX();
   if (!c || !begin || !end) return fail(AF_EINVAL, "NULL argument");
   if (f < 0 || f > c->n_pool) return fail(AF_EINVAL, "f out of [0, n_pool]");
   *begin = c->sb_of_f[f];
@@ -268,11 +274,13 @@ af_status af_ctx_shard_of(const af_ctx *c, int32_t f, int64_t *begin, int64_t *e
 }
 
 af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
+  AF_NVTX();
   if (!c || !scratch_dev) return fail(AF_EINVAL, "NULL argument");
   if (c->accum_bytes && !accum_dev) return fail(AF_EINVAL, "accum buffer required");
   if (!aligned(scratch_dev, 256) || (accum_dev && !aligned(accum_dev, 256)))
     return fail(AF_EINVAL, "workspace buffers must be 256-byte aligned");
   int sms = 0;
+  AF_CUDA(cudaGetDevice(&c->device), "cudaGetDevice");
   cudaError_t e = static_cast<cudaError_t>(device_sm_count(&sms));
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
   e = static_cast<cudaError_t>(preload_norm_kernels(c->dtype, c->cfg.world));
@@ -312,6 +320,7 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
 }
 
 af_status af_nccl_unique_id(void *id_128B) {
+  AF_NVTX();
   if (!id_128B) return fail(AF_EINVAL, "NULL argument");
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   ncclUniqueId id;
@@ -322,6 +331,7 @@ af_status af_nccl_unique_id(void *id_128B) {
 }
 
 af_status af_ctx_set_comm(af_ctx *c, const void *id_128B) {
+  AF_NVTX();
   if (!c || !id_128B) return fail(AF_EINVAL, "NULL argument");
   if (c->comm) return fail(AF_ESTATE, "communicator already set");
   ncclUniqueId id;
@@ -334,6 +344,7 @@ af_status af_ctx_set_comm(af_ctx *c, const void *id_128B) {
 }
 
 af_status af_ctx_exchange_rows(af_ctx *c, double **ss_all_dev) {
+  AF_NVTX();
   if (!c || !ss_all_dev) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   *ss_all_dev = c->at<double>(c->o_ssall);
@@ -377,6 +388,7 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   c->reverse = !c->reverse;
   p.first = c->armed ? 0 : 1;
   p.end = end ? 1 : 0;
+  p.dbg_tail_delay_ns = c->dbg_tail_delay_ns;
   p.commit = dry ? 0 : 1;
   if (c->peers) {
     p.xworld = c->cfg.world;
@@ -454,6 +466,7 @@ af_status check_norm_args(af_ctx *c, const void *grad_dev) {
 extern "C" {
 
 af_status af_layer_norms(af_ctx *c, const void *grad_dev, uint32_t flags, void *stream) {
+  AF_NVTX();
   af_status st = check_norm_args(c, grad_dev);
   if (st != AF_OK) return st;
   if (flags & ~(AF_INTERVAL_END | AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
@@ -509,6 +522,7 @@ extern "C" {
 af_status af_adamw_step(af_ctx *c, float *params_dev, float *exp_avg_dev, float *exp_avg_sq_dev,
                         const void *grad_dev, const af_adamw *hp, uint32_t flags, af_decision *out_host,
                         void *stream) {
+  AF_NVTX();
   if (c && c->active) return fail(AF_ESTATE, "af_adamw_step needs static shards (shard_active = 0)");
   af_status st = check_norm_args(c, grad_dev);
   if (st != AF_OK) return st;
@@ -551,6 +565,7 @@ af_status af_adamw_step(af_ctx *c, float *params_dev, float *exp_avg_dev, float 
 }
 
 af_status af_update_and_decide(af_ctx *c, uint32_t flags, af_decision *out_host, void *stream) {
+  AF_NVTX();
   if (!c) return fail(AF_EINVAL, "NULL ctx");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   if (flags & ~(AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
@@ -566,6 +581,7 @@ af_status af_update_and_decide(af_ctx *c, uint32_t flags, af_decision *out_host,
 }
 
 af_status af_interval_end(af_ctx *c, const void *grad_dev, uint32_t flags, af_decision *out_host, void *stream) {
+  AF_NVTX();
   af_status st = check_norm_args(c, grad_dev);
   if (st != AF_OK) return st;
   if (flags & ~(AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
@@ -626,6 +642,7 @@ static af_status upload_peers(af_ctx *c, const std::vector<char *> &scratch_of) 
 }
 
 af_status af_ctx_exchange_ipc_handle(af_ctx *c, void *handle_out) {
+  AF_NVTX();
   if (!c || !handle_out) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   IpcRef r{};
@@ -646,6 +663,7 @@ af_status af_ctx_exchange_ipc_handle(af_ctx *c, void *handle_out) {
 }
 
 af_status af_ctx_set_peers_ipc(af_ctx *c, const void *handles) {
+  AF_NVTX();
   if (!c || !handles) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   if (c->peers) return fail(AF_ESTATE, "peers already set");
@@ -667,12 +685,14 @@ af_status af_ctx_set_peers_ipc(af_ctx *c, const void *handles) {
 }
 
 af_status af_ctx_clear_peers(af_ctx *c) {
+  AF_NVTX();
   if (!c) return fail(AF_EINVAL, "NULL ctx");
   c->peers = false;  // mappings stay open until af_ctx_destroy
   return AF_OK;
 }
 
 af_status af_ctx_set_peers_local(af_ctx *c, af_ctx *const *peers) {
+  AF_NVTX();
   if (!c || !peers) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   if (c->peers) return fail(AF_ESTATE, "peers already set");
@@ -682,12 +702,16 @@ af_status af_ctx_set_peers_local(af_ctx *c, af_ctx *const *peers) {
     if (!q || !q->bound || q->cfg.rank != r || q->cfg.world != c->cfg.world || q->L != c->L ||
         q->o_xrows != c->o_xrows || q->o_xflags != c->o_xflags || q->o_rsflags != c->o_rsflags)
       return fail(AF_EINVAL, "peer context mismatch");
+    // a peer bound on another device: its scratch is reached over NVLink
+    const af_status st = enable_peer_access(q->device);
+    if (st != AF_OK) return st;
     scratch_of[r] = q->scratch;
   }
   return upload_peers(c, scratch_of);
 }
 
 af_status af_ctx_set_max_ctas(af_ctx *c, int32_t max_ctas) {
+  AF_NVTX();
   if (!c) return fail(AF_EINVAL, "NULL ctx");
   if (max_ctas < 0) return fail(AF_EINVAL, "max_ctas < 0");
   c->max_ctas = max_ctas;
@@ -713,6 +737,7 @@ static af_status upload_grads(af_ctx *c, const std::vector<const void *> &g) {
 }
 
 af_status af_ctx_grad_ipc_handle(af_ctx *c, const void *grad_dev, void *handle_out) {
+  AF_NVTX();
   if (!c || !grad_dev || !handle_out) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   if (!aligned(grad_dev, 16)) return fail(AF_EINVAL, "gradient buffer must be 16-byte aligned");
@@ -733,6 +758,7 @@ af_status af_ctx_grad_ipc_handle(af_ctx *c, const void *grad_dev, void *handle_o
 }
 
 af_status af_ctx_set_grad_peers_ipc(af_ctx *c, const void *handles) {
+  AF_NVTX();
   if (!c || !handles) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   if (c->cfg.world > kMaxRsWorld) return fail(AF_EINVAL, "fused reduce-scatter supports world <= 8");
@@ -756,12 +782,15 @@ af_status af_ctx_set_grad_peers_ipc(af_ctx *c, const void *handles) {
 }
 
 af_status af_ctx_set_grad_peers_local(af_ctx *c, const void *const *grads_dev) {
+  AF_NVTX();
   if (!c || !grads_dev) return fail(AF_EINVAL, "NULL argument");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
   if (c->cfg.world > kMaxRsWorld) return fail(AF_EINVAL, "fused reduce-scatter supports world <= 8");
   std::vector<const void *> g(c->cfg.world);
   for (int r = 0; r < c->cfg.world; ++r) {
     if (!grads_dev[r] || !aligned(grads_dev[r], 16)) return fail(AF_EINVAL, "gradient buffers must be 16-byte aligned");
+    const af_status st = enable_peer_access_to(grads_dev[r]);
+    if (st != AF_OK) return st;
     g[r] = grads_dev[r];
   }
   c->own_grad = g[c->cfg.rank];
@@ -821,12 +850,14 @@ extern "C" {
 
 af_status af_reduce_scatter_step(af_ctx *c, float scale, float *grad_shard_out_dev, uint32_t flags,
                                  af_decision *out_host, void *stream) {
+  AF_NVTX();
   return rs_step(c, scale, grad_shard_out_dev, nullptr, nullptr, nullptr, nullptr, flags, out_host, stream);
 }
 
 af_status af_reduce_scatter_adamw_step(af_ctx *c, float scale, float *params_dev, float *exp_avg_dev,
                                        float *exp_avg_sq_dev, const af_adamw *hp, float *grad_shard_out_dev,
                                        uint32_t flags, af_decision *out_host, void *stream) {
+  AF_NVTX();
   const af_status st = check_adam(hp, params_dev, exp_avg_dev, exp_avg_sq_dev);
   if (st != AF_OK) return st;
   return rs_step(c, scale, grad_shard_out_dev, hp, params_dev, exp_avg_dev, exp_avg_sq_dev, flags, out_host, stream);
@@ -840,6 +871,7 @@ struct StateBlob {
 };
 
 af_status af_get_state(af_ctx *c, void *buf, size_t *len) {
+  AF_NVTX();
   if (!c || !len) return fail(AF_EINVAL, "NULL argument");
   if (!buf) {
     *len = sizeof(StateBlob);
@@ -868,6 +900,7 @@ af_status af_get_state(af_ctx *c, void *buf, size_t *len) {
 }
 
 af_status af_set_state(af_ctx *c, const void *buf, size_t len) {
+  AF_NVTX();
   if (!c || !buf) return fail(AF_EINVAL, "NULL argument");
   if (len < sizeof(StateBlob)) return fail(AF_EINVAL, "state blob too small");
   if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
@@ -897,7 +930,37 @@ af_status af_set_state(af_ctx *c, const void *buf, size_t len) {
   return AF_OK;
 }
 
+af_status af_ctx_read_record(af_ctx *c, int32_t interval, af_decision *out) {
+  AF_NVTX();
+  if (!c || !out) return fail(AF_EINVAL, "NULL argument");
+  if (!c->bound) return fail(AF_EWORKSPACE, "workspace not bound");
+  if (interval < 0) return fail(AF_ERANGE, "interval < 0");
+  AF_CUDA(cudaDeviceSynchronize(), "read_record sync");
+  af_decision r;
+  AF_CUDA(cudaMemcpy(&r, c->at<af_decision>(c->o_ring) + (interval % kRing), sizeof(r), cudaMemcpyDeviceToHost),
+          "cudaMemcpy(ring record)");
+  // an untouched slot is all zero: interval 0 is told apart by its flags (a decided
+  // record always carries at least one flag bit or a finite threshold)
+  const bool empty = r.interval == 0 && r.flags == 0 && !(r.threshold == r.threshold);
+  if (r.interval != interval || (interval == 0 && empty)) return fail(AF_ERANGE, "interval not in the ring");
+  *out = r;
+  return AF_OK;
+}
+
+af_status af_ctx_set_debug(af_ctx *c, int32_t key, int64_t value) {
+  AF_NVTX();
+  if (!c) return fail(AF_EINVAL, "NULL ctx");
+  switch (key) {
+    case AF_DEBUG_TAIL_DELAY_NS:
+      if (value < 0 || value > 1000000000ll) return fail(AF_EINVAL, "tail delay out of [0, 1e9] ns");
+      c->dbg_tail_delay_ns = static_cast<uint32_t>(value);
+      return AF_OK;
+    default: return fail(AF_EINVAL, "unknown debug key");
+  }
+}
+
 af_status af_ctx_destroy(af_ctx *c) {
+  AF_NVTX();
   if (!c) return fail(AF_EINVAL, "NULL ctx");
   if (c->comm) ncclCommDestroy(c->comm);
   ipc_release(c->ipc_opened);

@@ -31,6 +31,32 @@ int device_sm_count(int *sms) {
   return static_cast<int>(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
 }
 
+af_status enable_peer_access(int device) {
+  int cur = 0;
+  AF_CUDA(cudaGetDevice(&cur), "cudaGetDevice");
+  if (device < 0 || device == cur) return AF_OK;
+  int can = 0;
+  AF_CUDA(cudaDeviceCanAccessPeer(&can, cur, device), "cudaDeviceCanAccessPeer");
+  if (!can) return fail(AF_EINVAL, "peer device not accessible from the current device (no P2P)");
+  const cudaError_t e = cudaDeviceEnablePeerAccess(device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky "already enabled"
+    return AF_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  return AF_OK;
+}
+
+af_status enable_peer_access_to(const void *ptr) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return AF_OK;
+  }
+  if (a.type != cudaMemoryTypeDevice) return AF_OK;
+  return enable_peer_access(a.device);
+}
+
 af_status ipc_export(const void *ptr, IpcRef *out) {
   typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
   void *fn = nullptr;
@@ -111,6 +137,7 @@ const char *af_last_error(void) { return af::g_last_error_cstr(); }
 const char *af_version(void) { return "0.1.0"; }
 
 int af_should_cache(int32_t frozen_layers, double t_layer_fwd_s, double t_batch_read_s) {
+  AF_NVTX();
   if (frozen_layers <= 0 || !(t_layer_fwd_s >= 0.0) || !(t_batch_read_s >= 0.0)) return 0;
   return static_cast<double>(frozen_layers) * t_layer_fwd_s > t_batch_read_s ? 1 : 0;
 }

@@ -2,6 +2,7 @@
 // (error reporting, alignment, device queries, CUDA IPC export/import).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <string>
@@ -22,9 +23,25 @@ const char *g_last_error_cstr();
     if (e_ != cudaSuccess) return ::af::cuda_fail(e_, where); \
   } while (0)
 
+// NVTX range around every C-ABI entry point (SURVEY.md §5 tracing): nsys / ncu
+// timelines show each af_* call with the kernels it enqueued.  Header-only NVTX3;
+// a push/pop costs a few ns when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define AF_NVTX() ::af::NvtxRange af_nvtx_range_(__func__)
+
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 int device_sm_count(int *sms);
+// Peer access from the current device to `device` (no-op for the same device or
+// device < 0; AF_EINVAL when the hardware cannot; "already enabled" is success).
+af_status enable_peer_access(int device);
+// The same for the device that owns allocation `ptr` (host / unregistered: no-op).
+af_status enable_peer_access_to(const void *ptr);
 
 // CUDA IPC export of a pointer that may sit inside a larger allocation (the
 // caller's allocator sub-allocates): handle of the allocation base + offset.

@@ -169,7 +169,13 @@ struct NormParams {
   unsigned long long *rs_flags;    // local [2][world]: ready / done epoch reached by each rank
   unsigned long long *const *peer_rs_flags;  // [world] each rank's rs_flags
   DecideParams dec;
+  uint32_t dbg_tail_delay_ns;      // AF_DEBUG_TAIL_DELAY_NS: the last CTA waits this long before its tail
 };
+
+// Flag value a rank stores into its peers' flag slots after it timed out waiting
+// for one of them (exchange or reduce-scatter barrier): larger than any epoch, so
+// a peer spinning on the slot stops at once and records the timeout too.
+constexpr unsigned long long kPoisonEpoch = ~0ull;
 
 // Cache records: one 16-byte meta word per owned id.  Direct mode: `readers`
 // counts the chunks of a get that have read {depth, valid}; the last one applies

@@ -509,7 +509,12 @@ __device__ __forceinline__ double process_tile_rs(const NormParams &p, const Til
 // which = 0: "my gradient is ready to be read" (every CTA, before its first
 // load), which = 1: "I have finished reading" (the last CTA, before the kernel
 // may complete and the caller's next backward overwrite the buffers).
-__device__ __noinline__ void rs_barrier(const NormParams &p, int which, unsigned long long e) {
+// A timeout is made collective as far as it can be: the rank stores kPoisonEpoch
+// into its slot at every peer, so a peer arriving later stops on it and flags the
+// timeout as well instead of proceeding alone.  Returns true (CTA-uniform) when
+// this CTA saw a timeout or poison: the caller then skips every peer load and
+// every store of the step (the peers' buffers may be incomplete or reused).
+__device__ __noinline__ bool rs_barrier(const NormParams &p, int which, unsigned long long e) {
   const int tid = threadIdx.x, P = p.rs_world;
   __shared__ int s_to;
   if (tid == 0) s_to = 0;
@@ -523,6 +528,10 @@ __device__ __noinline__ void rs_barrier(const NormParams &p, int which, unsigned
     unsigned long long v = 0;
     for (long long spin = 0;; ++spin) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      if (v == kPoisonEpoch) {
+        s_to = 1;
+        break;
+      }
       if (v >= e) break;
       if (spin > (1ll << 22)) {
         s_to = 1;
@@ -532,7 +541,18 @@ __device__ __noinline__ void rs_barrier(const NormParams &p, int which, unsigned
     }
   }
   __syncthreads();
-  if (s_to && tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 2u);
+  const bool to = s_to != 0;
+  if (to && tid < P) {
+    unsigned long long *flag = p.peer_rs_flags[tid] + which * P + p.rs_rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(kPoisonEpoch) : "memory");
+  }
+  if (to && tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 2u);
+  return to;
+}
+
+// the sticky timeout bits, read past L1 (another CTA of this launch may have set them)
+__device__ __forceinline__ uint32_t sticky_of(const NormParams &p) {
+  return *reinterpret_cast<const volatile uint32_t *>(&p.state->sticky);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -562,6 +582,13 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
   const int32_t *stb = seg_ranges<ACT>(p, f);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (AF_TIMING && !WIDE && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
+  if (p.dbg_tail_delay_ns) {  // AF_DEBUG_TAIL_DELAY_NS (ordering tests only)
+    if (tid == 0) {
+      const unsigned long long t0 = gtimer();
+      while (gtimer() - t0 < p.dbg_tail_delay_ns) __nanosleep(1000);
+    }
+    __syncthreads();
+  }
   // peer exchange: this interval end's epoch selects the exchange buffer
   const bool xchg = p.xworld > 1 && p.end;
   __shared__ unsigned long long s_epoch;
@@ -615,7 +642,10 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
       if (lane == 0) publish(l, s);
     }
   }
-  if (xchg) {
+  if (xchg && (sticky_of(p) & 3u)) {
+    // an earlier exchange or barrier timed out (sticky until af_set_state): no peer
+    // stores any more; the peers time out on this rank and flag it as well
+  } else if (xchg) {
     // NVLink one-shot exchange: push this rank's row into every peer's matrix
     // (P x L fp64 stores over peer memory), publish the epoch in every peer's
     // flag slot for this rank, then wait until every rank's epoch has arrived.
@@ -640,6 +670,10 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
       unsigned long long v = 0;
       for (long long spin = 0;; ++spin) {
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+        if (v == kPoisonEpoch) {  // that peer timed out on someone: fail together
+          s_timeout = 1;
+          break;
+        }
         if (v >= e) break;
         if (spin > (1ll << 22)) {  // ~seconds: a peer never arrived -- flag it, do not hang the GPU
           s_timeout = 1;
@@ -649,6 +683,10 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
       }
     }
     __syncthreads();
+    if (s_timeout && tid < p.xworld) {  // make the timeout collective: poison this rank's slot everywhere
+      unsigned long long *flag = p.peer_flags[tid] + p.xrank;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(kPoisonEpoch) : "memory");
+    }
     if (s_timeout && tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 1u);
   }
   if (AF_TIMING) {
@@ -735,13 +773,20 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
   const int first_tile = p.first_tile_of_f[f];
   const int n_end = table_end<ACT>(p, f);  // static: the constant n_tiles
   const GT *rs_g[PM];
+  bool rs_skip = false;  // CTA-uniform: a barrier timed out -- no peer loads, no stores this step
   if constexpr (RS) {
 #pragma unroll
     for (int r = 0; r < PM; ++r) rs_g[r] = r < p.rs_world ? static_cast<const GT *>(p.rs_grads[r]) : nullptr;
     if (p.rs_world > 1) {
-      if (tid == 0) s_rs_epoch = p.state->rs_epoch + 1ull;  // advanced by the last CTA only
+      if (tid == 0) {
+        s_rs_epoch = p.state->rs_epoch + 1ull;  // advanced by the last CTA only
+        s_last = (sticky_of(p) & 3u) != 0u;  // an earlier step timed out (sticky)
+      }
       __syncthreads();
-      rs_barrier(p, 0, s_rs_epoch);  // every rank's gradient is complete before any peer load
+      rs_skip = s_last != 0;
+      __syncthreads();
+      // every rank's gradient is complete before any peer load
+      if (!rs_skip) rs_skip = rs_barrier(p, 0, s_rs_epoch);
     }
   }
 
@@ -790,8 +835,9 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
     if constexpr (MODE == kAdamAccum || MODE == kAdamEnd)
       v = process_tile_adam<MODE == kAdamEnd, GT, RD>(p, t);
     else if constexpr (RS)
-      v = process_tile_rs<MODE == kRsEnd || MODE == kRsAdamEnd, MODE == kRsAdamAccum || MODE == kRsAdamEnd, GT, RD,
-                          PM>(p, t, rs_g);
+      v = rs_skip ? 0.0
+                  : process_tile_rs<MODE == kRsEnd || MODE == kRsAdamEnd, MODE == kRsAdamAccum || MODE == kRsAdamEnd,
+                                    GT, RD, PM>(p, t, rs_g);
     else
       v = process_tile<MODE, GT, RD>(p, t);
     if (tid == 0) {
@@ -854,7 +900,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
     p.sched->done = 0;
   }
   if constexpr (RS) {
-    if (p.rs_world > 1) {
+    if (p.rs_world > 1 && !(sticky_of(p) & 3u)) {
       rs_barrier(p, 1, s_rs_epoch);  // no rank reads this rank's gradient any more
       if (tid == 0) const_cast<DevState *>(p.state)->rs_epoch = s_rs_epoch;
     }

@@ -216,6 +216,35 @@ def test_unbound_calls_report_workspace():
     assert L.lib.af_update_and_decide(fm._h, 0, None, None) == L.AF_EWORKSPACE
 
 
+def test_debug_knob_and_ring_read_host_checks():
+    lay = uniform_layout(1 << 12, 4)
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="f32", bind=False)
+    assert L.lib.af_ctx_set_debug(fm._h, L.AF_DEBUG_TAIL_DELAY_NS, 1000) == L.AF_OK
+    assert L.lib.af_ctx_set_debug(fm._h, L.AF_DEBUG_TAIL_DELAY_NS, -1) == L.AF_EINVAL
+    assert L.lib.af_ctx_set_debug(fm._h, L.AF_DEBUG_TAIL_DELAY_NS, 2 * 10 ** 9) == L.AF_EINVAL
+    assert L.lib.af_ctx_set_debug(fm._h, 99, 0) == L.AF_EINVAL
+    assert L.lib.af_ctx_set_debug(None, L.AF_DEBUG_TAIL_DELAY_NS, 0) == L.AF_EINVAL
+    rec = L.AfDecision()
+    assert L.lib.af_ctx_read_record(fm._h, 0, ctypes.byref(rec)) == L.AF_EWORKSPACE
+    assert L.lib.af_ctx_read_record(fm._h, 0, None) == L.AF_EINVAL
+    fm.close()
+
+
+def test_binding_validates_tensors_before_the_abi():
+    # the ABI sees raw pointers only: the binding refuses wrong dtype / size /
+    # layout / device before any call (out-of-bounds device access)
+    import torch
+    lay = uniform_layout(1 << 12, 4)
+    fm = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="f32", bind=False)
+    with pytest.raises(ValueError):
+        fm.layer_norms(torch.zeros(lay.n))                      # host tensor
+    c = af.ActivationCache(100, 64, bind=False)
+    with pytest.raises(ValueError):
+        c.put(torch.zeros(3, dtype=torch.int64), torch.zeros((3, 64), dtype=torch.uint8), 1)
+    fm.close()
+    c.close()
+
+
 def test_reduce_scatter_host_checks():
     # NEXT 1 (ZeRO form): argument / state errors are synchronous host checks
     lay = uniform_layout(1 << 12, 4)

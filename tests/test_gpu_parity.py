@@ -486,6 +486,90 @@ def test_cache_get_overlapping_the_interval_end():
     assert st == L.AF_EINVAL
 
 
+def _freezing_schedule_step(lay, dt, seed):
+    """g_t = a_l(T) z_l with the tiny config's closed-form schedule a_l(T) =
+    1 + 0.9 rho_l^T (rho rising with depth): the front blocks' eta shrinks first,
+    so the boundary f grows over the intervals (SURVEY.md §8(c) closed form)."""
+    from afinputs import tiny_schedule_a
+    z = np.random.default_rng(seed).standard_normal(lay.n).astype(np.float32) * np.float32(1e-3)
+    n_pool = sum(1 for k in lay.kinds if k == 1)
+    rho, j = [], 0
+    for k in lay.kinds:
+        if k == 1:
+            rho.append(0.3 + 0.6 * j / max(1, n_pool - 1))
+            j += 1
+        else:
+            rho.append(0.3 if k == 0 else 0.95)
+
+    def fn(T, t):
+        amp = np.repeat(np.array([tiny_schedule_a(T, r) for r in rho], np.float32), np.diff(lay.offsets))
+        x = z * amp
+        return f32_to_bf16_bits(x) if dt == "bf16" else x
+    return fn
+
+
+@pytest.mark.parametrize("delay_us", [0, 300])
+def test_overlapped_get_keeps_stream_order_over_committed_intervals(delay_us):
+    """AF_CACHE_OVERLAP_PREV behind COMMITTED interval ends, chained with no host
+    sync and no event between the kernels (records read from the device ring at
+    the end): the first accumulate of each interval follows the overlapped get
+    directly and must see the boundary the interval end committed -- Delta after
+    it equals the oracle's bit for bit (a stale f would overwrite the newly frozen
+    segments' Delta), every decision equals the oracle's, and the boundary chain
+    is continuous.  delay_us widens the window with a busy-wait in the interval
+    end's last CTA before it sums and decides (AF_DEBUG_TAIL_DELAY_NS)."""
+    from paper_2102_01386_b200 import _lib as L
+    from afinputs import cache_rows
+    lay = _ragged_layout()
+    dt, S, n_int = "bf16", 3, 9
+    step = _freezing_schedule_step(lay, dt, 17)
+    fm, oz = _fm(lay, dt), _oracle(lay, dt)
+    fm.set_debug(L.AF_DEBUG_TAIL_DELAY_NS, delay_us * 1000)
+    num, rb = 4000, 24_592
+    gc, oc = _cache_pair(num, rb)
+    ids_all = np.random.default_rng(5).permutation(num)[:3000]
+    rows = cache_rows(3, 2, len(ids_all), rb)
+    gc.put(_ids(ids_all), torch.from_numpy(rows).cuda(), 3)
+    oc.put(ids_all, rows, 3)
+    # every input resident before the chain: no copy between the kernels
+    grads = [[to_device_grad(step(T, t), dt) for t in range(S)] for T in range(n_int)]
+    qs = [np.random.default_rng(200 + T).permutation(num)[:500] for T in range(n_int)]
+    qds = [_ids(q) for q in qs]
+    outs = [torch.full((len(q), rb), 7, dtype=torch.uint8, device="cuda") for q in qs]
+    deps = [torch.zeros(len(q), dtype=torch.int32, device="cuda") for q in qs]
+    snaps = []
+    torch.cuda.synchronize()
+    for T in range(n_int):
+        for t in range(S - 1):
+            fm.layer_norms(grads[T][t])
+            if t == 0:
+                snaps.append(fm.accum[: 4 * lay.n].clone())   # after the step right behind the get
+        fm.interval_end(grads[T][S - 1], copy_record=False)
+        gc.get(qds[T], 3 + (T % 2), outs[T], deps[T], overlap_prev=True)
+    torch.cuda.synchronize()
+    want_snaps, f_seen = [], set()
+    for T in range(n_int):
+        for t in range(S):
+            oz.layer_norms(step(T, t), t == S - 1)
+            if t == 0:
+                want_snaps.append(oz.delta.copy())
+        orr = oz.update_and_decide()
+        gr = fm.read_record(T)
+        compare_records(gr, orr, lay.n_segments, tag=f"T={T}")
+        assert gr["boundary_after"] == orr["boundary_after"], T
+        if T > 0:
+            assert gr["boundary_before"] == fm.read_record(T - 1)["boundary_after"], T
+        f_seen.add(orr["boundary_after"])
+        out_o = np.full((len(qs[T]), rb), 7, np.uint8)
+        dep_o = oc.get(qs[T], 3 + (T % 2), out_o)
+        assert np.array_equal(deps[T].cpu().numpy(), dep_o), T
+        assert np.array_equal(outs[T].cpu().numpy(), out_o), T
+    assert len(f_seen) >= 3, f_seen   # the boundary moved: the ordering was exercised
+    for T in range(n_int):
+        got = snaps[T].view(torch.float32).cpu().numpy()
+        assert np.array_equal(got, want_snaps[T]), f"Delta after the first step of interval {T}"
+
+
 def test_cache_owner_and_range_errors():
     gc, oc = _cache_pair(10, 64, rank=1, world=4)
     rows = torch.zeros((4, 64), dtype=torch.uint8, device="cuda")
@@ -815,6 +899,48 @@ def test_near_tie_is_flagged_on_both_sides():
     g, o = recs[1]
     assert o["flags"] & O.FLAG_NEAR_TIE and g["flags"] & O.FLAG_NEAR_TIE
     assert g["near_tie_seg"] == o["near_tie_seg"] == 0
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_near_tie_window_golden_cases(fused):
+    """GPU twin of the CPU pins (tests/golden/near_tie_window.json, Q16): the same
+    eta injected through the exchange rows gives bit-equal k, flags and
+    near_tie_seg on the decide kernel and on the fused interval end's last CTA."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "near_tie_window.json")) as fh:
+        cases = json.load(fh)["cases"]
+    for c in cases:
+        n_pool = len(c["etas"])
+        lay = uniform_layout(16 * (n_pool + 2), n_pool, pre=1, head=1)
+        fm, oz = _fm(lay, "f32", percentile=c["N"]), _oracle(lay, "f32", percentile=c["N"])
+        cur = np.ones(lay.n_segments)
+        cur[1:1 + n_pool] = 1.0 - np.asarray(c["etas"])
+        if fused:
+            g = torch.zeros(lay.n, device="cuda")
+            rows = fm.exchange_rows()
+            recs = []
+            for ss in (np.ones(lay.n_segments), cur * cur):
+                # the fused launch writes its own sums into the row; inject by making
+                # them the sums of a gradient: g = sqrt(ss) on the segment's first element
+                gh = np.zeros(lay.n, np.float32)
+                for l in range(lay.n_segments):
+                    gh[lay.offsets[l]] = np.float32(math.sqrt(ss[l]))
+                ss32 = np.array([float(gh[lay.offsets[l]]) ** 2 for l in range(lay.n_segments)])
+                fm.interval_end(torch.from_numpy(gh).cuda())
+                oz.pending = ss32
+                recs.append((fm.decision(), oz.update_and_decide()))
+            del rows, g
+        else:
+            recs = _inject(fm, oz, [np.ones(lay.n_segments), cur * cur], lay)
+        gr, orr = recs[1]
+        want_seg = c["near_tie_pool_index"] + 1 if c["near_tie_pool_index"] >= 0 else -1
+        for r in (gr, orr):
+            assert r["boundary_after"] - r["boundary_before"] == c["k"], (c["name"], fused)
+            assert bool(r["flags"] & O.FLAG_NEAR_TIE) == c["near_tie"], (c["name"], fused)
+            assert r["near_tie_seg"] == want_seg, (c["name"], fused)
+        assert gr["flags"] == orr["flags"] and gr["threshold"] == orr["threshold"], c["name"]
+        assert np.array_equal(np.array(gr["eta"][:lay.n_segments]), orr["eta"]), c["name"]
 
 
 def test_min_active_and_percentile_100():

@@ -302,6 +302,46 @@ def test_embedding_frozen_with_first_block_head_never():
     assert 13 in O.active_segments(lay.kinds, 11)
 
 
+# ------------------------------------------------------------------ near-tie window (Q16)
+
+def _near_tie_case(c):
+    """Drive the oracle through a first interval with every norm 1, then one with
+    current norm 1 - eta per active POOL layer (one PRE and one HEAD around the pool,
+    so a pool index maps to segment index + 1)."""
+    n_pool = len(c["etas"])
+    lay = uniform_layout(16 * (n_pool + 2), n_pool, pre=1, head=1)
+    fz = O.Freezer(lay.offsets, lay.kinds, O.DT_F32, percentile=c["N"])
+    fz.pending = np.ones(lay.n_segments)
+    fz.update_and_decide()
+    cur = np.ones(lay.n_segments)
+    cur[1:1 + n_pool] = 1.0 - np.asarray(c["etas"])
+    fz.pending = cur * cur
+    return fz.update_and_decide()
+
+
+def test_near_tie_golden_thresholds_are_the_exact_type7_values(golden):
+    # the derivation in the fixture: thr is within 1e-12 of the exact rational
+    # Hyndman-Fan 7 value, so the 1e-6 margins around the window hold
+    for c in golden("near_tie_window.json")["cases"]:
+        rec = _near_tie_case(c)
+        assert abs(Fraction(rec["threshold"]) - _type7_exact(c["etas"], c["N"])) < Fraction(1, 10 ** 12), c["name"]
+
+
+def test_near_tie_window_scans_up_to_and_including_the_first_failure(golden):
+    """Q16 / Alg. 1: (i) a near-tie before the break is flagged; (ii) a
+    first failure inside the window is flagged; (iii) a near-tie only after the
+    first failure is NOT flagged; (iv) a self-tie (t = 0, distance 0) is not."""
+    cases = golden("near_tie_window.json")["cases"]
+    for tag in ("i_", "ii_", "iii_", "iv_"):
+        assert any(c["name"].startswith(tag) for c in cases), tag
+    for c in cases:
+        rec = _near_tie_case(c)
+        assert rec["boundary_after"] - rec["boundary_before"] == c["k"], c["name"]
+        assert bool(rec["flags"] & O.FLAG_NEAR_TIE) == c["near_tie"], c["name"]
+        want_seg = c["near_tie_pool_index"] + 1 if c["near_tie_pool_index"] >= 0 else -1
+        assert rec["near_tie_seg"] == want_seg, c["name"]
+
+
 def test_update_without_interval_end_raises():
     lay = tiny_layout()
     fz = O.Freezer(lay.offsets, lay.kinds)
