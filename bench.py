@@ -67,6 +67,9 @@ def parse():
                          "interval end are af_reduce_scatter_step (the gradient sync fused in, peer pulls)")
     ap.add_argument("--unfused", action="store_true",
                     help="interval end as af_layer_norms(END) + af_update_and_decide (two launches)")
+    ap.add_argument("--no-shard-probe", action="store_true",
+                    help="N = 1: skip the per-rank shard probe of the 8-GPU BERT-large run (rank_shard_p8)")
+    ap.add_argument("--shard-probe-only", action="store_true", help="print only the rank_shard_p8 probe")
     ap.add_argument("--sweep", action="store_true",
                     help="configs[4]: layers x elements sweep, one JSON line per point (not the bench line)")
     return ap.parse_args()
@@ -433,6 +436,8 @@ def run_ours(args, rank, world, local):
         result["e2e"] = run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(lay, dt, s_g, B, budget_s=12.0)
+    if world == 1 and not args.no_shard_probe and args.workload == "bert-large-f32":
+        result["rank_shard_p8"] = rank_shard_probe(args, dev)
     if world == 1 and not args.no_secondary:
         result["secondary"] = secondary_workload(args)
     if rank == 0:
@@ -721,6 +726,93 @@ def rs_probe(lay, dt, s_g, grads, dev, reps=20):
                              "frac_of_peak": round(by_end / (ms_end * 1e-3) / 1e9 / peak, 4)}}
 
 
+def rank_shard_probe(args, dev, P=8, ranks=(0, 3, 7), rounds=3):
+    """One rank's share of the P-GPU run, timed on this GPU (BERT-large at P = 8:
+    ~41.9M elements per rank).  All P contexts live here with the
+    NVLink one-shot exchange registered locally (set_peers_local); only rank r's
+    kernels run, with AF_DEBUG_PEERS_ARRIVED so its exchange pushes its row to
+    the 7 peer contexts but does not wait for theirs.  So the numbers exclude the
+    NVLink store latency (~1-2 us) and cross-rank skew, and include everything
+    else of the rank's interval end (streaming, finalize, exchange stores,
+    decision).  In-step = marginal device time in graph-replayed [accumulate,
+    interval end] steps (with minus without the interval end); alone = the
+    interval end replayed back to back."""
+    import torch
+
+    import paper_2102_01386_b200 as af
+    from paper_2102_01386_b200 import _lib as L
+    from afinputs import bert_layout
+    which, dt = WORKLOADS[args.workload]
+    lay = bert_layout(which)
+    s_g = 2 if dt == "bf16" else 4
+    peak, _ = measured_peaks()
+    fms = [af.FreezingModule(lay.offsets, lay.kinds, grad_dtype=dt, rank=r, world=P, device=dev,
+                             shard_active=True) for r in range(P)]
+    for fm in fms:
+        fm.set_peers_local(fms)
+    g = [device_grad(lay, dt, 1000 + k, dev) for k in range(2)]
+    steps = max(20, min(args.steps, 200))
+    res = {"world_emulated": P, "workload": args.workload,
+           "method": rank_shard_probe.__doc__.split("\n\n")[0].replace("\n", " ").strip()[:400]}
+    worst = None
+    for r in ranks:
+        fm = fms[r]
+        fm.set_debug(L.AF_DEBUG_PEERS_ARRIVED, 1)
+        fm.layer_norms(g[0])
+        fm.interval_end(g[1])
+        fm.layer_norms(g[0])               # Delta armed; T = 1: every dry decision does the full test
+        torch.cuda.synchronize()
+        info = fm.info()
+        n_loc = info["shard_end"] - info["shard_begin"]
+
+        def graph(with_acc, with_end, reps=8):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                for i in range(reps):
+                    if with_acc:
+                        fm.layer_norms(g[i & 1], dry_run=True)
+                    if with_end:
+                        fm.interval_end(g[(i + 1) & 1], dry_run=True, copy_record=False)
+            return gph, reps
+        sets = {"full": graph(True, True), "acc": graph(True, False), "end": graph(False, True)}
+        t = {k: [] for k in sets}
+        for _ in range(rounds):
+            for k, (gph, reps) in sets.items():
+                for _ in range(3):
+                    gph.replay()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                n_rep = max(1, steps // reps)
+                a.record()
+                for _ in range(n_rep):
+                    gph.replay()
+                b.record()
+                torch.cuda.synchronize()
+                t[k].append(a.elapsed_time(b) / (n_rep * reps))
+        full, acc, alone = (statistics.median(t[k]) for k in ("full", "acc", "end"))
+        in_step = full - acc
+        by = n_loc * (s_g + 4)
+        row = {"n_local": n_loc, "interval_end_in_step_us": round(in_step * 1e3, 2),
+               "gbs_in_step": round(by / (in_step * 1e-3) / 1e9, 1),
+               "frac_in_step": round(by / (in_step * 1e-3) / 1e9 / peak, 4),
+               "interval_end_alone_us": round(alone * 1e3, 2),
+               "gbs_alone": round(by / (alone * 1e-3) / 1e9, 1),
+               "frac_alone": round(by / (alone * 1e-3) / 1e9 / peak, 4),
+               "accumulate_us": round(acc * 1e3, 2),
+               "accumulate_frac": round(n_loc * (s_g + 8) / (acc * 1e-3) / 1e9 / peak, 4)}
+        res[f"rank{r}"] = row
+        if worst is None or row["interval_end_in_step_us"] > worst["interval_end_in_step_us"]:
+            worst = dict(row, rank=r)
+        fm.set_debug(L.AF_DEBUG_PEERS_ARRIVED, 0)
+        del sets
+    res["max_over_ranks"] = worst
+    for fm in fms:
+        fm.close()
+    del fms, g
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_sweep(args, local):
     """configs[4]: uniform layouts, L in {1,2,4,12,24,48} POOL segments x n in
     {1M..1B} elements, fp32 and bf16, one GPU; accumulate and interval-end GB/s."""
@@ -933,6 +1025,11 @@ def main():
         return
     if args.sweep:
         run_sweep(args, local)
+        return
+    if args.shard_probe_only:
+        import torch
+        torch.cuda.set_device(local)
+        print(json.dumps({"rank_shard_p8": rank_shard_probe(args, torch.device("cuda", local))}), flush=True)
         return
     run_ours(args, rank, world, local)
 

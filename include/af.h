@@ -157,10 +157,10 @@ typedef struct {
                                        into the concatenated per-f tables when shard_active) */
   int32_t n_tiles_acc;              /* tiles of the accumulate kernel (finer, no partials) */
   int32_t tile_elems_acc;
-  int32_t n_fin_ctas;               /* > 0: interval ends launch a second, wide finalize
-                                       kernel of this many CTAs after the streaming kernel */
-  int32_t n_fin_chunks;             /* > 0: the interval end's partials are reduced in chunks
-                                       of 2048 tiles (wide finalize, in-kernel or launched) */
+  int32_t n_fin_ctas;               /* 0: no second launch (the finalize runs inside the
+                                       streaming kernel; kept for layout compatibility) */
+  int32_t n_fin_chunks;             /* chunks of 256 tiles in which the streaming grid's CTAs
+                                       reduce the interval end's per-tile partials */
 } af_info;
 
 typedef struct af_ctx af_ctx;
@@ -216,7 +216,7 @@ AF_API af_status af_ctx_exchange_rows(af_ctx *ctx, double **ss_all_dev);
  * peer's flag slot (st.release.sys) and waits for all ranks' epochs
  * (ld.acquire.sys, bounded spin: a missing peer sets AF_DEC_EXCHANGE_TIMEOUT
  * instead of hanging) -- af_interval_end needs no collective launch at any
- * world size (the streaming kernel, plus the wide finalize when n_fin_ctas > 0).
+ * world size (one streaming kernel; its CTAs also reduce the partials).
  * A timeout is FATAL for the job: the rank that timed out poisons its flag slot
  * in every peer, so a peer that arrives later flags EXCHANGE_TIMEOUT too instead
  * of committing alone (best effort: a peer that had already read the rank's
@@ -256,10 +256,10 @@ AF_API af_status af_update_and_decide(af_ctx *ctx, uint32_t flags, af_decision *
 
 /* Fused interval end: exactly af_layer_norms(AF_INTERVAL_END |
  * flags) followed by af_update_and_decide(flags), same results and state.  With
- * world == 1 or peers registered, no host involvement: the streaming kernel, then
- * (af_info.n_fin_ctas > 0) a wide finalize kernel chained by programmatic
- * dependent launch; the last CTA sums the segments, exchanges rows with the peers
- * and runs the decision.  With world > 1 and only a communicator: kernel, NCCL
+ * world == 1 or peers registered, no host involvement and ONE kernel launch: the
+ * streaming kernel's CTAs reduce the per-tile partials as they run out of tiles,
+ * and the CTA finishing the last chunk sums the segments, exchanges rows with the
+ * peers and runs the decision.  With world > 1 and only a communicator: kernel, NCCL
  * all-gather, decide kernel.  flags: AF_DRY_RUN only. */
 AF_API af_status af_interval_end(af_ctx *ctx, const void *grad_dev, uint32_t flags, af_decision *out_host,
                                  void *stream);
@@ -351,6 +351,11 @@ AF_API af_status af_ctx_read_record(af_ctx *ctx, int32_t interval, af_decision *
  * widening the window in which later kernels could observe an uncommitted
  * decision (ordering tests). */
 #define AF_DEBUG_TAIL_DELAY_NS 1
+/* AF_DEBUG_PEERS_ARRIVED (0/1): with peers registered, the interval end pushes
+ * its row and epoch to every peer but does not wait for theirs -- times ONE rank's
+ * interval end on a single GPU (the other ranks' contexts registered locally,
+ * never launched).  The decision then uses whatever rows the peers hold. */
+#define AF_DEBUG_PEERS_ARRIVED 2
 AF_API af_status af_ctx_set_debug(af_ctx *ctx, int32_t key, int64_t value);
 
 AF_API af_status af_ctx_destroy(af_ctx *ctx);

@@ -281,12 +281,23 @@ __global__ void __launch_bounds__(kCacheThreads) cache_kernel(const CacheParams 
   // AF_CACHE_OVERLAP_PREV: the copy above ran without waiting for the preceding
   // kernel, but the get must not COMPLETE before it -- every later kernel waits
   // only on the get, and the preceding interval end may still be committing f /
-  // prev / T in its last CTA (or spinning on peers there).  Waiting here keeps
-  // PDL's transitive order: get complete => predecessor complete.
-#ifndef AF_CACHE_OVERLAP_UNSAFE  // diagnostic build only: the round-1 behaviour the ordering test must catch
-  if (p.no_wait) pdl_wait();
-#endif
+  // prev / T in its last CTA (or spinning on peers there).  So the last CTA to
+  // finish its copies waits for the predecessor before it exits: get complete
+  // => predecessor complete, while every other CTA retires at once and frees its
+  // SM for the next kernels (all CTAs waiting cost ~9 us per step,
+  // profiles/r02_v7_*).
   pdl_launch_dependents();
+#ifndef AF_CACHE_OVERLAP_UNSAFE  // diagnostic build only: the round-1 behaviour the ordering test must catch
+  if (p.no_wait) {
+    __shared__ int s_last_get;
+    if (threadIdx.x == 0) s_last_get = atomicAdd(p.retire, 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (s_last_get && threadIdx.x == 0) {
+      *p.retire = 0u;  // every CTA has counted: re-armed for the next call
+      pdl_wait();
+    }
+  }
+#endif
   if (threadIdx.x == 0) bulk_wait_all();  // all stores complete before the CTA retires its shared memory
 }
 

@@ -146,6 +146,7 @@ static af_status cache_common(af_cache *c, const int64_t *ids, int32_t n, const 
   p.payload = c->payload;
   p.meta = reinterpret_cast<CacheMeta *>(c->meta + kMetaHeader);
   p.err = reinterpret_cast<unsigned int *>(c->meta);
+  p.retire = reinterpret_cast<unsigned int *>(c->meta + 64);  // header word (CacheHeader is 16 B of 256)
   p.ids = ids;
   p.n = n;
   p.row_bytes = c->row_bytes;

@@ -46,7 +46,7 @@ struct af_ctx {
   size_t accum_bytes = 0, scratch_bytes = 0;
   size_t o_state = 0, o_sched = 0, o_pool = 0, o_part = 0, o_part2 = 0, o_chunk = 0, o_ssall = 0,
          o_ssacc = 0, o_last = 0, o_ring = 0, o_xrows = 0,
-         o_xflags = 0, o_peer_rows = 0, o_peer_flags = 0, o_rsflags = 0, o_peer_rsflags = 0, o_rs_grads = 0;
+         o_peer_rows = 0, o_rsflags = 0, o_peer_rsflags = 0, o_rs_grads = 0;
   float *accum = nullptr;
   char *scratch = nullptr;
   bool bound = false;
@@ -65,6 +65,7 @@ struct af_ctx {
   const void *own_grad = nullptr;   // this rank's buffer (af_ctx_grad_ipc_handle)
   int device = -1;                  // the device the workspace was bound on
   uint32_t dbg_tail_delay_ns = 0;   // AF_DEBUG_TAIL_DELAY_NS
+  int32_t dbg_peers_arrived = 0;    // AF_DEBUG_PEERS_ARRIVED
 
   template <typename T>
   T *at(size_t o) const {
@@ -142,6 +143,7 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   }
   c->sb = c->sb_of_f[0];
   c->se = c->se_of_f[0];
+
   // segment-aligned tile tables (tile edges on a global grid of tile_elems)
   const bool bf16 = (c->dtype == AF_DT_BF16);
   c->ts[0].tile_elems = bf16 ? AF_TILE_ACC_BF16 : AF_TILE_ACC_F32;
@@ -209,10 +211,8 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   // address each other's exchange buffers by these offsets), then the tile tables
   c->o_state = take(sizeof(DevState));
   c->o_sched = take(4 * sizeof(Sched));
-  c->o_xrows = take(2 * static_cast<size_t>(cfg->world) * L * sizeof(double));
-  c->o_xflags = take(static_cast<size_t>(cfg->world) * sizeof(unsigned long long));
+  c->o_xrows = take(2 * static_cast<size_t>(cfg->world) * L * 2 * sizeof(unsigned long long));  // LL words
   c->o_peer_rows = take(static_cast<size_t>(cfg->world) * sizeof(void *));
-  c->o_peer_flags = take(static_cast<size_t>(cfg->world) * sizeof(void *));
   c->o_rsflags = take(2 * static_cast<size_t>(cfg->world) * sizeof(unsigned long long));
   c->o_peer_rsflags = take(static_cast<size_t>(cfg->world) * sizeof(void *));
   c->o_rs_grads = take(static_cast<size_t>(cfg->world) * sizeof(void *));
@@ -221,6 +221,7 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
   c->o_last = take(sizeof(af_decision));
   c->o_ring = take(kRing * sizeof(af_decision));
   c->o_pool = take(n_pool * sizeof(int32_t));
+
   for (auto &T : c->ts) {
     T.o_ftf = take((n_pool + 1) * sizeof(int32_t));
     T.o_tef = take((n_pool + 1) * sizeof(int32_t));
@@ -228,8 +229,7 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
     T.o_tiles = take(T.tiles.size() * sizeof(Tile));
   }
   c->o_part = take(c->ts[1].tiles.size() * sizeof(double));
-  c->o_part2 = take((static_cast<size_t>(c->ts[1].max_tiles) / kFinChunkMin + L + 2) * sizeof(double));
-  c->o_chunk = take((static_cast<size_t>(c->ts[1].max_tiles) / kFinChunk + 2) * sizeof(unsigned int));
+  c->o_part2 = take((static_cast<size_t>(c->ts[1].max_tiles) / kFinChunk + L + 2) * sizeof(double));
   c->scratch_bytes = o;
   *out = c;
   return AF_OK;
@@ -258,8 +258,8 @@ af_status af_ctx_info(const af_ctx *c, af_info *info) {
   info->tile_elems = c->ts[1].tile_elems;
   info->n_tiles_acc = c->ts[0].max_tiles;
   info->tile_elems_acc = c->ts[0].tile_elems;
-  info->n_fin_chunks = af::fin_ctas(c->cfg.acc_mode == AF_ACC_DELTA ? kEndDelta : kStepSq, c->ts[1].max_tiles);
-  info->n_fin_ctas = AF_FIN_WIDE == 1 ? info->n_fin_chunks : 0;
+  info->n_fin_chunks = (c->ts[1].max_tiles + kFinChunk - 1) / kFinChunk;
+  info->n_fin_ctas = 0;  // the finalize runs inside the streaming kernel (fin_worker)
   for (int j = 0; j <= c->n_pool; ++j) info->first_tile_of_pool[j] = c->ts[1].first_tile_of_f[j];
   return AF_OK;
 }
@@ -312,6 +312,12 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
   }
   AF_CUDA(cudaMemcpy(c->scratch + c->o_pool, c->pool_seg.data(), c->pool_seg.size() * 4, cudaMemcpyHostToDevice),
           "cudaMemcpy(pool_seg)");
+  {  // every partial slot starts empty (the finalize waits for non-empty slots)
+    const std::vector<unsigned long long> empty(c->ts[1].tiles.size(), kPartialEmpty);
+    if (!empty.empty())
+      AF_CUDA(cudaMemcpy(c->scratch + c->o_part, empty.data(), empty.size() * 8, cudaMemcpyHostToDevice),
+              "cudaMemcpy(partials)");
+  }
   AF_CUDA(cudaDeviceSynchronize(), "bind");
   c->bound = true;
   c->armed = false;
@@ -380,7 +386,6 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   p.partials = c->at<double>(c->o_part);
   p.part2 = c->at<double>(c->o_part2);
   p.fin_sched = c->at<Sched>(c->o_sched) + 2;
-  p.chunk_cnt = c->at<unsigned int>(c->o_chunk);
   p.ss_out = c->at<double>(c->o_ssall) + static_cast<size_t>(c->cfg.rank) * c->L;
   p.ss_acc = c->at<double>(c->o_ssacc);
   p.n_pool = c->n_pool;
@@ -389,14 +394,14 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   p.first = c->armed ? 0 : 1;
   p.end = end ? 1 : 0;
   p.dbg_tail_delay_ns = c->dbg_tail_delay_ns;
+
+  p.dbg_peers_arrived = c->dbg_peers_arrived;
   p.commit = dry ? 0 : 1;
   if (c->peers) {
     p.xworld = c->cfg.world;
     p.xrank = c->cfg.rank;
-    p.xrows = c->at<double>(c->o_xrows);
-    p.peer_rows = c->at<double *const>(c->o_peer_rows);
-    p.xflags = c->at<unsigned long long>(c->o_xflags);
-    p.peer_flags = c->at<unsigned long long *const>(c->o_peer_flags);
+    p.xrows = c->at<unsigned long long>(c->o_xrows);
+    p.peer_rows = c->at<unsigned long long *const>(c->o_peer_rows);
   }
   return p;
 }
@@ -408,8 +413,7 @@ int norm_mode(const af_ctx *c, bool end) {
 
 DecideParams decide_params(af_ctx *c, bool dry, af_decision *out_host) {
   DecideParams p{};
-  p.ss_all = c->peers ? c->at<double>(c->o_xrows) : c->at<double>(c->o_ssall);
-  p.xparity = c->peers ? 1 : 0;
+  p.ss_all = c->at<double>(c->o_ssall);  // the peer exchange assembles its rows here too
   p.world = c->cfg.world;
   p.L = c->L;
   p.n_pool = c->n_pool;
@@ -614,18 +618,16 @@ af_status af_interval_end(af_ctx *c, const void *grad_dev, uint32_t flags, af_de
 struct IpcHandle {  // AF_IPC_HANDLE_BYTES
   cudaIpcMemHandle_t h;
   uint64_t offset;                 // scratch offset inside the exported allocation
-  uint64_t xrows_off, xflags_off;  // exchange-area offsets inside the scratch
+  uint64_t xrows_off, pad0;        // exchange-area offset inside the scratch
   uint64_t rsflags_off;            // fused reduce-scatter flags inside the scratch
   int32_t rank, world, L, pad;
 };
 static_assert(sizeof(IpcHandle) <= AF_IPC_HANDLE_BYTES, "ipc handle size");
 
 static af_status upload_peers(af_ctx *c, const std::vector<char *> &scratch_of) {
-  std::vector<double *> rows(c->cfg.world);
-  std::vector<unsigned long long *> flags(c->cfg.world), rsflags(c->cfg.world);
+  std::vector<unsigned long long *> rows(c->cfg.world), rsflags(c->cfg.world);
   for (int r = 0; r < c->cfg.world; ++r) {
-    rows[r] = reinterpret_cast<double *>(scratch_of[r] + c->o_xrows);
-    flags[r] = reinterpret_cast<unsigned long long *>(scratch_of[r] + c->o_xflags);
+    rows[r] = reinterpret_cast<unsigned long long *>(scratch_of[r] + c->o_xrows);
     rsflags[r] = reinterpret_cast<unsigned long long *>(scratch_of[r] + c->o_rsflags);
   }
   AF_CUDA(cudaMemcpy(c->scratch + c->o_peer_rsflags, rsflags.data(), rsflags.size() * sizeof(void *),
@@ -633,9 +635,6 @@ static af_status upload_peers(af_ctx *c, const std::vector<char *> &scratch_of) 
           "cudaMemcpy(peer rs flags)");
   AF_CUDA(cudaMemcpy(c->scratch + c->o_peer_rows, rows.data(), rows.size() * sizeof(void *), cudaMemcpyHostToDevice),
           "cudaMemcpy(peer rows)");
-  AF_CUDA(cudaMemcpy(c->scratch + c->o_peer_flags, flags.data(), flags.size() * sizeof(void *),
-                     cudaMemcpyHostToDevice),
-          "cudaMemcpy(peer flags)");
   AF_CUDA(cudaDeviceSynchronize(), "set peers");
   c->peers = true;
   return AF_OK;
@@ -652,7 +651,6 @@ af_status af_ctx_exchange_ipc_handle(af_ctx *c, void *handle_out) {
   h.h = r.h;
   h.offset = r.offset;
   h.xrows_off = c->o_xrows;
-  h.xflags_off = c->o_xflags;
   h.rsflags_off = c->o_rsflags;
   h.rank = c->cfg.rank;
   h.world = c->cfg.world;
@@ -672,7 +670,7 @@ af_status af_ctx_set_peers_ipc(af_ctx *c, const void *handles) {
     IpcHandle h;
     std::memcpy(&h, static_cast<const char *>(handles) + static_cast<size_t>(r) * AF_IPC_HANDLE_BYTES, sizeof(h));
     if (h.rank != r || h.world != c->cfg.world || h.L != c->L || h.xrows_off != c->o_xrows ||
-        h.xflags_off != c->o_xflags || h.rsflags_off != c->o_rsflags)
+        h.rsflags_off != c->o_rsflags)
       return fail(AF_EINVAL, "peer handle mismatch");
     if (r == c->cfg.rank) {
       scratch_of[r] = c->scratch;
@@ -700,7 +698,7 @@ af_status af_ctx_set_peers_local(af_ctx *c, af_ctx *const *peers) {
   for (int r = 0; r < c->cfg.world; ++r) {
     const af_ctx *q = peers[r];
     if (!q || !q->bound || q->cfg.rank != r || q->cfg.world != c->cfg.world || q->L != c->L ||
-        q->o_xrows != c->o_xrows || q->o_xflags != c->o_xflags || q->o_rsflags != c->o_rsflags)
+        q->o_xrows != c->o_xrows || q->o_rsflags != c->o_rsflags)
       return fail(AF_EINVAL, "peer context mismatch");
     // a peer bound on another device: its scratch is reached over NVLink
     const af_status st = enable_peer_access(q->device);
@@ -954,6 +952,10 @@ af_status af_ctx_set_debug(af_ctx *c, int32_t key, int64_t value) {
     case AF_DEBUG_TAIL_DELAY_NS:
       if (value < 0 || value > 1000000000ll) return fail(AF_EINVAL, "tail delay out of [0, 1e9] ns");
       c->dbg_tail_delay_ns = static_cast<uint32_t>(value);
+      return AF_OK;
+    case AF_DEBUG_PEERS_ARRIVED:
+      if (value != 0 && value != 1) return fail(AF_EINVAL, "peers-arrived knob is 0 or 1");
+      c->dbg_peers_arrived = static_cast<int32_t>(value);
       return AF_OK;
     default: return fail(AF_EINVAL, "unknown debug key");
   }

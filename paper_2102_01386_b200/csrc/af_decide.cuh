@@ -35,25 +35,18 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
 
   // Latency-bound: every global load below is independent of the others, so
   // they are in flight together (one L2 round trip) -- the state words, this
-  // segment's previous norm, the POOL map, and the exchange rows of BOTH
-  // buffers when they are double-buffered (the epoch's parity picks one after
-  // the loads; each is summed in rank order, the other discarded).
+  // segment's previous norm, the POOL map and the P exchange rows (summed in
+  // rank order).
   const int t = threadIdx.x;
   const int L = p.L;
   const int T = p.state->T;
   int f = p.state->f;
-  const unsigned long long epoch = p.xparity ? p.state->epoch : 0ull;
   const double pv = (t < L) ? p.state->prev[t] : 0.0;
   if (t < p.n_pool) s_pool[t] = p.pool_seg[t];
-  double ss = 0.0, ss_odd = 0.0;
+  double ss = 0.0;
   if (t < L) {
-    const size_t stride = static_cast<size_t>(p.world) * L;
-    for (int r = 0; r < p.world; ++r) {
-      ss = __dadd_rn(ss, __ldcg(p.ss_all + r * L + t));
-      if (p.xparity) ss_odd = __dadd_rn(ss_odd, __ldcg(p.ss_all + stride + r * L + t));
-    }
+    for (int r = 0; r < p.world; ++r) ss = __dadd_rn(ss, __ldcg(p.ss_all + r * L + t));
   }
-  if (epoch & 1ull) ss = ss_odd;
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int n_act = p.n_pool - f;
 
@@ -72,7 +65,7 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
   __syncthreads();
 
   // a peer never arrived: at the exchange (bit 0) or at a fused reduce-scatter barrier (bit 1)
-  const bool xfail = (p.xparity && (p.state->sticky & 1u)) || (p.state->sticky & 2u);
+  const bool xfail = (p.state->sticky & 3u) != 0u;
   const bool nonfinite = s_nonfinite != 0 || xfail;
   unsigned int flags = p.commit ? 0u : AF_DEC_DRY_RUN;
   if (xfail) flags |= AF_DEC_EXCHANGE_TIMEOUT;

@@ -66,21 +66,18 @@ struct DevState {
   double prev[AF_MAX_SEGMENTS];  // ||Delta_{T-1,l}||
 };
 
-#ifndef AF_FIN_WIDE  // 0: the streaming kernel's last CTA sums all partials; 1: a second, wide
-#define AF_FIN_WIDE 1   // finalize launch; 2: chunks reduced inside the streaming kernel as they
-#endif              // complete; 3: the streaming kernel's last-retiring CTAs reduce the chunks
-#ifndef AF_FIN3_CHUNK  // AF_FIN_WIDE == 3: partials per chunk (one load per thread at 256)
-#define AF_FIN3_CHUNK 256
-#endif
-#ifndef AF_FIN3_MIN_TILES  // AF_FIN_WIDE == 3 above this many tiles (the last CTA alone below)
-#define AF_FIN3_MIN_TILES 2048
-#endif
 #ifndef AF_ALTERNATE_ORDER  // alternate the streaming kernels' tile order per launch (L2 reuse)
 #define AF_ALTERNATE_ORDER 1
 #endif
-constexpr int kFinChunk = 2048;  // partials per fin_kernel CTA (8 per thread)
-constexpr int kFin3Chunk = AF_FIN3_CHUNK;
-constexpr int kFinChunkMin = kFin3Chunk < kFinChunk ? kFin3Chunk : kFinChunk;  // sizes part2
+#ifndef AF_FIN_CHUNK  // tiles per finalize chunk (a multiple of the 256 threads)
+#define AF_FIN_CHUNK 256
+#endif
+constexpr int kFinChunk = AF_FIN_CHUNK;
+static_assert(kFinChunk % 256 == 0, "finalize chunk: whole loads per thread");
+// An empty partial slot: a signalling-NaN bit pattern, which no fp64 arithmetic
+// produces (NaN results are quiet), so the store of a tile's partial is its own
+// ready flag.  Every slot holds it between launches.
+constexpr unsigned long long kPartialEmpty = 0x7FF0DEADBEEF0001ull;
 
 enum Mode : int {
   kAccum = 0, kEndDelta = 1, kStepSq = 2, kAdamAccum = 3, kAdamEnd = 4,
@@ -113,7 +110,6 @@ struct DecideParams {
   double tie_rel_eps;
   int32_t min_active;
   int32_t commit;           // 0 under AF_DRY_RUN
-  int32_t xparity;          // peer exchange: rows live in buffer (state->epoch & 1) of 2
 };
 
 // Arguments of the streaming kernels (accumulate / interval-end sum of squares).
@@ -130,16 +126,11 @@ struct NormParams {
   int32_t stb_stride;              // 0: one table (static shards); L + 1: one per f (active-suffix shards)
   const DevState *state;           // reads f
   Sched *sched;
-  double *partials;                // [n_tiles]
-  // wide finalize (n_tiles > kFinChunk): the streaming kernel only writes the
-  // partials; fin_kernel's CTAs reduce chunks of kFinChunk partials into
-  // part2[chunk + segment] and its last CTA combines them in chunk order
-  int32_t wide_fin;                // 0: narrow; 1: fin_kernel launch; 2: chunks reduced in-kernel;
-                                   // 3: chunks reduced by the last-retiring CTAs
-  int32_t fin_chunk;               // tiles per chunk (kFinChunk; kFin3Chunk when wide_fin == 3)
-  double *part2;                   // [n_tiles / fin_chunk + L + 2]
-  Sched *fin_sched;                // done counter of fin_kernel
-  unsigned int *chunk_cnt;         // [n_tiles / kFinChunk + 1] finished tiles per chunk (in-kernel form)
+  double *partials;                // [n_tiles] one fp64 partial per tile; kPartialEmpty between launches
+  // finalize (fin_worker): chunks of kFinChunk partials, reduced by the CTAs that
+  // ran out of tiles, into part2[chunk + segment]; combined in chunk order
+  double *part2;                   // [n_tiles / kFinChunk + L + 2]
+  Sched *fin_sched;                // next: chunk claims; done: chunks finished
   double *ss_out;                  // [L] this rank's row of the exchange matrix
   double *ss_acc;                  // [L] STEP_SUMSQ accumulator
   int32_t n_pool;
@@ -151,14 +142,14 @@ struct NormParams {
   // kAdamAccum / kAdamEnd: AdamW update of the same elements (full flat fp32 buffers)
   float *params, *exp_avg, *exp_avg_sq;
   AdamConst adam;
-  // NVLink one-shot exchange (peers registered): the last CTA writes this rank's
-  // row into every peer's double-buffered exchange matrix, raises its flag there
-  // and waits for all peers' flags before deciding.
+  // NVLink one-shot exchange (peers registered): the CTA finishing the segment sums
+  // stores this rank's row into every peer's exchange buffer as LL words (each
+  // 8-byte store carries 32 bits of an fp64 sum and the 32-bit epoch, so data and
+  // "ready" arrive together and no fence is needed) and polls its own buffer
+  // until every peer's words carry the epoch.
   int32_t xworld, xrank;           // xworld == 0: no peer exchange
-  double *xrows;                   // local exchange matrices [2][world][L]
-  double *const *peer_rows;        // [world] device pointers to each rank's xrows
-  unsigned long long *xflags;      // local flags [world]: epoch reached by each rank
-  unsigned long long *const *peer_flags;  // [world] pointers to each rank's xflags
+  unsigned long long *xrows;       // local LL exchange buffers [2][world][L][2]
+  unsigned long long *const *peer_rows;  // [world] device pointers to each rank's xrows
   // kRsAccum / kRsEnd (NEXT 1, ZeRO form): the gradient is the rank-order sum of
   // the world's full gradient buffers (read over peer memory) times rs_scale;
   // this rank's shard of it is written to rs_out (optional) and accumulated.
@@ -170,12 +161,14 @@ struct NormParams {
   unsigned long long *const *peer_rs_flags;  // [world] each rank's rs_flags
   DecideParams dec;
   uint32_t dbg_tail_delay_ns;      // AF_DEBUG_TAIL_DELAY_NS: the last CTA waits this long before its tail
+  int32_t dbg_peers_arrived;       // AF_DEBUG_PEERS_ARRIVED: the exchange pushes but does not wait
 };
 
 // Flag value a rank stores into its peers' flag slots after it timed out waiting
 // for one of them (exchange or reduce-scatter barrier): larger than any epoch, so
 // a peer spinning on the slot stops at once and records the timeout too.
 constexpr unsigned long long kPoisonEpoch = ~0ull;
+constexpr uint32_t kPoisonEpoch32 = 0xFFFFFFFFu;  // the same in the 32-bit epoch of an LL exchange word
 
 // Cache records: one 16-byte meta word per owned id.  Direct mode: `readers`
 // counts the chunks of a get that have read {depth, valid}; the last one applies
@@ -214,6 +207,7 @@ struct CacheParams {
   int32_t depth;            // put
   int32_t cur_boundary;     // get
   int32_t no_wait;          // get: skip the PDL dependency wait (AF_CACHE_OVERLAP_PREV, caller-guaranteed)
+  unsigned int *retire;     // get with no_wait: CTAs done with their copies (the last one waits)
   // tiered mode (rowslot != nullptr): the plan kernel already resolved each row's slot
   const int32_t *rowslot;   // [n] slot per row of the call, -1 = skip
   char *host;               // device alias of the page-locked host tier
@@ -282,9 +276,6 @@ inline cudaError_t ensure_smem_attr(int smem) {
 
 // Launchers (defined in the .cu files).  Return cudaError_t as int.
 int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *stream);
-// CTAs of the wide finalize launch that follows the streaming kernel of `mode`
-// (0: the streaming kernel's last CTA finalizes)
-int fin_ctas(int mode, int n_tiles);
 int launch_decide(const DecideParams &p, void *stream);
 int launch_cache_put(const CacheParams &p, int grid, void *stream);
 int launch_cache_get(const CacheParams &p, int grid, void *stream);

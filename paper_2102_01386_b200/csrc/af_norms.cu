@@ -577,11 +577,13 @@ __device__ __forceinline__ int table_end(const NormParams &p, int f) {
   return ACT ? p.tile_end_of_f[f] : p.n_tiles;
 }
 
-template <int MODE, bool WIDE, bool ACT>
-__device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, int f) {
-  const int32_t *stb = seg_ranges<ACT>(p, f);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (AF_TIMING && !WIDE && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
+// The last CTA's tail, common to every finalize: (debug delay,) the exchange
+// epoch and this rank's row, the per-segment sums (`sums(publish)`, which calls
+// publish(l, s) for every segment l), the optional NVLink one-shot exchange and
+// the fused decision.  Every thread of the CTA calls it.
+template <int MODE, typename SumFn>
+__device__ __forceinline__ void tail_common(const NormParams &p, SumFn sums) {
+  const int tid = threadIdx.x;
   if (p.dbg_tail_delay_ns) {  // AF_DEBUG_TAIL_DELAY_NS (ordering tests only)
     if (tid == 0) {
       const unsigned long long t0 = gtimer();
@@ -589,10 +591,11 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
     }
     __syncthreads();
   }
-  // peer exchange: this interval end's epoch selects the exchange buffer
+  // peer exchange: this interval end's epoch (identical on every rank) tags the LL
+  // words and its parity selects one of two buffers (a peer is at most one epoch
+  // ahead: it cannot finish epoch e without this rank's row of epoch e)
   const bool xchg = p.xworld > 1 && p.end;
   __shared__ unsigned long long s_epoch;
-  double *ss_row = p.ss_out;
   if (xchg) {
     if (tid == 0) {
       DevState *st = const_cast<DevState *>(p.state);
@@ -600,10 +603,9 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
       st->epoch = s_epoch;
     }
     __syncthreads();
-    ss_row = p.xrows + (s_epoch & 1ull) * p.xworld * p.L + static_cast<size_t>(p.xrank) * p.L;
   }
-  // each segment's active tiles' partials in tile order: one warp per segment,
-  // lane-strided with 8 loads in flight, then the xor tree (deterministic)
+  // this rank's row of the exchange matrix ss_all[world][L] (the rows the decision sums)
+  double *ss_row = p.ss_out;
   auto publish = [&](int l, double s) {
     if (MODE == kEndDelta) {
       ss_row[l] = s;
@@ -613,81 +615,71 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
       if (p.end) ss_row[l] = acc;
     }
   };
-  if constexpr (WIDE) {
-    // the chunk sums: segment l's active tiles span chunks [c_lo, c_hi]
-    // (chunk c = tiles first_tile + [c*CH, (c+1)*CH), CH = p.fin_chunk), whose
-    // pieces of l sit at part2[c + l]; summed in chunk order
-    const int CH = p.fin_chunk;
-    for (int l = tid; l < p.L; l += kNormBlock) {
-      int tb = stb[l];
-      tb = tb < first_tile ? first_tile : tb;
-      const int te = stb[l + 1];
-      double s = 0.0;
-      if (te > tb) {
-        const int c_lo = (tb - first_tile) / CH, c_hi = (te - 1 - first_tile) / CH;
-#pragma unroll 8
-        for (int c = c_lo; c <= c_hi; ++c) s += __ldcg(p.part2 + c + l);
-      }
-      publish(l, s);
-    }
-  } else {
-    for (int l = warp; l < p.L && warp < kNormBlock / 32; l += kNormBlock / 32) {
-      int tb = stb[l];
-      tb = tb < first_tile ? first_tile : tb;
-      const int te = stb[l + 1];
-      double s = 0.0;
-#pragma unroll 8
-      for (int k = tb + lane; k < te; k += 32) s += __ldcg(p.partials + k);
-      s = warp_sum(s);
-      if (lane == 0) publish(l, s);
-    }
-  }
+  sums(publish);
   if (xchg && (sticky_of(p) & 3u)) {
     // an earlier exchange or barrier timed out (sticky until af_set_state): no peer
     // stores any more; the peers time out on this rank and flag it as well
   } else if (xchg) {
-    // NVLink one-shot exchange: push this rank's row into every peer's matrix
-    // (P x L fp64 stores over peer memory), publish the epoch in every peer's
-    // flag slot for this rank, then wait until every rank's epoch has arrived.
-    __syncthreads();
+    // NVLink one-shot exchange, LL protocol: word 2l+h of this rank's row in every
+    // peer's buffer = {32 bits of ss_l (h = 0 low, 1 high), epoch32}; 8-byte stores
+    // are single-copy atomic, so a reader that sees the epoch sees the data -- no
+    // fence, no separate flag.  Then poll the own buffer until every peer's words
+    // carry the epoch (bounded: a missing peer flags a timeout instead of hanging).
+    __syncthreads();  // the row is published
     const unsigned long long e = s_epoch;
-    const size_t off = (e & 1ull) * p.xworld * p.L + static_cast<size_t>(p.xrank) * p.L;
-    for (int i = tid; i < p.xworld * p.L && tid < kNormBlock; i += kNormBlock) {
-      const int r = i / p.L, l = i % p.L;
-      p.peer_rows[r][off + l] = ss_row[l];
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (tid < p.xworld) {
-      unsigned long long *flag = p.peer_flags[tid] + p.xrank;
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(e) : "memory");
+    const uint32_t e32 = static_cast<uint32_t>(e);
+    const int W = p.xworld, L = p.L, b = static_cast<int>(e & 1ull);
+    const size_t my = (static_cast<size_t>(b) * W + p.xrank) * L;
+    for (int i = tid; i < W * L; i += kNormBlock) {
+      const int q = i / L, l = i % L;
+      if (q == p.xrank) continue;
+      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(ss_row[l]));
+      const unsigned long long lo = (bits & 0xFFFFFFFFull) | (static_cast<unsigned long long>(e32) << 32);
+      const unsigned long long hi = (bits >> 32) | (static_cast<unsigned long long>(e32) << 32);
+      asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p.peer_rows[q] + 2 * (my + l)), "l"(lo),
+                   "l"(hi)
+                   : "memory");
     }
     __shared__ int s_timeout;
     if (tid == 0) s_timeout = 0;
     __syncthreads();
-    if (tid < p.xworld) {
-      const unsigned long long *flag = p.xflags + tid;
-      unsigned long long v = 0;
-      for (long long spin = 0;; ++spin) {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-        if (v == kPoisonEpoch) {  // that peer timed out on someone: fail together
-          s_timeout = 1;
-          break;
+    if (!p.dbg_peers_arrived) {
+      for (int i = tid; i < W * L; i += kNormBlock) {
+        const int q = i / L, l = i % L;
+        if (q == p.xrank) continue;
+        const unsigned long long *w = p.xrows + 2 * ((static_cast<size_t>(b) * W + q) * L + l);
+        unsigned long long lo, hi;
+        for (long long spin = 0;; ++spin) {
+          asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(w) : "memory");
+          const uint32_t f0 = static_cast<uint32_t>(lo >> 32), f1 = static_cast<uint32_t>(hi >> 32);
+          if (f0 == kPoisonEpoch32 || f1 == kPoisonEpoch32) {  // that peer timed out: fail together
+            s_timeout = 1;
+            break;
+          }
+          if (f0 == e32 && f1 == e32) {
+            p.ss_out[static_cast<ptrdiff_t>(q - p.xrank) * L + l] =
+                __longlong_as_double(static_cast<long long>((lo & 0xFFFFFFFFull) | (hi << 32)));
+            break;
+          }
+          if (spin > (1ll << 22)) {  // ~seconds: a peer never arrived -- flag it, do not hang the GPU
+            s_timeout = 1;
+            break;
+          }
+          __nanosleep(32);
         }
-        if (v >= e) break;
-        if (spin > (1ll << 22)) {  // ~seconds: a peer never arrived -- flag it, do not hang the GPU
-          s_timeout = 1;
-          break;
-        }
-        __nanosleep(64);
       }
     }
     __syncthreads();
-    if (s_timeout && tid < p.xworld) {  // make the timeout collective: poison this rank's slot everywhere
-      unsigned long long *flag = p.peer_flags[tid] + p.xrank;
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(kPoisonEpoch) : "memory");
+    if (s_timeout) {  // make the timeout collective: poison this rank's row everywhere
+      const unsigned long long poison = static_cast<unsigned long long>(kPoisonEpoch32) << 32;
+      for (int i = tid; i < W * L; i += kNormBlock) {
+        const int q = i / L, l = i % L;
+        if (q == p.xrank) continue;
+        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %1};" ::"l"(p.peer_rows[q] + 2 * (my + l)), "l"(poison)
+                     : "memory");
+      }
+      if (tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 1u);
     }
-    if (s_timeout && tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 1u);
   }
   if (AF_TIMING) {
     __syncthreads();
@@ -703,50 +695,45 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
   }
 }
 
-template <int CH, bool ACT>
-__device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int f, int c, double *s_p);
-
-// AF_FIN_WIDE == 3.  `ticket` = this CTA's place in the grid's retirement order.
-// The last W = min(chunks, grid) CTAs to retire become workers: each waits until
-// the whole grid has retired (every partial published), reduces chunks w, w+W, ...
-// of kFin3Chunk partials as fin_kernel's CTAs would (chunk_reduce, fixed order),
-// and the last worker to finish returns true and carries on as the grid's last
-// CTA (segment sums from the pieces, exchange, decision) -- no second launch and
-// no kernel boundary between the streaming and the finalize.  The wait cannot
-// deadlock: the scheduler is drained, so every CTA not yet retired is resident
-// or starts, finds no tile and retires, in a slot a retired non-worker freed (or
-// its own: the grid is sized to the device's co-resident limit).
-template <bool ACT>
-__device__ __noinline__ bool retire_finalize(const NormParams &p, int first_tile, int f, int ticket, double *s_p) {
+// Tail of the streaming kernels: each segment's sum from the finalize's chunk
+// pieces -- segment l's active tiles span chunks [c_lo, c_hi] (chunk c = tiles
+// first_tile + [c*kFinChunk, (c+1)*kFinChunk)), whose pieces of l sit at
+// part2[c + l]; summed in chunk order by one thread per segment.  The pieces
+// (n_chunks + L of them) are staged in shared memory with one coalesced round
+// trip when they fit s_p.
+template <int MODE, bool ACT>
+__device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, int n_end, int f, double *s_p) {
+  const int32_t *stb = seg_ranges<ACT>(p, f);
   const int tid = threadIdx.x;
-  const int G = static_cast<int>(gridDim.x);
-  const int nch = (table_end<ACT>(p, f) - first_tile + kFin3Chunk - 1) / kFin3Chunk;
-  const int W = nch < G ? nch : G;
-  const int w = ticket - (G - W);
-  if (nch <= 0) return ticket == G - 1;  // no active tile: the last CTA carries on
-  if (w < 0) return false;
-  __shared__ int s_fin_last;
-  if (tid == 0) {
-    for (;;) {
-      unsigned int v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&p.sched->done) : "memory");
-      if (v >= static_cast<unsigned int>(G)) break;
-      __nanosleep(20);
+  const int nch = n_end > first_tile ? (n_end - first_tile + kFinChunk - 1) / kFinChunk : 0;
+  const int n_pc = nch + p.L;
+  const bool staged = n_pc <= kFinChunk;
+  if (staged) {
+    for (int i = tid; i < n_pc; i += kNormBlock) s_p[i] = __ldcg(p.part2 + i);
+    __syncthreads();
+  }
+  tail_common<MODE>(p, [&](auto &publish) {
+    for (int l = tid; l < p.L; l += kNormBlock) {
+      int tb = stb[l];
+      tb = tb < first_tile ? first_tile : tb;
+      const int te = stb[l + 1];
+      double sum = 0.0;
+      if (te > tb) {
+        const int c_lo = (tb - first_tile) / kFinChunk, c_hi = (te - 1 - first_tile) / kFinChunk;
+        if (staged) {
+          for (int c = c_lo; c <= c_hi; ++c) sum += s_p[c + l];
+        } else {
+#pragma unroll 8
+          for (int c = c_lo; c <= c_hi; ++c) sum += __ldcg(p.part2 + c + l);
+        }
+      }
+      publish(l, sum);
     }
-    if (AF_TIMING && ticket == G - 1) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
-  }
-  __syncthreads();
-  for (int c = w; c < nch; c += W) chunk_reduce<kFin3Chunk, ACT>(p, first_tile, f, c, s_p);
-  if (tid == 0) {
-    __threadfence();
-    s_fin_last = atomicAdd(&p.fin_sched->done, 1u) == static_cast<unsigned int>(W - 1);
-  }
-  __syncthreads();
-  if (!s_fin_last) return false;
-  __threadfence();
-  if (tid == 0) p.fin_sched->done = 0u;
-  return true;
+  });
 }
+
+template <bool ACT>
+__device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int n_end, int f, double *s_p);
 
 template <int MODE, typename GT, bool RD, int PM = 1, bool ACT = false>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccum)
@@ -755,17 +742,13 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
     norms_kernel(const NormParams p) {
   constexpr bool RS = MODE == kRsAccum || MODE == kRsEnd || MODE == kRsAdamAccum || MODE == kRsAdamEnd;
   constexpr bool PARTIALS = MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum && MODE != kRsAdamAccum;
-  // in-kernel wide finalize (AF_FIN_WIDE == 2): the CTA that completes a chunk of
-  // kFinChunk tiles reduces it (staging buffer below) between its own tiles
-  __shared__ double s_fin[(PARTIALS && AF_FIN_WIDE == 2) ? kFinChunk : ((PARTIALS && AF_FIN_WIDE == 3) ? kFin3Chunk : 1)];
-  __shared__ int s_chunk;
+  __shared__ double s_fin[PARTIALS ? kFinChunk : 1];  // a finalize chunk's partials
   __shared__ int s_tile[3];
   __shared__ Tile s_desc[3];
   __shared__ double s_red[kNormBlock / 32];
   __shared__ int s_last;
   __shared__ unsigned long long s_rs_epoch;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_chunk = -1;
   pdl_wait();  // f, Delta and the counters are written by the preceding kernels
   if (AF_TIMING && blockIdx.x == 0 && threadIdx.x == 0) const_cast<DevState *>(p.state)->tmark[0] = gtimer();
   int f = p.state->f;
@@ -852,382 +835,122 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
         double s = 0.0;
 #pragma unroll
         for (int k = 0; k < kNormBlock / 32; ++k) s += s_red[k];
-        p.partials[tile] = s;
-        if (AF_FIN_WIDE == 2 && p.wide_fin == 2) {
-          // count the chunk's finished tiles; the CTA finishing its last one reduces it
-          __threadfence();
-          const int c = (tile - first_tile) / kFinChunk;
-          const int nc = min(kFinChunk, n_end - first_tile - c * kFinChunk);
-          s_chunk = (atomicAdd(p.chunk_cnt + c, 1u) == static_cast<unsigned>(nc - 1)) ? c : -1;
-        }
+        p.partials[tile] = s;  // a plain 8-byte store: the value is its own ready flag (fin_worker)
       }
     }
     __syncthreads();
-    if constexpr (PARTIALS && AF_FIN_WIDE == 2) {
-      if (p.wide_fin == 2) {
-        const int c = s_chunk;
-        if (c >= 0) {
-          chunk_reduce<kFinChunk, ACT>(p, first_tile, f, c, s_fin);
-          if (tid == 0) p.chunk_cnt[c] = 0u;  // every tile of the chunk has counted: reset for the next launch
-        }
-      }
-    }
   }
   pdl_launch_dependents();
+  if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
+  // finalize: a CTA out of tiles reduces chunks of partials while the grid's last
+  // tiles are still streaming; the finisher of the last chunk runs the tail
+  bool tail = false;
+  if constexpr (PARTIALS) tail = fin_worker<ACT>(p, first_tile, n_end, f, s_fin);
 
-  // grid completion: the last CTA resets the scheduler, sums the segments and
-  // (fused interval end, world == 1) runs the decision
+  // grid completion: every CTA has finished its tiles and claimed its last chunk;
+  // the last one resets the schedulers (and, fused reduce-scatter, closes the
+  // barrier on this rank's gradient)
   __syncthreads();
   if (tid == 0) {
     __threadfence();
     const unsigned int d = atomicAdd(&p.sched->done, 1u);
     s_last = (d == gridDim.x - 1);
-    s_chunk = static_cast<int>(d);  // retirement ticket (wide_fin == 3)
   }
   __syncthreads();
-  if constexpr (PARTIALS && AF_FIN_WIDE == 3) {
-    // the last W CTAs to retire wait for the grid to drain, reduce the chunks of
-    // partials in parallel, and the last of them continues as "the last CTA"
-    if (p.wide_fin == 3) {
-      if (!retire_finalize<ACT>(p, first_tile, f, s_chunk, s_fin)) return;
-      s_last = 1;  // (uniform: every thread of this CTA took the same branch)
+  if (s_last) {
+    __threadfence();
+    if (tid == 0) {
+      p.sched->next = 0;
+      p.sched->done = 0;
+      if (PARTIALS) p.fin_sched->next = 0u;
+    }
+    if constexpr (RS) {
+      if (p.rs_world > 1 && !(sticky_of(p) & 3u)) {
+        rs_barrier(p, 1, s_rs_epoch);  // no rank reads this rank's gradient any more
+        if (tid == 0) const_cast<DevState *>(p.state)->rs_epoch = s_rs_epoch;
+      }
+    }
+    if constexpr (PARTIALS) {
+      if (n_end <= first_tile) tail = true;  // no active tile, no chunk: the last CTA publishes the zeros
     }
   }
-  if (!s_last) return;
-  __threadfence();
-  if (tid == 0) {
-    p.sched->next = 0;
-    p.sched->done = 0;
+  if constexpr (PARTIALS) {
+    constexpr int TM = (MODE == kAdamEnd || MODE == kRsEnd || MODE == kRsAdamEnd) ? kEndDelta : MODE;
+    if (tail) last_cta_tail<TM, ACT>(p, first_tile, n_end, ACT ? f : 0, s_fin);
   }
-  if constexpr (RS) {
-    if (p.rs_world > 1 && !(sticky_of(p) & 3u)) {
-      rs_barrier(p, 1, s_rs_epoch);  // no rank reads this rank's gradient any more
-      if (tid == 0) const_cast<DevState *>(p.state)->rs_epoch = s_rs_epoch;
-    }
-  }
-  if constexpr (!PARTIALS) return;
-  constexpr int TM = (MODE == kAdamEnd || MODE == kRsEnd || MODE == kRsAdamEnd) ? kEndDelta : MODE;
-  if (p.wide_fin == 1) {  // fin_kernel sums the partials
-    if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
-    return;
-  }
-  if (p.wide_fin >= 2) {  // every chunk already reduced: combine the pieces
-    if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
-    last_cta_tail<TM, true, ACT>(p, first_tile, ACT ? f : 0);
-    return;
-  }
-  last_cta_tail<TM, false, ACT>(p, first_tile, ACT ? f : 0);
 }
 
-// Chunk c of the wide finalize (n_tiles > kFinChunk): the fp64 partials of tiles
-// first_tile + [c*kFinChunk, (c+1)*kFinChunk) are staged in shared memory (8
-// coalesced loads per thread, one round trip); each segment's piece of them is
-// reduced by one warp (lane-strided, xor tree) into part2[c + l] -- piece (c, l)
-// is the (c + l)-th piece in tile order, so the index needs no search.  Every
-// thread of the CTA calls it.  Fixed order: deterministic.
-template <int CH, bool ACT>
-__device__ __noinline__ void chunk_reduce(const NormParams &p, int first_tile, int f, int c, double *s_p) {
+// The finalize of the per-tile partials, done by the streaming grid itself as its
+// CTAs run out of tiles (no second launch, no kernel boundary): the active tiles
+// form chunks of kFinChunk consecutive tiles; a CTA whose scheduler is drained
+// claims chunks (in the order the tiles were processed, so the first-claimed
+// chunks are complete) and reduces each: every thread takes one tile's partial,
+// waiting until it is no longer the sentinel (kPartialEmpty -- the partial's
+// plain 8-byte store is its own ready flag, so the streaming loop needs no fence
+// or counter per tile), re-arms the slot for the next launch, and each segment's
+// piece of the chunk is summed by one warp in tile order (lane-strided, xor
+// tree) into part2[c + l] (piece (c, l) is the (c+l)-th piece in tile order, so
+// the index needs no search).  The CTA that completes the last chunk returns
+// true and runs the tail (segment sums in chunk order, exchange, decision).
+// Deterministic: the reduction order depends only on the tile table.  Cannot
+// deadlock: a claimed tile belongs to a running CTA, which writes its partial
+// without waiting on anything.
+template <bool ACT>
+__device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int n_end, int f, double *s_p) {
   const int32_t *stb = seg_ranges<ACT>(p, f);
-  const int tile_end = table_end<ACT>(p, f);
-  static_assert(CH % kNormBlock == 0, "chunk = whole loads per thread");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int c0 = first_tile + c * CH;
-  if (c0 >= tile_end) return;  // uniform over the CTA
-  const int n = min(CH, tile_end - c0);
+  const int nch = (n_end - first_tile + kFinChunk - 1) / kFinChunk;
+  __shared__ int s_c, s_tail;
+  if (tid == 0) s_tail = 0;
+  auto *slots = reinterpret_cast<unsigned long long *>(p.partials);
+  for (;;) {
+    if (tid == 0) {
+      const int w = static_cast<int>(atomicAdd(&p.fin_sched->next, 1u));
+      s_c = w < nch ? (p.reverse ? nch - 1 - w : w) : -1;
+    }
+    __syncthreads();
+    const int c = s_c;
+    if (c < 0) break;
+    const int c0 = first_tile + c * kFinChunk;
+    const int n = min(kFinChunk, n_end - c0);
 #pragma unroll
-  for (int u = 0; u < CH / kNormBlock; ++u) {
-    const int k = u * kNormBlock + tid;
-    if (k < n) s_p[k] = __ldcg(p.partials + c0 + k);
-  }
-  const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
-  __syncthreads();
-  for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {
-    int a = stb[l], b = stb[l + 1];
-    a = (a < c0 ? c0 : a) - c0;
-    b = (b > c0 + n ? c0 + n : b) - c0;
-    double s = 0.0;
+    for (int u = 0; u < kFinChunk / kNormBlock; ++u) {
+      const int k = u * kNormBlock + tid;
+      if (k < n) {
+        unsigned long long v;
+        for (;;) {
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slots + c0 + k) : "memory");
+          if (v != kPartialEmpty) break;
+          __nanosleep(32);
+        }
+        s_p[k] = __longlong_as_double(static_cast<long long>(v));
+        slots[c0 + k] = kPartialEmpty;  // re-armed for the next launch
+      }
+    }
+    const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
+    __syncthreads();
+    for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {
+      int a = stb[l], b = stb[l + 1];
+      a = (a < c0 ? c0 : a) - c0;
+      b = (b > c0 + n ? c0 + n : b) - c0;
+      double sum = 0.0;
 #pragma unroll 8
-    for (int k = a + lane; k < b; k += 32) s += s_p[k];
-    s = warp_sum(s);
-    if (lane == 0) {
-      p.part2[c + l] = s;
-      __threadfence();  // before the CTA reports completion (done counters)
+      for (int k = a + lane; k < b; k += 32) sum += s_p[k];
+      sum = warp_sum(sum);
+      if (lane == 0) p.part2[c + l] = sum;
     }
-  }
-  __syncthreads();  // s_p is free again
-}
-
-// Wide finalize as a second launch (AF_FIN_WIDE == 1): CTA c reduces chunk c and
-// the grid's last CTA combines the pieces of each segment in chunk order, then
-// exchanges and decides as the streaming kernel's last CTA would.
-template <int MODE, bool ACT>
-__global__ void __launch_bounds__(kNormBlock) fin_kernel(const NormParams p) {
-  __shared__ double s_p[kFinChunk];
-  __shared__ int s_last;
-  const int tid = threadIdx.x;
-  pdl_wait();  // the streaming kernel's partials
-  int f = p.state->f;
-  f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
-  const int first_tile = p.first_tile_of_f[f];
-  chunk_reduce<kFinChunk, ACT>(p, first_tile, f, blockIdx.x, s_p);
-  pdl_launch_dependents();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned int d = atomicAdd(&p.fin_sched->done, 1u);
-    s_last = (d == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  if (tid == 0) p.fin_sched->done = 0;
-  last_cta_tail<MODE, true, ACT>(p, first_tile, ACT ? f : 0);
-}
-
-
-// ---------------------------------------------------------------- TMA-staged variant
-//
-// Same work, tiles, scheduler and per-tile reduction order as norms_kernel, but
-// the vector body of each tile moves HBM -> shared memory with TMA bulk copies
-// (cp.async.bulk ... mbarrier::complete_tx) in chunks of kTmaChunk elements
-// through a kTmaStages ring; thread 0 is the producer (it also fetches the
-// tiles) and every thread consumes from shared memory.  One CTA per SM; the
-// bytes in flight no longer depend on registers.  Unaligned segment edges are
-// read directly (as in norms_kernel).  kAccum writes Delta back with st.global.
-#ifndef AF_TMA
-#define AF_TMA 0  // 0: LDG kernels only (measured faster, profiles/r01_v8_*); 1: TMA for the interval end; 2: also the accumulate
-#endif
-constexpr int kTmaStages = 4;
-constexpr int kTmaChunk = 4096;
-
-struct StageMeta {
-  int64_t c0;         // first element of the chunk (aligned)
-  int64_t tb, te;     // the tile's element range (for the scalar edges)
-  int32_t tile, n;    // tile index (-1: no more work), elements in the chunk
-  int32_t first, last;
-};
-
-__device__ __forceinline__ uint32_t smem_u32a(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void tma_mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32a(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void tma_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32a(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32a(bar)) : "memory");
-}
-__device__ __forceinline__ void tma_wait(uint64_t *bar, uint32_t parity) {
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32a(bar)), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void tma_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32a(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32a(bar))
-      : "memory");
-}
-
-template <typename GT>
-__host__ __device__ constexpr int tma_stage_bytes() {
-  return kTmaChunk * static_cast<int>(sizeof(GT)) + kTmaChunk * 4;
-}
-template <typename GT>
-__host__ __device__ constexpr int tma_smem_bytes() {
-  return 1024 + kTmaStages * tma_stage_bytes<GT>();
-}
-
-constexpr int kTmaThreads = kNormBlock + 32;  // 8 consumer warps + 1 producer warp
-
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kNormBlock) : "memory"); }
-
-template <int MODE, typename GT, bool RD>
-__global__ void __launch_bounds__(kTmaThreads, 1) norms_tma_kernel(const NormParams p) {
-  static_assert(MODE == kAccum || MODE == kEndDelta, "TMA variant: accumulate and interval end");
-  extern __shared__ __align__(1024) unsigned char tsm[];
-  constexpr int VE = VT<GT>::VE;
-  constexpr int DV = VE / 4;
-  constexpr int GB = kTmaChunk * static_cast<int>(sizeof(GT));
-  constexpr int SB = tma_stage_bytes<GT>();
-  uint64_t *full = reinterpret_cast<uint64_t *>(tsm);
-  uint64_t *empty = full + kTmaStages;
-  StageMeta *meta = reinterpret_cast<StageMeta *>(tsm + 128);
-  unsigned char *bufs = tsm + 1024;
-  __shared__ double s_red[kNormBlock / 32];
-  __shared__ int s_last;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
-      tma_mbar_init(&full[s], 1);
-      tma_mbar_init(&empty[s], kNormBlock / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  pdl_wait();
-  int f = p.state->f;
-  f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
-  const int first_tile = p.first_tile_of_f[f];
-  const GT *__restrict__ g = static_cast<const GT *>(p.grad);
-  float *__restrict__ d = p.delta - p.shard_begin;
-
-  if (warp == kNormBlock / 32) {
-    // ---------------- producer warp: lane 0 fetches tiles (one ahead) and issues bulk copies
-    if (lane == 0) {
-      int nxt = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
-      Tile nxt_t{0, 0, 0, 0, 0, 0};
-      if (nxt < p.n_tiles) nxt_t = p.tiles[nxt];
-      uint32_t issued = 0;
-      for (;;) {
-        const int tile = nxt;
-        const Tile tt = nxt_t;
-        if (tile < p.n_tiles) {  // prefetch the next tile while this one streams
-          nxt = static_cast<int>(atomicAdd(&p.sched->next, 1u)) + first_tile;
-          if (nxt < p.n_tiles) nxt_t = p.tiles[nxt];
-        }
-        const bool done = tile >= p.n_tiles;
-        int64_t vb = 0, ve = 0;
-        int nch = 1;
-        if (!done) {
-          vb = ((tt.begin + VE - 1) / VE) * VE;
-          ve = (tt.end / VE) * VE;
-          if (vb > ve) vb = ve = tt.end;
-          nch = static_cast<int>((ve - vb + kTmaChunk - 1) / kTmaChunk);
-          if (nch < 1) nch = 1;
-        }
-        for (int ch = 0; ch < nch; ++ch) {
-          const int s = static_cast<int>(issued % kTmaStages);
-          if (issued >= static_cast<uint32_t>(kTmaStages)) tma_wait(&empty[s], ((issued / kTmaStages) - 1u) & 1u);
-          StageMeta &m = meta[s];
-          if (done) {
-            m.tile = -1;
-            tma_arrive(&full[s]);
-          } else {
-            const int64_t c0 = vb + static_cast<int64_t>(ch) * kTmaChunk;
-            const int64_t rem = ve - c0;
-            const int n = static_cast<int>(rem < kTmaChunk ? (rem > 0 ? rem : 0) : kTmaChunk);
-            m.c0 = c0;
-            m.tb = tt.begin;
-            m.te = tt.end;
-            m.tile = tile;
-            m.n = n;
-            m.first = (ch == 0);
-            m.last = (ch == nch - 1);
-            const uint32_t gbytes = static_cast<uint32_t>(n) * sizeof(GT);
-            const uint32_t dbytes = RD ? static_cast<uint32_t>(n) * 4u : 0u;
-            tma_expect_tx(&full[s], gbytes + dbytes);
-            if (n > 0) {
-              unsigned char *st = bufs + static_cast<size_t>(s) * SB;
-              tma_g2s(st, g + c0, gbytes, &full[s]);
-              if (RD) tma_g2s(st + GB, d + c0, dbytes, &full[s]);
-            }
-          }
-          ++issued;
-        }
-        if (done) break;
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---------------- consumer warps
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (uint32_t k = 0;; ++k) {
-      const int s = static_cast<int>(k % kTmaStages);
-      tma_wait(&full[s], (k / kTmaStages) & 1u);
-      const StageMeta m = meta[s];
-      if (m.tile < 0) break;
-      const unsigned char *st = bufs + static_cast<size_t>(s) * SB;
-      const uint4 *gs = reinterpret_cast<const uint4 *>(st);
-      const float4 *ds = reinterpret_cast<const float4 *>(st + GB);
-      const int nv = m.n / VE;
-      for (int v = tid; v < nv; v += kNormBlock) {
-        float x[VE];
-        unpack<VE>(gs[v], x);
-        if (RD) {
-#pragma unroll
-          for (int q = 0; q < DV; ++q) {
-            const float4 dv = ds[v * DV + q];
-            x[4 * q + 0] = __fadd_rn(dv.x, x[4 * q + 0]);
-            x[4 * q + 1] = __fadd_rn(dv.y, x[4 * q + 1]);
-            x[4 * q + 2] = __fadd_rn(dv.z, x[4 * q + 2]);
-            x[4 * q + 3] = __fadd_rn(dv.w, x[4 * q + 3]);
-          }
-        }
-        if (MODE == kAccum) {
-          float4 *dst = reinterpret_cast<float4 *>(d + m.c0) + static_cast<int64_t>(v) * DV;
-#pragma unroll
-          for (int q = 0; q < DV; ++q)
-            __stcs(dst + q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
-        } else {
-#pragma unroll
-          for (int k2 = 0; k2 < VE; k2 += 4) {
-            a0 = sq_acc(x[k2 + 0], a0);
-            a1 = sq_acc(x[k2 + 1], a1);
-            a2 = sq_acc(x[k2 + 2], a2);
-            a3 = sq_acc(x[k2 + 3], a3);
-          }
-        }
-      }
-      // unaligned segment edges of the tile, read directly (< VE elements each)
-      if (m.first) {
-        const int nh = static_cast<int>(m.c0 - m.tb);
-        if (tid < nh) elem<MODE, GT, RD>(p, g, d, m.tb + tid, a0);
-      }
-      if (m.last) {
-        const int64_t ve = m.c0 + m.n;
-        const int nt = static_cast<int>(m.te - ve);
-        if (tid >= 128 && tid - 128 < nt) elem<MODE, GT, RD>(p, g, d, ve + (tid - 128), a1);
-      }
-      __syncwarp();
-      if (lane == 0) tma_arrive(&empty[s]);
-      if (MODE == kEndDelta && m.last) {
-        const double w = warp_sum((a0 + a1) + (a2 + a3));
-        a0 = a1 = a2 = a3 = 0.0;
-        if (lane == 0) s_red[warp] = w;
-        consumers_sync();
-        if (tid == 0) {
-          double sum = 0.0;
-#pragma unroll
-          for (int q = 0; q < kNormBlock / 32; ++q) sum += s_red[q];
-          p.partials[m.tile] = sum;
-        }
-        consumers_sync();
+    __syncthreads();  // the pieces are written; s_p is free again
+    if (tid == 0) {
+      __threadfence();  // this chunk's pieces before its completion count
+      if (atomicAdd(&p.fin_sched->done, 1u) == static_cast<unsigned int>(nch - 1)) {
+        s_tail = 1;
+        p.fin_sched->done = 0u;  // every chunk counted: nobody else touches it in this launch
       }
     }
   }
-  pdl_launch_dependents();
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const unsigned int dn = atomicAdd(&p.sched->done, 1u);
-    s_last = (dn == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  if (tid == 0) {
-    p.sched->next = 0;
-    p.sched->done = 0;
-  }
-  if (MODE == kAccum) return;
-  last_cta_tail<kEndDelta, false, false>(p, first_tile, 0);
-}
-
-template <int MODE, typename GT, bool RD>
-int launch_tma(const NormParams &p, int grid, void *stream) {
-  constexpr int smem = tma_smem_bytes<GT>();
-  const cudaError_t e = ensure_smem_attr<norms_tma_kernel<MODE, GT, RD>>(smem);
-  if (e != cudaSuccess) return static_cast<int>(e);
-  return static_cast<int>(launch_pdl(norms_tma_kernel<MODE, GT, RD>, dim3(grid), dim3(kTmaThreads),
-                                     static_cast<size_t>(smem), static_cast<cudaStream_t>(stream), p));
+  if (s_tail) __threadfence();  // every other chunk's pieces are visible
+  return s_tail != 0;
 }
 
 using NormKernel = void (*)(const NormParams);
@@ -1284,10 +1007,6 @@ NormKernel kernel_for(int mode, bool rd, int world, bool act = false) {
 template <typename GT>
 int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
   const bool rd = !p.first;
-  if (mode == kAccum && AF_TMA >= 2 && p.stb_stride == 0)  // the TMA-staged variants: static tables only
-    return rd ? launch_tma<kAccum, GT, true>(p, grid, stream) : launch_tma<kAccum, GT, false>(p, grid, stream);
-  if (mode == kEndDelta && AF_TMA >= 1 && p.stb_stride == 0)
-    return rd ? launch_tma<kEndDelta, GT, true>(p, grid, stream) : launch_tma<kEndDelta, GT, false>(p, grid, stream);
   if (mode < 0 || mode >= kNumModes) return static_cast<int>(cudaErrorInvalidValue);
   return static_cast<int>(launch_pdl(kernel_for<GT>(mode, rd, p.rs_world, p.stb_stride != 0), dim3(grid),
                                      dim3(kNormBlock), 0,
@@ -1296,32 +1015,8 @@ int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
 
 }  // namespace
 
-int fin_ctas(int mode, int n_tiles) {
-  const bool end_mode = mode == kEndDelta || mode == kStepSq || mode == kAdamEnd || mode == kRsEnd || mode == kRsAdamEnd;
-  if (!AF_FIN_WIDE || !end_mode || (mode == kEndDelta && AF_TMA >= 1)) return 0;
-  if (AF_FIN_WIDE == 3) return n_tiles <= AF_FIN3_MIN_TILES ? 0 : (n_tiles + kFin3Chunk - 1) / kFin3Chunk;
-  if (n_tiles <= kFinChunk) return 0;
-  return (n_tiles + kFinChunk - 1) / kFinChunk;
-}
-
-int launch_norms(const NormParams &p_in, int mode, int grad_dtype, int grid, void *stream) {
-  NormParams p = p_in;
-  const int nfin = fin_ctas(mode, p.n_tiles);
-  p.wide_fin = nfin > 0 ? AF_FIN_WIDE : 0;
-  p.fin_chunk = AF_FIN_WIDE == 3 ? kFin3Chunk : kFinChunk;
-  const int e = grad_dtype == AF_DT_BF16 ? launch_dt<uint16_t>(p, mode, grid, stream)
-                                         : launch_dt<float>(p, mode, grid, stream);
-  if (e != 0 || !nfin || AF_FIN_WIDE != 1) return e;
-  const bool act = p.stb_stride != 0;
-#ifdef AF_NO_ACT
-  auto *fk = mode == kStepSq ? fin_kernel<kStepSq, false> : fin_kernel<kEndDelta, false>;
-  (void)act;
-#else
-  auto *fk = mode == kStepSq ? (act ? fin_kernel<kStepSq, true> : fin_kernel<kStepSq, false>)
-                             : (act ? fin_kernel<kEndDelta, true> : fin_kernel<kEndDelta, false>);
-#endif
-  return static_cast<int>(
-      launch_pdl(fk, dim3(nfin), dim3(kNormBlock), 0, static_cast<cudaStream_t>(stream), p));
+int launch_norms(const NormParams &p, int mode, int grad_dtype, int grid, void *stream) {
+  return grad_dtype == AF_DT_BF16 ? launch_dt<uint16_t>(p, mode, grid, stream) : launch_dt<float>(p, mode, grid, stream);
 }
 
 // Load every kernel this context can launch now.  Under CUDA's lazy module
@@ -1345,27 +1040,10 @@ static cudaError_t preload_dt(int world) {
 int preload_norm_kernels(int grad_dtype, int world) {
   cudaError_t e = grad_dtype == AF_DT_BF16 ? preload_dt<uint16_t>(world) : preload_dt<float>(world);
   if (e != cudaSuccess) return static_cast<int>(e);
-  cudaFuncAttributes a;
-  for (const void *k : {reinterpret_cast<const void *>(fin_kernel<kEndDelta, false>),
-                        reinterpret_cast<const void *>(fin_kernel<kStepSq, false>),
-#ifndef AF_NO_ACT
-                        reinterpret_cast<const void *>(fin_kernel<kEndDelta, true>),
-                        reinterpret_cast<const void *>(fin_kernel<kStepSq, true>)
-#else
-                        reinterpret_cast<const void *>(fin_kernel<kStepSq, false>)
-#endif
-                       }) {
-    e = cudaFuncGetAttributes(&a, k);
-    if (e != cudaSuccess) return static_cast<int>(e);
-  }
   return 0;
 }
 
 int norms_max_blocks_per_sm(int mode, int grad_dtype, int world, int *blocks, bool act) {
-  if ((mode == kEndDelta && AF_TMA >= 1) || (mode == kAccum && AF_TMA >= 2)) {
-    *blocks = 1;  // the TMA-staged kernels run one CTA per SM
-    return 0;
-  }
   NormKernel k = grad_dtype == AF_DT_BF16 ? kernel_for<uint16_t>(mode, true, world, act)
                                          : kernel_for<float>(mode, true, world, act);
   if (mode == kStepSq) k = grad_dtype == AF_DT_BF16 ? kernel_for<uint16_t>(mode, false, world, act)

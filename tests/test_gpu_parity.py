@@ -313,10 +313,10 @@ def test_fake_sharded_parity(P):
     (36_000_001, 2, 17, 5, "f32", "delta", False),                # segments span many chunks
 ])
 def test_wide_finalize_parity(n, L, pre, head, dt, acc, fused):
-    """More than kFinChunk interval-end tiles: the streaming kernel leaves the
-    partials to the second, wide finalize launch (chunk sums + chunk-order
-    combine).  Records match the oracle while the frozen prefix moves the first
-    active tile off the chunk grid."""
+    """Many finalize chunks (256 tiles each, reduced by the streaming grid's CTAs
+    as they run out of tiles; chunk sums + chunk-order combine).  Records match
+    the oracle while the frozen prefix moves the first active tile off the chunk
+    grid."""
     lay = uniform_layout(n, L, pre=pre, head=head)
     recs, _, fm, oz = run_both(lay, dt, _decaying_step(lay, dt, 41), [2, 1, 2, 1, 2, 1], check_delta=False,
                                fused=fused, acc_mode=acc)

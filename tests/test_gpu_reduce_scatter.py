@@ -111,8 +111,8 @@ def test_fused_reduce_scatter_parity(P, dt, seed):
 
 
 def test_fused_reduce_scatter_wide_finalize_and_scale():
-    # > kFinChunk interval-end tiles per rank (the second, wide finalize launch;
-    # bf16 interval-end tiles are 24576 elements: > 2048 x 24576 per rank)
+    # many finalize chunks per rank (256 interval-end tiles each; bf16 interval-end
+    # tiles are 24576 elements)
     lay = uniform_layout(2 * 52_000_003, 40, pre=1_000_001, head=3_333)
     recs, fms = _run(lay, "bf16", 2, [2, 1, 2], seed=7, scale=1.0)
     assert fms[0].info()["n_fin_chunks"] > 1
