@@ -422,6 +422,7 @@ DecideParams decide_params(af_ctx *c, bool dry, af_decision *out_host) {
   p.last = c->at<af_decision>(c->o_last);
   p.ring = c->at<af_decision>(c->o_ring);
   p.percentile = c->cfg.percentile;
+  p.pct_q = c->cfg.percentile / 100.0;
   p.pct_method = c->cfg.pct_method;
   p.tie_rel_eps = c->cfg.tie_rel_eps;
   p.min_active = c->cfg.min_active;

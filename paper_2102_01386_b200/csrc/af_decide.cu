@@ -10,7 +10,9 @@ namespace {
 __global__ void __launch_bounds__(kDecideThreads) decide_kernel(const DecideParams p) {
   pdl_wait();  // the sums come from the preceding kernel / all-gather
   pdl_launch_dependents();
-  decide_block(p);
+  const DecideIn in = decide_load(p);
+  __syncthreads();
+  decide_block(p, nullptr, in);
 }
 
 }  // namespace

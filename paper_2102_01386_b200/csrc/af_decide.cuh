@@ -22,36 +22,69 @@ namespace af {
 
 constexpr int kDecideThreads = 256;
 
+// AF_TIMING builds: %globaltimer at step i of the decision (tools/end_breakdown_probe.py)
+#define AF_DMARK(i)                                                          \
+  do {                                                                       \
+    if (AF_TIMING && threadIdx.x == 0) p.state->dmark[(i)] = gtimer();       \
+  } while (0)
+
+// The decision's inputs from the device state -- T, f, this thread's segment's
+// previous norm and the POOL map (into shared memory) -- loaded in one round trip
+// by every thread of the CTA.  The fused interval end issues this at the start
+// of its tail, so the loads overlap the segment sums; nothing but this CTA's own
+// commit changes them before the decision.
+struct DecideIn {
+  int T, f;
+  double pv;
+  const int *pool;  // shared memory, [n_pool]
+};
+static __device__ __forceinline__ DecideIn decide_load(const DecideParams &p) {
+  __shared__ int s_pool[AF_MAX_SEGMENTS];
+  const int t = threadIdx.x;
+  DecideIn in;
+  in.T = p.state->T;
+  in.f = p.state->f;
+  in.pv = (t < p.L) ? p.state->prev[t] : 0.0;
+  if (t < p.n_pool) s_pool[t] = p.pool_seg[t];
+  in.pool = s_pool;
+  return in;  // (s_pool is read after the caller's next __syncthreads)
+}
+
 // Alg. 1 on the gathered sums; every one of the 256 threads of the calling CTA
-// must call it (it synchronises the block).
-static __device__ __noinline__ void decide_block(const DecideParams &p) {
+// must call it (it synchronises the block) after decide_load and a barrier.
+// ss_sum: the rank-order sums already formed in shared memory by the caller (the
+// fused interval end), or nullptr to sum the P rows of p.ss_all here.
+static __device__ __noinline__ void decide_block(const DecideParams &p, const double *ss_sum, const DecideIn in) {
   __shared__ double s_eta[AF_MAX_SEGMENTS];
   __shared__ double s_act[AF_MAX_SEGMENTS];
   __shared__ double s_sorted[AF_MAX_SEGMENTS];
-  __shared__ int s_pool[AF_MAX_SEGMENTS];
-  __shared__ double s_thr;
+  __shared__ double s_thr, s_win;
   __shared__ int s_k, s_near, s_nonfinite;
   __shared__ unsigned int s_flags;
 
-  // Latency-bound: every global load below is independent of the others, so
-  // they are in flight together (one L2 round trip) -- the state words, this
-  // segment's previous norm, the POOL map and the P exchange rows (summed in
-  // rank order).
+  // Latency-bound.  With ss_sum == nullptr the P exchange rows are loaded here
+  // (in flight together, one L2 round trip) and summed in rank order.
+  AF_DMARK(0);
   const int t = threadIdx.x;
   const int L = p.L;
-  const int T = p.state->T;
-  int f = p.state->f;
-  const double pv = (t < L) ? p.state->prev[t] : 0.0;
-  if (t < p.n_pool) s_pool[t] = p.pool_seg[t];
+  const int T = in.T;
+  int f = in.f;
+  const double pv = in.pv;
+  const int *s_pool = in.pool;
   double ss = 0.0;
   if (t < L) {
-    for (int r = 0; r < p.world; ++r) ss = __dadd_rn(ss, __ldcg(p.ss_all + r * L + t));
+    if (ss_sum != nullptr) {
+      ss = ss_sum[t];
+    } else {
+      for (int r = 0; r < p.world; ++r) ss = __dadd_rn(ss, __ldcg(p.ss_all + r * L + t));
+    }
   }
   f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
   const int n_act = p.n_pool - f;
 
   if (t == 0) s_nonfinite = 0;
   __syncthreads();
+  AF_DMARK(1);
 
   double nrm = 0.0, et = 0.0;
   if (t < L) {
@@ -63,6 +96,7 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
   __syncthreads();
   if (t < n_act) s_act[t] = s_eta[s_pool[f + t]];
   __syncthreads();
+  AF_DMARK(2);
 
   // a peer never arrived: at the exchange (bit 0) or at a fused reduce-scatter barrier (bit 1)
   const bool xfail = (p.state->sticky & 3u) != 0u;
@@ -92,16 +126,17 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
       s_sorted[r] = v;
     }
     __syncthreads();
+    AF_DMARK(3);
     if (t == 0) {
       const int n = n_act;
       double thr;
       if (p.pct_method == AF_PCT_NEAREST_RANK) {
-        int rank = static_cast<int>(ceil(__dmul_rn(__ddiv_rn(p.percentile, 100.0), static_cast<double>(n))));
+        int rank = static_cast<int>(ceil(__dmul_rn(p.pct_q, static_cast<double>(n))));
         rank = rank < 1 ? 1 : (rank > n ? n : rank);
         thr = s_sorted[rank - 1];
       } else {
         // numpy "linear": h = (n-1) * (N/100); gamma = h - floor(h); two-branch lerp
-        const double q = __ddiv_rn(p.percentile, 100.0);
+        const double q = p.pct_q;  // N / 100, rounded once on the host (numpy's q)
         const double h = __dmul_rn(static_cast<double>(n - 1), q);
         if (h >= static_cast<double>(n - 1)) {
           thr = s_sorted[n - 1];
@@ -114,26 +149,28 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
           thr = (gm >= 0.5) ? __dsub_rn(b, __dmul_rn(dba, __dsub_rn(1.0, gm))) : __dadd_rn(a, __dmul_rn(dba, gm));
         }
       }
-      // Alg. 1 scan with break; near-tie window over the comparisons that decide k
-      int k = 0, near = -1;
-      unsigned int fl2 = 0;
-      const double win = __dmul_rn(p.tie_rel_eps, thr);
-      for (int i = 0; i < n; ++i) {
-        const double e = s_act[i];
-        const double dd = fabs(__dsub_rn(e, thr));
-        if (dd > 0.0 && dd <= win) {
-          fl2 |= AF_DEC_NEAR_TIE;
-          if (near < 0) near = s_pool[f + i];
-        }
-        if (e < thr)
-          ++k;
-        else
-          break;
-      }
       s_thr = thr;
-      s_k = k;
-      s_near = near;
-      s_flags = fl2;
+      s_win = __dmul_rn(p.tie_rel_eps, thr);
+      s_k = n;      // no failure: every active layer freezes
+      s_near = n;   // no near-tie
+    }
+    __syncthreads();
+    // Alg. 1 scan with break, in parallel: k = the first position whose eta is not
+    // below the threshold (smem atomicMin -- order-free, so exact); the near-tie
+    // window covers the comparisons that decide k, positions 0..k.
+    AF_DMARK(4);
+    const double thr = s_thr;
+    if (t < n_act && !(s_act[t] < thr)) atomicMin(&s_k, t);
+    __syncthreads();
+    if (t < n_act && t <= s_k) {
+      const double dd = fabs(__dsub_rn(s_act[t], thr));
+      if (dd > 0.0 && dd <= s_win) atomicMin(&s_near, t);
+    }
+    __syncthreads();
+    if (t == 0) {
+      const int near = s_near;
+      s_flags = near < n_act ? AF_DEC_NEAR_TIE : 0u;
+      s_near = near < n_act ? s_pool[f + near] : -1;
     }
   } else if (t == 0) {
     s_thr = __longlong_as_double(0x7FF8000000000000LL);  // NaN: no threshold
@@ -145,6 +182,7 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
   flags |= s_flags;
   const int k = nonfinite ? 0 : s_k;
   const int f_new = f + k;
+  AF_DMARK(5);
 
   // record: device copy, ring slot and (if mapped) the caller's pinned host struct
   af_decision *recs[3] = {p.last, p.ring + (T % kRing), p.host};
@@ -167,6 +205,7 @@ static __device__ __noinline__ void decide_block(const DecideParams &p) {
       r->near_tie_seg = s_near;
     }
   }
+  AF_DMARK(6);
   // commit (not under AF_DRY_RUN, not on non-finite sums)
   if (p.commit && !nonfinite) {
     __syncthreads();  // every thread has read state->prev / T / f

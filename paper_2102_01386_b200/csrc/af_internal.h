@@ -64,6 +64,7 @@ struct DevState {
   unsigned long long tmark[4];   // AF_TIMING builds: %globaltimer at kernel start / tail start / after sums / end
   unsigned long long rs_epoch;   // fused reduce-scatter steps completed (identical on all ranks)
   double prev[AF_MAX_SEGMENTS];  // ||Delta_{T-1,l}||
+  unsigned long long dmark[8];   // AF_TIMING builds: %globaltimer at the decision's steps
 };
 
 #ifndef AF_ALTERNATE_ORDER  // alternate the streaming kernels' tile order per launch (L2 reuse)
@@ -106,6 +107,7 @@ struct DecideParams {
   af_decision *ring;        // [kRing]
   af_decision *host;        // mapped page-locked host record or nullptr
   double percentile;
+  double pct_q;             // percentile / 100 in fp64 (host-rounded, as numpy forms q)
   int32_t pct_method;
   double tie_rel_eps;
   int32_t min_active;
@@ -233,7 +235,15 @@ struct CachePlanParams {
   int32_t rank, world;
 };
 
+#ifndef AF_TIMING
+#define AF_TIMING 0
+#endif
 #ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 // Programmatic dependent launch: our kernels are launched with programmatic stream
 // serialization, so a kernel may be scheduled while its predecessor drains; each
 // kernel calls pdl_wait() before touching global memory the predecessor may write

@@ -31,14 +31,6 @@
 // Tunables (compile-time; defaults chosen from the B200 variant sweep in
 // profiles/r01_v3_variants.jsonl): vectors in flight per thread
 // and load cache hints.
-#ifndef AF_TIMING
-#define AF_TIMING 0
-#endif
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 #ifndef AF_U_END
 #define AF_U_END 4
 #endif
@@ -71,6 +63,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #endif
 #ifndef AF_MINB_END
 #define AF_MINB_END 1
+#endif
+#ifndef AF_MINB_END_BF16  // bf16 interval end / STEP_SUMSQ: min resident CTAs per SM (register cap)
+#define AF_MINB_END_BF16 1
 #endif
 #ifndef AF_U_RS_VEC  // fused reduce-scatter: gradient vectors in flight per thread (over all ranks)
 #define AF_U_RS_VEC 8
@@ -581,9 +576,13 @@ __device__ __forceinline__ int table_end(const NormParams &p, int f) {
 // epoch and this rank's row, the per-segment sums (`sums(publish)`, which calls
 // publish(l, s) for every segment l), the optional NVLink one-shot exchange and
 // the fused decision.  Every thread of the CTA calls it.
+// s_x: >= kFinChunk doubles of shared scratch (the peers' rows when world x L fits).
 template <int MODE, typename SumFn>
-__device__ __forceinline__ void tail_common(const NormParams &p, SumFn sums) {
+__device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, SumFn sums) {
   const int tid = threadIdx.x;
+  // the decision's state inputs: in flight during the sums and the exchange
+  DecideIn din{};
+  if (p.fuse_decide) din = decide_load(p.dec);
   if (p.dbg_tail_delay_ns) {  // AF_DEBUG_TAIL_DELAY_NS (ordering tests only)
     if (tid == 0) {
       const unsigned long long t0 = gtimer();
@@ -604,18 +603,23 @@ __device__ __forceinline__ void tail_common(const NormParams &p, SumFn sums) {
     }
     __syncthreads();
   }
-  // this rank's row of the exchange matrix ss_all[world][L] (the rows the decision sums)
+  // this rank's row of the exchange matrix ss_all[world][L] (the rows the decision
+  // sums), also kept in shared memory for the fused decision
   double *ss_row = p.ss_out;
+  __shared__ double s_ss[AF_MAX_SEGMENTS];
   auto publish = [&](int l, double s) {
     if (MODE == kEndDelta) {
       ss_row[l] = s;
+      s_ss[l] = s;
     } else {
       const double acc = p.first ? s : p.ss_acc[l] + s;
       if (p.commit) p.ss_acc[l] = acc;
       if (p.end) ss_row[l] = acc;
+      s_ss[l] = acc;
     }
   };
   sums(publish);
+  bool ss_in_smem = !xchg;  // world 1: the own row is the sum
   if (xchg && (sticky_of(p) & 3u)) {
     // an earlier exchange or barrier timed out (sticky until af_set_state): no peer
     // stores any more; the peers time out on this rank and flag it as well
@@ -657,8 +661,9 @@ __device__ __forceinline__ void tail_common(const NormParams &p, SumFn sums) {
             break;
           }
           if (f0 == e32 && f1 == e32) {
-            p.ss_out[static_cast<ptrdiff_t>(q - p.xrank) * L + l] =
-                __longlong_as_double(static_cast<long long>((lo & 0xFFFFFFFFull) | (hi << 32)));
+            const double v = __longlong_as_double(static_cast<long long>((lo & 0xFFFFFFFFull) | (hi << 32)));
+            p.ss_out[static_cast<ptrdiff_t>(q - p.xrank) * L + l] = v;
+            if (W * L <= kFinChunk) s_x[i] = v;
             break;
           }
           if (spin > (1ll << 22)) {  // ~seconds: a peer never arrived -- flag it, do not hang the GPU
@@ -680,6 +685,14 @@ __device__ __forceinline__ void tail_common(const NormParams &p, SumFn sums) {
       }
       if (tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 1u);
     }
+    if (!s_timeout && !p.dbg_peers_arrived && W * L <= kFinChunk && tid < L) {
+      // the rank-order sum the decision takes (the decide kernel's order: 0 + row_0 + ...)
+      double tot = 0.0;
+      for (int q = 0; q < W; ++q) tot = __dadd_rn(tot, q == p.xrank ? s_ss[tid] : s_x[q * L + tid]);
+      s_ss[tid] = tot;
+      ss_in_smem = true;
+    }
+    ss_in_smem = ss_in_smem && !s_timeout && !p.dbg_peers_arrived && W * L <= kFinChunk;
   }
   if (AF_TIMING) {
     __syncthreads();
@@ -687,7 +700,7 @@ __device__ __forceinline__ void tail_common(const NormParams &p, SumFn sums) {
   }
   if (p.fuse_decide) {
     __syncthreads();
-    decide_block(p.dec);
+    decide_block(p.dec, ss_in_smem ? s_ss : nullptr, din);
   }
   if (AF_TIMING) {
     __syncthreads();
@@ -712,7 +725,7 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
     for (int i = tid; i < n_pc; i += kNormBlock) s_p[i] = __ldcg(p.part2 + i);
     __syncthreads();
   }
-  tail_common<MODE>(p, [&](auto &publish) {
+  tail_common<MODE>(p, s_p, [&](auto &publish) {
     for (int l = tid; l < p.L; l += kNormBlock) {
       int tb = stb[l];
       tb = tb < first_tile ? first_tile : tb;
@@ -738,7 +751,7 @@ __device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int
 template <int MODE, typename GT, bool RD, int PM = 1, bool ACT = false>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccum)
                                   ? 2
-                                  : ((MODE >= kAdamAccum) ? 1 : AF_MINB_END))
+                                  : ((MODE >= kAdamAccum) ? 1 : (sizeof(GT) == 2 ? AF_MINB_END_BF16 : AF_MINB_END)))
     norms_kernel(const NormParams p) {
   constexpr bool RS = MODE == kRsAccum || MODE == kRsEnd || MODE == kRsAdamAccum || MODE == kRsAdamEnd;
   constexpr bool PARTIALS = MODE != kAccum && MODE != kAdamAccum && MODE != kRsAccum && MODE != kRsAdamAccum;

@@ -1,9 +1,9 @@
 """Where does one interval end's time go at a per-rank shard size?
 
 Needs an AF_TIMING=1 build (the kernels stamp %globaltimer into the device
-state: tmark[0] = block 0 past its dependency wait, tmark[1] = last CTA's tail
-start, tmark[2] = after the segment sums + exchange, tmark[3] = after the
-decision).  For each context, single dry-run interval ends (synchronised, event
+state: tmark[0] = block 0 past its dependency wait, tmark[1] = the last CTA to
+leave its tile loop, tmark[2] = after the segment sums + exchange, tmark[3] =
+after the decision; dmark[0..6] = the decision's steps).  For each context, single dry-run interval ends (synchronised, event
 pair around each) and a back-to-back series; prints per-phase medians in us.
 
     AF_NVCC_EXTRA="-DAF_TIMING=1" python tools/end_breakdown_probe.py
@@ -62,10 +62,17 @@ def main():
             fm.interval_end(g, dry_run=True, copy_record=False)
             e.record()
             torch.cuda.synchronize()
-            t = struct.unpack_from("<4Q", fm.scratch[:64].cpu().numpy().tobytes(), 24)
-            rows.append({"event_us": a.elapsed_time(e) * 1e3, "stream_us": (t[1] - t[0]) / 1e3,
-                         "sums_exchange_us": (t[2] - t[1]) / 1e3, "decide_us": (t[3] - t[2]) / 1e3,
-                         "t0_to_t3_us": (t[3] - t[0]) / 1e3})
+            raw = fm.scratch[:2176].cpu().numpy().tobytes()
+            t = struct.unpack_from("<4Q", raw, 24)
+            dm = struct.unpack_from("<8Q", raw, 2112)   # DevState.dmark: the decision's steps
+            row = {"event_us": a.elapsed_time(e) * 1e3, "stream_us": (t[1] - t[0]) / 1e3,
+                   "sums_exchange_us": (t[2] - t[1]) / 1e3, "decide_us": (t[3] - t[2]) / 1e3,
+                   "t0_to_t3_us": (t[3] - t[0]) / 1e3}
+            names = ("d_loads", "d_eta", "d_sort", "d_thr", "d_scan", "d_records", "d_commit")
+            ends = list(dm[1:7]) + [t[3]]
+            for k, nm in enumerate(names):
+                row[nm + "_us"] = (ends[k] - dm[k]) / 1e3
+            rows.append(row)
         rows = rows[3:]
         med = {k: round(statistics.median(r[k] for r in rows), 2) for k in rows[0]}
         a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
