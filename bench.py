@@ -400,6 +400,16 @@ def run_ours(args, rank, world, local):
                               else "static"),
                    "launch": "eager" if args.no_graph else "CUDA graph per step (8 graphs rotating id batches)",
                    "l2": "inputs larger than L2: each step streams >= 4 GB/rank through the 126 MB L2"},
+        "value_composition": "whole step: accumulate + interval end (grad-norm + decide) + cache get + put "
+                             "(all SURVEY.md 8(a) rows); the metric's grad-norm+decide quantity alone is "
+                             "grad_norm_decide_in_step",
+        **({"grad_norm_decide_in_step": {
+            "us": round(marg["grad_norm_decide"] * 1e3, 2),
+            "gbs": round(bytes_rank["grad_norm_decide"] / (marg["grad_norm_decide"] * 1e-3) / 1e9, 1),
+            "frac_of_peak": round(bytes_rank["grad_norm_decide"] / (marg["grad_norm_decide"] * 1e-3) / 1e9 / peak, 4),
+            "bytes_per_launch": bytes_rank["grad_norm_decide"],
+            "method": "marginal device time of af_interval_end in the graph-replayed step (phases_in_step)"}}
+           if marg else {}),
         "grad_norm_decide_gbs": round(gn_dec, 1),
         "grad_norm_decide_frac_of_hbm_peak": round(gn_dec / peak, 4),
         "cache_gbs": round(cache_gbs, 1),
@@ -428,6 +438,8 @@ def run_ours(args, rank, world, local):
     if not args.no_cache_sweep:
         result["cache_gbs_by_batch"] = cache_sweep(cache, my_ids, rows, dev, world, dist)
         result["cache_host_tier"] = host_tier_probe(rows, dev)
+        if world == 1:
+            result["cache_epoch_c4"] = cache_epoch_c4(dev)
     if not args.no_extras:
         result["next1_fused_adamw"] = adamw_probe(fm, lay, dt, s_g, n_loc, grads, dev)
         if world == 1:
@@ -436,6 +448,7 @@ def run_ours(args, rank, world, local):
         result["e2e"] = run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(lay, dt, s_g, B, budget_s=12.0)
+        result["cpu_baseline_all_cores"] = cpu_baseline_all_cores(lay, dt, s_g, B)
     if world == 1 and not args.no_shard_probe and args.workload == "bert-large-f32":
         result["rank_shard_p8"] = rank_shard_probe(args, dev)
     if world == 1 and not args.no_secondary:
@@ -636,6 +649,73 @@ def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(6, 32, 256, 1024
         out[str(B)] = res
     del flush
     return out
+
+
+def cache_epoch_c4(dev, world_emul=8, B=256, seed=3):
+    """the frozen-prefix cache over epochs, one rank's
+    partition of 100k examples x 196,608 B at P = 8 (12,500 ids, 2.46 GB), with
+    the boundary change 4 -> 7 (records written at depth 4 are
+    evicted on read once 7 blocks are frozen, then re-cached at depth 7):
+      epoch 0  put every owned id at depth 4 (permutation pi_0, batches of B)
+      epoch 1  boundary 7: get in pi_1 (every record hits at depth 4 and is
+               evicted), then re-put each batch at depth 7
+      epoch 2  get in pi_2 (hits at depth 7, nothing evicted)
+    Eager calls on one stream, CUDA events around each epoch; GB/s = 2 x rows x
+    row_bytes per call.  Counts are checked as the epochs run."""
+    import torch
+
+    import paper_2102_01386_b200 as af
+    peak, _ = measured_peaks()
+    rank = 0
+    cache = af.ActivationCache(NUM_EXAMPLES, ROW_BYTES, rank=rank, world=world_emul, device=dev)
+    ids = torch.arange(rank, NUM_EXAMPLES, world_emul, device=dev, dtype=torch.int64)
+    n = ids.numel()
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    rows = torch.randint(0, 256, (B, ROW_BYTES), dtype=torch.uint8, device=dev, generator=gen)
+    out = torch.empty_like(rows)
+    dep = torch.empty(B, dtype=torch.int32, device=dev)
+
+    def perm(e):
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed * 1000 + e)
+        p = ids[torch.randperm(n, device=dev, generator=g)]
+        return [p[i:i + B].contiguous() for i in range(0, n, B)]
+
+    res = {"partition_rows": n, "row_bytes": ROW_BYTES, "batch": B, "world_emulated": world_emul,
+           "l2": "cold: each epoch walks 2.46 GB of records in a fresh permutation"}
+
+    def epoch(name, batches, fn, calls_per_batch):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for bt in batches:
+            fn(bt)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        byts = sum(2 * bt.numel() * ROW_BYTES for bt in batches) * calls_per_batch
+        gbs = byts / (ms * 1e-3) / 1e9
+        res[name] = {"ms": round(ms, 3), "calls": len(batches) * calls_per_batch, "gbs": round(gbs, 1),
+                     "frac_of_peak": round(gbs / peak, 4)}
+
+    epoch("epoch0_put_depth4", perm(0), lambda bt: cache.put(bt, rows[:bt.numel()], 4), 1)
+    assert cache.status() == (0, n)
+
+    def get_evict_reput(bt):
+        cache.get(bt, 7, out[:bt.numel()], dep[:bt.numel()])
+        cache.put(bt, out[:bt.numel()], 7)
+    epoch("epoch1_get_evict_reput_depth7", perm(1), get_evict_reput, 2)
+    assert cache.status() == (0, n)           # every record evicted on read and re-cached
+    torch.cuda.synchronize()
+    res["epoch1_depths_seen"] = sorted(set(dep.tolist()))
+    epoch("epoch2_get_hits_depth7", perm(2), lambda bt: cache.get(bt, 7, out[:bt.numel()], dep[:bt.numel()]), 1)
+    torch.cuda.synchronize()
+    assert cache.status() == (0, n) and set(dep.tolist()) == {7}
+    cache.close()
+    del cache
+    torch.cuda.empty_cache()
+    return res
 
 
 def host_tier_probe(rows, dev, reps=10):
@@ -927,20 +1007,31 @@ def run_e2e(args, fm, cache, info, lay, dt, s_g, B, id_batches, rows, dev, world
 
 # ------------------------------------------------------------------ the oracle (CPU baseline / reference arm)
 
-def oracle_step_runner(lay, dt, s_g, B, n_sample):
-    """The oracle as it stands, on the first n_sample elements of the workload's
-    flat buffer (a prefix of its segments) plus B cache rows."""
+def oracle_step_runner(lay, dt, s_g, B, n_sample, lo=0, fast_inputs=False):
+    """The oracle as it stands, on elements [lo, lo + n_sample) of the workload's
+    flat buffer (the segments clipped to that slice) plus B cache rows.
+    fast_inputs: draw the slice's values directly (same distribution, no full-size
+    draw) -- for the all-core timing, whose processes each take one slice."""
     import numpy as np
 
     import oracle as O
-    from afinputs import bert_grad_step, cache_rows
-    offs = [o for o in lay.offsets if o < n_sample] + [n_sample]
-    kinds = lay.kinds[:len(offs) - 1]
+    from afinputs import bert_grad_step, cache_rows, f32_to_bf16_bits
+    hi = lo + n_sample
+    offs = [0] + [o - lo for o in lay.offsets if lo < o < hi] + [n_sample]
+    first = max(l for l in range(lay.n_segments) if lay.offsets[l] <= lo)
+    kinds = lay.kinds[first:first + len(offs) - 1]
     if O.SEG_POOL not in kinds:           # keep a valid layout: treat the sample as one POOL
         kinds = [O.SEG_POOL] * len(kinds)
     kinds = [k if k != O.SEG_HEAD else O.SEG_POOL for k in kinds]
+    if O.SEG_PRE in kinds and kinds[0] != O.SEG_PRE:
+        kinds = [O.SEG_POOL if k == O.SEG_PRE else k for k in kinds]
     fz = O.Freezer(offs, kinds, O.DT_BF16 if dt == "bf16" else O.DT_F32)
-    g = [bert_grad_step(lay, 0, 0, t, dtype=dt, hi=n_sample) for t in range(2)]
+    if fast_inputs:
+        rng = np.random.default_rng([lo, 0xAF])
+        x = [(rng.random(n_sample, dtype=np.float32) * np.float32(2e-3) - np.float32(1e-3)) for _ in range(2)]
+        g = [f32_to_bf16_bits(v) if dt == "bf16" else v for v in x]
+    else:
+        g = [bert_grad_step(lay, 0, 0, t, dtype=dt, lo=lo, hi=hi) for t in range(2)]
     cache = O.Cache(NUM_EXAMPLES, ROW_BYTES)
     ids = np.arange(B)
     rows = cache_rows(0, 0, B, ROW_BYTES)
@@ -976,6 +1067,69 @@ def cpu_baseline(lay, dt, s_g, B, budget_s=12.0):
     return {"value": round(nbytes / dt_s / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"{k} oracle steps on the first {n_sample:,} elements of the {lay.name} flat buffer "
                       f"(+{B} cache rows), numpy single-threaded, {dt_s:.3f} s/step"}
+
+
+def _all_core_worker(q, barrier, lay, dt, s_g, B, n_slice, lo, budget_s):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    try:
+        step, nbytes = oracle_step_runner(lay, dt, s_g, B, n_slice, lo=lo, fast_inputs=True)
+        step(0)
+    except Exception as e:  # noqa: BLE001
+        barrier.abort()
+        q.put(("error", repr(e)))
+        return
+    try:
+        barrier.wait(timeout=300)
+    except Exception:  # noqa: BLE001
+        q.put(("error", "barrier broken"))
+        return
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        step(k)
+        k += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    q.put((k * nbytes, time.perf_counter() - t0))
+
+
+def cpu_baseline_all_cores(lay, dt, s_g, B, budget_s=8.0, n_sample=48_000_000):
+    """The same oracle in nproc independent processes, each on a disjoint slice
+    of the workload's flat buffer (n_sample / nproc elements, at least 8M so a
+    slice does not sit in the host caches; the oracle itself is not
+    parallelised): aggregate GB/s over the concurrent processes."""
+    import multiprocessing as mp
+    import platform
+    nproc = os.cpu_count() or 1
+    model = platform.processor() or ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    n_slice = max(8_000_000, n_sample // nproc)   # >= 96 MB per process: past the host caches
+    ctx = mp.get_context("fork")
+    q, barrier = ctx.Queue(), ctx.Barrier(nproc)
+    procs = [ctx.Process(target=_all_core_worker, args=(q, barrier, lay, dt, s_g, max(1, B // nproc), n_slice,
+                                                       i * n_slice % max(1, lay.n - n_slice), budget_s))
+             for i in range(nproc)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=900) for _ in procs]
+    for p in procs:
+        p.join()
+    errs = [r[1] for r in res if r[0] == "error"]
+    if errs:
+        return {"error": errs[0], "cores": nproc, "kind": "oracle"}
+    total_bytes = sum(b for b, _ in res)
+    wall = max(t for _, t in res)
+    return {"value": round(total_bytes / wall / 1e9, 3), "unit": "GB/s", "cores": nproc, "kind": "oracle",
+            "cpu_model": model,
+            "sample": f"{nproc} concurrent oracle processes (numpy, 1 thread each), each on a disjoint "
+                      f"{n_slice:,}-element slice of the {lay.name} flat buffer + B/nproc cache rows, "
+                      f"{budget_s:.0f} s each"}
 
 
 def run_reference(args, rank, world):
@@ -1017,8 +1171,21 @@ def run_reference(args, rank, world):
     }), flush=True)
 
 
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one command for N GPUs: re-launch this script under torchrun (one rank per GPU)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)

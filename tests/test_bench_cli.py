@@ -40,3 +40,15 @@ def test_reference_arm_rank0_only_under_torchrun():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = _lines(r.stdout)
     assert len(lines) == 1 and lines[0]["impl"] == "reference"
+
+
+def test_gpus_flag_self_launches_torchrun():
+    # `python bench.py --gpus 2` without torchrun re-launches itself under
+    # torch.distributed.run (one rank per GPU); the reference arm prints on rank 0 only
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "bert-base-bf16", "--gpus",
+                        "2", "--steps", "1", "--warmup", "0"], cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env={k: v for k, v in dict(os.environ, CUDA_VISIBLE_DEVICES="").items()
+                            if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = _lines(r.stdout)
+    assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
