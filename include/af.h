@@ -105,6 +105,7 @@ typedef enum { AF_PCT_LINEAR = 0, AF_PCT_NEAREST_RANK = 1 } af_pct_method;
 /* af_cache_status device error flags (sticky) */
 #define AF_CACHE_ERR_RANGE 0x1u /* an id outside [0, num_examples)               */
 #define AF_CACHE_ERR_OWNER 0x2u /* an id with id % world != rank (P:335 partition) */
+#define AF_CACHE_ERR_IO 0x4u    /* a disk-tier read or write failed (host callback)  */
 
 typedef struct {
   int32_t n_segments;          /* L, 1..AF_MAX_SEGMENTS                                   */
@@ -419,6 +420,25 @@ AF_API af_status af_cache_host_bytes(const af_cache *c, size_t *host_bytes);
  * torch pin_memory: device-mapped under UVA), 16-byte aligned. */
 AF_API af_status af_cache_bind_host(af_cache *c, void *host_pinned);
 
+/* Disk tier (§3.2: "We store the intermediate output to disk when it no
+ * longer fits in CPU memory"; reader and writer processes).  Host only,
+ * after af_cache_set_capacity and before af_cache_bind: disk_rows more record
+ * slots, [hbm_rows + host_rows, I), as rows of the file at `path` (created or
+ * truncated, sized disk_rows x row_bytes; the library closes but never deletes
+ * it).  Slots are handed out HBM first, then host, then disk.  Rows routed to the
+ * disk by a call's plan kernel move through a caller-owned page-locked staging
+ * area (af_cache_disk_stage_bytes; bound with af_cache_bind_disk_stage) of
+ * stage_rows rows, by stream-ordered host callbacks (cudaLaunchHostFunc: the
+ * reader pread()s before the copy kernel of a get, the writer pwrite()s after
+ * the copy kernel of a put); calls are split into passes of stage_rows rows.
+ * All calls on one disk-tier cache must be issued on one stream (the callbacks
+ * take their work list from the staging area).  An I/O error sets the sticky
+ * AF_CACHE_ERR_IO.  Without GPUDirect Storage (not in this build) the disk is
+ * reached through host memory. */
+AF_API af_status af_cache_set_disk_tier(af_cache *c, int64_t disk_rows, int32_t stage_rows, const char *path);
+AF_API af_status af_cache_disk_stage_bytes(const af_cache *c, size_t *stage_bytes);
+AF_API af_status af_cache_bind_disk_stage(af_cache *c, void *stage_pinned);
+
 /* cross-GPU cache get / put for samplers that are not
  * rank-affine.  Every rank registers every rank's direct-mapped store (CUDA IPC
  * of payload + meta, handles exchanged by the caller; or contexts of one
@@ -444,6 +464,7 @@ typedef struct {
   int64_t n_valid, n_hbm, n_host;
   int64_t n_dropped;         /* puts refused for lack of room (tiered) */
   int64_t free_slots;
+  int64_t n_disk;            /* valid records in the disk tier */
 } af_cache_info;
 /* Synchronous: counters of the store. */
 AF_API af_status af_cache_stats(af_cache *c, af_cache_info *out);

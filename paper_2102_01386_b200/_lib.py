@@ -24,7 +24,7 @@ AF_DEC_FIRST_INTERVAL, AF_DEC_SKIPPED_FEW, AF_DEC_NEAR_TIE, AF_DEC_NONFINITE, AF
 AF_DEC_EXCHANGE_TIMEOUT = 32
 AF_IPC_HANDLE_BYTES = 128
 AF_CACHE_IPC_HANDLE_BYTES = 256
-AF_CACHE_ERR_RANGE, AF_CACHE_ERR_OWNER = 1, 2
+AF_CACHE_ERR_RANGE, AF_CACHE_ERR_OWNER, AF_CACHE_ERR_IO = 1, 2, 4
 
 
 class AfLayout(ctypes.Structure):
@@ -62,7 +62,7 @@ class AfAdamW(ctypes.Structure):
 class AfCacheInfo(ctypes.Structure):
     _fields_ = [("error_flags", c_uint32), ("pad", c_uint32), ("partition", c_int64), ("capacity", c_int64),
                 ("n_valid", c_int64), ("n_hbm", c_int64), ("n_host", c_int64), ("n_dropped", c_int64),
-                ("free_slots", c_int64)]
+                ("free_slots", c_int64), ("n_disk", c_int64)]
 
 
 # name -> (restype, argtypes); every af_* symbol declared in include/af.h
@@ -106,6 +106,9 @@ SIGNATURES = {
     "af_cache_set_capacity": (c_int, [c_void_p, c_int64, c_int64]),
     "af_cache_host_bytes": (c_int, [c_void_p, POINTER(c_size_t)]),
     "af_cache_bind_host": (c_int, [c_void_p, c_void_p]),
+    "af_cache_set_disk_tier": (c_int, [c_void_p, c_int64, c_int32, c_char_p]),
+    "af_cache_disk_stage_bytes": (c_int, [c_void_p, POINTER(c_size_t)]),
+    "af_cache_bind_disk_stage": (c_int, [c_void_p, c_void_p]),
     "af_cache_stats": (c_int, [c_void_p, POINTER(AfCacheInfo)]),
     "af_cache_exchange_ipc_handle": (c_int, [c_void_p, c_void_p]),
     "af_cache_set_peers_ipc": (c_int, [c_void_p, c_void_p]),

@@ -5,6 +5,7 @@ torch.distributed for the NCCL-id bootstrap.  Every step of the path runs in the
 library's sm_100a kernels; nothing here computes.
 """
 import ctypes
+import os
 from ctypes import byref, c_int64, c_size_t, c_uint32, c_void_p
 
 import torch
@@ -321,24 +322,40 @@ class ActivationCache:
 
     Direct-mapped in HBM by default (room for every owned id).  With
     hbm_rows/host_rows it is tiered with admission (af_cache_set_capacity): room
-    for I = hbm_rows + host_rows records, the host part in page-locked memory;
-    puts of new ids beyond I are dropped (drop-newest)."""
+    for I = hbm_rows + host_rows (+ disk_rows) records, the host part in
+    page-locked memory, the disk part in a file (af_cache_set_disk_tier; a
+    temporary file unless disk_path is given, deleted on close); puts of new ids
+    beyond I are dropped (drop-newest)."""
 
     def __init__(self, num_examples, row_bytes, rank=0, world=1, device=None, bind=True,
-                 hbm_rows=None, host_rows=0):
+                 hbm_rows=None, host_rows=0, disk_rows=0, stage_rows=256, disk_path=None):
         h = c_void_p()
         check(lib.af_cache_create(int(num_examples), int(row_bytes), int(rank), int(world), byref(h)),
               "af_cache_create")
         self._h = h
         self.num_examples, self.row_bytes, self.rank, self.world = int(num_examples), int(row_bytes), rank, world
         self.tiered = hbm_rows is not None or host_rows
-        if self.tiered:
+        self._tmp_disk = None
+        if self.tiered or disk_rows:
+            self.tiered = True
             check(lib.af_cache_set_capacity(h, int(hbm_rows or 0), int(host_rows)), "af_cache_set_capacity")
+        if disk_rows:
+            if disk_path is None:
+                import tempfile
+                fd, disk_path = tempfile.mkstemp(prefix="af_cache_disk_", suffix=".bin")
+                os.close(fd)
+                self._tmp_disk = disk_path
+            check(lib.af_cache_set_disk_tier(h, int(disk_rows), int(stage_rows), str(disk_path).encode()),
+                  "af_cache_set_disk_tier")
+        self.disk_path = disk_path
         p, m, hb = c_size_t(), c_size_t(), c_size_t()
         check(lib.af_cache_storage_bytes(h, byref(p), byref(m)), "af_cache_storage_bytes")
         check(lib.af_cache_host_bytes(h, byref(hb)), "af_cache_host_bytes")
         self.payload_bytes, self.meta_bytes, self.host_bytes = p.value, m.value, hb.value
-        self.payload = self.meta = self.host_tier = None
+        sb = c_size_t()
+        check(lib.af_cache_disk_stage_bytes(h, byref(sb)), "af_cache_disk_stage_bytes")
+        self.stage_bytes = sb.value
+        self.payload = self.meta = self.host_tier = self.disk_stage = None
         self.device = None
         if bind:
             self.bind(device)
@@ -354,6 +371,11 @@ class ActivationCache:
             if self.host_bytes:
                 self.host_tier = torch.empty(self.host_bytes, dtype=torch.uint8, pin_memory=True)
                 check(lib.af_cache_bind_host(self._h, c_void_p(self.host_tier.data_ptr())), "af_cache_bind_host")
+            if self.stage_bytes:
+                # page-locked staging of the disk tier; pinned tensors are 256-byte aligned
+                self.disk_stage = torch.empty(self.stage_bytes, dtype=torch.uint8, pin_memory=True)
+                check(lib.af_cache_bind_disk_stage(self._h, c_void_p(self.disk_stage.data_ptr())),
+                      "af_cache_bind_disk_stage")
 
     def _ids(self, ids):
         return _dev_tensor(ids, "ids", self.device, dtypes=(torch.int64,))
@@ -435,6 +457,12 @@ class ActivationCache:
         if getattr(self, "_h", None):
             lib.af_cache_destroy(self._h)
             self._h = None
+        if getattr(self, "_tmp_disk", None):
+            try:
+                os.remove(self._tmp_disk)
+            except OSError:
+                pass
+            self._tmp_disk = None
 
     def __del__(self):
         try:

@@ -137,9 +137,12 @@ __device__ __forceinline__ Desc item_addr(const CacheParams &p, int64_t j) {
   if (p.rowslot) {  // tiered: the plan kernel resolved the row's slot (and its meta / eviction)
     const int32_t slot = p.rowslot[i];
     if (slot < 0) return dsc;
-    rec = (slot < p.hbm_rows ? p.payload + static_cast<int64_t>(slot) * p.row_bytes
-                             : p.host + (static_cast<int64_t>(slot) - p.hbm_rows) * p.row_bytes) +
-          off;
+    if (p.disk_base > 0 && slot >= p.disk_base)  // disk tier: this pass's staging row i (host callbacks move it)
+      rec = p.stage + static_cast<int64_t>(i) * p.row_bytes + off;
+    else
+      rec = (slot < p.hbm_rows ? p.payload + static_cast<int64_t>(slot) * p.row_bytes
+                               : p.host + (static_cast<int64_t>(slot) - p.hbm_rows) * p.row_bytes) +
+            off;
   } else {
     rec = payload + (id / p.world) * p.row_bytes + off;
   }
@@ -344,6 +347,10 @@ __global__ void __launch_bounds__(kPlanThreads) cache_plan_kernel(const CachePla
   if (threadIdx.x == 0) {
     s_top = p.hdr->top;
     s_dropped = 0u;
+    if (p.manifest) {  // disk tier: the host callback's work list for this pass
+      p.manifest[0] = p.n;
+      p.manifest[1] = p.put;
+    }
   }
   __syncthreads();
   for (int base = 0; base < p.n; base += kPlanThreads) {
@@ -389,6 +396,7 @@ __global__ void __launch_bounds__(kPlanThreads) cache_plan_kernel(const CachePla
           reinterpret_cast<int4 *>(p.meta)[lid] = make_int4(m.x, 0, 0, -1);
         }
       }
+      if (p.manifest) p.manifest[2 + i] = (slot >= 0 && slot >= p.disk_base) ? slot - p.disk_base : -1;
     }
     __syncthreads();
     if (threadIdx.x == 0) {

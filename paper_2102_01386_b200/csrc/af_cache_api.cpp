@@ -1,8 +1,14 @@
 // af_cache_api.cpp -- the storage manager's C-ABI entry points (af_cache_*):
 // direct-mapped and tiered stores, admission, statistics, peer (global) access.
+#include <fcntl.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <cerrno>
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "af_host.h"
@@ -13,9 +19,21 @@ struct af_cache {
   int64_t num_examples = 0, row_bytes = 0;
   int64_t capacity = 0;  // owned ids of this rank (the partition size D_local)
   int32_t rank = 0, world = 1;
-  // tiered mode (af_cache_set_capacity): I = hbm_rows + host_rows < D slots
+  // tiered mode (af_cache_set_capacity): I = hbm_rows + host_rows (+ disk_rows) slots
   bool tiered = false;
   int64_t hbm_rows = 0, host_rows = 0;
+  // disk tier (af_cache_set_disk_tier): slots [hbm + host, I) are rows of a file,
+  // moved through a page-locked staging area by stream-ordered host callbacks
+  int64_t disk_rows = 0;
+  int fd = -1;
+  std::string disk_path;
+  int32_t stage_rows = 0;            // rows per plan pass when a disk tier exists
+  char *stage_host = nullptr;        // caller's page-locked staging: [manifest | rows]
+  char *stage_dev = nullptr;         // its device alias
+  bool disk_bound = false;
+  std::atomic<unsigned int> disk_err{0};  // AF_CACHE_ERR_IO from the host callbacks
+  int64_t slots() const { return hbm_rows + host_rows + disk_rows; }
+  size_t manifest_bytes() const { return (static_cast<size_t>(stage_rows) + 2) * 4 + 255 & ~size_t(255); }
   int32_t max_batch = 65536;  // rows per plan pass (larger calls are split)
   char *payload = nullptr;
   char *meta = nullptr;  // [CacheHeader | pad to 256 B][CacheMeta x capacity][free x I][rowslot x max_batch]
@@ -26,12 +44,12 @@ struct af_cache {
   int grid = 0;
   size_t o_peer_table() const {
     size_t b = kMetaHeaderBytes + static_cast<size_t>(capacity) * sizeof(CacheMeta);
-    if (tiered) b += static_cast<size_t>(hbm_rows + host_rows) * 4 + static_cast<size_t>(max_batch) * 4;
+    if (tiered) b += static_cast<size_t>(slots()) * 4 + static_cast<size_t>(max_batch) * 4;
     return (b + 255) / 256 * 256;
   }
   size_t meta_bytes() const { return o_peer_table() + 2 * AF_MAX_WORLD * sizeof(void *); }
   size_t o_free() const { return kMetaHeaderBytes + static_cast<size_t>(capacity) * sizeof(CacheMeta); }
-  size_t o_rowslot() const { return o_free() + static_cast<size_t>(hbm_rows + host_rows) * 4; }
+  size_t o_rowslot() const { return o_free() + static_cast<size_t>(slots()) * 4; }
   static constexpr size_t kMetaHeaderBytes = 256;
 };
 
@@ -71,6 +89,52 @@ af_status af_cache_set_capacity(af_cache *c, int64_t hbm_rows, int64_t host_rows
   c->tiered = true;
   c->hbm_rows = hbm_rows;
   c->host_rows = host_rows;
+  return AF_OK;
+}
+
+af_status af_cache_set_disk_tier(af_cache *c, int64_t disk_rows, int32_t stage_rows, const char *path) {
+  AF_NVTX();
+  if (!c || !path) return fail(AF_EINVAL, "NULL argument");
+  if (c->bound) return fail(AF_ESTATE, "set the disk tier before binding storage");
+  if (!c->tiered) return fail(AF_ESTATE, "the disk tier extends a tiered store (af_cache_set_capacity first)");
+  if (c->fd >= 0) return fail(AF_ESTATE, "disk tier already set");
+  if (disk_rows < 1 || stage_rows < 1 || stage_rows > 65536) return fail(AF_EINVAL, "bad disk_rows / stage_rows");
+  if (c->hbm_rows + c->host_rows + disk_rows > (int64_t(1) << 31) - 1) return fail(AF_ERANGE, "capacity too large");
+  const int fd = ::open(path, O_RDWR | O_CREAT | O_TRUNC | O_CLOEXEC, 0600);
+  if (fd < 0) return fail(AF_EINVAL, "cannot open the disk-tier file");
+  if (::ftruncate(fd, static_cast<off_t>(disk_rows) * c->row_bytes) != 0) {
+    ::close(fd);
+    return fail(AF_ERANGE, "cannot size the disk-tier file");
+  }
+  c->fd = fd;
+  c->disk_path = path;
+  c->disk_rows = disk_rows;
+  c->stage_rows = stage_rows;
+  c->max_batch = stage_rows;  // a plan pass stages at most this many rows
+  return AF_OK;
+}
+
+af_status af_cache_disk_stage_bytes(const af_cache *c, size_t *stage_bytes) {
+  AF_NVTX();
+  if (!c || !stage_bytes) return fail(AF_EINVAL, "NULL argument");
+  *stage_bytes = c->fd >= 0 ? c->manifest_bytes() + static_cast<size_t>(c->stage_rows) * c->row_bytes : 0;
+  return AF_OK;
+}
+
+af_status af_cache_bind_disk_stage(af_cache *c, void *stage_pinned) {
+  AF_NVTX();
+  if (!c || !stage_pinned) return fail(AF_EINVAL, "NULL argument");
+  if (c->fd < 0) return fail(AF_ESTATE, "no disk tier configured");
+  if (!aligned(stage_pinned, 256)) return fail(AF_EINVAL, "staging must be 256-byte aligned");
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, stage_pinned);
+  if (e != cudaSuccess || a.type != cudaMemoryTypeHost || !a.devicePointer) {
+    cudaGetLastError();
+    return fail(AF_EINVAL, "staging must be page-locked, device-mapped memory (cudaHostAlloc / pin_memory)");
+  }
+  c->stage_host = static_cast<char *>(stage_pinned);
+  c->stage_dev = static_cast<char *>(a.devicePointer);
+  c->disk_bound = true;
   return AF_OK;
 }
 
@@ -122,8 +186,8 @@ af_status af_cache_bind(af_cache *c, void *payload_dev, void *meta_dev) {
   c->meta = static_cast<char *>(meta_dev);
   AF_CUDA(cudaMemset(c->meta, 0, c->meta_bytes()), "cudaMemset(meta)");
   if (c->tiered) {
-    // every record slot free: the stack pops slot 0 first (HBM before host)
-    const int32_t I = static_cast<int32_t>(c->hbm_rows + c->host_rows);
+    // every record slot free: the stack pops slot 0 first (HBM, then host, then disk)
+    const int32_t I = static_cast<int32_t>(c->slots());
     std::vector<int32_t> fr(static_cast<size_t>(I));
     for (int32_t k = 0; k < I; ++k) fr[k] = I - 1 - k;
     AF_CUDA(cudaMemcpy(c->meta + c->o_free(), fr.data(), fr.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy(free)");
@@ -156,8 +220,41 @@ static af_status cache_common(af_cache *c, const int64_t *ids, int32_t n, const 
   return AF_OK;
 }
 
+// The disk tier's reader / writer (the paper's reader and writer processes,
+// P:259): a stream-ordered host callback that moves the rows the plan kernel
+// routed to disk slots between the file and the page-locked staging area.  The
+// plan kernel wrote the manifest {n, put, disk index per row (-1: not on disk)}
+// into the staging area, so the callback needs no per-call arguments (calls of
+// one cache are issued on one stream: the next plan runs after this callback).
+static void CUDART_CB disk_io(void *user) {
+  af_cache *c = static_cast<af_cache *>(user);
+  const volatile int32_t *man = reinterpret_cast<const volatile int32_t *>(c->stage_host);
+  const int32_t n = man[0], put = man[1];
+  char *rows = c->stage_host + c->manifest_bytes();
+  for (int32_t i = 0; i < n && i < c->stage_rows; ++i) {
+    const int32_t d = man[2 + i];
+    if (d < 0) continue;
+    char *buf = rows + static_cast<size_t>(i) * c->row_bytes;
+    off_t off = static_cast<off_t>(d) * c->row_bytes;
+    size_t left = static_cast<size_t>(c->row_bytes);
+    while (left > 0) {
+      const ssize_t k = put ? ::pwrite(c->fd, buf, left, off) : ::pread(c->fd, buf, left, off);
+      if (k < 0 && errno == EINTR) continue;
+      if (k <= 0) {
+        c->disk_err.fetch_or(AF_CACHE_ERR_IO);
+        break;
+      }
+      buf += k;
+      off += k;
+      left -= static_cast<size_t>(k);
+    }
+  }
+}
+
 static af_status cache_tiered(af_cache *c, CacheParams &p, bool put, void *stream) {
   if (c->host_rows > 0 && !c->host_bound) return fail(AF_EWORKSPACE, "host tier not bound (af_cache_bind_host)");
+  if (c->fd >= 0 && !c->disk_bound) return fail(AF_EWORKSPACE, "disk staging not bound (af_cache_bind_disk_stage)");
+  const bool disk = c->fd >= 0;
   const int32_t n_all = p.n;
   for (int32_t b0 = 0; b0 < n_all; b0 += c->max_batch) {
     const int32_t n = std::min(c->max_batch, n_all - b0);
@@ -175,20 +272,32 @@ static af_status cache_tiered(af_cache *c, CacheParams &p, bool put, void *strea
     q.num_examples = c->num_examples;
     q.rank = c->rank;
     q.world = c->world;
+    if (disk) {
+      q.manifest = reinterpret_cast<int32_t *>(c->stage_dev);
+      q.disk_base = static_cast<int32_t>(c->hbm_rows + c->host_rows);
+    }
     int e = launch_cache_plan(q, stream);
     if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache plan launch");
+    if (disk && !put)  // reader: disk records -> staging, before the copy kernel
+      AF_CUDA(cudaLaunchHostFunc(static_cast<cudaStream_t>(stream), disk_io, c), "cudaLaunchHostFunc(read)");
     CacheParams r = p;
     r.ids = p.ids + b0;
     r.n = n;
     r.rowslot = q.rowslot;
     r.host = c->host;
     r.hbm_rows = c->hbm_rows;
+    if (disk) {
+      r.stage = c->stage_dev + c->manifest_bytes();
+      r.disk_base = c->hbm_rows + c->host_rows;
+    }
     if (put)
       r.src_rows = p.src_rows + static_cast<int64_t>(b0) * c->row_bytes;
     else
       r.dst_rows = p.dst_rows + static_cast<int64_t>(b0) * c->row_bytes;
     e = put ? launch_cache_put(r, c->grid, stream) : launch_cache_get(r, c->grid, stream);
     if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache copy launch");
+    if (disk && put)  // writer: staging -> disk records, after the copy kernel
+      AF_CUDA(cudaLaunchHostFunc(static_cast<cudaStream_t>(stream), disk_io, c), "cudaLaunchHostFunc(write)");
   }
   return AF_OK;
 }
@@ -251,15 +360,18 @@ af_status af_cache_stats(af_cache *c, af_cache_info *out) {
   std::memset(out, 0, sizeof(*out));
   out->error_flags = h.err;
   out->partition = c->capacity;
-  out->capacity = c->tiered ? c->hbm_rows + c->host_rows : c->capacity;
+  out->capacity = c->tiered ? c->slots() : c->capacity;
   for (const auto &x : m) {
     if (!x.valid) continue;
     out->n_valid++;
-    if (c->tiered && x.slot >= c->hbm_rows)
+    if (c->tiered && x.slot >= c->hbm_rows + c->host_rows)
+      out->n_disk++;
+    else if (c->tiered && x.slot >= c->hbm_rows)
       out->n_host++;
     else
       out->n_hbm++;
   }
+  out->error_flags |= c->disk_err.load();
   out->n_dropped = c->tiered ? h.dropped : 0;
   out->free_slots = c->tiered ? h.top : c->capacity - out->n_valid;
   return AF_OK;
@@ -272,7 +384,7 @@ af_status af_cache_status(af_cache *c, uint32_t *device_error_flags, int64_t *n_
   AF_CUDA(cudaDeviceSynchronize(), "cache status sync");
   unsigned int err = 0;
   AF_CUDA(cudaMemcpy(&err, c->meta, sizeof(err), cudaMemcpyDeviceToHost), "cudaMemcpy(err)");  // CacheHeader.err
-  *device_error_flags = err;
+  *device_error_flags = err | c->disk_err.load();
   if (n_valid) {
     std::vector<CacheMeta> m(static_cast<size_t>(c->capacity));
     if (c->capacity)
@@ -420,6 +532,7 @@ af_status af_cache_destroy(af_cache *c) {
   AF_NVTX();
   if (!c) return fail(AF_EINVAL, "NULL cache");
   ipc_release(c->ipc_opened);
+  if (c->fd >= 0) ::close(c->fd);  // the file stays (the caller named it)
   delete c;
   return AF_OK;
 }

@@ -213,7 +213,9 @@ struct CacheParams {
   // tiered mode (rowslot != nullptr): the plan kernel already resolved each row's slot
   const int32_t *rowslot;   // [n] slot per row of the call, -1 = skip
   char *host;               // device alias of the page-locked host tier
-  int64_t hbm_rows;         // slots [0, hbm_rows) in `payload`, the rest in `host`
+  int64_t hbm_rows;         // slots [0, hbm_rows) in `payload`, then `host`
+  char *stage;              // disk tier: device alias of the staging rows (row i of the pass at i)
+  int64_t disk_base;        // slots >= disk_base live on disk (staged); 0: no disk tier
   // global mode (NEXT 4): any id; the owner's (id % world) store is reached through
   // its mapped payload / meta (peer memory over NVLink)
   char *const *peer_payload;     // [world]
@@ -233,6 +235,8 @@ struct CachePlanParams {
   int32_t *depth_out;
   int64_t num_examples;
   int32_t rank, world;
+  int32_t *manifest;        // disk tier: {n, put, disk index per row or -1} (page-locked, mapped)
+  int32_t disk_base;
 };
 
 #ifndef AF_TIMING

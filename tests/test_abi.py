@@ -245,6 +245,27 @@ def test_binding_validates_tensors_before_the_abi():
     c.close()
 
 
+def test_disk_tier_host_checks(tmp_path):
+    h = ctypes.c_void_p()
+    assert L.lib.af_cache_create(1000, 64, 0, 1, ctypes.byref(h)) == L.AF_OK
+    path = str(tmp_path / "tier.bin").encode()
+    assert L.lib.af_cache_set_disk_tier(h, 10, 8, path) == L.AF_ESTATE        # needs a tiered store first
+    assert L.lib.af_cache_set_capacity(h, 5, 5) == L.AF_OK
+    assert L.lib.af_cache_set_disk_tier(h, 0, 8, path) == L.AF_EINVAL
+    assert L.lib.af_cache_set_disk_tier(h, 10, 0, path) == L.AF_EINVAL
+    assert L.lib.af_cache_set_disk_tier(h, 10, 8, b"/nonexistent-dir/x") == L.AF_EINVAL
+    assert L.lib.af_cache_set_disk_tier(h, 10, 8, path) == L.AF_OK
+    assert L.lib.af_cache_set_disk_tier(h, 10, 8, path) == L.AF_ESTATE        # once
+    assert os.path.getsize(tmp_path / "tier.bin") == 10 * 64
+    sb = ctypes.c_size_t()
+    assert L.lib.af_cache_disk_stage_bytes(h, ctypes.byref(sb)) == L.AF_OK
+    assert sb.value >= 8 * 64 + 10 * 4 and sb.value % 256 == 8 * 64 % 256
+    assert L.lib.af_cache_bind_disk_stage(h, None) == L.AF_EINVAL
+    info = L.AfCacheInfo()
+    assert L.lib.af_cache_stats(h, ctypes.byref(info)) == L.AF_EWORKSPACE    # not bound
+    assert L.lib.af_cache_destroy(h) == L.AF_OK
+
+
 def test_reduce_scatter_host_checks():
     # NEXT 1 (ZeRO form): argument / state errors are synchronous host checks
     lay = uniform_layout(1 << 12, 4)

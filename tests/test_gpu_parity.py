@@ -1,6 +1,7 @@
 """GPU parity: the sm_100a path (through the C ABI) vs the fp64 oracle on the
 same seeded inputs.  Run on a B200 with `pytest -m gpu`."""
 import math
+import os
 import struct
 
 import numpy as np
@@ -759,15 +760,21 @@ def test_cache_admission_printed_example_gpu():
     assert np.array_equal(dep.cpu().numpy(), do) and np.array_equal(out.cpu().numpy(), oo)
 
 
-@pytest.mark.parametrize("rank,world,hbm,host", [(0, 1, 300, 200), (2, 4, 100, 150), (0, 1, 0, 400)])
-def test_tiered_cache_epochs_match_oracle(rank, world, hbm, host):
+@pytest.mark.parametrize("rank,world,hbm,host,disk", [(0, 1, 300, 200, 0), (2, 4, 100, 150, 0), (0, 1, 0, 400, 0),
+                                                     (0, 1, 150, 100, 250), (1, 2, 0, 0, 380), (0, 1, 40, 60, 300)])
+def test_tiered_cache_epochs_match_oracle(rank, world, hbm, host, disk):
     """Scripted epochs with boundary changes: evict-on-read frees slots that the
-    re-cache of the same epoch reuses; drops, depths and bytes match the oracle."""
+    re-cache of the same epoch reuses; drops, depths and bytes match the capacity
+    oracle (I = hbm + host + disk) -- with a disk tier the records routed to
+    disk slots go through the staging area and the file (host callbacks), in
+    passes of 64 rows."""
     import paper_2102_01386_b200 as af
     from afinputs import cache_rows, epoch_permutation, rank_ids
     num, rb = 3000, 1024 + 16
-    gc = af.ActivationCache(num, rb, rank=rank, world=world, hbm_rows=hbm, host_rows=host)
-    oc = O.Cache(num, rb, rank, world, capacity=hbm + host)
+    gc = af.ActivationCache(num, rb, rank=rank, world=world, hbm_rows=hbm, host_rows=host, disk_rows=disk,
+                            stage_rows=64)
+    oc = O.Cache(num, rb, rank, world, capacity=hbm + host + disk)
+    host = host + disk   # the assertions below count host + disk as the off-HBM tiers
     mine = rank_ids(num, rank, world)
     for epoch, (depth, bnd) in enumerate([(4, 4), (4, 7), (7, 7), (7, 9)]):
         perm = epoch_permutation(1, epoch, mine)
@@ -787,9 +794,56 @@ def test_tiered_cache_epochs_match_oracle(rank, world, hbm, host):
                 oc.put(miss, rows, depth)
         st = gc.stats()
         assert st["n_valid"] == len(oc.store) and st["n_dropped"] == oc.dropped, (epoch, st, oc.dropped)
-        assert st["n_valid"] <= hbm + host and st["n_hbm"] <= hbm and st["n_host"] <= host
+        assert st["n_valid"] <= hbm + host and st["n_hbm"] <= hbm and st["n_host"] + st["n_disk"] <= host
         assert st["n_valid"] + st["free_slots"] == hbm + host
+        assert st["n_disk"] <= disk and (disk == 0 or epoch == 0 or st["n_disk"] > 0)
+        assert st["error_flags"] == 0
     assert oc.dropped > 0                                   # admission was exercised
+    if disk:
+        assert os.path.getsize(gc.disk_path) == disk * rb
+    gc.close()
+
+
+@pytest.mark.parametrize("tiered", [False, True])
+def test_get_async_prefetch_parity(tiered):
+    """The paper's reader (Fig. 8): the next batch's get is issued on a side
+    stream while the compute stream accumulates gradients; the consumer stream
+    waits on the returned event.  Bytes, depths and evictions equal the oracle's
+    (tiered: HBM + host + disk tiers, every cache call on the side stream)."""
+    import paper_2102_01386_b200 as af
+    from afinputs import cache_rows
+    num, rb = 4000, 8192
+    kw = dict(hbm_rows=300, host_rows=300, disk_rows=600, stage_rows=128) if tiered else {}
+    gc = af.ActivationCache(num, rb, **kw)
+    oc = O.Cache(num, rb, capacity=1200 if tiered else None)
+    side = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    ids_all = np.random.default_rng(8).permutation(num)[:1100]
+    rows = cache_rows(4, 4, len(ids_all), rb)
+    rows_d, ids_d = torch.from_numpy(rows).cuda(), _ids(ids_all)
+    side.wait_stream(main)
+    gc.put(ids_d, rows_d, 3, stream=side)
+    oc.put(ids_all, rows, 3)
+    lay = _ragged_layout()
+    fm = _fm(lay, "bf16")
+    g = to_device_grad(_decaying_step(lay, "bf16", 2)(0, 0), "bf16")
+    for i in range(6):
+        q = np.random.default_rng(300 + i).permutation(num)[:400]
+        qd = _ids(q)
+        out = torch.full((len(q), rb), 9, dtype=torch.uint8, device="cuda")
+        dep = torch.zeros(len(q), dtype=torch.int32, device="cuda")
+        side.wait_stream(main)                       # ids / outputs were made on the compute stream
+        ev = gc.get_async(qd, 3 + (i % 2), out, dep, side)
+        for _ in range(3):
+            fm.layer_norms(g)                        # compute overlapping the prefetch
+        main.wait_event(ev)
+        out_o = np.full((len(q), rb), 9, np.uint8)
+        dep_o = oc.get(q, 3 + (i % 2), out_o)
+        assert np.array_equal(dep.cpu().numpy(), dep_o), i
+        assert np.array_equal(out.cpu().numpy(), out_o), i
+    side.synchronize()
+    assert gc.stats()["n_valid"] == len(oc.store)
+    gc.close()
 
 
 def test_calibrate_read_seconds_and_should_cache():
