@@ -414,7 +414,8 @@ AF_API af_status af_cache_get_ex(af_cache *c, const int64_t *ids_dev, int32_t n,
  * re-cache balance).  Each call is planned by a one-CTA kernel (block scans in
  * call order, deterministic), then copied by the TMA kernel.  Without this call
  * the cache is direct-mapped with room for every owned id. */
-AF_API af_status af_cache_set_capacity(af_cache *c, int64_t hbm_rows, int64_t host_rows);
+AF_API af_status af_cache_set_capacity(af_cache *c, int64_t hbm_rows, int64_t host_rows);  /* >= 0 each; the
+                       store needs >= 1 slot in all (a disk tier may provide them): AF_EINVAL at bind */
 AF_API af_status af_cache_host_bytes(const af_cache *c, size_t *host_bytes);
 /* Synchronous: binds the caller-owned page-locked host tier (cudaHostAlloc /
  * torch pin_memory: device-mapped under UVA), 16-byte aligned. */

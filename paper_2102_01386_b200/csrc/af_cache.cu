@@ -137,7 +137,7 @@ __device__ __forceinline__ Desc item_addr(const CacheParams &p, int64_t j) {
   if (p.rowslot) {  // tiered: the plan kernel resolved the row's slot (and its meta / eviction)
     const int32_t slot = p.rowslot[i];
     if (slot < 0) return dsc;
-    if (p.disk_base > 0 && slot >= p.disk_base)  // disk tier: this pass's staging row i (host callbacks move it)
+    if (p.stage != nullptr && slot >= p.disk_base)  // disk tier: this pass's staging row i (host callbacks move it)
       rec = p.stage + static_cast<int64_t>(i) * p.row_bytes + off;
     else
       rec = (slot < p.hbm_rows ? p.payload + static_cast<int64_t>(slot) * p.row_bytes

@@ -84,7 +84,7 @@ af_status af_cache_set_capacity(af_cache *c, int64_t hbm_rows, int64_t host_rows
   AF_NVTX();
   if (!c) return fail(AF_EINVAL, "NULL cache");
   if (c->bound) return fail(AF_ESTATE, "set the capacity before binding storage");
-  if (hbm_rows < 0 || host_rows < 0 || hbm_rows + host_rows < 1) return fail(AF_EINVAL, "bad capacity");
+  if (hbm_rows < 0 || host_rows < 0) return fail(AF_EINVAL, "bad capacity");  // >= 1 slot in all: at bind
   if (hbm_rows + host_rows > (int64_t(1) << 31) - 1) return fail(AF_ERANGE, "capacity too large");
   c->tiered = true;
   c->hbm_rows = hbm_rows;
@@ -176,6 +176,7 @@ af_status af_cache_bind(af_cache *c, void *payload_dev, void *meta_dev) {
   if (!c || !meta_dev || (rows > 0 && !payload_dev)) return fail(AF_EINVAL, "NULL argument");
   if ((payload_dev && !aligned(payload_dev, 16)) || !aligned(meta_dev, 256))
     return fail(AF_EINVAL, "payload must be 16-byte and meta 256-byte aligned");
+  if (c->tiered && c->slots() < 1) return fail(AF_EINVAL, "a tiered store needs at least one record slot");
   int sms = 0;
   cudaError_t e = static_cast<cudaError_t>(device_sm_count(&sms));
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");

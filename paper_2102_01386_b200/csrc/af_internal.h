@@ -215,7 +215,7 @@ struct CacheParams {
   char *host;               // device alias of the page-locked host tier
   int64_t hbm_rows;         // slots [0, hbm_rows) in `payload`, then `host`
   char *stage;              // disk tier: device alias of the staging rows (row i of the pass at i)
-  int64_t disk_base;        // slots >= disk_base live on disk (staged); 0: no disk tier
+  int64_t disk_base;        // with stage != nullptr: slots >= disk_base live on disk (staged)
   // global mode (NEXT 4): any id; the owner's (id % world) store is reached through
   // its mapped payload / meta (peer memory over NVLink)
   char *const *peer_payload;     // [world]
