@@ -65,10 +65,6 @@ def parse():
     ap.add_argument("--zero", action="store_true",
                     help="ZeRO form (NEXT 1): every rank holds its own full gradient; the step's accumulate and "
                          "interval end are af_reduce_scatter_step (the gradient sync fused in, peer pulls)")
-    ap.add_argument("--separate-cache", action="store_true",
-                    help="the step's cache get and put as their own launches after the interval end (default: "
-                         "fused into the accumulate's launch with af_layer_norms_io -- the next batch's get "
-                         "prefetched, this batch's put written behind)")
     ap.add_argument("--unfused", action="store_true",
                     help="interval end as af_layer_norms(END) + af_update_and_decide (two launches)")
     ap.add_argument("--no-shard-probe", action="store_true",
@@ -283,30 +279,10 @@ def run_ours(args, rank, world, local):
     stream = torch.cuda.current_stream()
     n_ev = 5
 
-    fused_io = not (args.separate_cache or args.zero)
-
     def step(i, evs=None, skip=()):
         g = grads[i & 1]
         ids = id_batches[i % len(id_batches)]
         if evs: evs[0].record(stream)
-        if fused_io:
-            # a2 + a11 + a10 in one launch: this step's accumulate with the NEXT batch's
-            # get (prefetch) and THIS batch's put (write-behind) on the same grid
-            if "accumulate" not in skip:
-                if "cache" in skip:
-                    fm.layer_norms(g, dry_run=True)
-                else:
-                    fm.layer_norms_io(g, cache, get_ids=id_batches[(i + 1) % len(id_batches)], cur_boundary=4,
-                                      rows_out=out_rows, depth_out=depth_out, put_ids=ids, put_rows=rows,
-                                      put_depth=4, dry_run=True)
-            if evs: evs[1].record(stream)
-            if "grad_norm_decide" not in skip:
-                fm.interval_end(grads[(i + 1) & 1], dry_run=True)     # a3-a9
-            if evs:
-                evs[2].record(stream)
-                evs[3].record(stream)
-                evs[4].record(stream)
-            return
         if "accumulate" in skip:
             pass
         elif args.zero:
@@ -391,26 +367,17 @@ def run_ours(args, rank, world, local):
     step_bytes_all = sum(bytes_rank.values()) * world   # every rank moves ~the same bytes
     value = step_bytes_all / (ms_per_step * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
-    # bytes per eager phase: with the fused cache I/O the accumulate launch carries the
-    # get and put rows too, and there are no separate cache launches
-    ph_bytes = dict(bytes_rank)
-    if fused_io:
-        ph_bytes["accumulate"] += bytes_rank["cache_get"] + bytes_rank["cache_put"]
-        ph_bytes["cache_get"] = ph_bytes["cache_put"] = 0
     # dominant kernel roofline (per-launch CUDA-event durations on the launch stream)
     dom = max(("accumulate", "grad_norm_decide", "cache_get", "cache_put"), key=lambda p: ph_ms[p])
-    ach = ph_bytes[dom] / (ph_ms[dom] * 1e-3) / 1e9
+    ach = bytes_rank[dom] / (ph_ms[dom] * 1e-3) / 1e9
     phase_report = {p: {"ms": round(ph_ms[p], 5),
-                        "gbs": (round(ph_bytes[p] / (ph_ms[p] * 1e-3) / 1e9, 1) if ph_bytes[p] else None),
-                        "frac_of_peak": (round(ph_bytes[p] / (ph_ms[p] * 1e-3) / 1e9 / peak, 4)
-                                         if ph_bytes[p] else None)} for p in phases}
-    if fused_io:
-        phase_report["note"] = ("cache I/O fused into the accumulate launch (af_layer_norms_io): the accumulate "
-                                "phase carries the get + put bytes; cache_get / cache_put have no launches")
+                        "gbs": (round(bytes_rank[p] / (ph_ms[p] * 1e-3) / 1e9, 1) if bytes_rank[p] else None),
+                        "frac_of_peak": (round(bytes_rank[p] / (ph_ms[p] * 1e-3) / 1e9 / peak, 4)
+                                         if bytes_rank[p] else None)} for p in phases}
     gn_dec_ms = ph_ms["grad_norm_decide"]
     gn_dec = bytes_rank["grad_norm_decide"] / (gn_dec_ms * 1e-3) / 1e9
-    cache_gbs = ((bytes_rank["cache_get"] + bytes_rank["cache_put"]) / (
-        (ph_ms["cache_get"] + ph_ms["cache_put"]) * 1e-3) / 1e9 if not fused_io else None)
+    cache_gbs = (bytes_rank["cache_get"] + bytes_rank["cache_put"]) / (
+        (ph_ms["cache_get"] + ph_ms["cache_put"]) * 1e-3) / 1e9
     if cache_marg is not None:   # in-step device time of get + put (step_marginals)
         cache_marg_gbs = (bytes_rank["cache_get"] + bytes_rank["cache_put"]) / (cache_marg * 1e-3) / 1e9
         cache_in_step = {"us": round(cache_marg * 1e3, 2), "gbs": round(cache_marg_gbs, 1),
@@ -432,8 +399,6 @@ def run_ours(args, rank, world, local):
                    "shards": ("active-suffix (re-split per boundary f)" if (world > 1 and not args.zero)
                               else "static"),
                    "launch": "eager" if args.no_graph else "CUDA graph per step (8 graphs rotating id batches)",
-                   "cache_io": ("fused into the accumulate launch (af_layer_norms_io): get of the next batch, put "
-                                "of this batch" if fused_io else "separate get / put launches after the interval end"),
                    "l2": "inputs larger than L2: each step streams >= 4 GB/rank through the 126 MB L2"},
         "value_composition": "whole step: accumulate + interval end (grad-norm + decide) + cache get + put "
                              "(all SURVEY.md 8(a) rows); the metric's grad-norm+decide quantity alone is "
@@ -447,16 +412,15 @@ def run_ours(args, rank, world, local):
            if marg else {}),
         "grad_norm_decide_gbs": round(gn_dec, 1),
         "grad_norm_decide_frac_of_hbm_peak": round(gn_dec / peak, 4),
-        "cache_gbs": round(cache_gbs, 1) if cache_gbs is not None else None,
+        "cache_gbs": round(cache_gbs, 1),
         **({"cache_in_step": cache_in_step} if cache_marg is not None else {}),
         **({"phases_in_step": {
             "method": "marginal device time: the step's CUDA graphs replayed with and without the phase, K steps "
                       "each, alternating, difference of medians (max over ranks); includes what the phase adds "
                       "through overlap (PDL) and L2 state",
             **{k: {"ms": round(v, 5),
-                   **({"gbs": round(phase_bytes(bytes_rank, k, fused_io) / (v * 1e-3) / 1e9, 1),
-                       "frac_of_peak": round(phase_bytes(bytes_rank, k, fused_io) / (v * 1e-3) / 1e9 / peak, 4)}
-                      if v > 0 else {})}
+                   **({"gbs": round(phase_bytes(bytes_rank, k) / (v * 1e-3) / 1e9, 1),
+                       "frac_of_peak": round(phase_bytes(bytes_rank, k) / (v * 1e-3) / 1e9 / peak, 4)} if v > 0 else {})}
                for k, v in marg.items() if k != "full"}}} if marg else {}),
         "step_ms_dist": dist_ms,
         "frozen_half": frozen,
@@ -466,7 +430,7 @@ def run_ours(args, rank, world, local):
                      "algorithmic_bytes_per_launch": bytes_rank[dom],
                      **ncu_traffic(args.workload if world == 1 else None, dom)},
         # accumulate + interval end (+ wide finalize) (+ decide kernel, NCCL all-gather) + cache get + put
-        "gpu_launches": ((2 if fused_io else 4) + (1 if info["n_fin_ctas"] else 0)
+        "gpu_launches": (4 + (1 if info["n_fin_ctas"] else 0)
                          + (1 if (args.unfused or (world > 1 and exchange != "p2p")) else 0)
                          + (1 if (world > 1 and exchange != "p2p") else 0)) * args.steps,
         "clocks": clk.summary(),
@@ -476,8 +440,6 @@ def run_ours(args, rank, world, local):
         result["cache_host_tier"] = host_tier_probe(rows, dev)
         if world == 1:
             result["cache_epoch_c4"] = cache_epoch_c4(dev)
-        if not args.zero:
-            result["cache_fused_by_batch"] = cache_fused_sweep(fm, cache, my_ids, rows, grads, dev)
     if not args.no_extras:
         result["next1_fused_adamw"] = adamw_probe(fm, lay, dt, s_g, n_loc, grads, dev)
         if world == 1:
@@ -571,15 +533,8 @@ def frozen_point(args, fm, lay, info, s_g, B, run, stream, world, dist, dev, g):
             "note": "algorithmic bytes count active (unfrozen) elements only; GB/s on those bytes"}
 
 
-def phase_bytes(bytes_rank, phase, fused_io=False):
-    """Algorithmic bytes of an in-step phase.  With the fused cache I/O, dropping the
-    accumulate also drops the cache items it carries."""
-    cache = bytes_rank["cache_get"] + bytes_rank["cache_put"]
-    if phase == "cache":
-        return cache
-    if phase == "accumulate" and fused_io:
-        return bytes_rank["accumulate"] + cache
-    return bytes_rank[phase]
+def phase_bytes(bytes_rank, phase):
+    return bytes_rank["cache_get"] + bytes_rank["cache_put"] if phase == "cache" else bytes_rank[phase]
 
 
 def step_marginals(args, graphs, step, stream, world, dist, rounds=3):
@@ -761,56 +716,6 @@ def cache_epoch_c4(dev, world_emul=8, B=256, seed=3):
     del cache
     torch.cuda.empty_cache()
     return res
-
-
-def cache_fused_sweep(fm, cache, my_ids, rows, grads, dev, batches=(6, 32, 256, 1024), reps=10, rounds=3):
-    """Cache get + put fused into the accumulate (af_layer_norms_io), per batch
-    size: the marginal device time of carrying B get rows + B put rows (disjoint
-    ids) on the accumulate's launch -- CUDA graphs of reps x [accumulate with the
-    I/O] minus reps x [accumulate alone], alternating, median.  The accumulate
-    streams GBs per launch, so every record read is cold in L2.  GB/s = 2 x 2 x B
-    x row_bytes / marginal time."""
-    import torch
-    peak, _ = measured_peaks()
-    B0 = rows.shape[0]
-    big = rows.repeat((max(batches) + B0 - 1) // B0, 1)[: max(batches)].contiguous()
-    out = {"method": cache_fused_sweep.__doc__.split("\n\n")[0].replace("\n", " ").strip()}
-    for B in batches:
-        if 2 * B > my_ids.numel():
-            continue
-        sets = [my_ids[torch.randperm(my_ids.numel(), device=dev)[:2 * B]].contiguous() for _ in range(reps)]
-        dst = torch.empty((B, ROW_BYTES), dtype=torch.uint8, device=dev)
-        dep = torch.empty(B, dtype=torch.int32, device=dev)
-        src = big[:B]
-        gs = {}
-        for w in (True, False):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                for r in range(reps):
-                    if w:
-                        fm.layer_norms_io(grads[r & 1], cache, get_ids=sets[r][:B], cur_boundary=4, rows_out=dst,
-                                          depth_out=dep, put_ids=sets[r][B:], put_rows=src, put_depth=4,
-                                          dry_run=True)
-                    else:
-                        fm.layer_norms(grads[r & 1], dry_run=True)
-            gs[w] = g
-        t = {True: [], False: []}
-        for _ in range(rounds):
-            for w in (True, False):
-                gs[w].replay()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                torch.cuda.synchronize()
-                a.record()
-                gs[w].replay()
-                b.record()
-                torch.cuda.synchronize()
-                t[w].append(a.elapsed_time(b))
-        us = (statistics.median(t[True]) - statistics.median(t[False])) / reps * 1e3
-        gbs = 4 * B * ROW_BYTES / (us * 1e-6) / 1e9 if us > 0 else None
-        out[str(B)] = {"us_get_plus_put": round(us, 2), "gbs": round(gbs, 1) if gbs else None,
-                       "frac_of_peak": round(gbs / peak, 4) if gbs else None}
-        del gs
-    return out
 
 
 def host_tier_probe(rows, dev, reps=10):

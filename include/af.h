@@ -403,32 +403,6 @@ AF_API af_status af_cache_get(af_cache *c, const int64_t *ids_dev, int32_t n, in
 AF_API af_status af_cache_get_ex(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
                                  void *rows_out_dev, int32_t *depth_out_dev, uint32_t flags, void *stream);
 
-/* A step's Storage Manager I/O fused into its gradient accumulate (the paper's
- * reader / writer: the next batch's records prefetched and this batch's
- * outputs written behind while the step streams its gradient).  Exactly
- *   af_cache_get(cache, get_ids, get_n, cur_boundary, get_rows_out, get_depth_out)
- *   af_cache_put(cache, put_ids, put_n, put_rows, put_depth)
- *   af_layer_norms(ctx, grad_dev, flags)            (flags: AF_DRY_RUN only)
- * in ONE launch: the cache rows, cut into 32 KiB items, are claimed from the
- * accumulate's persistent tile scheduler ahead of the gradient tiles, so the
- * calls pay no launch, ramp or drain of their own.  Requirements: a bound
- * direct-mapped cache (no tiers, no peers: AF_ESTATE), acc_mode AF_ACC_DELTA, and
- * get_ids disjoint from put_ids (the items run concurrently; overlapping ids are
- * undefined).  Either side may be empty (n = 0).  Buffers as in af_cache_get /
- * af_cache_put; the cache's work completes with the kernel. */
-typedef struct {
-  af_cache *cache;
-  const int64_t *get_ids;  /* device */
-  int32_t get_n, cur_boundary;
-  void *get_rows_out;      /* device, get_n x row_bytes */
-  int32_t *get_depth_out;  /* device, get_n (-1 = miss) */
-  const int64_t *put_ids;  /* device */
-  int32_t put_n, put_depth;
-  const void *put_rows;    /* device, put_n x row_bytes */
-} af_cache_io;
-AF_API af_status af_layer_norms_io(af_ctx *ctx, const void *grad_dev, uint32_t flags, const af_cache_io *io,
-                                   void *stream);
-
 /* Storage-manager tiers and admission (§3.2).
  * Host only, before af_cache_storage_bytes / af_cache_bind: room for I =
  * hbm_rows + host_rows records (I may be < D = the rank's owned ids): hbm_rows in

@@ -59,12 +59,6 @@ class AfAdamW(ctypes.Structure):
                 ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float), ("step", c_int32)]
 
 
-class AfCacheIO(ctypes.Structure):
-    _fields_ = [("cache", c_void_p), ("get_ids", c_void_p), ("get_n", c_int32), ("cur_boundary", c_int32),
-                ("get_rows_out", c_void_p), ("get_depth_out", c_void_p), ("put_ids", c_void_p),
-                ("put_n", c_int32), ("put_depth", c_int32), ("put_rows", c_void_p)]
-
-
 class AfCacheInfo(ctypes.Structure):
     _fields_ = [("error_flags", c_uint32), ("pad", c_uint32), ("partition", c_int64), ("capacity", c_int64),
                 ("n_valid", c_int64), ("n_hbm", c_int64), ("n_host", c_int64), ("n_dropped", c_int64),
@@ -86,7 +80,6 @@ SIGNATURES = {
     "af_ctx_set_peers_local": (c_int, [c_void_p, c_void_p]),
     "af_ctx_clear_peers": (c_int, [c_void_p]),
     "af_layer_norms": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p]),
-    "af_layer_norms_io": (c_int, [c_void_p, c_void_p, c_uint32, POINTER(AfCacheIO), c_void_p]),
     "af_update_and_decide": (c_int, [c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_interval_end": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p, c_void_p]),
     "af_adamw_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(AfAdamW), c_uint32,

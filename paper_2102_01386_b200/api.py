@@ -253,27 +253,6 @@ class FreezingModule:
         check(lib.af_layer_norms(self._h, c_void_p(grad.data_ptr()), flags, _stream_handle(stream)),
               "af_layer_norms")
 
-    def layer_norms_io(self, grad, cache, get_ids=None, cur_boundary=0, rows_out=None, depth_out=None,
-                       put_ids=None, put_rows=None, put_depth=1, dry_run=False, stream=None):
-        """af_layer_norms_io: an accumulate step with the step's cache get (the next
-        batch's records, prefetched) and put (this batch's outputs, written behind)
-        riding on the same launch.  get_ids and put_ids must be disjoint."""
-        self._grad(grad)
-        gn = 0 if get_ids is None else int(cache._ids(get_ids).numel())
-        pn = 0 if put_ids is None else int(cache._ids(put_ids).numel())
-        if gn:
-            cache._rows(rows_out, gn, "rows_out")
-            cache._depth_out(depth_out, gn)
-        if pn:
-            cache._rows(put_rows, pn, "put_rows")
-        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        io = L.AfCacheIO(cache._h.value, ptr(get_ids) if gn else None, gn, int(cur_boundary),
-                         ptr(rows_out) if gn else None, ptr(depth_out) if gn else None,
-                         ptr(put_ids) if pn else None, pn, int(put_depth), ptr(put_rows) if pn else None)
-        flags = L.AF_DRY_RUN if dry_run else 0
-        check(lib.af_layer_norms_io(self._h, c_void_p(grad.data_ptr()), flags, byref(io), _stream_handle(stream)),
-              "af_layer_norms_io")
-
     def update_and_decide(self, dry_run=False, stream=None, copy_record=True):
         flags = L.AF_DRY_RUN if dry_run else 0
         out = c_void_p(self._rec_host.data_ptr()) if copy_record else c_void_p(0)

@@ -347,49 +347,6 @@ af_status af_cache_get_ex(af_cache *c, const int64_t *ids_dev, int32_t n, int32_
   return AF_OK;
 }
 
-}  // extern "C"
-
-af_status af::cache_io_params(const af_cache_io *io, CacheIO *out) {
-  af_cache *c = io->cache;
-  if (!c) return fail(AF_EINVAL, "NULL cache");
-  if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
-  if (c->tiered || c->peers) return fail(AF_ESTATE, "fused cache I/O needs a direct-mapped store without peers");
-  if (io->get_n < 0 || io->put_n < 0) return fail(AF_EINVAL, "n < 0");
-  if (io->get_n > 0 && (!io->get_ids || !io->get_rows_out || !io->get_depth_out))
-    return fail(AF_EINVAL, "NULL get buffers");
-  if (io->put_n > 0 && (!io->put_ids || !io->put_rows)) return fail(AF_EINVAL, "NULL put buffers");
-  if ((io->get_n > 0 && (!aligned(io->get_rows_out, 16) || !aligned(io->get_ids, 8))) ||
-      (io->put_n > 0 && (!aligned(io->put_rows, 16) || !aligned(io->put_ids, 8))))
-    return fail(AF_EINVAL, "rows must be 16-byte aligned");
-  if (io->get_n > 0 && io->cur_boundary < 0) return fail(AF_EINVAL, "cur_boundary < 0");
-  if (io->put_n > 0 && io->put_depth < 1) return fail(AF_EINVAL, "depth must be >= 1 (frozen POOL count)");
-  const int64_t nch = (c->row_bytes + kIoChunk - 1) / kIoChunk;
-  const int64_t items = (static_cast<int64_t>(io->get_n) + io->put_n) * nch;
-  if (items > (int64_t(1) << 30)) return fail(AF_ERANGE, "too many cache rows in one step");
-  CacheIO q{};
-  q.payload = c->payload;
-  q.meta = reinterpret_cast<CacheMeta *>(c->meta + kMetaHeader);
-  q.err = reinterpret_cast<unsigned int *>(c->meta);
-  q.row_bytes = c->row_bytes;
-  q.num_examples = c->num_examples;
-  q.rank = c->rank;
-  q.world = c->world;
-  q.n_chunks = static_cast<int32_t>(nch);
-  q.get_items = static_cast<int32_t>(io->get_n * nch);
-  q.items = static_cast<int32_t>(items);
-  q.get_ids = io->get_ids;
-  q.get_out = static_cast<char *>(io->get_rows_out);
-  q.depth_out = io->get_depth_out;
-  q.cur_boundary = io->cur_boundary;
-  q.depth = io->put_depth;
-  q.put_ids = io->put_ids;
-  q.put_rows = static_cast<const char *>(io->put_rows);
-  *out = q;
-  return AF_OK;
-}
-
-extern "C" {
-
 af_status af_cache_stats(af_cache *c, af_cache_info *out) {
   AF_NVTX();
   if (!c || !out) return fail(AF_EINVAL, "NULL argument");

@@ -490,27 +490,6 @@ af_status af_layer_norms(af_ctx *c, const void *grad_dev, uint32_t flags, void *
   return AF_OK;
 }
 
-af_status af_layer_norms_io(af_ctx *c, const void *grad_dev, uint32_t flags, const af_cache_io *io, void *stream) {
-  AF_NVTX();
-  af_status st = check_norm_args(c, grad_dev);
-  if (st != AF_OK) return st;
-  if (!io) return fail(AF_EINVAL, "NULL io");
-  if (flags & ~AF_DRY_RUN) return fail(AF_EINVAL, "af_layer_norms_io: accumulate steps only (flags: AF_DRY_RUN)");
-  if (c->cfg.acc_mode != AF_ACC_DELTA) return fail(AF_ESTATE, "af_layer_norms_io needs acc_mode AF_ACC_DELTA");
-  CacheIO q{};
-  st = cache_io_params(io, &q);
-  if (st != AF_OK) return st;
-  if (q.items == 0) return af_layer_norms(c, grad_dev, flags, stream);
-  const bool dry = flags & AF_DRY_RUN;
-  NormParams p = norm_params(c, grad_dev, false, dry);
-  p.io = q;
-  const int grid = grid_for(c, kAccum, p.n_tiles + q.items);
-  const int e = launch_norms(p, kAccum, c->dtype, grid, stream);
-  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "accumulate + cache I/O kernel launch");
-  if (!dry) c->armed = true;
-  return AF_OK;
-}
-
 }  // extern "C"
 
 namespace {

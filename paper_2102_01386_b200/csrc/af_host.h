@@ -53,8 +53,4 @@ af_status ipc_export(const void *ptr, IpcRef *out);
 af_status ipc_import(const IpcRef &r, std::vector<void *> &opened, char **out);
 void ipc_release(const std::vector<void *> &opened);  // drop the references ipc_import took
 
-// The storage-manager half of af_layer_norms_io: validates `io` and fills the
-// kernel's CacheIO (af_cache_api.cpp owns the cache's layout).
-af_status cache_io_params(const af_cache_io *io, CacheIO *out);
-
 }  // namespace af

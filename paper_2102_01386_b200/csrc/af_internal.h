@@ -114,27 +114,6 @@ struct DecideParams {
   int32_t commit;           // 0 under AF_DRY_RUN
 };
 
-// Storage-manager I/O riding on the accumulate's persistent grid
-// (af_layer_norms_io): the step's cache get and put on a direct-mapped store, cut
-// into items of kIoChunk bytes of one row, claimed from the same scheduler as the
-// gradient tiles (before them).  The semantics of af_cache_get + af_cache_put.
-constexpr int kIoChunk = 32 * 1024;
-struct CacheMeta;
-struct CacheIO {
-  char *payload;                 // direct-mapped records, slot = id / world
-  CacheMeta *meta;
-  unsigned int *err;             // sticky AF_CACHE_ERR_* of the store
-  int64_t row_bytes, num_examples;
-  int32_t rank, world, n_chunks;  // n_chunks = ceil(row_bytes / kIoChunk)
-  int32_t get_items, items;      // get items first: [0, get_items) get, [get_items, items) put
-  const int64_t *get_ids;
-  char *get_out;
-  int32_t *depth_out;
-  int32_t cur_boundary, depth;
-  const int64_t *put_ids;
-  const char *put_rows;
-};
-
 // Arguments of the streaming kernels (accumulate / interval-end sum of squares).
 struct NormParams {
   const void *grad;          // full flat buffer base
@@ -183,7 +162,6 @@ struct NormParams {
   unsigned long long *rs_flags;    // local [2][world]: ready / done epoch reached by each rank
   unsigned long long *const *peer_rs_flags;  // [world] each rank's rs_flags
   DecideParams dec;
-  CacheIO io;                      // af_layer_norms_io (kAccum only); io.items == 0: none
   uint32_t dbg_tail_delay_ns;      // AF_DEBUG_TAIL_DELAY_NS: the last CTA waits this long before its tail
   int32_t dbg_peers_arrived;       // AF_DEBUG_PEERS_ARRIVED: the exchange pushes but does not wait
 };

@@ -496,82 +496,6 @@ __device__ __forceinline__ double process_tile_rs(const NormParams &p, const Til
   return (a0 + a1) + (a2 + a3);
 }
 
-// One item of the storage-manager I/O fused into the accumulate (af_layer_norms_io):
-// chunk c (kIoChunk bytes) of row i of the step's cache get (j < get_items) or put,
-// copied by the whole CTA -- each thread moves up to 8 x 16 B with all loads in
-// flight before the stores.  A get loads the record speculatively while thread 0
-// reads its meta word (the cache kernel's scheme), stores it only on a hit, and
-// the last chunk of a row to read the meta applies the evict-on-read;
-// a put writes {depth, valid} with its first chunk.  Semantics of af_cache_get /
-// af_cache_put on a direct-mapped store (slot = id / world).
-__device__ __noinline__ void process_io_item(const CacheIO &io, int j) {
-  __shared__ int64_t s_id;
-  __shared__ int s_ok, s_hit, s_depth;
-  const int tid = threadIdx.x;
-  const bool get = j < io.get_items;
-  const int jj = get ? j : j - io.get_items;
-  const int i = jj / io.n_chunks, c = jj % io.n_chunks;
-  const int64_t off = static_cast<int64_t>(c) * kIoChunk;
-  const int64_t rem = io.row_bytes - off;
-  const int nv = static_cast<int>((rem < kIoChunk ? rem : kIoChunk) / 16);
-  if (tid == 0) {
-    const int64_t id = get ? io.get_ids[i] : io.put_ids[i];
-    int ok = 1;
-    if (id < 0 || id >= io.num_examples) {
-      ok = 0;
-      if (c == 0) atomicOr(io.err, AF_CACHE_ERR_RANGE);
-    } else if (id % io.world != io.rank) {
-      ok = 0;
-      if (c == 0) atomicOr(io.err, AF_CACHE_ERR_OWNER);
-    }
-    if (!ok && get && c == 0) io.depth_out[i] = -1;
-    s_id = id;
-    s_ok = ok;
-  }
-  __syncthreads();
-  if (s_ok) {
-    const int64_t slot = s_id / io.world;
-    char *rec = io.payload + slot * io.row_bytes + off;
-    const uint4 *src = get ? reinterpret_cast<const uint4 *>(rec)
-                           : reinterpret_cast<const uint4 *>(io.put_rows + static_cast<int64_t>(i) * io.row_bytes + off);
-    uint4 *dst = get ? reinterpret_cast<uint4 *>(io.get_out + static_cast<int64_t>(i) * io.row_bytes + off)
-                     : reinterpret_cast<uint4 *>(rec);
-    int4 mv = make_int4(0, 0, 0, 0);
-    if (get && tid == 0) mv = __ldcg(reinterpret_cast<const int4 *>(io.meta) + slot);  // {depth, valid, readers, -}
-    uint4 v[kIoChunk / 16 / kNormBlock];
-#pragma unroll
-    for (int u = 0; u < kIoChunk / 16 / kNormBlock; ++u) {
-      const int k = u * kNormBlock + tid;
-      if (k < nv) v[u] = ld_stream<1>(src + k);
-    }
-    if (tid == 0) {
-      s_hit = get ? (mv.y != 0) : 1;
-      s_depth = mv.x;
-      if (!get && c == 0) *reinterpret_cast<int2 *>(io.meta + slot) = make_int2(io.depth, 1);  // {depth, valid}
-    }
-    __syncthreads();
-    if (s_hit) {
-#pragma unroll
-      for (int u = 0; u < kIoChunk / 16 / kNormBlock; ++u) {
-        const int k = u * kNormBlock + tid;
-        if (k < nv) dst[k] = v[u];
-      }
-    }
-    if (get && tid == 0) {
-      if (c == 0) io.depth_out[i] = s_hit ? s_depth : -1;
-      if (s_hit) {  // evict on read once every chunk of the row has read the record
-        __threadfence();
-        const unsigned int seen = atomicAdd(&io.meta[slot].readers, 1u);
-        if (seen == static_cast<unsigned int>(io.n_chunks) - 1u) {
-          if (s_depth < io.cur_boundary) io.meta[slot].valid = 0;
-          io.meta[slot].readers = 0u;
-        }
-      }
-    }
-  }
-  __syncthreads();  // the s_* words are reused by the next item
-}
-
 // Cross-GPU epoch barrier of the fused reduce-scatter: threads r < P store the
 // epoch into rank r's flag word for this rank (st.release.sys over peer memory),
 // then wait until every rank's word in the local array reached it (ld.acquire.sys,
@@ -824,7 +748,7 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
 template <bool ACT>
 __device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int n_end, int f, double *s_p);
 
-template <int MODE, typename GT, bool RD, int PM = 1, bool ACT = false, bool IO = false>
+template <int MODE, typename GT, bool RD, int PM = 1, bool ACT = false>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccum)
                                   ? 2
                                   : ((MODE >= kAdamAccum) ? 1 : (sizeof(GT) == 2 ? AF_MINB_END_BF16 : AF_MINB_END)))
@@ -871,22 +795,16 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
   // previous kernel's last ~100 MB (Delta written back, g just read) in the
   // 126 MB L2.  The order never changes a result: every tile's partial has a fixed
   // reduction tree and the segments are summed in tile-index order.
-  // With fused storage-manager I/O (IO), claims [0, io.items) are cache items
-  // (returned as -1 - item) and the gradient tiles follow.
   const int n_act_tiles = n_end - first_tile;
   auto tile_of = [&](unsigned int k) -> int {
-    int kk = static_cast<int>(k);
-    if constexpr (IO) {
-      if (kk < p.io.items) return -1 - kk;
-      kk -= p.io.items;
-    }
+    const int kk = static_cast<int>(k);
     if (kk >= n_act_tiles) return n_end;  // past the end: the loop's stop value
     return p.reverse ? n_end - 1 - kk : first_tile + kk;
   };
   if (tid == 0) {
     const int t0 = tile_of(atomicAdd(&p.sched->next, 1u));
     s_tile[0] = t0;
-    if (t0 >= 0 && t0 < n_end) s_desc[0] = p.tiles[t0];
+    if (t0 < n_end) s_desc[0] = p.tiles[t0];
     s_tile[1] = tile_of(atomicAdd(&p.sched->next, 1u));
   }
   __syncthreads();
@@ -899,7 +817,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
     if (tid == 0) {
       next2 = tile_of(atomicAdd(&p.sched->next, 1u));
       const int n1 = s_tile[slot1];
-      if (n1 >= 0 && n1 < n_end) {
+      if (n1 < n_end) {
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_desc[slot1]));
         const Tile *src = p.tiles + n1;
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -908,17 +826,6 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
                      : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    if constexpr (IO) {
-      if (tile < 0) {  // a storage-manager item: no gradient, no partial
-        process_io_item(p.io, -1 - tile);
-        if (tid == 0) {
-          s_tile[slot2] = next2;
-          asm volatile("cp.async.wait_all;" ::: "memory");
-        }
-        __syncthreads();
-        continue;
-      }
     }
     double v;
     if constexpr (MODE == kAdamAccum || MODE == kAdamEnd)
@@ -1111,22 +1018,8 @@ NormKernel kernel_for(int mode, bool rd, int world, bool act = false) {
 }
 
 template <typename GT>
-NormKernel io_kernel(bool rd, bool act) {
-#ifdef AF_NO_ACT
-  act = false;
-#endif
-  return act ? (rd ? norms_kernel<kAccum, GT, true, 1, true, true> : norms_kernel<kAccum, GT, false, 1, true, true>)
-             : (rd ? norms_kernel<kAccum, GT, true, 1, false, true> : norms_kernel<kAccum, GT, false, 1, false, true>);
-}
-
-template <typename GT>
 int launch_dt(const NormParams &p, int mode, int grid, void *stream) {
   const bool rd = !p.first;
-  if (p.io.items > 0) {  // af_layer_norms_io: the accumulate with the storage-manager items
-    if (mode != kAccum) return static_cast<int>(cudaErrorInvalidValue);
-    return static_cast<int>(launch_pdl(io_kernel<GT>(rd, p.stb_stride != 0), dim3(grid), dim3(kNormBlock), 0,
-                                       static_cast<cudaStream_t>(stream), p));
-  }
   if (mode < 0 || mode >= kNumModes) return static_cast<int>(cudaErrorInvalidValue);
   return static_cast<int>(launch_pdl(kernel_for<GT>(mode, rd, p.rs_world, p.stb_stride != 0), dim3(grid),
                                      dim3(kNormBlock), 0,
@@ -1152,10 +1045,6 @@ static cudaError_t preload_dt(int world) {
       for (int act = 0; act < 2; ++act) {
         const cudaError_t e = cudaFuncGetAttributes(&a, kernel_for<GT>(m, rd != 0, world, act != 0));
         if (e != cudaSuccess) return e;
-        if (m == kAccum) {
-          const cudaError_t e2 = cudaFuncGetAttributes(&a, io_kernel<GT>(rd != 0, act != 0));
-          if (e2 != cudaSuccess) return e2;
-        }
       }
     }
   return cudaSuccess;

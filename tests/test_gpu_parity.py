@@ -804,56 +804,6 @@ def test_tiered_cache_epochs_match_oracle(rank, world, hbm, host, disk):
     gc.close()
 
 
-@pytest.mark.parametrize("dt,rb", [("bf16", 196_608), ("f32", 24_592), ("bf16", 100_016)])
-def test_layer_norms_io_equals_separate_calls(dt, rb):
-    """af_layer_norms_io (the step's cache get + put riding on the accumulate's
-    grid) == af_cache_get + af_cache_put + af_layer_norms: Delta bit-exact, and
-    bytes, depths, evictions and error flags equal the oracle's, over steps that
-    prefetch batch i+1 while writing batch i behind (disjoint ids), with a
-    boundary change (evict-on-read) and wrong-owner / out-of-range ids."""
-    import paper_2102_01386_b200 as af
-    from afinputs import cache_rows
-    lay = _ragged_layout()
-    step = _decaying_step(lay, dt, 33)
-    fm, oz = _fm(lay, dt), _oracle(lay, dt)
-    num, world, rank = 3000, 2, 1
-    gc = af.ActivationCache(num, rb, rank=rank, world=world)
-    oc = O.Cache(num, rb, rank, world)
-    mine = np.arange(rank, num, world)
-    seed_ids = np.random.default_rng(11).permutation(mine)[:300]
-    seed_rows = cache_rows(1, 1, len(seed_ids), rb)
-    gc.put(_ids(seed_ids), torch.from_numpy(seed_rows).cuda(), 3)
-    oc.put(seed_ids, seed_rows, 3)
-    batches = np.array_split(np.random.default_rng(12).permutation(mine), 12)
-    for i in range(6):
-        g = step(0, i)
-        get_ids = batches[i + 1].copy()
-        put_ids = batches[i].copy()
-        if i == 2:
-            get_ids = np.concatenate([get_ids, [0, num + 5]])      # wrong owner (0 % 2 != 1), out of range
-        bnd = 3 if i < 3 else 5                                    # boundary 5 > depth 3: evict on read
-        out = torch.full((len(get_ids), rb), 7, dtype=torch.uint8, device="cuda")
-        dep = torch.zeros(len(get_ids), dtype=torch.int32, device="cuda")
-        rows = cache_rows(2, i, len(put_ids), rb)
-        fm.layer_norms_io(to_device_grad(g, dt), gc, get_ids=_ids(get_ids), cur_boundary=bnd, rows_out=out,
-                          depth_out=dep, put_ids=_ids(put_ids), put_rows=torch.from_numpy(rows).cuda(),
-                          put_depth=3 + i)
-        oz.layer_norms(g, False)
-        out_o = np.full((len(get_ids), rb), 7, np.uint8)
-        dep_o = oc.get(get_ids, bnd, out_o)
-        oc.put(put_ids, rows, 3 + i)
-        torch.cuda.synchronize()
-        assert np.array_equal(dep.cpu().numpy(), dep_o), i
-        assert np.array_equal(out.cpu().numpy(), out_o), i
-        assert np.array_equal(delta_host(fm, lay.n), oz.delta), i
-    assert gc.status() == (oc.error_flags, len(oc.store)) and oc.error_flags == 3
-    # empty sides and a dry run: the accumulate alone (Delta still moves, as AF_DRY_RUN documents)
-    fm.layer_norms_io(to_device_grad(step(0, 7), dt), gc, dry_run=True)
-    oz.layer_norms(step(0, 7), False, dry_run=True)
-    torch.cuda.synchronize()
-    assert np.array_equal(delta_host(fm, lay.n), oz.delta)
-
-
 @pytest.mark.parametrize("tiered", [False, True])
 def test_get_async_prefetch_parity(tiered):
     """The paper's reader (Fig. 8): the next batch's get is issued on a side
