@@ -58,7 +58,7 @@ static __device__ __noinline__ void decide_block(const DecideParams &p, const do
   __shared__ double s_eta[AF_MAX_SEGMENTS];
   __shared__ double s_act[AF_MAX_SEGMENTS];
   __shared__ double s_sorted[AF_MAX_SEGMENTS];
-  __shared__ double s_thr, s_win;
+  __shared__ double s_thr;
   __shared__ int s_k, s_near, s_nonfinite;
   __shared__ unsigned int s_flags;
 
@@ -149,28 +149,30 @@ static __device__ __noinline__ void decide_block(const DecideParams &p, const do
           thr = (gm >= 0.5) ? __dsub_rn(b, __dmul_rn(dba, __dsub_rn(1.0, gm))) : __dadd_rn(a, __dmul_rn(dba, gm));
         }
       }
+      // Alg. 1 scan with break; near-tie window over the comparisons that decide k
+      // (positions 0..k).  Serial on one thread: over <= 256 values it is not what
+      // the decision waits on (a parallel ballot / atomicMin form measured slower,
+      // profiles/r01_v44_*).
+      AF_DMARK(4);
+      int k = 0, near = -1;
+      unsigned int fl2 = 0;
+      const double win = __dmul_rn(p.tie_rel_eps, thr);
+      for (int i = 0; i < n; ++i) {
+        const double e = s_act[i];
+        const double dd = fabs(__dsub_rn(e, thr));
+        if (dd > 0.0 && dd <= win) {
+          fl2 |= AF_DEC_NEAR_TIE;
+          if (near < 0) near = s_pool[f + i];
+        }
+        if (e < thr)
+          ++k;
+        else
+          break;
+      }
       s_thr = thr;
-      s_win = __dmul_rn(p.tie_rel_eps, thr);
-      s_k = n;      // no failure: every active layer freezes
-      s_near = n;   // no near-tie
-    }
-    __syncthreads();
-    // Alg. 1 scan with break, in parallel: k = the first position whose eta is not
-    // below the threshold (smem atomicMin -- order-free, so exact); the near-tie
-    // window covers the comparisons that decide k, positions 0..k.
-    AF_DMARK(4);
-    const double thr = s_thr;
-    if (t < n_act && !(s_act[t] < thr)) atomicMin(&s_k, t);
-    __syncthreads();
-    if (t < n_act && t <= s_k) {
-      const double dd = fabs(__dsub_rn(s_act[t], thr));
-      if (dd > 0.0 && dd <= s_win) atomicMin(&s_near, t);
-    }
-    __syncthreads();
-    if (t == 0) {
-      const int near = s_near;
-      s_flags = near < n_act ? AF_DEC_NEAR_TIE : 0u;
-      s_near = near < n_act ? s_pool[f + near] : -1;
+      s_k = k;
+      s_near = near;
+      s_flags = fl2;
     }
   } else if (t == 0) {
     s_thr = __longlong_as_double(0x7FF8000000000000LL);  // NaN: no threshold
