@@ -452,6 +452,23 @@ AF_API af_status af_cache_bind_disk_stage(af_cache *c, void *stage_pinned);
 AF_API af_status af_cache_exchange_ipc_handle(af_cache *c, void *handle_out);
 AF_API af_status af_cache_set_peers_ipc(af_cache *c, const void *handles);
 AF_API af_status af_cache_set_peers_local(af_cache *c, af_cache *const *peers);
+/* NEXT 4, second half: the cache get fused into the first active layer's GEMM
+ * operand load.  For each of the n examples: if its record is valid (a hit),
+ *   y[i * rows_per_record + r][j] = bf16_rne( sum_k rec_i[r][k] * w[j][k] )
+ * (fp32 accumulation on the tensor cores, tcgen05), i.e. y = x W^T with x the
+ * cached layer output (rows_per_record x K bf16 per record; row_bytes must be
+ * rows_per_record x K x 2) and W a bf16 [N][K] weight (a torch Linear weight,
+ * 16-byte aligned); depth_out[i] = the record's depth, and the record is evicted
+ * once read if depth < cur_boundary -- the semantics of af_cache_get, without
+ * the batch copy: the GEMM's TMA loads read the record straight out of the
+ * store.  A miss leaves y's rows untouched and sets depth_out[i] = -1 (the
+ * caller runs the frozen prefix for those examples).  y: bf16 [n x
+ * rows_per_record][N] row-major, 16-byte aligned.  Requirements: direct-mapped
+ * store without peers (AF_ESTATE), rows_per_record a multiple of 128, K of 64,
+ * N of 32 (AF_EINVAL).  Ids unique (as af_cache_get). */
+AF_API af_status af_cache_get_gemm(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
+                                   int32_t rows_per_record, int32_t K, const void *w_dev, int32_t N, void *y_dev,
+                                   int32_t *depth_out_dev, void *stream);
 AF_API af_status af_cache_put_global(af_cache *c, const int64_t *ids_dev, int32_t n, const void *rows_dev,
                                      int32_t depth, void *stream);
 AF_API af_status af_cache_get_global(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,

@@ -11,7 +11,7 @@ import sysconfig
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-SOURCES = ["af_host.cpp", "af_ctx.cpp", "af_cache_api.cpp", "af_norms.cu", "af_decide.cu", "af_cache.cu"]
+SOURCES = ["af_host.cpp", "af_ctx.cpp", "af_cache_api.cpp", "af_norms.cu", "af_decide.cu", "af_cache.cu", "af_gemm.cu"]
 HEADERS = ["af_internal.h", "af_host.h", "af_decide.cuh"]
 LIB = os.path.join(PKG, "libautofreeze.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -114,6 +114,8 @@ SIGNATURES = {
     "af_cache_set_peers_ipc": (c_int, [c_void_p, c_void_p]),
     "af_cache_set_peers_local": (c_int, [c_void_p, c_void_p]),
     "af_cache_put_global": (c_int, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_void_p]),
+    "af_cache_get_gemm": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32, c_void_p, c_int32, c_void_p,
+                                  c_void_p, c_void_p]),
     "af_cache_get_global": (c_int, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     "af_cache_destroy": (c_int, [c_void_p]),
     "af_should_cache": (c_int, [c_int32, c_double, c_double]),

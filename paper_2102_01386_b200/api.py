@@ -429,6 +429,22 @@ class ActivationCache:
         with torch.cuda.device(self.device):
             check(lib.af_cache_set_peers_ipc(self._h, buf), "af_cache_set_peers_ipc")
 
+    def get_gemm(self, ids, cur_boundary, weight, y, depth_out, rows_per_record, stream=None):
+        """af_cache_get_gemm (NEXT 4): y[i] = record_i @ weight.T for the hits, the
+        records read by the GEMM's TMA loads straight from the store (no batch
+        copy); weight is a bf16 [N, K] tensor (torch Linear layout), y bf16
+        [n * rows_per_record, N]; misses leave y untouched (depth_out = -1)."""
+        n = int(self._ids(ids).numel())
+        _dev_tensor(weight, "weight", self.device, dtypes=(torch.bfloat16,))
+        if weight.dim() != 2:
+            raise ValueError("weight must be [N, K]")
+        N, K = weight.shape
+        _dev_tensor(y, "y", self.device, dtypes=(torch.bfloat16,), min_numel=n * rows_per_record * N)
+        self._depth_out(depth_out, n)
+        check(lib.af_cache_get_gemm(self._h, c_void_p(ids.data_ptr()), n, int(cur_boundary), int(rows_per_record),
+                                    int(K), c_void_p(weight.data_ptr()), int(N), c_void_p(y.data_ptr()),
+                                    c_void_p(depth_out.data_ptr()), _stream_handle(stream)), "af_cache_get_gemm")
+
     def put_global(self, ids, rows, depth, stream=None):
         self._rows(rows, int(self._ids(ids).numel()), "rows")
         check(lib.af_cache_put_global(self._h, c_void_p(ids.data_ptr()), int(ids.numel()),

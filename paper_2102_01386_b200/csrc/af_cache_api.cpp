@@ -1,5 +1,6 @@
 // af_cache_api.cpp -- the storage manager's C-ABI entry points (af_cache_*):
 // direct-mapped and tiered stores, admission, statistics, peer (global) access.
+#include <cuda.h>
 #include <fcntl.h>
 #include <unistd.h>
 
@@ -182,6 +183,7 @@ af_status af_cache_bind(af_cache *c, void *payload_dev, void *meta_dev) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
   c->grid = std::max(1, sms);
   e = static_cast<cudaError_t>(preload_cache_kernels());
+  if (e == cudaSuccess) e = static_cast<cudaError_t>(preload_cache_gemm_kernel());
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes (kernel preload)");
   c->payload = static_cast<char *>(payload_dev);
   c->meta = static_cast<char *>(meta_dev);
@@ -344,6 +346,84 @@ af_status af_cache_get_ex(af_cache *c, const int64_t *ids_dev, int32_t n, int32_
   if (c->tiered) return cache_tiered(c, p, false, stream);
   const int e = launch_cache_get(p, c->grid, stream);
   if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache get launch");
+  return AF_OK;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static af_status encode_tiled(CUtensorMap *m, void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides,
+                              const cuuint32_t *box) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    AF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q), "cudaGetDriverEntryPoint");
+    if (!p || q != cudaDriverEntryPointSuccess) return fail(AF_ECUDA, "cuTensorMapEncodeTiled not found");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, static_cast<cuuint32_t>(rank), base, dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(AF_EINVAL, "cuTensorMapEncodeTiled rejected the operand layout");
+  return AF_OK;
+}
+
+af_status af_cache_get_gemm(af_cache *c, const int64_t *ids_dev, int32_t n, int32_t cur_boundary,
+                            int32_t rows_per_record, int32_t K, const void *w_dev, int32_t N, void *y_dev,
+                            int32_t *depth_out_dev, void *stream) {
+  AF_NVTX();
+  if (!c) return fail(AF_EINVAL, "NULL cache");
+  if (!c->bound) return fail(AF_EWORKSPACE, "cache storage not bound");
+  if (c->tiered || c->peers) return fail(AF_ESTATE, "af_cache_get_gemm needs a direct-mapped store without peers");
+  if (n < 0 || cur_boundary < 0) return fail(AF_EINVAL, "n < 0 or cur_boundary < 0");
+  if (n == 0) return AF_OK;
+  if (!ids_dev || !w_dev || !y_dev || !depth_out_dev) return fail(AF_EINVAL, "NULL argument");
+  if (rows_per_record <= 0 || rows_per_record % 128 != 0) return fail(AF_EINVAL, "rows_per_record: a multiple of 128");
+  if (K <= 0 || K % 64 != 0 || N <= 0 || N % 32 != 0) return fail(AF_EINVAL, "K: a multiple of 64, N: of 32");
+  if (static_cast<int64_t>(rows_per_record) * K * 2 != c->row_bytes)
+    return fail(AF_EINVAL, "row_bytes != rows_per_record x K x 2 (bf16 records)");
+  if (!aligned(w_dev, 16) || !aligned(y_dev, 16) || !aligned(ids_dev, 8)) return fail(AF_EINVAL, "misaligned buffer");
+  if (c->capacity < 1) return fail(AF_EINVAL, "empty partition");
+  alignas(64) CUtensorMap ta, tb;
+  {  // the store as [slot][row][k] bf16: example i's record is the box at (k, m, slot_i)
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows_per_record),
+                                static_cast<cuuint64_t>(c->capacity)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 2, static_cast<cuuint64_t>(c->row_bytes)};
+    const cuuint32_t box[3] = {64, 128, 1};
+    af_status st = encode_tiled(&ta, c->payload, 3, dims, strides, box);
+    if (st != AF_OK) return st;
+  }
+  {  // W as [N][K] bf16 (a torch Linear weight): box of 256 rows x 64 k
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
+    const cuuint32_t box[2] = {64, 256};
+    af_status st = encode_tiled(&tb, const_cast<void *>(w_dev), 2, dims, strides, box);
+    if (st != AF_OK) return st;
+  }
+  CacheGemmParams p{};
+  p.meta = reinterpret_cast<CacheMeta *>(c->meta + kMetaHeader);
+  p.err = reinterpret_cast<unsigned int *>(c->meta);
+  p.ids = ids_dev;
+  p.n = n;
+  p.cur_boundary = cur_boundary;
+  p.depth_out = depth_out_dev;
+  p.num_examples = c->num_examples;
+  p.rank = c->rank;
+  p.world = c->world;
+  p.rows = rows_per_record;
+  p.n_tiles_m = rows_per_record / 128;
+  p.n_tiles_n = (N + 255) / 256;
+  p.N = N;
+  p.K = K;
+  p.y = y_dev;
+  p.ldy = N;
+  if (static_cast<int64_t>(n) * p.n_tiles_m * p.n_tiles_n > (int64_t(1) << 31) - 1) return fail(AF_ERANGE, "grid too large");
+  const int e = launch_cache_gemm(p, &ta, &tb, stream);
+  if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache get + GEMM launch");
   return AF_OK;
 }
 

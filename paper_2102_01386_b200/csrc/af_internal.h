@@ -222,6 +222,23 @@ struct CacheParams {
   CacheMeta *const *peer_meta;   // [world]
 };
 
+// NEXT 4: the cache get fused into the consumer GEMM's operand load (af_gemm.cu).
+struct CacheGemmParams {
+  CacheMeta *meta;
+  unsigned int *err;
+  const int64_t *ids;
+  int32_t n;                // examples
+  int32_t cur_boundary;
+  int32_t *depth_out;
+  int64_t num_examples;
+  int32_t rank, world;
+  int32_t n_tiles_m, n_tiles_n;  // rows / 128, ceil(N / 256)
+  int32_t rows;             // rows per record (multiple of 128)
+  int32_t N, K;
+  void *y;                  // bf16 [n * rows][ldy]
+  int64_t ldy;
+};
+
 struct CachePlanParams {
   CacheMeta *meta;
   CacheHeader *hdr;
@@ -294,6 +311,9 @@ int launch_decide(const DecideParams &p, void *stream);
 int launch_cache_put(const CacheParams &p, int grid, void *stream);
 int launch_cache_get(const CacheParams &p, int grid, void *stream);
 int launch_cache_plan(const CachePlanParams &p, void *stream);
+// tmap_a / tmap_b: CUtensorMap (128 B each) of the store's records and of W
+int launch_cache_gemm(const CacheGemmParams &p, const void *tmap_a, const void *tmap_b, void *stream);
+int preload_cache_gemm_kernel();
 int norms_max_blocks_per_sm(int mode, int grad_dtype, int world, int *blocks, bool act = false);
 // force-load the kernels (lazy module loading must not happen while peers spin)
 int preload_norm_kernels(int grad_dtype, int world);

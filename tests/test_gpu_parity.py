@@ -804,6 +804,58 @@ def test_tiered_cache_epochs_match_oracle(rank, world, hbm, host, disk):
     gc.close()
 
 
+@pytest.mark.parametrize("rows,K,N,rank,world", [(128, 768, 2304, 0, 1), (256, 128, 320, 1, 2), (128, 64, 32, 0, 1)])
+def test_cache_get_gemm_parity(rows, K, N, rank, world):
+    """NEXT 4: the cache get fused into the consumer GEMM's operand load
+    (af_cache_get_gemm, tcgen05 + TMA).  Depths, evictions and error flags equal
+    the oracle cache's get; for every hit y = record @ W^T within the bf16-output
+    bound (half an ulp of bf16, <= 2^-8 relative, plus fp32 accumulation over K,
+    1e-4 x sum|a||w|) of an fp64 reference; rows of misses are untouched."""
+    import paper_2102_01386_b200 as af
+    num, rb = 700, rows * K * 2
+    gc = af.ActivationCache(num, rb, rank=rank, world=world)
+    oc = O.Cache(num, rb, rank, world)
+    rng = np.random.default_rng(rows + K + N)
+    mine = np.arange(rank, num, world)
+    put_ids = rng.permutation(mine)[:120]
+    recs = (rng.random((len(put_ids), rows, K), dtype=np.float32) * 2 - 1)
+    rec_bits = f32_to_bf16_bits(recs.reshape(-1)).reshape(len(put_ids), rows * K)
+    rec_bytes = rec_bits.view(np.uint8)
+    depths = np.where(np.arange(len(put_ids)) % 3 == 0, 2, 5)
+    for d in (2, 5):
+        sel = depths == d
+        gc.put(_ids(put_ids[sel]), torch.from_numpy(np.ascontiguousarray(rec_bytes[sel])).cuda(), d)
+        oc.put(put_ids[sel], rec_bytes[sel], d)
+    w32 = (rng.random((N, K), dtype=np.float32) * 2 - 1) * np.float32(0.5)
+    w_bits = f32_to_bf16_bits(w32.reshape(-1)).reshape(N, K)
+    w = torch.from_numpy(w_bits.view(np.int16)).view(torch.bfloat16).cuda()
+    w64 = torch.from_numpy(w_bits.astype(np.uint32) << 16).view(torch.float32).double()
+    for trial, bnd in enumerate((4, 4)):            # boundary 4 > depth 2: those records evict on the first read
+        q = np.concatenate([rng.permutation(put_ids)[:60], rng.permutation(np.setdiff1d(mine, put_ids))[:10]])
+        if trial == 1:
+            q = np.concatenate([q, [num + 3]])      # out of range: flagged, a miss
+        y = torch.full((len(q) * rows, N), 3.0, dtype=torch.bfloat16, device="cuda")
+        dep = torch.zeros(len(q), dtype=torch.int32, device="cuda")
+        gc.get_gemm(_ids(q), bnd, w, y, dep, rows)
+        out_o = np.zeros((len(q), rb), np.uint8)
+        dep_o = oc.get(q, bnd, out_o)
+        torch.cuda.synchronize()
+        assert np.array_equal(dep.cpu().numpy(), dep_o), trial
+        yh = y.float().cpu().double()
+        for i in range(len(q)):
+            yi = yh[i * rows:(i + 1) * rows]
+            if dep_o[i] < 0:
+                assert torch.all(yi == 3.0), (trial, i)
+                continue
+            a = torch.from_numpy(out_o[i].view(np.uint16).astype(np.uint32) << 16).view(torch.float32).double()
+            a = a.view(rows, K)
+            ref = a @ w64.T
+            bound = ref.abs() * 2.0 ** -8 + 1e-4 * (a.abs() @ w64.abs().T) + 1e-30
+            assert torch.all((yi - ref).abs() <= bound), (trial, i, float(((yi - ref).abs() / bound).max()))
+    assert gc.status() == (oc.error_flags, len(oc.store))
+    gc.close()
+
+
 @pytest.mark.parametrize("tiered", [False, True])
 def test_get_async_prefetch_parity(tiered):
     """The paper's reader (Fig. 8): the next batch's get is issued on a side
