@@ -12,14 +12,15 @@
 // tensor map over [slot][row][k] gathers example i's tile with the coordinate
 // z = slot(id_i) -- and the 5th-generation tensor cores multiply it:
 //
-//   per CTA = (example i, 256-column tile of N): thread 0 resolves id -> slot
-//   and the record's {depth, valid} (a miss skips the tile: depth_out = -1, y
-//   untouched); a 4-stage TMA ring (A 128x64 + B 256x64 bf16, 128-byte swizzle,
-//   48 KiB per stage) feeds one elected thread issuing tcgen05.mma (kind::f16,
-//   M = 128, N = 256, K = 16, fp32 accumulator in 256 TMEM columns); the four
-//   warps drain TMEM with tcgen05.ld (32 lanes x 32 columns per load), round to
-//   bf16 (RNE) and store y rows; the last of the row's N tiles to read the meta
-//   word applies the evict-on-read (depth < cur_boundary).
+//   tile = (example i, 128-row M tile of its record, 256-column N tile); the
+//   producer resolves id -> slot and the record's {depth, valid} (a miss skips
+//   the tile: depth_out = -1, y untouched); a 4-stage TMA ring (A 128x64 + B
+//   256x64 bf16, 128-byte swizzle, 48 KiB per stage) feeds one thread issuing
+//   tcgen05.mma (kind::f16, M = 128, N = 256, K = 16, fp32 accumulators in TMEM,
+//   two of 256 columns); four epilogue warps drain TMEM with tcgen05.ld (32
+//   lanes x 32 columns per load), round to bf16 (RNE) and store y rows; the last
+//   of a record's tiles to read its meta word applies the evict-on-read (depth <
+//   cur_boundary).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -33,7 +34,6 @@ constexpr int kGM = 128, kGN = 256, kGK = 64, kGStages = 4;
 constexpr int kGABytes = kGM * kGK * 2;             // 16 KiB
 constexpr int kGBBytes = kGN * kGK * 2;             // 32 KiB
 constexpr int kGStageBytes = kGABytes + kGBBytes;   // 48 KiB
-constexpr int kGThreads = 128;
 constexpr int kGSmem = kGStages * kGStageBytes + 1024;  // + alignment slack for the 1024-B swizzle atoms
 
 __device__ __forceinline__ uint32_t s_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -78,23 +78,38 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t *>(&v);
 }
 
-__global__ void __launch_bounds__(kGThreads, 1)
+// Persistent, warp-specialised: one CTA per SM walks tiles blockIdx.x, +grid, ...
+// (tile = (example, M tile, N tile), N fastest, so the N tiles of one record run
+// side by side and share its A tiles in L2).  Warp 0 lane 0 = producer: resolves
+// the tile's id -> slot and {depth, valid} ONCE (the tile info the other roles
+// read, so an eviction by another tile cannot change a tile's view), then
+// streams its k-blocks through a 4-stage TMA ring; warp 1 lane 0 = MMA issuer;
+// warps 2-5 = epilogue.  Two TMEM accumulators (2 x 256 columns) let tile j+1's
+// MMAs run while tile j is drained.  A miss flows through the same barriers with
+// no loads and no MMAs, so every role keeps the same phase bookkeeping.
+constexpr int kGRoles = 2 * 32;                 // producer warp + MMA warp
+constexpr int kGEpi = 128;                      // epilogue warps 2..5
+constexpr int kGThreadsP = kGRoles + kGEpi;
+
+struct TileInfo {
+  int64_t slot;
+  int32_t hit, depth, ex, mt, nt, pad;
+};
+
+__global__ void __launch_bounds__(kGThreadsP, 1)
     cache_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                       const CacheGemmParams p) {
   extern __shared__ unsigned char g_smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(g_smem_raw) + 1023) &
                                                          ~static_cast<uintptr_t>(1023));
-  __shared__ __align__(8) uint64_t full[kGStages], empty[kGStages], accum;
+  __shared__ __align__(8) uint64_t full[kGStages], empty[kGStages];
+  __shared__ __align__(8) uint64_t info_full[2], tmem_full[2], tmem_empty[2];
+  __shared__ TileInfo tinfo[2];
   __shared__ uint32_t s_tmem;
-  __shared__ int s_hit, s_depth;
-  __shared__ int64_t s_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // CTA = (example, M tile of its record, N tile)
-  const int tiles = p.n_tiles_m * p.n_tiles_n;
-  const int ex = static_cast<int>(blockIdx.x) / tiles;
-  const int mt = (static_cast<int>(blockIdx.x) % tiles) / p.n_tiles_n;
-  const int nt = static_cast<int>(blockIdx.x) % p.n_tiles_n;
-  const bool first_tile = mt == 0 && nt == 0;
+  const int tiles_per_ex = p.n_tiles_m * p.n_tiles_n;
+  const int64_t total = static_cast<int64_t>(p.n) * tiles_per_ex;
+  const int G = static_cast<int>(gridDim.x);
 
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_a) : "memory");
@@ -103,133 +118,172 @@ __global__ void __launch_bounds__(kGThreads, 1)
       g_mbar_init(&full[s], 1);
       g_mbar_init(&empty[s], 1);
     }
-    g_mbar_init(&accum, 1);
+    for (int a = 0; a < 2; ++a) {
+      g_mbar_init(&info_full[a], 1);
+      g_mbar_init(&tmem_full[a], 1);
+      g_mbar_init(&tmem_empty[a], kGEpi / 32);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {  // 256 TMEM columns: the 128 x 256 fp32 accumulator
+  if (warp == 1) {  // 512 TMEM columns: two 128 x 256 fp32 accumulators
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(&s_tmem)),
-                 "r"(256u));
+                 "r"(512u));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
-  }
-  pdl_wait();  // ids (and the store) may come from the preceding kernels
-  if (tid == 32) {
-    const int64_t id = p.ids[ex];
-    int hit = 0, depth = 0;
-    int64_t slot = 0;
-    if (id < 0 || id >= p.num_examples) {
-      if (first_tile) atomicOr(p.err, AF_CACHE_ERR_RANGE);
-    } else if (id % p.world != p.rank) {
-      if (first_tile) atomicOr(p.err, AF_CACHE_ERR_OWNER);
-    } else {
-      slot = id / p.world;
-      const int4 mv = __ldcg(reinterpret_cast<const int4 *>(p.meta) + slot);  // {depth, valid, readers, -}
-      hit = mv.y != 0;
-      depth = mv.x;
-    }
-    if (first_tile) p.depth_out[ex] = hit ? depth : -1;
-    s_hit = hit;
-    s_depth = depth;
-    s_slot = slot;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
   const int nk = p.K / kGK;
+  pdl_wait();  // ids (and the store) may come from the preceding kernels
 
-  if (s_hit) {
-    if (warp == 0 && lane == 0) {
-      // TMA producer: stage s holds A (record rows x 64 k) then B (256 n x 64 k)
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kGStages;
-        if (kb >= kGStages) g_mbar_wait(&empty[s], ((kb / kGStages) - 1) & 1);
-        unsigned char *sa = smem + s * kGStageBytes;
-        unsigned char *sb = sa + kGABytes;
-        g_mbar_expect_tx(&full[s], kGStageBytes);
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-            "[%5];" ::"r"(s_u32(sa)),
-            "l"(&tmap_a), "r"(kb * kGK), "r"(mt * kGM), "r"(static_cast<int>(s_slot)), "r"(s_u32(&full[s]))
-            : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-                "r"(s_u32(sb)),
-            "l"(&tmap_b), "r"(kb * kGK), "r"(nt * kGN), "r"(s_u32(&full[s]))
-            : "memory");
-      }
-    } else if (warp == 1 && lane == 0) {
-      // MMA issuer: 4 x (M128 N256 K16) per stage into the TMEM accumulator
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kGStages;
-        g_mbar_wait(&full[s], (kb / kGStages) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t sa = s_u32(smem + s * kGStageBytes), sb = sa + kGABytes;
-#pragma unroll
-        for (int k = 0; k < kGK / 16; ++k) {
-          const uint64_t da = umma_desc_sw128(sa + k * 32), db = umma_desc_sw128(sb + k * 32);
-          const uint32_t acc = (kb | k) != 0 ? 1u : 0u;
+  if (warp == 0) {
+    if (lane == 0) {  // ===== producer
+      uint32_t q = 0;  // k-blocks issued so far (hit tiles only)
+      int j = 0;
+      for (int64_t t = blockIdx.x; t < total; t += G, ++j) {
+        const int a = j & 1;
+        if (j >= 2) g_mbar_wait(&tmem_empty[a], ((j >> 1) - 1) & 1);  // tinfo[a] no longer read
+        TileInfo ti{};
+        ti.ex = static_cast<int32_t>(t / tiles_per_ex);
+        const int r = static_cast<int>(t % tiles_per_ex);
+        ti.mt = r / p.n_tiles_n;
+        ti.nt = r % p.n_tiles_n;
+        const int64_t id = p.ids[ti.ex];
+        const bool first_tile = r == 0;
+        if (id < 0 || id >= p.num_examples) {
+          if (first_tile) atomicOr(p.err, AF_CACHE_ERR_RANGE);
+        } else if (id % p.world != p.rank) {
+          if (first_tile) atomicOr(p.err, AF_CACHE_ERR_OWNER);
+        } else {
+          ti.slot = id / p.world;
+          const int4 mv = __ldcg(reinterpret_cast<const int4 *>(p.meta) + ti.slot);  // {depth, valid, readers, -}
+          ti.hit = mv.y != 0;
+          ti.depth = mv.x;
+        }
+        if (first_tile) p.depth_out[ti.ex] = ti.hit ? ti.depth : -1;
+        tinfo[a] = ti;
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&info_full[a])) : "memory");
+        if (!ti.hit) continue;
+        for (int kb = 0; kb < nk; ++kb, ++q) {
+          const int s = static_cast<int>(q % kGStages);
+          if (q >= static_cast<uint32_t>(kGStages)) g_mbar_wait(&empty[s], ((q / kGStages) - 1) & 1);
+          unsigned char *sa = smem + s * kGStageBytes;
+          unsigned char *sb = sa + kGABytes;
+          g_mbar_expect_tx(&full[s], kGStageBytes);
           asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-              "l"(da), "l"(db), "r"(kIdesc), "r"(acc)
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+              "[%5];" ::"r"(s_u32(sa)),
+              "l"(&tmap_a), "r"(kb * kGK), "r"(ti.mt * kGM), "r"(static_cast<int>(ti.slot)), "r"(s_u32(&full[s]))
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+              "[%4];" ::"r"(s_u32(sb)),
+              "l"(&tmap_b), "r"(kb * kGK), "r"(ti.nt * kGN), "r"(s_u32(&full[s]))
               : "memory");
         }
-        // the stage is free once these MMAs have read it
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ===== MMA issuer
+      uint32_t q = 0;
+      int j = 0;
+      for (int64_t t = blockIdx.x; t < total; t += G, ++j) {
+        const int a = j & 1;
+        g_mbar_wait(&info_full[a], (j >> 1) & 1);
+        if (j >= 2) g_mbar_wait(&tmem_empty[a], ((j >> 1) - 1) & 1);  // accumulator a drained
+        if (!tinfo[a].hit) {
+          asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&tmem_full[a])) : "memory");
+          continue;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc_cols = tmem + static_cast<uint32_t>(a * kGN);
+        for (int kb = 0; kb < nk; ++kb, ++q) {
+          const int s = static_cast<int>(q % kGStages);
+          g_mbar_wait(&full[s], (q / kGStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = s_u32(smem + s * kGStageBytes), sb = sa + kGABytes;
+#pragma unroll
+          for (int k = 0; k < kGK / 16; ++k) {
+            const uint64_t da = umma_desc_sw128(sa + k * 32), db = umma_desc_sw128(sb + k * 32);
+            const uint32_t acc = (kb | k) != 0 ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_cols),
+                "l"(da), "l"(db), "r"(kIdesc), "r"(acc)
+                : "memory");
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           s_u32(&empty[s]))
+                       : "memory");
+        }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         s_u32(&empty[s]))
+                         s_u32(&tmem_full[a]))
                      : "memory");
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       s_u32(&accum))
-                   : "memory");
     }
-    // epilogue: warp w owns TMEM lanes (= output rows) 32w .. 32w + 31
-    g_mbar_wait(&accum, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int row = warp * 32 + lane;
-    __nv_bfloat16 *yrow = reinterpret_cast<__nv_bfloat16 *>(p.y) +
-                          (static_cast<int64_t>(ex) * p.rows + static_cast<int64_t>(mt) * kGM + row) * p.ldy +
-                          static_cast<int64_t>(nt) * kGN;
+  } else {
+    // ===== epilogue: warp w accesses TMEM lanes 32 (w % 4) .. + 31 (= output rows)
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    int j = 0;
+    for (int64_t t = blockIdx.x; t < total; t += G, ++j) {
+      const int a = j & 1;
+      g_mbar_wait(&info_full[a], (j >> 1) & 1);  // acquire the producer's tile info directly
+      g_mbar_wait(&tmem_full[a], (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const TileInfo ti = tinfo[a];
+      if (ti.hit) {
+        __nv_bfloat16 *yrow = reinterpret_cast<__nv_bfloat16 *>(p.y) +
+                              (static_cast<int64_t>(ti.ex) * p.rows + static_cast<int64_t>(ti.mt) * kGM + row) * p.ldy +
+                              static_cast<int64_t>(ti.nt) * kGN;
 #pragma unroll 1
-    for (int c0 = 0; c0 < kGN; c0 += 32) {
-      uint32_t v[32];
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c0);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-          "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (nt * kGN + c0 < p.N) {
-        uint4 *dst = reinterpret_cast<uint4 *>(yrow + c0);
+        for (int c0 = 0; c0 < kGN; c0 += 32) {
+          uint32_t v[32];
+          const uint32_t taddr =
+              tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(a * kGN + c0);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+              "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (ti.nt * kGN + c0 < p.N) {
+            uint4 *dst = reinterpret_cast<uint4 *>(yrow + c0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
-          w.y = pack_bf16(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
-          w.z = pack_bf16(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
-          w.w = pack_bf16(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
-          dst[q] = w;
+            for (int qv = 0; qv < 4; ++qv) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(v[8 * qv + 0]), __uint_as_float(v[8 * qv + 1]));
+              w.y = pack_bf16(__uint_as_float(v[8 * qv + 2]), __uint_as_float(v[8 * qv + 3]));
+              w.z = pack_bf16(__uint_as_float(v[8 * qv + 4]), __uint_as_float(v[8 * qv + 5]));
+              w.w = pack_bf16(__uint_as_float(v[8 * qv + 6]), __uint_as_float(v[8 * qv + 7]));
+              dst[qv] = w;
+            }
+          }
+        }
+        if (warp == 2 && lane == 0) {  // evict on read once every tile of the record has read its meta
+          CacheMeta *m = p.meta + ti.slot;
+          const unsigned int seen = atomicAdd(&m->readers, 1u);
+          if (seen == static_cast<unsigned int>(tiles_per_ex) - 1u) {
+            if (ti.depth < p.cur_boundary) m->valid = 0;
+            m->readers = 0u;
+          }
         }
       }
-    }
-    if (tid == 0) {  // evict on read once every N tile of the row has read the record
-      __threadfence();
-      CacheMeta *m = p.meta + s_slot;
-      const unsigned int seen = atomicAdd(&m->readers, 1u);
-      if (seen == static_cast<unsigned int>(tiles) - 1u) {
-        if (s_depth < p.cur_boundary) m->valid = 0;
-        m->readers = 0u;
-      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&tmem_empty[a])) : "memory");
     }
   }
   pdl_launch_dependents();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256u));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
 }
 
 }  // namespace
@@ -241,10 +295,13 @@ int launch_cache_gemm(const CacheGemmParams &p, const void *tmap_a, const void *
   if (e != cudaSuccess) return static_cast<int>(e);
   const CUtensorMap &ta = *static_cast<const CUtensorMap *>(tmap_a);
   const CUtensorMap &tb = *static_cast<const CUtensorMap *>(tmap_b);
-  return static_cast<int>(launch_pdl(cache_gemm_kernel,
-                                     dim3(static_cast<unsigned>(p.n) * p.n_tiles_m * p.n_tiles_n),
-                                     dim3(kGThreads), static_cast<size_t>(kGSmem), static_cast<cudaStream_t>(stream),
-                                     ta, tb, p));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t total = static_cast<int64_t>(p.n) * p.n_tiles_m * p.n_tiles_n;
+  const int grid = static_cast<int>(total < sms ? total : sms);  // persistent: one CTA per SM
+  return static_cast<int>(launch_pdl(cache_gemm_kernel, dim3(grid), dim3(kGThreadsP), static_cast<size_t>(kGSmem),
+                                     static_cast<cudaStream_t>(stream), ta, tb, p));
 }
 
 int preload_cache_gemm_kernel() {
