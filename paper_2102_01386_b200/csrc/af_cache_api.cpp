@@ -397,10 +397,11 @@ af_status af_cache_get_gemm(af_cache *c, const int64_t *ids_dev, int32_t n, int3
     af_status st = encode_tiled(&ta, c->payload, 3, dims, strides, box);
     if (st != AF_OK) return st;
   }
-  {  // W as [N][K] bf16 (a torch Linear weight): box of 256 rows x 64 k
+  {  // W as [N][K] bf16 (a torch Linear weight): box of 128 rows x 64 k (each CTA of a pair
+     // loads one half of a 256-row N tile, multicast to both)
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(N)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
-    const cuuint32_t box[2] = {64, 256};
+    const cuuint32_t box[2] = {64, 128};
     af_status st = encode_tiled(&tb, const_cast<void *>(w_dev), 2, dims, strides, box);
     if (st != AF_OK) return st;
   }

@@ -78,23 +78,39 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t *>(&v);
 }
 
-// Persistent, warp-specialised: one CTA per SM walks tiles blockIdx.x, +grid, ...
-// (tile = (example, M tile, N tile), N fastest, so the N tiles of one record run
-// side by side and share its A tiles in L2).  Warp 0 lane 0 = producer: resolves
-// the tile's id -> slot and {depth, valid} ONCE (the tile info the other roles
-// read, so an eviction by another tile cannot change a tile's view), then
-// streams its k-blocks through a 4-stage TMA ring; warp 1 lane 0 = MMA issuer;
-// warps 2-5 = epilogue.  Two TMEM accumulators (2 x 256 columns) let tile j+1's
-// MMAs run while tile j is drained.  A miss flows through the same barriers with
-// no loads and no MMAs, so every role keeps the same phase bookkeeping.
+// Persistent, warp-specialised, clusters of two CTAs sharing the B operand:
+// cluster c walks pair tiles u = c, c + C, ...; pair tile u = (N tile, a pair of
+// row tiles) and CTA rank r of the cluster takes row tile 2 (u / n_tiles_n) + r
+// (row tile = (example, 128-row M tile of its record)).  Each CTA TMA-loads its
+// own A tile and HALF of the shared 256-row B tile, multicast into both CTAs'
+// shared memory, so the L2 -> SM operand traffic per tile is A + B/2 instead
+// of A + B (B200's tensor cores outrun the L2 at 128 x 256 tiles otherwise).
+// Warp 0 lane 0 = producer: resolves the tile's id -> slot and {depth, valid}
+// ONCE (the tile info the epilogue reads, so an eviction by another tile cannot
+// change a tile's view) and streams its k-blocks through a 4-stage ring; warp 1
+// lane 0 = MMA issuer (tcgen05.mma cta_group::1, M128 N256 K16; its commit
+// frees the stage in BOTH CTAs); warps 2-5 = epilogue.  Two TMEM accumulators
+// (2 x 256 columns) let tile j+1's MMAs run while tile j is drained.  A missed
+// or absent row tile still loads (slot 0) and multiplies -- its partner needs
+// its half of B and both CTAs keep the same phases -- and stores nothing.
 constexpr int kGRoles = 2 * 32;                 // producer warp + MMA warp
 constexpr int kGEpi = 128;                      // epilogue warps 2..5
 constexpr int kGThreadsP = kGRoles + kGEpi;
+constexpr int kGBHalf = kGBBytes / 2;           // one CTA's half of the B tile (128 rows x 64 k)
 
 struct TileInfo {
   int64_t slot;
   int32_t hit, depth, ex, mt, nt, pad;
 };
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 __global__ void __launch_bounds__(kGThreadsP, 1)
     cache_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -107,16 +123,18 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
   __shared__ TileInfo tinfo[2];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = static_cast<int>(cluster_rank());
   const int tiles_per_ex = p.n_tiles_m * p.n_tiles_n;
-  const int64_t total = static_cast<int64_t>(p.n) * tiles_per_ex;
-  const int G = static_cast<int>(gridDim.x);
+  const int64_t row_tiles = static_cast<int64_t>(p.n) * p.n_tiles_m;
+  const int64_t pair_tiles = (row_tiles + 1) / 2 * p.n_tiles_n;
+  const int C = static_cast<int>(gridDim.x) / 2, cid = static_cast<int>(blockIdx.x) / 2;
 
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_b) : "memory");
     for (int s = 0; s < kGStages; ++s) {
       g_mbar_init(&full[s], 1);
-      g_mbar_init(&empty[s], 1);
+      g_mbar_init(&empty[s], 2);  // both CTAs' MMA commits release a stage
     }
     for (int a = 0; a < 2; ++a) {
       g_mbar_init(&info_full[a], 1);
@@ -131,7 +149,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  cluster_sync_all();  // the partner's barriers exist before any multicast signals them
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
   const int nk = p.K / kGK;
@@ -139,47 +157,50 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ===== producer
-      uint32_t q = 0;  // k-blocks issued so far (hit tiles only)
+      uint32_t q = 0;  // k-blocks issued so far
       int j = 0;
-      for (int64_t t = blockIdx.x; t < total; t += G, ++j) {
+      for (int64_t u = cid; u < pair_tiles; u += C, ++j) {
         const int a = j & 1;
         if (j >= 2) g_mbar_wait(&tmem_empty[a], ((j >> 1) - 1) & 1);  // tinfo[a] no longer read
         TileInfo ti{};
-        ti.ex = static_cast<int32_t>(t / tiles_per_ex);
-        const int r = static_cast<int>(t % tiles_per_ex);
-        ti.mt = r / p.n_tiles_n;
-        ti.nt = r % p.n_tiles_n;
-        const int64_t id = p.ids[ti.ex];
-        const bool first_tile = r == 0;
-        if (id < 0 || id >= p.num_examples) {
-          if (first_tile) atomicOr(p.err, AF_CACHE_ERR_RANGE);
-        } else if (id % p.world != p.rank) {
-          if (first_tile) atomicOr(p.err, AF_CACHE_ERR_OWNER);
-        } else {
-          ti.slot = id / p.world;
-          const int4 mv = __ldcg(reinterpret_cast<const int4 *>(p.meta) + ti.slot);  // {depth, valid, readers, -}
-          ti.hit = mv.y != 0;
-          ti.depth = mv.x;
+        ti.nt = static_cast<int32_t>(u % p.n_tiles_n);
+        const int64_t rt = (u / p.n_tiles_n) * 2 + rank;
+        if (rt < row_tiles) {
+          ti.ex = static_cast<int32_t>(rt / p.n_tiles_m);
+          ti.mt = static_cast<int32_t>(rt % p.n_tiles_m);
+          const int64_t id = p.ids[ti.ex];
+          const bool first_tile = ti.mt == 0 && ti.nt == 0;
+          if (id < 0 || id >= p.num_examples) {
+            if (first_tile) atomicOr(p.err, AF_CACHE_ERR_RANGE);
+          } else if (id % p.world != p.rank) {
+            if (first_tile) atomicOr(p.err, AF_CACHE_ERR_OWNER);
+          } else {
+            const int64_t slot = id / p.world;
+            const int4 mv = __ldcg(reinterpret_cast<const int4 *>(p.meta) + slot);  // {depth, valid, readers, -}
+            ti.hit = mv.y != 0;
+            ti.depth = mv.x;
+            if (ti.hit) ti.slot = slot;
+          }
+          if (first_tile) p.depth_out[ti.ex] = ti.hit ? ti.depth : -1;
         }
-        if (first_tile) p.depth_out[ti.ex] = ti.hit ? ti.depth : -1;
         tinfo[a] = ti;
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&info_full[a])) : "memory");
-        if (!ti.hit) continue;
         for (int kb = 0; kb < nk; ++kb, ++q) {
           const int s = static_cast<int>(q % kGStages);
           if (q >= static_cast<uint32_t>(kGStages)) g_mbar_wait(&empty[s], ((q / kGStages) - 1) & 1);
           unsigned char *sa = smem + s * kGStageBytes;
-          unsigned char *sb = sa + kGABytes;
-          g_mbar_expect_tx(&full[s], kGStageBytes);
+          unsigned char *sb = sa + kGABytes + rank * kGBHalf;
+          g_mbar_expect_tx(&full[s], kGStageBytes);  // own A + both halves of B
           asm volatile(
               "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
               "[%5];" ::"r"(s_u32(sa)),
               "l"(&tmap_a), "r"(kb * kGK), "r"(ti.mt * kGM), "r"(static_cast<int>(ti.slot)), "r"(s_u32(&full[s]))
               : "memory");
           asm volatile(
-              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-              "[%4];" ::"r"(s_u32(sb)),
-              "l"(&tmap_b), "r"(kb * kGK), "r"(ti.nt * kGN), "r"(s_u32(&full[s]))
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+              "[%1, {%2, %3}], [%4], %5;" ::"r"(s_u32(sb)),
+              "l"(&tmap_b), "r"(kb * kGK), "r"(ti.nt * kGN + rank * (kGN / 2)), "r"(s_u32(&full[s])),
+              "h"(static_cast<uint16_t>(0x3))
               : "memory");
         }
       }
@@ -188,14 +209,9 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
     if (lane == 0) {  // ===== MMA issuer
       uint32_t q = 0;
       int j = 0;
-      for (int64_t t = blockIdx.x; t < total; t += G, ++j) {
+      for (int64_t u = cid; u < pair_tiles; u += C, ++j) {
         const int a = j & 1;
-        g_mbar_wait(&info_full[a], (j >> 1) & 1);
         if (j >= 2) g_mbar_wait(&tmem_empty[a], ((j >> 1) - 1) & 1);  // accumulator a drained
-        if (!tinfo[a].hit) {
-          asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&tmem_full[a])) : "memory");
-          continue;
-        }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc_cols = tmem + static_cast<uint32_t>(a * kGN);
         for (int kb = 0; kb < nk; ++kb, ++q) {
@@ -213,9 +229,12 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
                 "l"(da), "l"(db), "r"(kIdesc), "r"(acc)
                 : "memory");
           }
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                           s_u32(&empty[s]))
-                       : "memory");
+          // the stage (this CTA's A and its copy of B) is free in both CTAs once these MMAs have read it
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  s_u32(&empty[s])),
+              "h"(static_cast<uint16_t>(0x3))
+              : "memory");
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          s_u32(&tmem_full[a]))
@@ -227,7 +246,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
     int j = 0;
-    for (int64_t t = blockIdx.x; t < total; t += G, ++j) {
+    for (int64_t u = cid; u < pair_tiles; u += C, ++j) {
       const int a = j & 1;
       g_mbar_wait(&info_full[a], (j >> 1) & 1);  // acquire the producer's tile info directly
       g_mbar_wait(&tmem_full[a], (j >> 1) & 1);
@@ -283,6 +302,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
   pdl_launch_dependents();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  cluster_sync_all();  // no CTA leaves while its partner may still multicast into it
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
 }
 
@@ -298,10 +318,25 @@ int launch_cache_gemm(const CacheGemmParams &p, const void *tmap_a, const void *
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t total = static_cast<int64_t>(p.n) * p.n_tiles_m * p.n_tiles_n;
-  const int grid = static_cast<int>(total < sms ? total : sms);  // persistent: one CTA per SM
-  return static_cast<int>(launch_pdl(cache_gemm_kernel, dim3(grid), dim3(kGThreadsP), static_cast<size_t>(kGSmem),
-                                     static_cast<cudaStream_t>(stream), ta, tb, p));
+  const int64_t row_tiles = static_cast<int64_t>(p.n) * p.n_tiles_m;
+  const int64_t pairs = (row_tiles + 1) / 2 * p.n_tiles_n;
+  const int clusters = static_cast<int>(pairs < sms / 2 ? pairs : sms / 2);  // persistent: one CTA per SM
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * (clusters < 1 ? 1 : clusters)));
+  cfg.blockDim = dim3(kGThreadsP);
+  cfg.dynamicSmemBytes = static_cast<size_t>(kGSmem);
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t r = cudaLaunchKernelEx(&cfg, cache_gemm_kernel, ta, tb, p);
+  return static_cast<int>(r != cudaSuccess ? r : cudaGetLastError());
 }
 
 int preload_cache_gemm_kernel() {
