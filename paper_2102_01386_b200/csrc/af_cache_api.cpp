@@ -405,6 +405,14 @@ af_status af_cache_get_gemm(af_cache *c, const int64_t *ids_dev, int32_t n, int3
     af_status st = encode_tiled(&tb, const_cast<void *>(w_dev), 2, dims, strides, box);
     if (st != AF_OK) return st;
   }
+  alignas(64) CUtensorMap ty;
+  {  // y as [n * rows_per_record][N] bf16: the epilogue's TMA stores of 128 x 64 chunks
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(n) * rows_per_record};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * 2};
+    const cuuint32_t box[2] = {64, 128};
+    af_status st = encode_tiled(&ty, y_dev, 2, dims, strides, box);
+    if (st != AF_OK) return st;
+  }
   CacheGemmParams p{};
   p.meta = reinterpret_cast<CacheMeta *>(c->meta + kMetaHeader);
   p.err = reinterpret_cast<unsigned int *>(c->meta);
@@ -423,7 +431,7 @@ af_status af_cache_get_gemm(af_cache *c, const int64_t *ids_dev, int32_t n, int3
   p.y = y_dev;
   p.ldy = N;
   if (static_cast<int64_t>(n) * p.n_tiles_m * p.n_tiles_n > (int64_t(1) << 31) - 1) return fail(AF_ERANGE, "grid too large");
-  const int e = launch_cache_gemm(p, &ta, &tb, stream);
+  const int e = launch_cache_gemm(p, &ta, &tb, &ty, stream);
   if (e != 0) return cuda_fail(static_cast<cudaError_t>(e), "cache get + GEMM launch");
   return AF_OK;
 }

@@ -34,7 +34,8 @@ constexpr int kGM = 128, kGN = 256, kGK = 64, kGStages = 4;
 constexpr int kGABytes = kGM * kGK * 2;             // 16 KiB
 constexpr int kGBBytes = kGN * kGK * 2;             // 32 KiB
 constexpr int kGStageBytes = kGABytes + kGBBytes;   // 48 KiB
-constexpr int kGSmem = kGStages * kGStageBytes + 1024;  // + alignment slack for the 1024-B swizzle atoms
+constexpr int kGEpiBytes = kGM * 64 * 2;                // one 128 x 64 bf16 output chunk (16 KiB), double-buffered
+constexpr int kGSmem = kGStages * kGStageBytes + 2 * kGEpiBytes + 1024;  // + slack for 1024-B alignment
 
 __device__ __forceinline__ uint32_t s_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -114,7 +115,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 __global__ void __launch_bounds__(kGThreadsP, 1)
     cache_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                      const CacheGemmParams p) {
+                      const __grid_constant__ CUtensorMap tmap_y, const CacheGemmParams p) {
   extern __shared__ unsigned char g_smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(g_smem_raw) + 1023) &
                                                          ~static_cast<uintptr_t>(1023));
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_b) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_y) : "memory");
     for (int s = 0; s < kGStages; ++s) {
       g_mbar_init(&full[s], 1);
       g_mbar_init(&empty[s], 2);  // both CTAs' MMA commits release a stage
@@ -245,6 +247,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
     // ===== epilogue: warp w accesses TMEM lanes 32 (w % 4) .. + 31 (= output rows)
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
+    int epi_chunk = 0;  // output chunks staged so far (selects the staging buffer)
     int j = 0;
     for (int64_t u = cid; u < pair_tiles; u += C, ++j) {
       const int a = j & 1;
@@ -253,35 +256,53 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const TileInfo ti = tinfo[a];
       if (ti.hit) {
-        __nv_bfloat16 *yrow = reinterpret_cast<__nv_bfloat16 *>(p.y) +
-                              (static_cast<int64_t>(ti.ex) * p.rows + static_cast<int64_t>(ti.mt) * kGM + row) * p.ldy +
-                              static_cast<int64_t>(ti.nt) * kGN;
+        // TMEM -> registers -> bf16 -> shared memory in the 128-byte-swizzled layout of
+        // the y tensor map (row r's 16-byte chunk c at chunk c ^ (r % 8)) -> one TMA
+        // store per 128 x 64 chunk, double-buffered (coalesced, asynchronous)
+        const int64_t y_row0 = static_cast<int64_t>(ti.ex) * p.rows + static_cast<int64_t>(ti.mt) * kGM;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kGN; c0 += 32) {
-          uint32_t v[32];
-          const uint32_t taddr =
-              tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(a * kGN + c0);
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-              "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-              : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (ti.nt * kGN + c0 < p.N) {
-            uint4 *dst = reinterpret_cast<uint4 *>(yrow + c0);
+        for (int c0 = 0; c0 < kGN && ti.nt * kGN + c0 < p.N; c0 += 64, ++epi_chunk) {
+          unsigned char *buf = smem + kGStages * kGStageBytes + (epi_chunk & 1) * kGEpiBytes;
+          if (epi_chunk >= 2) {  // the TMA store that last read this buffer is done reading it
+            if (tid == kGRoles) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(kGEpi) : "memory");
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t v[32];
+            const uint32_t taddr =
+                tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(a * kGN + c0 + 32 * h);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+                "[%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int qv = 0; qv < 4; ++qv) {
-              uint4 w;
-              w.x = pack_bf16(__uint_as_float(v[8 * qv + 0]), __uint_as_float(v[8 * qv + 1]));
-              w.y = pack_bf16(__uint_as_float(v[8 * qv + 2]), __uint_as_float(v[8 * qv + 3]));
-              w.z = pack_bf16(__uint_as_float(v[8 * qv + 4]), __uint_as_float(v[8 * qv + 5]));
-              w.w = pack_bf16(__uint_as_float(v[8 * qv + 6]), __uint_as_float(v[8 * qv + 7]));
-              dst[qv] = w;
+              const int chunk = 4 * h + qv;  // 16-byte chunk of the row's 128 bytes
+              const uint32_t addr = s_u32(buf) + static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+                           "r"(pack_bf16(__uint_as_float(v[8 * qv + 0]), __uint_as_float(v[8 * qv + 1]))),
+                           "r"(pack_bf16(__uint_as_float(v[8 * qv + 2]), __uint_as_float(v[8 * qv + 3]))),
+                           "r"(pack_bf16(__uint_as_float(v[8 * qv + 4]), __uint_as_float(v[8 * qv + 5]))),
+                           "r"(pack_bf16(__uint_as_float(v[8 * qv + 6]), __uint_as_float(v[8 * qv + 7])))
+                           : "memory");
             }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async (TMA) proxy
+          asm volatile("bar.sync 1, %0;" ::"n"(kGEpi) : "memory");
+          if (tid == kGRoles) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tmap_y),
+                "r"(ti.nt * kGN + c0), "r"(static_cast<int>(y_row0)), "r"(s_u32(buf))
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
         if (warp == 2 && lane == 0) {  // evict on read once every tile of the record has read its meta
@@ -299,6 +320,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&tmem_empty[a])) : "memory");
     }
   }
+  if (tid == kGRoles) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // y written before exit
   pdl_launch_dependents();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -310,11 +332,13 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
 
 int cache_gemm_smem_bytes() { return kGSmem; }
 
-int launch_cache_gemm(const CacheGemmParams &p, const void *tmap_a, const void *tmap_b, void *stream) {
+int launch_cache_gemm(const CacheGemmParams &p, const void *tmap_a, const void *tmap_b, const void *tmap_y,
+                      void *stream) {
   const cudaError_t e = ensure_smem_attr<cache_gemm_kernel>(kGSmem);
   if (e != cudaSuccess) return static_cast<int>(e);
   const CUtensorMap &ta = *static_cast<const CUtensorMap *>(tmap_a);
   const CUtensorMap &tb = *static_cast<const CUtensorMap *>(tmap_b);
+  const CUtensorMap &ty = *static_cast<const CUtensorMap *>(tmap_y);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -335,7 +359,7 @@ int launch_cache_gemm(const CacheGemmParams &p, const void *tmap_a, const void *
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t r = cudaLaunchKernelEx(&cfg, cache_gemm_kernel, ta, tb, p);
+  cudaError_t r = cudaLaunchKernelEx(&cfg, cache_gemm_kernel, ta, tb, ty, p);
   return static_cast<int>(r != cudaSuccess ? r : cudaGetLastError());
 }
 

@@ -311,8 +311,9 @@ int launch_decide(const DecideParams &p, void *stream);
 int launch_cache_put(const CacheParams &p, int grid, void *stream);
 int launch_cache_get(const CacheParams &p, int grid, void *stream);
 int launch_cache_plan(const CachePlanParams &p, void *stream);
-// tmap_a / tmap_b: CUtensorMap (128 B each) of the store's records and of W
-int launch_cache_gemm(const CacheGemmParams &p, const void *tmap_a, const void *tmap_b, void *stream);
+// tmap_a / tmap_b / tmap_y: CUtensorMap (128 B each) of the store's records, W and y
+int launch_cache_gemm(const CacheGemmParams &p, const void *tmap_a, const void *tmap_b, const void *tmap_y,
+                      void *stream);
 int preload_cache_gemm_kernel();
 int norms_max_blocks_per_sm(int mode, int grad_dtype, int world, int *blocks, bool act = false);
 // force-load the kernels (lazy module loading must not happen while peers spin)
