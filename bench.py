@@ -442,6 +442,7 @@ def run_ours(args, rank, world, local):
             result["cache_epoch_c4"] = cache_epoch_c4(dev)
     if not args.no_extras:
         result["next1_fused_adamw"] = adamw_probe(fm, lay, dt, s_g, n_loc, grads, dev)
+        result["next4_cache_get_gemm"] = next4_get_gemm_probe(cache, my_ids, dev)
         if world == 1:
             result["next1_fused_reduce_scatter_p1"] = rs_probe(lay, dt, s_g, grads, dev)
     if not args.no_e2e and not args.zero:
@@ -715,6 +716,62 @@ def cache_epoch_c4(dev, world_emul=8, B=256, seed=3):
     cache.close()
     del cache
     torch.cuda.empty_cache()
+    return res
+
+
+def next4_get_gemm_probe(cache, my_ids, dev, B=256, N=2304, reps=10, rounds=5):
+    """NEXT 4: the cache get fused into the first active layer's GEMM operand load
+    (af_cache_get_gemm: TMA gathers each record as the A tile, tcgen05 MMAs)
+    against af_cache_get into a batch buffer + torch.matmul (cuBLAS bf16), on the
+    step's cache (records of 128 x 768 bf16 = BERT-base hidden states), B fresh
+    ids per call (cold records), W = BERT-base's QKV projection [2304, 768].
+    CUDA graphs of `reps` calls, median of rounds."""
+    import torch
+    K = ROW_BYTES // (128 * 2)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    w = (torch.randn(N, K, device=dev, generator=g) * 0.05).to(torch.bfloat16)
+    sets = [my_ids[torch.randperm(my_ids.numel(), device=dev, generator=g)[:B]].contiguous() for _ in range(reps)]
+    y = torch.empty(B * 128, N, dtype=torch.bfloat16, device=dev)
+    dep = torch.empty(B, dtype=torch.int32, device=dev)
+    buf = torch.empty(B, ROW_BYTES, dtype=torch.uint8, device=dev)
+
+    def fused(r):
+        cache.get_gemm(sets[r], 4, w, y, dep, 128)
+
+    def unfused(r):
+        cache.get(sets[r], 4, buf, dep)
+        torch.matmul(buf.view(torch.bfloat16).view(B * 128, K), w.t(), out=y)
+
+    res = {"examples": B, "M": B * 128, "N": N, "K": K}
+    flops = 2 * B * 128 * K * N
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    tf_peak = peaks.get("bf16_tflops", 2250.0)
+    for name, fn in (("fused_get_gemm", fused), ("get_then_cublas", unfused)):
+        fn(0)
+        gph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gph):
+            for r in range(reps):
+                fn(r)
+        ts = []
+        for _ in range(rounds):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record()
+            gph.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / reps * 1e3)
+        us = statistics.median(ts)
+        res[name] = {"us": round(us, 2), "tflops": round(flops / (us * 1e-6) / 1e12, 1)}
+        del gph
+    f = res["fused_get_gemm"]
+    res["roofline"] = {"bound": "tensor", "achieved": f["tflops"], "peak": tf_peak, "unit": "TFLOP/s",
+                       "frac": round(f["tflops"] / tf_peak, 4),
+                       "peak_source": "MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3, burst)"}
+    res["speedup_vs_unfused"] = round(res["get_then_cublas"]["us"] / f["us"], 3)
+    res["bytes_saved_per_example"] = 2 * ROW_BYTES
     return res
 
 

@@ -266,6 +266,17 @@ def test_disk_tier_host_checks(tmp_path):
     assert L.lib.af_cache_destroy(h) == L.AF_OK
 
 
+def test_cache_get_gemm_host_checks():
+    h = ctypes.c_void_p()
+    assert L.lib.af_cache_create(100, 128 * 64 * 2, 0, 1, ctypes.byref(h)) == L.AF_OK
+    buf = (ctypes.c_uint8 * 64)()
+    a = ctypes.addressof(buf) // 16 * 16 + 16
+    assert L.lib.af_cache_get_gemm(None, a, 1, 0, 128, 64, a, 32, a, a, None) == L.AF_EINVAL
+    assert L.lib.af_cache_get_gemm(h, a, 1, 0, 128, 64, a, 32, a, a, None) == L.AF_EWORKSPACE   # not bound
+    assert L.lib.af_cache_get_gemm(h, a, 0, 0, 128, 64, a, 32, a, a, None) == L.AF_EWORKSPACE
+    L.lib.af_cache_destroy(h)
+
+
 def test_reduce_scatter_host_checks():
     # NEXT 1 (ZeRO form): argument / state errors are synchronous host checks
     lay = uniform_layout(1 << 12, 4)

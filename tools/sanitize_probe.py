@@ -126,6 +126,26 @@ def main():
     c.put(ids, rows, 2)
     c.get_async(ids, 2, out, dep, s)
     torch.cuda.synchronize()
+    # round 2: disk tier (host callbacks), overlapped get over a committed interval end,
+    # the cache get fused into the consumer GEMM (TMA + tcgen05, clusters of two)
+    t = af.ActivationCache(100, 2048 + 16, hbm_rows=10, host_rows=10, disk_rows=30, stage_rows=16)
+    t.put(ids, rows, 2)
+    t.get(ids, 3, out, dep)
+    fm1 = af.FreezingModule(lay.offsets, lay.kinds, grad_dtype="f32")
+    g1 = torch.randn(lay.n, device="cuda") * 1e-3
+    fm1.layer_norms(g1)
+    fm1.interval_end(g1, copy_record=False)
+    c.get(ids, 2, out, dep, overlap_prev=True)
+    fm1.layer_norms(g1)
+    gc = af.ActivationCache(64, 128 * 128 * 2)
+    gids = torch.arange(0, 20, dtype=torch.int64, device="cuda")
+    grows = torch.randn(20, 128 * 128, device="cuda").to(torch.bfloat16)
+    gc.put(gids, grows.view(torch.uint8), 2)
+    w = torch.randn(96, 128, device="cuda").to(torch.bfloat16)
+    y = torch.zeros(22 * 128, 96, dtype=torch.bfloat16, device="cuda")
+    gdep = torch.empty(22, dtype=torch.int32, device="cuda")
+    gc.get_gemm(torch.arange(0, 22, dtype=torch.int64, device="cuda"), 3, w, y, gdep, 128)
+    torch.cuda.synchronize()
     print("sanitize probe done")
 
 
