@@ -509,6 +509,40 @@ def calibrate_read_seconds(row_bytes, batch_rows, device=None, reps=10):
     return a.elapsed_time(b) / reps * 1e-3
 
 
+def calibrate_forward_seconds(layer_forward, iters=5, warmup=2, stream=None):
+    """Measured time of one layer's forward pass (`layer_forward()`, the caller's
+    callable running one frozen block on one batch) on the current stream: the
+    t_layer_fwd of the cache-vs-recompute rule, taken over a few iterations of
+    training ("few iterations of training can indicate how many layers
+    ... need to be frozen before caching becomes advantageous"). Median of
+    `iters` CUDA-event-timed calls after `warmup`."""
+    s = stream if stream is not None else torch.cuda.current_stream()
+    for _ in range(warmup):
+        layer_forward()
+    ts = []
+    for _ in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        layer_forward()
+        b.record(s)
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def calibrate_should_cache(layer_forward, row_bytes, batch_rows, max_layers, device=None, iters=5):
+    """Both sides of the P:230-235 trade-off measured on this device: t_layer_fwd
+    from a few timed forward passes of one block (`layer_forward`) and
+    t_batch_read from timed cache gets of one batch; returns the smallest frozen
+    depth k <= max_layers at which af_should_cache(k, t_fwd, t_read) says caching
+    pays (None if none does) with the two times."""
+    t_fwd = calibrate_forward_seconds(layer_forward, iters=iters)
+    t_read = calibrate_read_seconds(row_bytes, batch_rows, device=device, reps=iters)
+    k = next((k for k in range(1, int(max_layers) + 1) if should_cache(k, t_fwd, t_read)), None)
+    return {"min_frozen_layers": k, "t_layer_fwd_s": t_fwd, "t_batch_read_s": t_read}
+
+
 def bootstrap_nccl_id(rank, group=None, device=None):
     """Rank 0 creates a 128-byte ncclUniqueId through the library; torch.distributed
     broadcasts it to every rank of `group` (gloo: CPU tensor, nccl: device tensor)."""

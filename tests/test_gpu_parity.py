@@ -898,6 +898,27 @@ def test_get_async_prefetch_parity(tiered):
     gc.close()
 
 
+def test_calibrate_should_cache_both_sides():
+    """the forward-time side measured too -- a BERT-base-sized block
+    stand-in (two 768x3072 projections on 32 x 128 tokens) against the read
+    time of 32 records of 128 x 768 bf16; the break-even depth is the smallest k
+    with k * t_fwd > t_read (af_should_cache), consistent with the two times."""
+    import paper_2102_01386_b200 as af
+    x = torch.randn(32 * 128, 768, device="cuda", dtype=torch.bfloat16)
+    w1 = torch.randn(3072, 768, device="cuda", dtype=torch.bfloat16) * 0.02
+    w2 = torch.randn(768, 3072, device="cuda", dtype=torch.bfloat16) * 0.02
+
+    def block():
+        return torch.nn.functional.linear(torch.nn.functional.gelu(torch.nn.functional.linear(x, w1)), w2)
+    r = af.calibrate_should_cache(block, 128 * 768 * 2, 32, max_layers=24)
+    assert r["t_layer_fwd_s"] > 0 and r["t_batch_read_s"] > 0
+    k = r["min_frozen_layers"]
+    if k is None:
+        assert 24 * r["t_layer_fwd_s"] <= r["t_batch_read_s"]
+    else:
+        assert k * r["t_layer_fwd_s"] > r["t_batch_read_s"] >= (k - 1) * r["t_layer_fwd_s"]
+
+
 def test_calibrate_read_seconds_and_should_cache():
     import paper_2102_01386_b200 as af
     t = af.calibrate_read_seconds(196_608, 256)
