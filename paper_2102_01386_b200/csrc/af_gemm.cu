@@ -30,10 +30,10 @@
 namespace af {
 namespace {
 
-constexpr int kGM = 128, kGN = 256, kGK = 64, kGStages = 4;
-constexpr int kGABytes = kGM * kGK * 2;             // 16 KiB
-constexpr int kGBBytes = kGN * kGK * 2;             // 32 KiB
-constexpr int kGStageBytes = kGABytes + kGBBytes;   // 48 KiB
+constexpr int kGM = 128, kGN = 256, kGK = 64, kGStages = 6;
+constexpr int kGABytes = kGM * kGK * 2;             // 16 KiB: this CTA's 128 rows of the pair's 256-row A tile
+constexpr int kGBBytes = kGN / 2 * kGK * 2;         // 16 KiB: this CTA's half (128 columns) of the 256-wide B tile
+constexpr int kGStageBytes = kGABytes + kGBBytes;   // 32 KiB per CTA (64 KiB per pair)
 constexpr int kGEpiBytes = kGM * 64 * 2;                // one 128 x 64 bf16 output chunk (16 KiB), double-buffered
 constexpr int kGSmem = kGStages * kGStageBytes + 2 * kGEpiBytes + 1024;  // + slack for 1024-B alignment
 
@@ -70,34 +70,40 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
   return d;
 }
 
-// Instruction descriptor (kind::f16): D fp32, A and B bf16, both K-major, N, M.
+// Instruction descriptor (kind::f16): D fp32, A and B bf16, both K-major, N = 256,
+// M = 256 (cta_group::2: the CTA pair's two 128-row halves).
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kGN >> 3) << 17) |
-                            (static_cast<uint32_t>(kGM >> 4) << 24);
+                            (static_cast<uint32_t>((2 * kGM) >> 4) << 24);
+// A shared::cluster address with the pair's peer bit cleared: the leader CTA's copy
+// (the TMA of either CTA completes its bytes on the leader's barrier)
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (lower address), RNE
   return *reinterpret_cast<const uint32_t *>(&v);
 }
 
-// Persistent, warp-specialised, clusters of two CTAs sharing the B operand:
+// Persistent, warp-specialised, CTA pairs (clusters of two) running 2-SM MMAs:
 // cluster c walks pair tiles u = c, c + C, ...; pair tile u = (N tile, a pair of
-// row tiles) and CTA rank r of the cluster takes row tile 2 (u / n_tiles_n) + r
-// (row tile = (example, 128-row M tile of its record)).  Each CTA TMA-loads its
-// own A tile and HALF of the shared 256-row B tile, multicast into both CTAs'
-// shared memory, so the L2 -> SM operand traffic per tile is A + B/2 instead
-// of A + B (B200's tensor cores outrun the L2 at 128 x 256 tiles otherwise).
-// Warp 0 lane 0 = producer: resolves the tile's id -> slot and {depth, valid}
-// ONCE (the tile info the epilogue reads, so an eviction by another tile cannot
-// change a tile's view) and streams its k-blocks through a 4-stage ring; warp 1
-// lane 0 = MMA issuer (tcgen05.mma cta_group::1, M128 N256 K16; its commit
-// frees the stage in BOTH CTAs); warps 2-5 = epilogue.  Two TMEM accumulators
-// (2 x 256 columns) let tile j+1's MMAs run while tile j is drained.  A missed
-// or absent row tile still loads (slot 0) and multiplies -- its partner needs
-// its half of B and both CTAs keep the same phases -- and stores nothing.
+// row tiles); CTA rank r of the pair takes row tile 2 (u / n_tiles_n) + r (row
+// tile = (example, 128-row M tile of its record)).  Each CTA TMA-loads its own A
+// tile (128 rows) and its half of the 256-wide B tile into its own shared memory,
+// both completing on the leader's stage barrier; the leader's single thread
+// issues tcgen05.mma.cta_group::2 (M = 256: the two CTAs' rows, N = 256, K = 16),
+// whose accumulator rows land in each CTA's own TMEM, and its commits release the
+// stage and signal the accumulator in both CTAs.  Per SM this moves 32 KiB of
+// operands per 64-deep k-block instead of 48 (one CTA alone, N = 256), so the
+// 6-stage ring covers more of the L2 latency.  Warp 0 lane 0 = producer: resolves
+// the tile's id -> slot and {depth, valid} ONCE (the tile info the epilogue
+// reads, so an eviction by another tile cannot change a tile's view); warp 1 lane
+// 0 of the leader = MMA issuer; warps 2-5 = epilogue (each CTA drains its own 128
+// TMEM lanes).  Two TMEM accumulators (2 x 256 columns) let tile j+1's MMAs run
+// while tile j is drained; the leader's MMA waits for BOTH CTAs' epilogues.  A
+// missed or absent row tile still loads (slot 0) and multiplies -- its partner's
+// MMA reads it and both CTAs keep the same phases -- and stores nothing.
 constexpr int kGRoles = 2 * 32;                 // producer warp + MMA warp
 constexpr int kGEpi = 128;                      // epilogue warps 2..5
 constexpr int kGThreadsP = kGRoles + kGEpi;
-constexpr int kGBHalf = kGBBytes / 2;           // one CTA's half of the B tile (128 rows x 64 k)
 
 struct TileInfo {
   int64_t slot;
@@ -112,6 +118,11 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t local_smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem_addr), "r"(rank));
+  return r;
+}
 
 __global__ void __launch_bounds__(kGThreadsP, 1)
     cache_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -120,7 +131,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
   unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(g_smem_raw) + 1023) &
                                                          ~static_cast<uintptr_t>(1023));
   __shared__ __align__(8) uint64_t full[kGStages], empty[kGStages];
-  __shared__ __align__(8) uint64_t info_full[2], tmem_full[2], tmem_empty[2];
+  __shared__ __align__(8) uint64_t info_full[2], info_free[2], tmem_full[2], tmem_empty[2];
   __shared__ TileInfo tinfo[2];
   __shared__ uint32_t s_tmem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -135,20 +146,21 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_b) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_y) : "memory");
     for (int s = 0; s < kGStages; ++s) {
-      g_mbar_init(&full[s], 1);
-      g_mbar_init(&empty[s], 2);  // both CTAs' MMA commits release a stage
+      g_mbar_init(&full[s], 1);   // (leader's) the leader producer's arrive + both CTAs' TMA bytes
+      g_mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
     }
     for (int a = 0; a < 2; ++a) {
       g_mbar_init(&info_full[a], 1);
-      g_mbar_init(&tmem_full[a], 1);
-      g_mbar_init(&tmem_empty[a], kGEpi / 32);  // one arrive per epilogue warp
+      g_mbar_init(&info_free[a], kGEpi / 32);           // this CTA's epilogue warps are done with tinfo[a]
+      g_mbar_init(&tmem_full[a], 1);                    // the leader's commit, multicast to both CTAs
+      g_mbar_init(&tmem_empty[a], 2 * kGEpi / 32);      // (leader's) both CTAs' epilogue warps drained it
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {  // 512 TMEM columns: two 128 x 256 fp32 accumulators
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(&s_tmem)),
+  if (warp == 1) {  // 512 TMEM columns in each CTA of the pair: two 128 x 256 fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(&s_tmem)),
                  "r"(512u));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();  // the partner's barriers exist before any multicast signals them
@@ -163,7 +175,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
       int j = 0;
       for (int64_t u = cid; u < pair_tiles; u += C, ++j) {
         const int a = j & 1;
-        if (j >= 2) g_mbar_wait(&tmem_empty[a], ((j >> 1) - 1) & 1);  // tinfo[a] no longer read
+        if (j >= 2) g_mbar_wait(&info_free[a], ((j >> 1) - 1) & 1);  // tinfo[a] no longer read
         TileInfo ti{};
         ti.nt = static_cast<int32_t>(u % p.n_tiles_n);
         const int64_t rt = (u / p.n_tiles_n) * 2 + rank;
@@ -191,24 +203,24 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
           const int s = static_cast<int>(q % kGStages);
           if (q >= static_cast<uint32_t>(kGStages)) g_mbar_wait(&empty[s], ((q / kGStages) - 1) & 1);
           unsigned char *sa = smem + s * kGStageBytes;
-          unsigned char *sb = sa + kGABytes + rank * kGBHalf;
-          g_mbar_expect_tx(&full[s], kGStageBytes);  // own A + both halves of B
+          unsigned char *sb = sa + kGABytes;
+          const uint32_t bar = s_u32(&full[s]) & kPeerBitMask;  // the leader's stage barrier
+          if (rank == 0) g_mbar_expect_tx(&full[s], 2 * kGStageBytes);  // both CTAs' A and B halves
           asm volatile(
-              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-              "[%5];" ::"r"(s_u32(sa)),
-              "l"(&tmap_a), "r"(kb * kGK), "r"(ti.mt * kGM), "r"(static_cast<int>(ti.slot)), "r"(s_u32(&full[s]))
+              "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+              "[%1, {%2, %3, %4}], [%5];" ::"r"(s_u32(sa)),
+              "l"(&tmap_a), "r"(kb * kGK), "r"(ti.mt * kGM), "r"(static_cast<int>(ti.slot)), "r"(bar)
               : "memory");
           asm volatile(
-              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
-              "[%1, {%2, %3}], [%4], %5;" ::"r"(s_u32(sb)),
-              "l"(&tmap_b), "r"(kb * kGK), "r"(ti.nt * kGN + rank * (kGN / 2)), "r"(s_u32(&full[s])),
-              "h"(static_cast<uint16_t>(0x3))
+              "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+              "[%1, {%2, %3}], [%4];" ::"r"(s_u32(sb)),
+              "l"(&tmap_b), "r"(kb * kGK), "r"(ti.nt * kGN + rank * (kGN / 2)), "r"(bar)
               : "memory");
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ===== MMA issuer
+    if (lane == 0 && rank == 0) {  // ===== MMA issuer (the pair's leader)
       uint32_t q = 0;
       int j = 0;
       for (int64_t u = cid; u < pair_tiles; u += C, ++j) {
@@ -227,20 +239,22 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
             const uint32_t acc = (kb | k) != 0 ? 1u : 0u;
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_cols),
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(acc_cols),
                 "l"(da), "l"(db), "r"(kIdesc), "r"(acc)
                 : "memory");
           }
-          // the stage (this CTA's A and its copy of B) is free in both CTAs once these MMAs have read it
+          // the stage is free in both CTAs once these MMAs have read it
           asm volatile(
-              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
                   s_u32(&empty[s])),
               "h"(static_cast<uint16_t>(0x3))
               : "memory");
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         s_u32(&tmem_full[a]))
-                     : "memory");
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                s_u32(&tmem_full[a])),
+            "h"(static_cast<uint16_t>(0x3))
+            : "memory");
       }
     }
   } else {
@@ -316,8 +330,12 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&tmem_empty[a])) : "memory");
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&info_free[a])) : "memory");
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                         map_to_rank(s_u32(&tmem_empty[a]), 0))
+                     : "memory");
+      }
     }
   }
   if (tid == kGRoles) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // y written before exit
@@ -325,7 +343,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   cluster_sync_all();  // no CTA leaves while its partner may still multicast into it
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
 }
 
 }  // namespace
