@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  cluster_sync_all();  // the partner's barriers exist before any multicast signals them
+  __syncthreads();     // the allocator's write of s_tmem is visible to the CTA
+  cluster_sync_all();  // the partner's barriers exist before any TMA or commit signals them
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
   const int nk = p.K / kGK;

@@ -20,11 +20,11 @@ def _sanitizer():
     pytest.fail("compute-sanitizer not found")
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_sanitizer_clean(tool):
     r = subprocess.run([_sanitizer(), "--tool", tool, "--error-exitcode", "3", sys.executable,
                         os.path.join(ROOT, "tools", "sanitize_probe.py")], cwd=ROOT, capture_output=True, text=True,
-                       timeout=900)
+                       timeout=900, env=dict(os.environ, AF_SANITIZE_TOOL=tool))
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-3000:]
     assert "sanitize probe done" in out
