@@ -353,9 +353,10 @@ AF_API af_status af_ctx_read_record(af_ctx *ctx, int32_t interval, af_decision *
  * decision (ordering tests). */
 #define AF_DEBUG_TAIL_DELAY_NS 1
 /* AF_DEBUG_PEERS_ARRIVED (0/1): with peers registered, the interval end pushes
- * its row and epoch to every peer but does not wait for theirs -- times ONE rank's
- * interval end on a single GPU (the other ranks' contexts registered locally,
- * never launched).  The decision then uses whatever rows the peers hold. */
+ * its row to every peer and reads every peer's words once without waiting for
+ * the epoch -- times ONE rank's interval end on a single GPU (the other ranks'
+ * contexts registered locally, never launched).  The decision then uses
+ * whatever rows the peers' buffers hold. */
 #define AF_DEBUG_PEERS_ARRIVED 2
 AF_API af_status af_ctx_set_debug(af_ctx *ctx, int32_t key, int64_t value);
 

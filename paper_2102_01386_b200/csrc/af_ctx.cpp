@@ -312,11 +312,15 @@ af_status af_ctx_bind(af_ctx *c, void *accum_dev, void *scratch_dev) {
   }
   AF_CUDA(cudaMemcpy(c->scratch + c->o_pool, c->pool_seg.data(), c->pool_seg.size() * 4, cudaMemcpyHostToDevice),
           "cudaMemcpy(pool_seg)");
-  {  // every partial slot starts empty (the finalize waits for non-empty slots)
+  {  // every partial and piece slot starts empty (the finalize waits for non-empty slots)
     const std::vector<unsigned long long> empty(c->ts[1].tiles.size(), kPartialEmpty);
     if (!empty.empty())
       AF_CUDA(cudaMemcpy(c->scratch + c->o_part, empty.data(), empty.size() * 8, cudaMemcpyHostToDevice),
               "cudaMemcpy(partials)");
+    const std::vector<unsigned long long> empty2(static_cast<size_t>(c->ts[1].max_tiles) / kFinChunk + c->L + 2,
+                                                 kPartialEmpty);
+    AF_CUDA(cudaMemcpy(c->scratch + c->o_part2, empty2.data(), empty2.size() * 8, cudaMemcpyHostToDevice),
+            "cudaMemcpy(pieces)");
   }
   AF_CUDA(cudaDeviceSynchronize(), "bind");
   c->bound = true;

@@ -583,6 +583,9 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Su
   // the decision's state inputs: in flight during the sums and the exchange
   DecideIn din{};
   if (p.fuse_decide) din = decide_load(p.dec);
+  // the peers' exchange-buffer pointers, likewise loaded ahead (one per rank)
+  __shared__ unsigned long long *s_peer[AF_MAX_WORLD];
+  if (p.xworld > 1 && p.end && tid < p.xworld) s_peer[tid] = p.peer_rows[tid];
   if (p.dbg_tail_delay_ns) {  // AF_DEBUG_TAIL_DELAY_NS (ordering tests only)
     if (tid == 0) {
       const unsigned long long t0 = gtimer();
@@ -640,14 +643,16 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Su
       const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(ss_row[l]));
       const unsigned long long lo = (bits & 0xFFFFFFFFull) | (static_cast<unsigned long long>(e32) << 32);
       const unsigned long long hi = (bits >> 32) | (static_cast<unsigned long long>(e32) << 32);
-      asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p.peer_rows[q] + 2 * (my + l)), "l"(lo),
+      asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(s_peer[q] + 2 * (my + l)), "l"(lo),
                    "l"(hi)
                    : "memory");
     }
     __shared__ int s_timeout;
     if (tid == 0) s_timeout = 0;
     __syncthreads();
-    if (!p.dbg_peers_arrived) {
+    {
+      // (AF_DEBUG_PEERS_ARRIVED: one read of every word, whatever epoch it holds --
+      // the real path's work without the wait, for one-GPU timing of a rank)
       for (int i = tid; i < W * L; i += kNormBlock) {
         const int q = i / L, l = i % L;
         if (q == p.xrank) continue;
@@ -656,11 +661,11 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Su
         for (long long spin = 0;; ++spin) {
           asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(w) : "memory");
           const uint32_t f0 = static_cast<uint32_t>(lo >> 32), f1 = static_cast<uint32_t>(hi >> 32);
-          if (f0 == kPoisonEpoch32 || f1 == kPoisonEpoch32) {  // that peer timed out: fail together
+          if ((f0 == kPoisonEpoch32 || f1 == kPoisonEpoch32) && !p.dbg_peers_arrived) {  // that peer timed out
             s_timeout = 1;
             break;
           }
-          if (f0 == e32 && f1 == e32) {
+          if ((f0 == e32 && f1 == e32) || p.dbg_peers_arrived) {
             const double v = __longlong_as_double(static_cast<long long>((lo & 0xFFFFFFFFull) | (hi << 32)));
             p.ss_out[static_cast<ptrdiff_t>(q - p.xrank) * L + l] = v;
             if (W * L <= kFinChunk) s_x[i] = v;
@@ -680,19 +685,19 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Su
       for (int i = tid; i < W * L; i += kNormBlock) {
         const int q = i / L, l = i % L;
         if (q == p.xrank) continue;
-        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %1};" ::"l"(p.peer_rows[q] + 2 * (my + l)), "l"(poison)
+        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %1};" ::"l"(s_peer[q] + 2 * (my + l)), "l"(poison)
                      : "memory");
       }
       if (tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 1u);
     }
-    if (!s_timeout && !p.dbg_peers_arrived && W * L <= kFinChunk && tid < L) {
+    if (!s_timeout && W * L <= kFinChunk && tid < L) {
       // the rank-order sum the decision takes (the decide kernel's order: 0 + row_0 + ...)
       double tot = 0.0;
       for (int q = 0; q < W; ++q) tot = __dadd_rn(tot, q == p.xrank ? s_ss[tid] : s_x[q * L + tid]);
       s_ss[tid] = tot;
       ss_in_smem = true;
     }
-    ss_in_smem = ss_in_smem && !s_timeout && !p.dbg_peers_arrived && W * L <= kFinChunk;
+    ss_in_smem = ss_in_smem && !s_timeout && W * L <= kFinChunk;
   }
   if (AF_TIMING) {
     __syncthreads();
@@ -708,23 +713,44 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Su
   }
 }
 
-// Tail of the streaming kernels: each segment's sum from the finalize's chunk
-// pieces -- segment l's active tiles span chunks [c_lo, c_hi] (chunk c = tiles
-// first_tile + [c*kFinChunk, (c+1)*kFinChunk)), whose pieces of l sit at
-// part2[c + l]; summed in chunk order by one thread per segment.  The pieces
-// (n_chunks + L of them) are staged in shared memory with one coalesced round
-// trip when they fit s_p.
+// Wait until an 8-byte slot no longer holds the sentinel; re-arm it; return it.
+__device__ __forceinline__ double take_slot(unsigned long long *slot) {
+  unsigned long long v;
+  for (;;) {
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slot) : "memory");
+    if (v != kPartialEmpty) break;
+  }
+  *slot = kPartialEmpty;  // re-armed for the next launch
+  return __longlong_as_double(static_cast<long long>(v));
+}
+
+// Tail of the streaming kernels, run by the CTA that claimed the last chunk:
+// each segment's sum from the chunk pieces -- segment l's active tiles span
+// chunks [c_lo, c_hi] (chunk c = tiles first_tile + [c*kFinChunk, (c+1)*kFinChunk)),
+// whose pieces of l sit at part2[c + l]; summed in chunk order by one thread per
+// segment.  Every index of part2[0, n_pc) is written exactly once per launch (the
+// pieces, and zeros in the gaps between chunks' index ranges), so the tail
+// simply waits for all n_pc slots (one wait per thread, in parallel) instead of
+// a completion counter; they are staged in shared memory when they fit s_p.
 template <int MODE, bool ACT>
 __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, int n_end, int f, double *s_p) {
   const int32_t *stb = seg_ranges<ACT>(p, f);
   const int tid = threadIdx.x;
   const int nch = n_end > first_tile ? (n_end - first_tile + kFinChunk - 1) / kFinChunk : 0;
-  const int n_pc = nch + p.L;
+  const int n_pc = nch > 0 ? nch - 1 + p.tiles[n_end - 1].seg + 1 : 0;  // last index: (nch-1) + seg(last tile)
   const bool staged = n_pc <= kFinChunk;
+  auto *slots = reinterpret_cast<unsigned long long *>(p.part2);
   if (staged) {
-    for (int i = tid; i < n_pc; i += kNormBlock) s_p[i] = __ldcg(p.part2 + i);
-    __syncthreads();
+    for (int i = tid; i < n_pc; i += kNormBlock) s_p[i] = take_slot(slots + i);
+  } else {
+    for (int i = tid; i < n_pc; i += kNormBlock) {  // wait for every slot; read them again below
+      unsigned long long v;
+      do {
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slots + i) : "memory");
+      } while (v == kPartialEmpty);
+    }
   }
+  __syncthreads();
   tail_common<MODE>(p, s_p, [&](auto &publish) {
     for (int l = tid; l < p.L; l += kNormBlock) {
       int tb = stb[l];
@@ -743,6 +769,10 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
       publish(l, sum);
     }
   });
+  if (!staged) {  // re-arm every slot (all were read above)
+    __syncthreads();
+    for (int i = tid; i < n_pc; i += kNormBlock) slots[i] = kPartialEmpty;
+  }
 }
 
 template <bool ACT>
@@ -889,7 +919,10 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
   }
   if constexpr (PARTIALS) {
     constexpr int TM = (MODE == kAdamEnd || MODE == kRsEnd || MODE == kRsAdamEnd) ? kEndDelta : MODE;
-    if (tail) last_cta_tail<TM, ACT>(p, first_tile, n_end, ACT ? f : 0, s_fin);
+    if (tail) {
+      if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->dmark[7] = gtimer();  // finalize done
+      last_cta_tail<TM, ACT>(p, first_tile, n_end, ACT ? f : 0, s_fin);
+    }
   }
 }
 
@@ -900,14 +933,16 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
 // chunks are complete) and reduces each: every thread takes one tile's partial,
 // waiting until it is no longer the sentinel (kPartialEmpty -- the partial's
 // plain 8-byte store is its own ready flag, so the streaming loop needs no fence
-// or counter per tile), re-arms the slot for the next launch, and each segment's
-// piece of the chunk is summed by one warp in tile order (lane-strided, xor
-// tree) into part2[c + l] (piece (c, l) is the (c+l)-th piece in tile order, so
-// the index needs no search).  The CTA that completes the last chunk returns
-// true and runs the tail (segment sums in chunk order, exchange, decision).
-// Deterministic: the reduction order depends only on the tile table.  Cannot
-// deadlock: a claimed tile belongs to a running CTA, which writes its partial
-// without waiting on anything.
+// or counter per tile), re-arms the slot, and each segment's piece of the chunk
+// is summed by one warp in tile order (lane-strided, xor tree) into part2[c + l]
+// (piece (c, l) is the (c+l)-th piece in tile order, so the index needs no
+// search); the indices between this chunk's pieces and the next chunk's get
+// zeros, so part2[0, n_pc) is written exactly once.  The CTA that claims the LAST
+// chunk (claim order) returns true and runs the tail, which waits for every
+// piece slot -- no completion counter, no fence.  Deterministic: the reduction
+// order depends only on the tile table.  Cannot deadlock: a claimed tile belongs
+// to a running CTA, which writes its partial without waiting on anything, and
+// every chunk is claimed by a CTA that finishes it without waiting on the tail.
 template <bool ACT>
 __device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int n_end, int f, double *s_p) {
   const int32_t *stb = seg_ranges<ACT>(p, f);
@@ -920,6 +955,7 @@ __device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int
     if (tid == 0) {
       const int w = static_cast<int>(atomicAdd(&p.fin_sched->next, 1u));
       s_c = w < nch ? (p.reverse ? nch - 1 - w : w) : -1;
+      if (w == nch - 1) s_tail = 1;
     }
     __syncthreads();
     const int c = s_c;
@@ -929,18 +965,11 @@ __device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int
 #pragma unroll
     for (int u = 0; u < kFinChunk / kNormBlock; ++u) {
       const int k = u * kNormBlock + tid;
-      if (k < n) {
-        unsigned long long v;
-        for (;;) {
-          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slots + c0 + k) : "memory");
-          if (v != kPartialEmpty) break;
-          __nanosleep(32);
-        }
-        s_p[k] = __longlong_as_double(static_cast<long long>(v));
-        slots[c0 + k] = kPartialEmpty;  // re-armed for the next launch
-      }
+      if (k < n) s_p[k] = take_slot(slots + c0 + k);
     }
     const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
+    // the next chunk's first segment (or, for the last chunk, none): zeros fill the gap
+    const int lN = c0 + n < n_end ? p.tiles[c0 + n].seg + 1 : lB + 1;
     __syncthreads();
     for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {
       int a = stb[l], b = stb[l + 1];
@@ -952,17 +981,13 @@ __device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int
       sum = warp_sum(sum);
       if (lane == 0) p.part2[c + l] = sum;
     }
-    __syncthreads();  // the pieces are written; s_p is free again
-    if (tid == 0) {
-      __threadfence();  // this chunk's pieces before its completion count
-      if (atomicAdd(&p.fin_sched->done, 1u) == static_cast<unsigned int>(nch - 1)) {
-        s_tail = 1;
-        p.fin_sched->done = 0u;  // every chunk counted: nobody else touches it in this launch
-      }
-    }
+    // zero pieces: indices [c + lB + 1, (c + 1) + lN - 1) between this chunk's and the
+    // next chunk's ranges, and [0, lA) before the first chunk's
+    for (int i = c + lB + 1 + tid; i < c + lN; i += kNormBlock) p.part2[i] = 0.0;
+    if (c == 0)
+      for (int i = tid; i < lA; i += kNormBlock) p.part2[i] = 0.0;
+    __syncthreads();  // s_p is free again
   }
-  __syncthreads();
-  if (s_tail) __threadfence();  // every other chunk's pieces are visible
   return s_tail != 0;
 }
 

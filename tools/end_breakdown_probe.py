@@ -72,6 +72,8 @@ def main():
             ends = list(dm[1:7]) + [t[3]]
             for k, nm in enumerate(names):
                 row[nm + "_us"] = (ends[k] - dm[k]) / 1e3
+            row["last_chunk_us"] = (dm[7] - t[1]) / 1e3       # last tile done -> its chunk reduced + counted
+            row["tail_sums_xchg_us"] = (t[2] - dm[7]) / 1e3   # pieces staged, segment sums, exchange
             rows.append(row)
         rows = rows[3:]
         med = {k: round(statistics.median(r[k] for r in rows), 2) for k in rows[0]}
