@@ -46,8 +46,24 @@ def run(epochs=4, small=False, seed=0, verbose=True):
     rate = torch.tensor(np.linspace(0.55, 0.97, lay.n_segments), device="cuda", dtype=torch.float32)
     rng = torch.Generator(device="cuda")
     rng.manual_seed(seed)
-    t_layer = 0.011                       # the caller's measured per-block forward time (P:234 uses 11 ms)
-    t_read = af.calibrate_read_seconds(hidden_bytes, batch)
+    # both sides of the cache-vs-recompute rule measured here: one block's
+    # forward (a BERT-base-shaped stand-in: 768 -> 3072 -> 768 on batch x 128 tokens)
+    # and one batch's cache read
+    tokens = batch * (16 if small else 128)
+    x = torch.randn(tokens, 768, device="cuda", dtype=torch.bfloat16)
+    w1 = torch.randn(3072, 768, device="cuda", dtype=torch.bfloat16) * 0.02
+    w2 = torch.randn(768, 3072, device="cuda", dtype=torch.bfloat16) * 0.02
+    cal = af.calibrate_should_cache(lambda: torch.nn.functional.linear(torch.nn.functional.gelu(
+        torch.nn.functional.linear(x, w1)), w2), hidden_bytes, batch, max_layers=lay.n_segments)
+    t_layer, t_read = cal["t_layer_fwd_s"], cal["t_batch_read_s"]
+    if verbose:
+        print(f"calibrated: block forward {t_layer * 1e6:.0f} us, batch read {t_read * 1e6:.0f} us, caching pays "
+              f"from {cal['min_frozen_layers']} frozen blocks")
+    # the first active block's QKV projection (768 -> 2304); with 128 x 768 bf16 records the
+    # cached rows feed it straight from the store (NEXT 4: no batch copy)
+    fused_gemm = hidden_bytes == 128 * 768 * 2
+    w_qkv = torch.randn(2304, 768, device="cuda", dtype=torch.bfloat16) * 0.02
+    qkv = torch.empty(batch * 128, 2304, device="cuda", dtype=torch.bfloat16) if fused_gemm else None
     frozen, trace, hits = 0, [], 0
     step = 0
     for epoch in range(epochs):
@@ -60,7 +76,10 @@ def run(epochs=4, small=False, seed=0, verbose=True):
             depth = torch.empty(batch, dtype=torch.int32, device="cuda")
             use_cache = frozen > 0 and af.should_cache(frozen, t_layer, t_read)
             if use_cache:
-                cache.get(ids, frozen, rows, depth)
+                if fused_gemm:   # get + the first active layer's projection in one kernel
+                    cache.get_gemm(ids, frozen, w_qkv, qkv, depth, 128)
+                else:
+                    cache.get(ids, frozen, rows, depth)
                 hits += int((depth >= 0).sum())
             # ... forward from each example's depth, backward through the active blocks ...
             decay = rate ** (step / interval)
