@@ -162,15 +162,18 @@ af_status af_ctx_create(const af_layout *layout, const af_config *cfg, af_ctx **
     T.seg_tile_begin.assign(static_cast<size_t>(n_tab) * (L + 1), 0);
     for (int q = 0; q < n_tab; ++q) {
       const int64_t sb = c->sb_of_f[q], se = c->se_of_f[q];
-      const int64_t big_until = sb + (se - sb) / 100 * AF_TILE_BIG_FRAC_PCT;
-      const int64_t TB = (k == 1) ? TE * AF_TILE_BIG_MULT : TE;
+      // interval-end tables: smaller tiles over AF_TILE_TAPER_PCT % of the range at
+      // EACH end (consecutive launches walk the tiles in opposite directions, so a
+      // launch's last tiles are at one end or the other) -- a shorter ragged finish
+      const int64_t taper = (k == 1) ? (se - sb) / 100 * AF_TILE_TAPER_PCT : 0;
+      const int64_t TS = std::max<int64_t>(TE / AF_TILE_TAPER_DIV, 1024);
       int32_t *stb = T.seg_tile_begin.data() + static_cast<size_t>(q) * (L + 1);
       const int32_t t0 = static_cast<int32_t>(T.tiles.size());
       for (int l = 0; l < L; ++l) {
         stb[l] = static_cast<int32_t>(T.tiles.size());
         const int64_t lo = std::max(c->offs[l], sb), hi = std::min(c->offs[l + 1], se);
         for (int64_t pos = lo; pos < hi;) {
-          const int64_t te = (pos < big_until) ? TB : TE;
+          const int64_t te = (pos < sb + taper || pos >= se - taper) ? TS : TE;
           const int64_t nxt = std::min(hi, (pos / te + 1) * te);
           T.tiles.push_back(Tile{pos, nxt, l, stb[l], 0, 0});
           pos = nxt;

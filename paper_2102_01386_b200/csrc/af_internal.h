@@ -19,11 +19,11 @@ constexpr int kNormBlock = 256;          // threads per CTA of the streaming ker
 #ifndef AF_TILE_ELEMS_BF16  // 24576: BERT-base interval end -0.8 us in the step vs 16384, 12288 +9 us
 #define AF_TILE_ELEMS_BF16 24576  // (profiles/r01_v59_variants_end_tiles_bf16.jsonl)
 #endif
-#ifndef AF_TILE_BIG_MULT  // interval-end tiles are this much larger in the bulk of the shard
-#define AF_TILE_BIG_MULT 1  // tapering measured slower (profiles/r01_v10_variants_taper.jsonl): off
+#ifndef AF_TILE_TAPER_PCT  // interval-end tiles: % of each table's range, at EACH end, cut into
+#define AF_TILE_TAPER_PCT 0   // tiles AF_TILE_TAPER_DIV times smaller (0: uniform tiles)
 #endif
-#ifndef AF_TILE_BIG_FRAC_PCT
-#define AF_TILE_BIG_FRAC_PCT 85
+#ifndef AF_TILE_TAPER_DIV
+#define AF_TILE_TAPER_DIV 4
 #endif
 #ifndef AF_TILE_SSQ_F32  // STEP_SUMSQ reads only g (s_g bytes per element): larger tiles in
 #define AF_TILE_SSQ_F32 32768  // elements keep the per-tile fixed costs small
