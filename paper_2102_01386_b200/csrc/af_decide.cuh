@@ -37,6 +37,7 @@ struct DecideIn {
   int T, f;
   double pv;
   const int *pool;  // shared memory, [n_pool]
+  uint32_t sticky;  // state->sticky (the caller ORs in what its own kernel flagged since)
 };
 static __device__ __forceinline__ DecideIn decide_load(const DecideParams &p) {
   __shared__ int s_pool[AF_MAX_SEGMENTS];
@@ -45,6 +46,7 @@ static __device__ __forceinline__ DecideIn decide_load(const DecideParams &p) {
   in.T = p.state->T;
   in.f = p.state->f;
   in.pv = (t < p.L) ? p.state->prev[t] : 0.0;
+  in.sticky = *reinterpret_cast<const volatile uint32_t *>(&p.state->sticky);
   if (t < p.n_pool) s_pool[t] = p.pool_seg[t];
   in.pool = s_pool;
   return in;  // (s_pool is read after the caller's next __syncthreads)
@@ -99,7 +101,7 @@ static __device__ __noinline__ void decide_block(const DecideParams &p, const do
   AF_DMARK(2);
 
   // a peer never arrived: at the exchange (bit 0) or at a fused reduce-scatter barrier (bit 1)
-  const bool xfail = (p.state->sticky & 3u) != 0u;
+  const bool xfail = (in.sticky & 3u) != 0u;
   const bool nonfinite = s_nonfinite != 0 || xfail;
   unsigned int flags = p.commit ? 0u : AF_DEC_DRY_RUN;
   if (xfail) flags |= AF_DEC_EXCHANGE_TIMEOUT;

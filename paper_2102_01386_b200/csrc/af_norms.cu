@@ -67,6 +67,9 @@
 #ifndef AF_MINB_END_BF16  // bf16 interval end / STEP_SUMSQ: min resident CTAs per SM (register cap)
 #define AF_MINB_END_BF16 1
 #endif
+#ifndef AF_STATIC_FIRST  // each CTA's first two tiles by its index instead of the scheduler's atomic
+#define AF_STATIC_FIRST 1
+#endif
 #ifndef AF_U_RS_VEC  // fused reduce-scatter: gradient vectors in flight per thread (over all ranks)
 #define AF_U_RS_VEC 8
 #endif
@@ -577,15 +580,42 @@ __device__ __forceinline__ int table_end(const NormParams &p, int f) {
 // publish(l, s) for every segment l), the optional NVLink one-shot exchange and
 // the fused decision.  Every thread of the CTA calls it.
 // s_x: >= kFinChunk doubles of shared scratch (the peers' rows when world x L fits).
-template <int MODE, typename SumFn>
-__device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, SumFn sums) {
+// What the tail reads from global memory besides the sums, issued before the
+// tail waits for anything (the last chunk's tiles are still streaming then):
+// the decision's state inputs, the exchange epoch, the sticky timeout bits and
+// (into s_peer) the peers' exchange-buffer pointers.
+__shared__ unsigned long long *s_peer[AF_MAX_WORLD];
+struct TailPre {
+  DecideIn din;
+  unsigned long long epoch;  // thread 0
+  uint32_t sticky;
+};
+// count_done: the CTA running the tail before its grid-completion count (every
+// mode but the fused reduce-scatter) counts itself here, from its last warp,
+// while the tail waits for the last partials -- the scheduler resets (by
+// whichever CTA counts last) then stay off the path after the decision.
+__device__ __forceinline__ TailPre tail_prefetch(const NormParams &p, bool count_done) {
   const int tid = threadIdx.x;
-  // the decision's state inputs: in flight during the sums and the exchange
-  DecideIn din{};
-  if (p.fuse_decide) din = decide_load(p.dec);
-  // the peers' exchange-buffer pointers, likewise loaded ahead (one per rank)
-  __shared__ unsigned long long *s_peer[AF_MAX_WORLD];
+  TailPre pre{};
+  if (p.fuse_decide) pre.din = decide_load(p.dec);
   if (p.xworld > 1 && p.end && tid < p.xworld) s_peer[tid] = p.peer_rows[tid];
+  if (tid == 0) pre.epoch = *reinterpret_cast<const volatile unsigned long long *>(&p.state->epoch);
+  pre.sticky = sticky_of(p);
+  if (count_done && tid == kNormBlock - 32) {
+    __threadfence();
+    if (atomicAdd(&p.sched->done, 1u) == gridDim.x - 1) {
+      __threadfence();
+      p.sched->next = 0;
+      p.sched->done = 0;
+      p.fin_sched->next = 0u;
+    }
+  }
+  return pre;  // (s_peer / the decision's s_pool are read after the caller's next __syncthreads)
+}
+
+template <int MODE, typename SumFn>
+__device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, TailPre pre, SumFn sums) {
+  const int tid = threadIdx.x;
   if (p.dbg_tail_delay_ns) {  // AF_DEBUG_TAIL_DELAY_NS (ordering tests only)
     if (tid == 0) {
       const unsigned long long t0 = gtimer();
@@ -600,9 +630,8 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Su
   __shared__ unsigned long long s_epoch;
   if (xchg) {
     if (tid == 0) {
-      DevState *st = const_cast<DevState *>(p.state);
-      s_epoch = st->epoch + 1ull;
-      st->epoch = s_epoch;
+      s_epoch = pre.epoch + 1ull;
+      const_cast<DevState *>(p.state)->epoch = s_epoch;
     }
     __syncthreads();
   }
@@ -623,7 +652,7 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Su
   };
   sums(publish);
   bool ss_in_smem = !xchg;  // world 1: the own row is the sum
-  if (xchg && (sticky_of(p) & 3u)) {
+  if (xchg && (pre.sticky & 3u)) {
     // an earlier exchange or barrier timed out (sticky until af_set_state): no peer
     // stores any more; the peers time out on this rank and flag it as well
   } else if (xchg) {
@@ -689,6 +718,7 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Su
                      : "memory");
       }
       if (tid == 0) atomicOr(const_cast<uint32_t *>(&p.state->sticky), 1u);
+      pre.sticky |= 1u;  // (s_timeout is CTA-uniform)
     }
     if (!s_timeout && W * L <= kFinChunk && tid < L) {
       // the rank-order sum the decision takes (the decide kernel's order: 0 + row_0 + ...)
@@ -705,6 +735,8 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Su
   }
   if (p.fuse_decide) {
     __syncthreads();
+    DecideIn din = pre.din;
+    din.sticky = pre.sticky;
     decide_block(p.dec, ss_in_smem ? s_ss : nullptr, din);
   }
   if (AF_TIMING) {
@@ -733,12 +765,14 @@ __device__ __forceinline__ double take_slot(unsigned long long *slot) {
 // simply waits for all n_pc slots (one wait per thread, in parallel) instead of
 // a completion counter; they are staged in shared memory when they fit s_p.
 template <int MODE, bool ACT>
-__device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, int n_end, int f, double *s_p) {
+__device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, int n_end, int f, double *s_p,
+                                          bool count_done) {
   const int32_t *stb = seg_ranges<ACT>(p, f);
   const int tid = threadIdx.x;
   const int nch = n_end > first_tile ? (n_end - first_tile + kFinChunk - 1) / kFinChunk : 0;
   const int n_pc = nch > 0 ? nch - 1 + p.tiles[n_end - 1].seg + 1 : 0;  // last index: (nch-1) + seg(last tile)
   const bool staged = n_pc <= kFinChunk;
+  const TailPre pre = tail_prefetch(p, count_done);
   auto *slots = reinterpret_cast<unsigned long long *>(p.part2);
   if (staged) {
     for (int i = tid; i < n_pc; i += kNormBlock) s_p[i] = take_slot(slots + i);
@@ -751,7 +785,7 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
     }
   }
   __syncthreads();
-  tail_common<MODE>(p, s_p, [&](auto &publish) {
+  tail_common<MODE>(p, s_p, pre, [&](auto &publish) {
     for (int l = tid; l < p.L; l += kNormBlock) {
       int tb = stb[l];
       tb = tb < first_tile ? first_tile : tb;
@@ -775,8 +809,73 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
   }
 }
 
+// The tail when the pieces fit shared memory (n_pc <= kFinChunk: every table up
+// to 65k tiles), run by the CTA that claimed the last chunk c -- before that
+// chunk's tiles have finished.  Everything the tail reads besides the sums is
+// loaded first (segment ranges, the chunk's segments, the decision's inputs,
+// the exchange epoch and peer pointers); then the other chunks' pieces are
+// taken (those chunks finish first), then chunk c's own tile partials.  Chunk c
+// is reduced straight into the staged pieces (its pieces never go through
+// part2: those slots stay armed), so after the grid's last tile the path is:
+// one partial's visibility, a shared-memory reduction, the segment sums, the
+// exchange and the decision.
+template <int MODE, bool ACT>
+__device__ __noinline__ void last_cta_tail_staged(const NormParams &p, int first_tile, int n_end, int f, int c,
+                                                  int n_pc, double *s_p, bool count_done) {
+  const int32_t *stb = seg_ranges<ACT>(p, f);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double s_pc[kFinChunk];
+  __shared__ int s_stb[AF_MAX_SEGMENTS + 1];
+  const int L = p.L;
+  for (int l = tid; l <= L; l += kNormBlock) s_stb[l] = stb[l];
+  const int c0 = first_tile + c * kFinChunk;
+  const int n = min(kFinChunk, n_end - c0);
+  const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
+  const int lN = c0 + n < n_end ? p.tiles[c0 + n].seg + 1 : lB + 1;
+  const TailPre pre = tail_prefetch(p, count_done);
+  // the other chunks' pieces: every index of [0, n_pc) outside chunk c's own
+  // ([c + lA, c + lN), and [0, lA) for chunk 0)
+  auto *slots = reinterpret_cast<unsigned long long *>(p.part2);
+  const bool own = (tid >= c + lA && tid < c + lN) || (c == 0 && tid < lA);
+  if (tid < n_pc && !own) s_pc[tid] = take_slot(slots + tid);
+  if (tid < n) s_p[tid] = take_slot(reinterpret_cast<unsigned long long *>(p.partials) + c0 + tid);
+  __syncthreads();
+  for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {  // chunk c's pieces, as fin_worker forms them
+    int a = s_stb[l], b = s_stb[l + 1];
+    a = (a < c0 ? c0 : a) - c0;
+    b = (b > c0 + n ? c0 + n : b) - c0;
+    double sum = 0.0;
+#pragma unroll 8
+    for (int k = a + lane; k < b; k += 32) sum += s_p[k];
+    sum = warp_sum(sum);
+    if (lane == 0) s_pc[c + l] = sum;
+  }
+  for (int i = c + lB + 1 + tid; i < c + lN; i += kNormBlock) s_pc[i] = 0.0;
+  if (c == 0)
+    for (int i = tid; i < lA; i += kNormBlock) s_pc[i] = 0.0;
+  __syncthreads();
+  tail_common<MODE>(p, s_p, pre, [&](auto &publish) {
+    for (int l = tid; l < L; l += kNormBlock) {
+      int tb = s_stb[l];
+      tb = tb < first_tile ? first_tile : tb;
+      const int te = s_stb[l + 1];
+      double sum = 0.0;
+      if (te > tb) {
+        const int c_lo = (tb - first_tile) / kFinChunk, c_hi = (te - 1 - first_tile) / kFinChunk;
+        for (int q = c_lo; q <= c_hi; ++q) sum += s_pc[q + l];
+      }
+      publish(l, sum);
+    }
+  });
+}
+
+// fin_worker's verdict: not the tail, the tail with every piece in part2, or
+// (>= 0) the tail of the staged form with its own chunk still to reduce
+constexpr int kNoTail = -1, kTailUnstaged = -2;
+
 template <bool ACT>
-__device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int n_end, int f, double *s_p);
+__device__ __noinline__ int fin_worker(const NormParams &p, int first_tile, int n_end, int f, double *s_p,
+                                       int *n_pc_out);
 
 template <int MODE, typename GT, bool RD, int PM = 1, bool ACT = false>
 __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccum)
@@ -792,12 +891,24 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
   __shared__ int s_last;
   __shared__ unsigned long long s_rs_epoch;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // Speculative prologue, before the dependency wait: the boundary f as the
+  // predecessor found it (it changes at most once per interval), its table
+  // bounds and this CTA's first tile descriptor (the table is immutable).  After
+  // the wait f is read again; the speculation is used only if it matches.
+  auto clamp_f = [&](int x) { return x < 0 ? 0 : (x > p.n_pool ? p.n_pool : x); };
+  const int f_spec = clamp_f(*reinterpret_cast<const volatile int32_t *>(&p.state->f));
+  const int ft_spec = p.first_tile_of_f[f_spec];
+  const int ne_spec = table_end<ACT>(p, f_spec);
+  Tile d_spec{};
+  const int k_first = AF_STATIC_FIRST ? static_cast<int>(blockIdx.x) : 0;
+  const int t_spec = k_first < ne_spec - ft_spec ? (p.reverse ? ne_spec - 1 - k_first : ft_spec + k_first) : -1;
+  if (AF_STATIC_FIRST && tid == 0 && t_spec >= 0) d_spec = p.tiles[t_spec];
   pdl_wait();  // f, Delta and the counters are written by the preceding kernels
   if (AF_TIMING && blockIdx.x == 0 && threadIdx.x == 0) const_cast<DevState *>(p.state)->tmark[0] = gtimer();
-  int f = p.state->f;
-  f = f < 0 ? 0 : (f > p.n_pool ? p.n_pool : f);
-  const int first_tile = p.first_tile_of_f[f];
-  const int n_end = table_end<ACT>(p, f);  // static: the constant n_tiles
+  const int f = clamp_f(p.state->f);
+  const bool spec_ok = f == f_spec;
+  const int first_tile = spec_ok ? ft_spec : p.first_tile_of_f[f];
+  const int n_end = spec_ok ? ne_spec : table_end<ACT>(p, f);  // static: the constant n_tiles
   const GT *rs_g[PM];
   bool rs_skip = false;  // CTA-uniform: a barrier timed out -- no peer loads, no stores this step
   if constexpr (RS) {
@@ -831,11 +942,23 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
     if (kk >= n_act_tiles) return n_end;  // past the end: the loop's stop value
     return p.reverse ? n_end - 1 - kk : first_tile + kk;
   };
+  // AF_STATIC_FIRST: the first two tiles of CTA b are k = b and k = G + b (no
+  // atomic: 296 CTAs serialised on one counter cost the grid's start ~1 us); the
+  // counter hands out k = 2G, 2G + 1, ...
+  const unsigned int k_base = AF_STATIC_FIRST ? 2u * gridDim.x : 0u;
+  auto claim = [&]() { return tile_of(k_base + atomicAdd(&p.sched->next, 1u)); };
   if (tid == 0) {
-    const int t0 = tile_of(atomicAdd(&p.sched->next, 1u));
-    s_tile[0] = t0;
-    if (t0 < n_end) s_desc[0] = p.tiles[t0];
-    s_tile[1] = tile_of(atomicAdd(&p.sched->next, 1u));
+    if (AF_STATIC_FIRST) {
+      const int t0 = tile_of(static_cast<unsigned int>(k_first));
+      s_tile[0] = t0;
+      if (t0 < n_end) s_desc[0] = (spec_ok && t0 == t_spec) ? d_spec : p.tiles[t0];
+      s_tile[1] = tile_of(gridDim.x + blockIdx.x);
+    } else {
+      const int t0 = claim();
+      s_tile[0] = t0;
+      if (t0 < n_end) s_desc[0] = p.tiles[t0];
+      s_tile[1] = claim();
+    }
   }
   __syncthreads();
   for (int it = 0;; ++it) {
@@ -845,7 +968,7 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
     const Tile t = s_desc[slot];
     int next2 = 0;
     if (tid == 0) {
-      next2 = tile_of(atomicAdd(&p.sched->next, 1u));
+      next2 = claim();
       const int n1 = s_tile[slot1];
       if (n1 < n_end) {
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_desc[slot1]));
@@ -886,9 +1009,26 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
   pdl_launch_dependents();
   if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
   // finalize: a CTA out of tiles reduces chunks of partials while the grid's last
-  // tiles are still streaming; the finisher of the last chunk runs the tail
-  bool tail = false;
-  if constexpr (PARTIALS) tail = fin_worker<ACT>(p, first_tile, n_end, f, s_fin);
+  // tiles are still streaming; the claimer of the last chunk runs the tail --
+  // at once (it waits only on chunk pieces and tile partials, never on the other
+  // CTAs' exit), except for the fused reduce-scatter, whose tail follows the
+  // closing barrier on this rank's gradient
+  constexpr int TM = (MODE == kAdamEnd || MODE == kRsEnd || MODE == kRsAdamEnd) ? kEndDelta : MODE;
+  int tail = kNoTail, n_pc = 0;
+  if constexpr (PARTIALS) tail = fin_worker<ACT>(p, first_tile, n_end, f, s_fin, &n_pc);
+  auto run_tail = [&](bool count_done) {
+    if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->dmark[7] = gtimer();  // tail start
+    if (tail >= 0)
+      last_cta_tail_staged<TM, ACT>(p, first_tile, n_end, ACT ? f : 0, tail, n_pc, s_fin, count_done);
+    else
+      last_cta_tail<TM, ACT>(p, first_tile, n_end, ACT ? f : 0, s_fin, count_done);
+  };
+  if constexpr (PARTIALS && !RS) {
+    if (tail != kNoTail) {
+      run_tail(true);  // counts this CTA's completion itself
+      return;
+    }
+  }
 
   // grid completion: every CTA has finished its tiles and claimed its last chunk;
   // the last one resets the schedulers (and, fused reduce-scatter, closes the
@@ -914,15 +1054,11 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
       }
     }
     if constexpr (PARTIALS) {
-      if (n_end <= first_tile) tail = true;  // no active tile, no chunk: the last CTA publishes the zeros
+      if (n_end <= first_tile) tail = kTailUnstaged;  // no active tile, no chunk: the last CTA publishes the zeros
     }
   }
   if constexpr (PARTIALS) {
-    constexpr int TM = (MODE == kAdamEnd || MODE == kRsEnd || MODE == kRsAdamEnd) ? kEndDelta : MODE;
-    if (tail) {
-      if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->dmark[7] = gtimer();  // finalize done
-      last_cta_tail<TM, ACT>(p, first_tile, n_end, ACT ? f : 0, s_fin);
-    }
+    if (tail != kNoTail) run_tail(false);
   }
 }
 
@@ -944,32 +1080,40 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
 // to a running CTA, which writes its partial without waiting on anything, and
 // every chunk is claimed by a CTA that finishes it without waiting on the tail.
 template <bool ACT>
-__device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int n_end, int f, double *s_p) {
+__device__ __noinline__ int fin_worker(const NormParams &p, int first_tile, int n_end, int f, double *s_p,
+                                       int *n_pc_out) {
   const int32_t *stb = seg_ranges<ACT>(p, f);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nch = (n_end - first_tile + kFinChunk - 1) / kFinChunk;
-  __shared__ int s_c, s_tail;
-  if (tid == 0) s_tail = 0;
+  __shared__ int s_c, s_tail, s_npc;
   auto *slots = reinterpret_cast<unsigned long long *>(p.partials);
   for (;;) {
     if (tid == 0) {
       const int w = static_cast<int>(atomicAdd(&p.fin_sched->next, 1u));
       s_c = w < nch ? (p.reverse ? nch - 1 - w : w) : -1;
-      if (w == nch - 1) s_tail = 1;
+      s_tail = w == nch - 1;
+      // the last chunk's claimer runs the tail: staged in shared memory when the
+      // piece count fits (the pieces' last index: (nch - 1) + seg(last tile))
+      if (w == nch - 1) s_npc = nch - 1 + p.tiles[n_end - 1].seg + 1;
     }
     __syncthreads();
     const int c = s_c;
     if (c < 0) break;
+    if (s_tail && s_npc <= kFinChunk) {
+      *n_pc_out = s_npc;
+      return c;  // last_cta_tail_staged reduces chunk c itself
+    }
     const int c0 = first_tile + c * kFinChunk;
     const int n = min(kFinChunk, n_end - c0);
+    // the chunk's segments, loaded before its partials are awaited
+    const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
+    // the next chunk's first segment (or, for the last chunk, none): zeros fill the gap
+    const int lN = c0 + n < n_end ? p.tiles[c0 + n].seg + 1 : lB + 1;
 #pragma unroll
     for (int u = 0; u < kFinChunk / kNormBlock; ++u) {
       const int k = u * kNormBlock + tid;
       if (k < n) s_p[k] = take_slot(slots + c0 + k);
     }
-    const int lA = p.tiles[c0].seg, lB = p.tiles[c0 + n - 1].seg;
-    // the next chunk's first segment (or, for the last chunk, none): zeros fill the gap
-    const int lN = c0 + n < n_end ? p.tiles[c0 + n].seg + 1 : lB + 1;
     __syncthreads();
     for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {
       int a = stb[l], b = stb[l + 1];
@@ -986,9 +1130,11 @@ __device__ __noinline__ bool fin_worker(const NormParams &p, int first_tile, int
     for (int i = c + lB + 1 + tid; i < c + lN; i += kNormBlock) p.part2[i] = 0.0;
     if (c == 0)
       for (int i = tid; i < lA; i += kNormBlock) p.part2[i] = 0.0;
+    const bool was_last = s_tail != 0;
     __syncthreads();  // s_p is free again
+    if (was_last) return kTailUnstaged;  // every chunk is claimed: no further claim
   }
-  return s_tail != 0;
+  return kNoTail;
 }
 
 using NormKernel = void (*)(const NormParams);

@@ -312,6 +312,9 @@ def test_fake_sharded_parity(P):
     (40_000_003, 150, 1_000_001, 3_333, "f32", "delta", True),    # chunks span ~120 segments
     (80_000_003, 150, 1_000_001, 3_333, "bf16", "step_sumsq", False),   # STEP_SUMSQ tiles are 32768
     (36_000_001, 2, 17, 5, "f32", "delta", False),                # segments span many chunks
+    # more pieces (chunks + segments) than the tail stages in shared memory:
+    # the last chunk goes through part2 like the others (the unstaged tail)
+    (120_000_007, 250, 999_999, 4_097, "f32", "delta", True),
 ])
 def test_wide_finalize_parity(n, L, pre, head, dt, acc, fused):
     """Many finalize chunks (256 tiles each, reduced by the streaming grid's CTAs
@@ -321,7 +324,10 @@ def test_wide_finalize_parity(n, L, pre, head, dt, acc, fused):
     lay = uniform_layout(n, L, pre=pre, head=head)
     recs, _, fm, oz = run_both(lay, dt, _decaying_step(lay, dt, 41), [2, 1, 2, 1, 2, 1], check_delta=False,
                                fused=fused, acc_mode=acc)
-    assert fm.info()["n_fin_chunks"] > 1
+    info = fm.info()
+    assert info["n_fin_chunks"] > 1
+    if L == 250:
+        assert info["n_fin_chunks"] + L > 256  # the unstaged tail
     if L > 2:
         assert max(r[0]["boundary_after"] for r in recs) >= 1
 
