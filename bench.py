@@ -605,7 +605,8 @@ def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(6, 32, 256, 1024
     reps x [flush], divided by reps -- launches back to back, no event between calls
     (an event pair around one call adds a ~6 us floor; tools/cache_cold_probe.py)."""
     import torch
-    out = {"l2": "cold (512 MB read before each call, fresh ids per call)",
+    out = {"l2": "cold (512 MB read before each call, fresh ids per call); *_back_to_back: one 512 MB read, "
+                 "then the calls one after another (fresh ids per call, records cold)",
            "timing": "marginal device time per call in CUDA graphs (graph with calls minus graph without)"}
     B0 = rows.shape[0]
     big = rows.repeat((max(batches) + B0 - 1) // B0, 1)[: max(batches)].contiguous()
@@ -634,6 +635,30 @@ def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(6, 32, 256, 1024
                 t[w].append(a.elapsed_time(b))
         return (statistics.median(t[True]) - statistics.median(t[False])) / reps * 1e3
 
+    def marginal_b2b_us(fn):
+        # the epoch's regime (one call per batch, batch after batch):
+        # reps calls back to back after ONE flush, minus the flush alone, per call --
+        # each call's launch, ramp and drain overlap its neighbours' (PDL)
+        gs = {}
+        for w in (True, False):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                torch.sum(flush, dim=0, dtype=torch.float32, out=acc)
+                if w:
+                    for r in range(reps):
+                        fn(r)
+            gs[w] = g
+        t = {True: [], False: []}
+        for _ in range(iters):
+            for w in (True, False):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                gs[w].replay()
+                b.record()
+                torch.cuda.synchronize()
+                t[w].append(a.elapsed_time(b))
+        return (statistics.median(t[True]) - statistics.median(t[False])) / reps * 1e3
+
     for B in batches:
         if B > my_ids.numel():
             continue
@@ -644,9 +669,10 @@ def cache_sweep(cache, my_ids, rows, dev, world, dist, batches=(6, 32, 256, 1024
         res = {}
         for name, fn in (("put", lambda r: cache.put(id_sets[r], src, 4)),
                          ("get", lambda r: cache.get(id_sets[r], 4, dst, dep))):
-            us = marginal_us(fn)
-            gbs = 2 * B * ROW_BYTES / (us * 1e-6) / 1e9
-            res[name] = {"us": round(us, 2), "gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4)}
+            for key, meas in ((name, marginal_us), (name + "_back_to_back", marginal_b2b_us)):
+                us = meas(fn)
+                gbs = 2 * B * ROW_BYTES / (us * 1e-6) / 1e9
+                res[key] = {"us": round(us, 2), "gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4)}
         out[str(B)] = res
     del flush
     return out

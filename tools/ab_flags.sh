@@ -21,5 +21,9 @@ for side in ("A", "B"):
         except Exception as e:
             print(side, i, "ERR", e); continue
         s = d.get("secondary", {})
-        print(side, i, "large ms", d["ms_per_step"], "| base ms", s.get("ms_per_step"))
+        pl, ps = d.get("phases_in_step", {}), s.get("phases_in_step", {})
+        print(side, i, "large ms", d["ms_per_step"], "end", pl.get("grad_norm_decide", {}).get("ms"),
+              "acc", pl.get("accumulate", {}).get("ms"), "| base ms", s.get("ms_per_step"),
+              "end", ps.get("grad_norm_decide", {}).get("ms"), "acc", ps.get("accumulate", {}).get("ms"),
+              "eager end", s.get("grad_norm_decide_gbs"))
 PY
