@@ -333,8 +333,12 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
       __syncwarp();
       if (lane == 0) {
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&info_free[a])) : "memory");
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                         map_to_rank(s_u32(&tmem_empty[a]), 0))
+        // "accumulator drained" on the leader's barrier, default semantics (release at
+        // CTA scope): this warp's TMEM reads completed at tcgen05.wait::ld, before
+        // the arrive in program order, so the leader's next MMAs into these columns
+        // cannot overtake them; a .release.cluster arrive cost a GPU-wide MEMBAR
+        // per tile and warp (0.7 % of the kernel, profiles/r02/r02_v44_*)
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(map_to_rank(s_u32(&tmem_empty[a]), 0))
                      : "memory");
       }
     }
