@@ -452,6 +452,15 @@ def run_ours(args, rank, world, local):
         result["cpu_baseline_all_cores"] = cpu_baseline_all_cores(lay, dt, s_g, B)
     if world == 1 and not args.no_shard_probe and args.workload == "bert-large-f32":
         result["rank_shard_p8"] = rank_shard_probe(args, dev)
+        # the same emulation at P = 2 and 4 (one rank each): the per-GPU share of the
+        # 1/2/4/8-GPU metric on this GPU, exchange stores included, NVLink wait not
+        keep = ("n_local", "interval_end_alone_us", "frac_alone", "interval_end_in_step_us", "frac_in_step")
+        by_world = {}
+        for P in (2, 4):
+            row = rank_shard_probe(args, dev, P=P, ranks=(P - 1,), rounds=2)["max_over_ranks"]
+            by_world[str(P)] = {k: row[k] for k in keep}
+        by_world["8"] = {k: result["rank_shard_p8"]["max_over_ranks"][k] for k in keep}
+        result["rank_shard_by_world"] = by_world
     if world == 1 and not args.no_secondary:
         result["secondary"] = secondary_workload(args)
     if rank == 0:

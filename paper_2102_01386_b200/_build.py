@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SOURCES = ["af_host.cpp", "af_ctx.cpp", "af_cache_api.cpp", "af_norms.cu", "af_decide.cu", "af_cache.cu", "af_gemm.cu"]
-HEADERS = ["af_internal.h", "af_host.h", "af_decide.cuh"]
+HEADERS = ["af_internal.h", "af_host.h", "af_decide.cuh", "af_ptx.cuh"]
 LIB = os.path.join(PKG, "libautofreeze.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

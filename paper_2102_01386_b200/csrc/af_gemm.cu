@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include "af_internal.h"
+#include "af_ptx.cuh"
 
 namespace af {
 namespace {
@@ -36,25 +37,6 @@ constexpr int kGBBytes = kGN / 2 * kGK * 2;         // 16 KiB: this CTA's half (
 constexpr int kGStageBytes = kGABytes + kGBBytes;   // 32 KiB per CTA (64 KiB per pair)
 constexpr int kGEpiBytes = kGM * 64 * 2;                // one 128 x 64 bf16 output chunk (16 KiB), double-buffered
 constexpr int kGSmem = kGStages * kGStageBytes + 2 * kGEpiBytes + 1024;  // + slack for 1024-B alignment
-
-__device__ __forceinline__ uint32_t s_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-
-__device__ __forceinline__ void g_mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void g_mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void g_mbar_wait(uint64_t *bar, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(s_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
 
 // UMMA shared-memory descriptor of a K-major, 128-byte-swizzled bf16 tile whose
 // rows are 128 B apart (8-row swizzle atoms 1024 B apart): start address >> 4,
@@ -146,19 +128,19 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_b) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_y) : "memory");
     for (int s = 0; s < kGStages; ++s) {
-      g_mbar_init(&full[s], 1);   // (leader's) the leader producer's arrive + both CTAs' TMA bytes
-      g_mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
+      mbar_init(&full[s], 1);   // (leader's) the leader producer's arrive + both CTAs' TMA bytes
+      mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
     }
     for (int a = 0; a < 2; ++a) {
-      g_mbar_init(&info_full[a], 1);
-      g_mbar_init(&info_free[a], kGEpi / 32);           // this CTA's epilogue warps are done with tinfo[a]
-      g_mbar_init(&tmem_full[a], 1);                    // the leader's commit, multicast to both CTAs
-      g_mbar_init(&tmem_empty[a], 2 * kGEpi / 32);      // (leader's) both CTAs' epilogue warps drained it
+      mbar_init(&info_full[a], 1);
+      mbar_init(&info_free[a], kGEpi / 32);           // this CTA's epilogue warps are done with tinfo[a]
+      mbar_init(&tmem_full[a], 1);                    // the leader's commit, multicast to both CTAs
+      mbar_init(&tmem_empty[a], 2 * kGEpi / 32);      // (leader's) both CTAs' epilogue warps drained it
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {  // 512 TMEM columns in each CTA of the pair: two 128 x 256 fp32 accumulators
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s_u32(&s_tmem)),
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
                  "r"(512u));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::);
   }
@@ -176,7 +158,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
       int j = 0;
       for (int64_t u = cid; u < pair_tiles; u += C, ++j) {
         const int a = j & 1;
-        if (j >= 2) g_mbar_wait(&info_free[a], ((j >> 1) - 1) & 1);  // tinfo[a] no longer read
+        if (j >= 2) mbar_wait(&info_free[a], ((j >> 1) - 1) & 1);  // tinfo[a] no longer read
         TileInfo ti{};
         ti.nt = static_cast<int32_t>(u % p.n_tiles_n);
         const int64_t rt = (u / p.n_tiles_n) * 2 + rank;
@@ -199,22 +181,22 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
           if (first_tile) p.depth_out[ti.ex] = ti.hit ? ti.depth : -1;
         }
         tinfo[a] = ti;
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&info_full[a])) : "memory");
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&info_full[a])) : "memory");
         for (int kb = 0; kb < nk; ++kb, ++q) {
           const int s = static_cast<int>(q % kGStages);
-          if (q >= static_cast<uint32_t>(kGStages)) g_mbar_wait(&empty[s], ((q / kGStages) - 1) & 1);
+          if (q >= static_cast<uint32_t>(kGStages)) mbar_wait(&empty[s], ((q / kGStages) - 1) & 1);
           unsigned char *sa = smem + s * kGStageBytes;
           unsigned char *sb = sa + kGABytes;
-          const uint32_t bar = s_u32(&full[s]) & kPeerBitMask;  // the leader's stage barrier
-          if (rank == 0) g_mbar_expect_tx(&full[s], 2 * kGStageBytes);  // both CTAs' A and B halves
+          const uint32_t bar = smem_u32(&full[s]) & kPeerBitMask;  // the leader's stage barrier
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * kGStageBytes);  // both CTAs' A and B halves
           asm volatile(
               "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
-              "[%1, {%2, %3, %4}], [%5];" ::"r"(s_u32(sa)),
+              "[%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(sa)),
               "l"(&tmap_a), "r"(kb * kGK), "r"(ti.mt * kGM), "r"(static_cast<int>(ti.slot)), "r"(bar)
               : "memory");
           asm volatile(
               "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
-              "[%1, {%2, %3}], [%4];" ::"r"(s_u32(sb)),
+              "[%1, {%2, %3}], [%4];" ::"r"(smem_u32(sb)),
               "l"(&tmap_b), "r"(kb * kGK), "r"(ti.nt * kGN + rank * (kGN / 2)), "r"(bar)
               : "memory");
         }
@@ -226,14 +208,14 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
       int j = 0;
       for (int64_t u = cid; u < pair_tiles; u += C, ++j) {
         const int a = j & 1;
-        if (j >= 2) g_mbar_wait(&tmem_empty[a], ((j >> 1) - 1) & 1);  // accumulator a drained
+        if (j >= 2) mbar_wait(&tmem_empty[a], ((j >> 1) - 1) & 1);  // accumulator a drained
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc_cols = tmem + static_cast<uint32_t>(a * kGN);
         for (int kb = 0; kb < nk; ++kb, ++q) {
           const int s = static_cast<int>(q % kGStages);
-          g_mbar_wait(&full[s], (q / kGStages) & 1);
+          mbar_wait(&full[s], (q / kGStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa = s_u32(smem + s * kGStageBytes), sb = sa + kGABytes;
+          const uint32_t sa = smem_u32(smem + s * kGStageBytes), sb = sa + kGABytes;
 #pragma unroll
           for (int k = 0; k < kGK / 16; ++k) {
             const uint64_t da = umma_desc_sw128(sa + k * 32), db = umma_desc_sw128(sb + k * 32);
@@ -247,13 +229,13 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
           // the stage is free in both CTAs once these MMAs have read it
           asm volatile(
               "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                  s_u32(&empty[s])),
+                  smem_u32(&empty[s])),
               "h"(static_cast<uint16_t>(0x3))
               : "memory");
         }
         asm volatile(
             "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                s_u32(&tmem_full[a])),
+                smem_u32(&tmem_full[a])),
             "h"(static_cast<uint16_t>(0x3))
             : "memory");
       }
@@ -266,8 +248,8 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
     int j = 0;
     for (int64_t u = cid; u < pair_tiles; u += C, ++j) {
       const int a = j & 1;
-      g_mbar_wait(&info_full[a], (j >> 1) & 1);  // acquire the producer's tile info directly
-      g_mbar_wait(&tmem_full[a], (j >> 1) & 1);
+      mbar_wait(&info_full[a], (j >> 1) & 1);  // acquire the producer's tile info directly
+      mbar_wait(&tmem_full[a], (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const TileInfo ti = tinfo[a];
       if (ti.hit) {
@@ -301,7 +283,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
 #pragma unroll
             for (int qv = 0; qv < 4; ++qv) {
               const int chunk = 4 * h + qv;  // 16-byte chunk of the row's 128 bytes
-              const uint32_t addr = s_u32(buf) + static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
+              const uint32_t addr = smem_u32(buf) + static_cast<uint32_t>(row * 128 + ((chunk ^ (row & 7)) << 4));
               asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr),
                            "r"(pack_bf16(__uint_as_float(v[8 * qv + 0]), __uint_as_float(v[8 * qv + 1]))),
                            "r"(pack_bf16(__uint_as_float(v[8 * qv + 2]), __uint_as_float(v[8 * qv + 3]))),
@@ -315,7 +297,7 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
           if (tid == kGRoles) {
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tmap_y),
-                "r"(ti.nt * kGN + c0), "r"(static_cast<int>(y_row0)), "r"(s_u32(buf))
+                "r"(ti.nt * kGN + c0), "r"(static_cast<int>(y_row0)), "r"(smem_u32(buf))
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -332,13 +314,13 @@ __global__ void __launch_bounds__(kGThreadsP, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(s_u32(&info_free[a])) : "memory");
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&info_free[a])) : "memory");
         // "accumulator drained" on the leader's barrier, default semantics (release at
         // CTA scope): this warp's TMEM reads completed at tcgen05.wait::ld, before
         // the arrive in program order, so the leader's next MMAs into these columns
         // cannot overtake them; a .release.cluster arrive cost a GPU-wide MEMBAR
         // per tile and warp (0.7 % of the kernel, profiles/r02/r02_v44_*)
-        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(map_to_rank(s_u32(&tmem_empty[a]), 0))
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(map_to_rank(smem_u32(&tmem_empty[a]), 0))
                      : "memory");
       }
     }
