@@ -358,6 +358,11 @@ AF_API af_status af_ctx_read_record(af_ctx *ctx, int32_t interval, af_decision *
  * contexts registered locally, never launched).  The decision then uses
  * whatever rows the peers' buffers hold. */
 #define AF_DEBUG_PEERS_ARRIVED 2
+/* AF_DEBUG_UNSTAGED_TAIL (0/1): the interval end's tail takes the path of tables
+ * whose finalize pieces do not fit shared memory (chunks + segments > the
+ * finalize chunk; > 10^9 fp32 elements otherwise) at any size -- parity tests of
+ * that path. */
+#define AF_DEBUG_UNSTAGED_TAIL 3
 AF_API af_status af_ctx_set_debug(af_ctx *ctx, int32_t key, int64_t value);
 
 AF_API af_status af_ctx_destroy(af_ctx *ctx);

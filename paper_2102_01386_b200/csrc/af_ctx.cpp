@@ -66,6 +66,7 @@ struct af_ctx {
   int device = -1;                  // the device the workspace was bound on
   uint32_t dbg_tail_delay_ns = 0;   // AF_DEBUG_TAIL_DELAY_NS
   int32_t dbg_peers_arrived = 0;    // AF_DEBUG_PEERS_ARRIVED
+  int32_t dbg_unstaged_tail = 0;    // AF_DEBUG_UNSTAGED_TAIL
 
   template <typename T>
   T *at(size_t o) const {
@@ -403,6 +404,7 @@ NormParams norm_params(af_ctx *c, const void *grad_dev, bool end, bool dry) {
   p.dbg_tail_delay_ns = c->dbg_tail_delay_ns;
 
   p.dbg_peers_arrived = c->dbg_peers_arrived;
+  p.dbg_unstaged_tail = c->dbg_unstaged_tail;
   p.commit = dry ? 0 : 1;
   if (c->peers) {
     p.xworld = c->cfg.world;
@@ -964,6 +966,10 @@ af_status af_ctx_set_debug(af_ctx *c, int32_t key, int64_t value) {
     case AF_DEBUG_PEERS_ARRIVED:
       if (value != 0 && value != 1) return fail(AF_EINVAL, "peers-arrived knob is 0 or 1");
       c->dbg_peers_arrived = static_cast<int32_t>(value);
+      return AF_OK;
+    case AF_DEBUG_UNSTAGED_TAIL:
+      if (value != 0 && value != 1) return fail(AF_EINVAL, "unstaged-tail knob is 0 or 1");
+      c->dbg_unstaged_tail = static_cast<int32_t>(value);
       return AF_OK;
     default: return fail(AF_EINVAL, "unknown debug key");
   }

@@ -71,7 +71,7 @@ struct DevState {
 #define AF_ALTERNATE_ORDER 1
 #endif
 #ifndef AF_FIN_CHUNK  // tiles per finalize chunk (a multiple of the 256 threads)
-#define AF_FIN_CHUNK 256
+#define AF_FIN_CHUNK 512
 #endif
 constexpr int kFinChunk = AF_FIN_CHUNK;
 static_assert(kFinChunk % 256 == 0, "finalize chunk: whole loads per thread");
@@ -164,6 +164,7 @@ struct NormParams {
   DecideParams dec;
   uint32_t dbg_tail_delay_ns;      // AF_DEBUG_TAIL_DELAY_NS: the last CTA waits this long before its tail
   int32_t dbg_peers_arrived;       // AF_DEBUG_PEERS_ARRIVED: the exchange pushes but does not wait
+  int32_t dbg_unstaged_tail;       // AF_DEBUG_UNSTAGED_TAIL: the tail never stages the pieces
 };
 
 // Flag value a rank stores into its peers' flag slots after it timed out waiting

@@ -587,7 +587,7 @@ __device__ __forceinline__ int table_end(const NormParams &p, int f) {
 __shared__ unsigned long long *s_peer[AF_MAX_WORLD];
 struct TailPre {
   DecideIn din;
-  unsigned long long epoch;  // thread 0
+  unsigned long long epoch;
   uint32_t sticky;
 };
 // count_done: the CTA running the tail before its grid-completion count (every
@@ -599,7 +599,7 @@ __device__ __forceinline__ TailPre tail_prefetch(const NormParams &p, bool count
   TailPre pre{};
   if (p.fuse_decide) pre.din = decide_load(p.dec);
   if (p.xworld > 1 && p.end && tid < p.xworld) s_peer[tid] = p.peer_rows[tid];
-  if (tid == 0) pre.epoch = *reinterpret_cast<const volatile unsigned long long *>(&p.state->epoch);
+  pre.epoch = *reinterpret_cast<const volatile unsigned long long *>(&p.state->epoch);  // one broadcast load per warp
   pre.sticky = sticky_of(p);
   if (count_done && tid == kNormBlock - 32) {
     __threadfence();
@@ -627,13 +627,11 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Ta
   // words and its parity selects one of two buffers (a peer is at most one epoch
   // ahead: it cannot finish epoch e without this rank's row of epoch e)
   const bool xchg = p.xworld > 1 && p.end;
-  __shared__ unsigned long long s_epoch;
-  if (xchg) {
-    if (tid == 0) {
-      s_epoch = pre.epoch + 1ull;
-      const_cast<DevState *>(p.state)->epoch = s_epoch;
-    }
-    __syncthreads();
+  const unsigned long long x_epoch = pre.epoch + 1ull;  // every thread holds it: no barrier
+  __shared__ int s_timeout;
+  if (xchg && tid == 0) {
+    const_cast<DevState *>(p.state)->epoch = x_epoch;
+    s_timeout = 0;  // visible after the barrier that publishes the row
   }
   // this rank's row of the exchange matrix ss_all[world][L] (the rows the decision
   // sums), also kept in shared memory for the fused decision
@@ -662,23 +660,20 @@ __device__ __forceinline__ void tail_common(const NormParams &p, double *s_x, Ta
     // fence, no separate flag.  Then poll the own buffer until every peer's words
     // carry the epoch (bounded: a missing peer flags a timeout instead of hanging).
     __syncthreads();  // the row is published
-    const unsigned long long e = s_epoch;
+    const unsigned long long e = x_epoch;
     const uint32_t e32 = static_cast<uint32_t>(e);
     const int W = p.xworld, L = p.L, b = static_cast<int>(e & 1ull);
     const size_t my = (static_cast<size_t>(b) * W + p.xrank) * L;
     for (int i = tid; i < W * L; i += kNormBlock) {
       const int q = i / L, l = i % L;
       if (q == p.xrank) continue;
-      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(ss_row[l]));
+      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(s_ss[l]));
       const unsigned long long lo = (bits & 0xFFFFFFFFull) | (static_cast<unsigned long long>(e32) << 32);
       const unsigned long long hi = (bits >> 32) | (static_cast<unsigned long long>(e32) << 32);
       asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(s_peer[q] + 2 * (my + l)), "l"(lo),
                    "l"(hi)
                    : "memory");
     }
-    __shared__ int s_timeout;
-    if (tid == 0) s_timeout = 0;
-    __syncthreads();
     {
       // (AF_DEBUG_PEERS_ARRIVED: one read of every word, whatever epoch it holds --
       // the real path's work without the wait, for one-GPU timing of a rank)
@@ -771,7 +766,7 @@ __device__ __noinline__ void last_cta_tail(const NormParams &p, int first_tile, 
   const int tid = threadIdx.x;
   const int nch = n_end > first_tile ? (n_end - first_tile + kFinChunk - 1) / kFinChunk : 0;
   const int n_pc = nch > 0 ? nch - 1 + p.tiles[n_end - 1].seg + 1 : 0;  // last index: (nch-1) + seg(last tile)
-  const bool staged = n_pc <= kFinChunk;
+  const bool staged = n_pc <= kFinChunk && !p.dbg_unstaged_tail;
   const TailPre pre = tail_prefetch(p, count_done);
   auto *slots = reinterpret_cast<unsigned long long *>(p.part2);
   if (staged) {
@@ -836,9 +831,12 @@ __device__ __noinline__ void last_cta_tail_staged(const NormParams &p, int first
   // the other chunks' pieces: every index of [0, n_pc) outside chunk c's own
   // ([c + lA, c + lN), and [0, lA) for chunk 0)
   auto *slots = reinterpret_cast<unsigned long long *>(p.part2);
-  const bool own = (tid >= c + lA && tid < c + lN) || (c == 0 && tid < lA);
-  if (tid < n_pc && !own) s_pc[tid] = take_slot(slots + tid);
-  if (tid < n) s_p[tid] = take_slot(reinterpret_cast<unsigned long long *>(p.partials) + c0 + tid);
+  for (int i = tid; i < n_pc; i += kNormBlock) {
+    const bool own = (i >= c + lA && i < c + lN) || (c == 0 && i < lA);
+    if (!own) s_pc[i] = take_slot(slots + i);
+  }
+  for (int i = tid; i < n; i += kNormBlock)
+    s_p[i] = take_slot(reinterpret_cast<unsigned long long *>(p.partials) + c0 + i);
   __syncthreads();
   for (int l = lA + warp; l <= lB; l += kNormBlock / 32) {  // chunk c's pieces, as fin_worker forms them
     int a = s_stb[l], b = s_stb[l + 1];
@@ -1099,7 +1097,7 @@ __device__ __noinline__ int fin_worker(const NormParams &p, int first_tile, int 
     __syncthreads();
     const int c = s_c;
     if (c < 0) break;
-    if (s_tail && s_npc <= kFinChunk) {
+    if (s_tail && s_npc <= kFinChunk && !p.dbg_unstaged_tail) {
       *n_pc_out = s_npc;
       return c;  // last_cta_tail_staged reduces chunk c itself
     }

@@ -12,6 +12,7 @@ import oracle as O
 from afinputs import (bert_grad_step, bert_layout, tiny_grad_step, tiny_layout, uniform_layout,
                       f32_to_bf16_bits)
 from gpu_util import canon, compare_records, delta_host, to_device_grad
+from paper_2102_01386_b200 import _lib as L_
 
 pytestmark = pytest.mark.gpu
 
@@ -36,10 +37,13 @@ def _oracle(lay, dt, **kw):
     return O.Freezer(lay.offsets, lay.kinds, O.DT_BF16 if dt == "bf16" else O.DT_F32, **m)
 
 
-def run_both(lay, dt, step_fn, schedule, check_delta=True, fused=False, **kw):
+def run_both(lay, dt, step_fn, schedule, check_delta=True, fused=False, setup=None, **kw):
     """schedule = list of steps-per-interval; step_fn(T, t) -> numpy gradient.
-    fused=True ends each interval with af_interval_end (the bench's launch)."""
+    fused=True ends each interval with af_interval_end (the bench's launch);
+    setup(fm) runs once after the context is created (debug knobs)."""
     fm, oz = _fm(lay, dt, **kw), _oracle(lay, dt, **kw)
+    if setup is not None:
+        setup(fm)
     n_local = lay.n
     ties, recs = 0, []
     for T, S in enumerate(schedule):
@@ -312,22 +316,23 @@ def test_fake_sharded_parity(P):
     (40_000_003, 150, 1_000_001, 3_333, "f32", "delta", True),    # chunks span ~120 segments
     (80_000_003, 150, 1_000_001, 3_333, "bf16", "step_sumsq", False),   # STEP_SUMSQ tiles are 32768
     (36_000_001, 2, 17, 5, "f32", "delta", False),                # segments span many chunks
-    # more pieces (chunks + segments) than the tail stages in shared memory:
-    # the last chunk goes through part2 like the others (the unstaged tail)
-    (120_000_007, 250, 999_999, 4_097, "f32", "delta", True),
+    (120_000_007, 250, 999_999, 4_097, "f32", "delta", True),     # 250 segments, many pieces
 ])
-def test_wide_finalize_parity(n, L, pre, head, dt, acc, fused):
-    """Many finalize chunks (256 tiles each, reduced by the streaming grid's CTAs
-    as they run out of tiles; chunk sums + chunk-order combine).  Records match
-    the oracle while the frozen prefix moves the first active tile off the chunk
-    grid."""
+@pytest.mark.parametrize("unstaged", [False, True])
+def test_wide_finalize_parity(n, L, pre, head, dt, acc, fused, unstaged):
+    """Many finalize chunks (kFinChunk tiles each, reduced by the streaming grid's
+    CTAs as they run out of tiles; chunk sums + chunk-order combine).  Records
+    match the oracle while the frozen prefix moves the first active tile off the
+    chunk grid.  unstaged: AF_DEBUG_UNSTAGED_TAIL -- the tail path of tables whose
+    pieces (chunks + segments) exceed the finalize chunk (> 10^9 fp32 elements):
+    the last chunk goes through part2 like the others and the tail reads the
+    pieces from global memory."""
     lay = uniform_layout(n, L, pre=pre, head=head)
+    setup = (lambda fm: fm.set_debug(L_.AF_DEBUG_UNSTAGED_TAIL, 1)) if unstaged else None
     recs, _, fm, oz = run_both(lay, dt, _decaying_step(lay, dt, 41), [2, 1, 2, 1, 2, 1], check_delta=False,
-                               fused=fused, acc_mode=acc)
+                               fused=fused, acc_mode=acc, setup=setup)
     info = fm.info()
     assert info["n_fin_chunks"] > 1
-    if L == 250:
-        assert info["n_fin_chunks"] + L > 256  # the unstaged tail
     if L > 2:
         assert max(r[0]["boundary_after"] for r in recs) >= 1
 
