@@ -363,6 +363,11 @@ AF_API af_status af_ctx_read_record(af_ctx *ctx, int32_t interval, af_decision *
  * finalize chunk; > 10^9 fp32 elements otherwise) at any size -- parity tests of
  * that path. */
 #define AF_DEBUG_UNSTAGED_TAIL 3
+/* AF_DEBUG_FORCE_NCCL (0/1): with a communicator set (af_ctx_set_comm) and no
+ * peers, interval ends take the world > 1 route -- streaming kernel, then
+ * ncclAllGather of the per-segment rows, then the decide kernel -- even at
+ * world == 1: runs the NCCL fallback's calls on a single GPU. */
+#define AF_DEBUG_FORCE_NCCL 4
 AF_API af_status af_ctx_set_debug(af_ctx *ctx, int32_t key, int64_t value);
 
 AF_API af_status af_ctx_destroy(af_ctx *ctx);

@@ -15,7 +15,7 @@ AF_MAX_WORLD = 64
 AF_OK, AF_EINVAL, AF_ESTATE, AF_EWORKSPACE, AF_ECUDA, AF_ENCCL, AF_ENONFINITE, AF_EOWNER, AF_ERANGE = range(9)
 AF_DT_F32, AF_DT_BF16 = 0, 1
 AF_CACHE_OVERLAP_PREV = 0x1
-AF_DEBUG_TAIL_DELAY_NS, AF_DEBUG_PEERS_ARRIVED, AF_DEBUG_UNSTAGED_TAIL = 1, 2, 3
+AF_DEBUG_TAIL_DELAY_NS, AF_DEBUG_PEERS_ARRIVED, AF_DEBUG_UNSTAGED_TAIL, AF_DEBUG_FORCE_NCCL = 1, 2, 3, 4
 AF_SEG_PRE, AF_SEG_POOL, AF_SEG_HEAD = 0, 1, 2
 AF_ACC_DELTA, AF_ACC_STEP_SUMSQ = 0, 1
 AF_PCT_LINEAR, AF_PCT_NEAREST_RANK = 0, 1

@@ -114,7 +114,12 @@ class FreezingModule:
     def set_comm(self, group=None):
         """Collective: create the library's NCCL communicator (rank 0 makes the id,
         torch.distributed broadcasts it over `group`)."""
-        uid = bootstrap_nccl_id(self.rank, group, self.device)
+        if self.world == 1:  # a one-rank communicator needs no bootstrap (AF_DEBUG_FORCE_NCCL tests)
+            buf = (ctypes.c_uint8 * 128)()
+            check(lib.af_nccl_unique_id(buf), "af_nccl_unique_id")
+            uid = bytes(buf)
+        else:
+            uid = bootstrap_nccl_id(self.rank, group, self.device)
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         with torch.cuda.device(self.device):
             check(lib.af_ctx_set_comm(self._h, buf), "af_ctx_set_comm")

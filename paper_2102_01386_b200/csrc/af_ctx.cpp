@@ -67,6 +67,7 @@ struct af_ctx {
   uint32_t dbg_tail_delay_ns = 0;   // AF_DEBUG_TAIL_DELAY_NS
   int32_t dbg_peers_arrived = 0;    // AF_DEBUG_PEERS_ARRIVED
   int32_t dbg_unstaged_tail = 0;    // AF_DEBUG_UNSTAGED_TAIL
+  int32_t dbg_force_nccl = 0;       // AF_DEBUG_FORCE_NCCL
 
   template <typename T>
   T *at(size_t o) const {
@@ -458,8 +459,11 @@ af_status copy_record_if_unmapped(af_ctx *c, const DecideParams &p, af_decision 
   return AF_OK;
 }
 
+// the NCCL route: world > 1 without peers (or forced by AF_DEBUG_FORCE_NCCL)
+bool nccl_route(const af_ctx *c) { return (c->cfg.world > 1 || c->dbg_force_nccl) && !c->peers; }
+
 af_status allgather_rows(af_ctx *c, void *stream) {
-  if (c->cfg.world > 1 && c->comm && !c->peers) {
+  if (nccl_route(c) && c->comm) {
     double *rows = c->at<double>(c->o_ssall);
     ncclResult_t r = ncclAllGather(rows + static_cast<size_t>(c->cfg.rank) * c->L, rows, c->L, ncclFloat64, c->comm,
                                    static_cast<cudaStream_t>(stream));
@@ -545,7 +549,7 @@ af_status af_adamw_step(af_ctx *c, float *params_dev, float *exp_avg_dev, float 
   if (c->cfg.acc_mode != AF_ACC_DELTA) return fail(AF_ESTATE, "af_adamw_step needs acc_mode AF_ACC_DELTA");
   if (flags & ~(AF_INTERVAL_END | AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
   const bool end = flags & AF_INTERVAL_END, dry = flags & AF_DRY_RUN;
-  if (end && c->cfg.world > 1 && !c->peers && !c->comm)
+  if (end && nccl_route(c) && !c->comm)
     return fail(AF_ESTATE, "interval end with world > 1 needs peers or a communicator");
   const int mode = end ? kAdamEnd : kAdamAccum;
   NormParams p = norm_params(c, grad_dev, end, dry);
@@ -553,7 +557,7 @@ af_status af_adamw_step(af_ctx *c, float *params_dev, float *exp_avg_dev, float 
   p.exp_avg = exp_avg_dev;
   p.exp_avg_sq = exp_avg_sq_dev;
   p.adam = adam_const(*hp);
-  const bool fuse = end && (c->cfg.world == 1 || c->peers);
+  const bool fuse = end && !nccl_route(c);
   if (fuse) {
     p.fuse_decide = 1;
     p.dec = decide_params(c, dry, out_host);
@@ -600,7 +604,7 @@ af_status af_interval_end(af_ctx *c, const void *grad_dev, uint32_t flags, af_de
   if (st != AF_OK) return st;
   if (flags & ~(AF_DRY_RUN)) return fail(AF_EINVAL, "unknown flags");
   const bool dry = flags & AF_DRY_RUN;
-  if (c->cfg.world > 1 && !c->peers) {  // kernel + all-gather + decide kernel
+  if (nccl_route(c)) {  // kernel + all-gather + decide kernel
     if (!c->comm)
       return fail(AF_ESTATE, "af_interval_end with world > 1 needs peers (af_ctx_set_peers_*) or a communicator");
     st = af_layer_norms(c, grad_dev, AF_INTERVAL_END | flags, stream);
@@ -966,6 +970,10 @@ af_status af_ctx_set_debug(af_ctx *c, int32_t key, int64_t value) {
     case AF_DEBUG_PEERS_ARRIVED:
       if (value != 0 && value != 1) return fail(AF_EINVAL, "peers-arrived knob is 0 or 1");
       c->dbg_peers_arrived = static_cast<int32_t>(value);
+      return AF_OK;
+    case AF_DEBUG_FORCE_NCCL:
+      if (value != 0 && value != 1) return fail(AF_EINVAL, "force-NCCL knob is 0 or 1");
+      c->dbg_force_nccl = static_cast<int32_t>(value);
       return AF_OK;
     case AF_DEBUG_UNSTAGED_TAIL:
       if (value != 0 && value != 1) return fail(AF_EINVAL, "unstaged-tail knob is 0 or 1");

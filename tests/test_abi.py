@@ -224,6 +224,8 @@ def test_debug_knob_and_ring_read_host_checks():
     assert L.lib.af_ctx_set_debug(fm._h, L.AF_DEBUG_TAIL_DELAY_NS, 2 * 10 ** 9) == L.AF_EINVAL
     assert L.lib.af_ctx_set_debug(fm._h, L.AF_DEBUG_UNSTAGED_TAIL, 1) == L.AF_OK
     assert L.lib.af_ctx_set_debug(fm._h, L.AF_DEBUG_UNSTAGED_TAIL, 2) == L.AF_EINVAL
+    assert L.lib.af_ctx_set_debug(fm._h, L.AF_DEBUG_FORCE_NCCL, 0) == L.AF_OK
+    assert L.lib.af_ctx_set_debug(fm._h, L.AF_DEBUG_FORCE_NCCL, -1) == L.AF_EINVAL
     assert L.lib.af_ctx_set_debug(fm._h, 99, 0) == L.AF_EINVAL
     assert L.lib.af_ctx_set_debug(None, L.AF_DEBUG_TAIL_DELAY_NS, 0) == L.AF_EINVAL
     rec = L.AfDecision()

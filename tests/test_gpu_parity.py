@@ -310,6 +310,21 @@ def test_fake_sharded_parity(P):
         compare_records(decs[0], oz.update_and_decide(), lay.n_segments, tag=f"P={P} T={T}")
 
 
+# ---------------------------------------------------------------- NCCL fallback route
+
+@pytest.mark.parametrize("dt,fused", [("f32", True), ("bf16", False)])
+def test_nccl_route_on_one_gpu(dt, fused):
+    """The world > 1 route without peers -- streaming kernel, ncclAllGather of the
+    per-segment rows, decide kernel -- forced at world == 1 (AF_DEBUG_FORCE_NCCL,
+    a one-rank communicator): records match the oracle, so the fallback's calls
+    and buffers are right on real hardware (P > 1 needs more GPUs)."""
+    lay = uniform_layout(3_000_017, 7, pre=100_003, head=555)
+    setup = lambda fm: (fm.set_comm(), fm.set_debug(L_.AF_DEBUG_FORCE_NCCL, 1))  # noqa: E731
+    recs, _, fm, oz = run_both(lay, dt, _decaying_step(lay, dt, 7), [2, 1, 3, 1, 2], check_delta=True,
+                               fused=fused, setup=setup)
+    assert len(recs) == 5
+
+
 # ---------------------------------------------------------------- wide finalize
 
 @pytest.mark.parametrize("n,L,pre,head,dt,acc,fused", [
