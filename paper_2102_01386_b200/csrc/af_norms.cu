@@ -7,9 +7,11 @@
 // HBM-bound elementwise/reduction work: no tensor cores (nothing is a
 // contraction).  Design:
 //  * persistent grid sized from the occupancy query (148 SMs x resident CTAs),
-//    dynamic tile scheduler (one atomic per 64 KiB tile, index two tiles and
-//    descriptor one tile ahead, reset by the last CTA) -- balances the two dies;
-//  * 128-bit streaming loads/stores (ld/st .cs), 4 vectors in flight per thread;
+//    each CTA's first two tiles by its index, then a dynamic tile scheduler (one
+//    atomic per tile, index two tiles and descriptor one tile ahead, reset by the
+//    last CTA to count itself done) -- balances the two dies;
+//  * 128-bit streaming loads/stores, 4 (interval end) / 8 (accumulate) vectors in
+//    flight per thread;
 //  * tiles never straddle a segment, so each tile's fp64 partial belongs to one
 //    layer; the partial's reduction order is fixed by the thread mapping
 //    (4 fp64 lane accumulators -> xor-shuffle tree -> 8 warps in order), so the
@@ -19,9 +21,11 @@
 //    with one DFMA (the square is exact; only the accumulation rounds), giving
 //    norms good to ~1e-15 relative (eta needs < 5e-11);
 //  * frozen tiles (segments before the device-resident boundary f) are skipped;
-//  * the last CTA of the grid sums each segment's partials in tile order and,
-//    for the fused interval end (world == 1), runs the decision
-//    (af_decide.cuh) -- one launch per interval.
+//  * the per-tile partials are reduced in chunks by the CTAs that run out of
+//    tiles (fin_worker); the claimer of the last chunk runs the tail (staged in
+//    shared memory while the grid's last tiles stream): per-segment sums in
+//    tile order, the NVLink one-shot exchange (P > 1) and the decision
+//    (af_decide.cuh) -- one launch per interval end.
 //  * programmatic dependent launch: pdl_wait() before the first dependent read.
 #include <cuda_runtime.h>
 
