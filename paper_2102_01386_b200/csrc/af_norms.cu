@@ -71,6 +71,9 @@
 #ifndef AF_MINB_END_BF16  // bf16 interval end / STEP_SUMSQ: min resident CTAs per SM (register cap)
 #define AF_MINB_END_BF16 1
 #endif
+#ifndef AF_TIMING_FIRST  // AF_TIMING builds: tmark[1] = the first CTA out of tiles instead of the last
+#define AF_TIMING_FIRST 0
+#endif
 #ifndef AF_STATIC_FIRST  // each CTA's first two tiles by its index instead of the scheduler's atomic
 #define AF_STATIC_FIRST 1
 #endif
@@ -906,7 +909,10 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
   const int t_spec = k_first < ne_spec - ft_spec ? (p.reverse ? ne_spec - 1 - k_first : ft_spec + k_first) : -1;
   if (AF_STATIC_FIRST && tid == 0 && t_spec >= 0) d_spec = p.tiles[t_spec];
   pdl_wait();  // f, Delta and the counters are written by the preceding kernels
-  if (AF_TIMING && blockIdx.x == 0 && threadIdx.x == 0) const_cast<DevState *>(p.state)->tmark[0] = gtimer();
+  if (AF_TIMING && blockIdx.x == 0 && threadIdx.x == 0) {
+    const_cast<DevState *>(p.state)->tmark[0] = gtimer();
+    if (AF_TIMING_FIRST) const_cast<DevState *>(p.state)->tmark[1] = ~0ull;
+  }
   const int f = clamp_f(p.state->f);
   const bool spec_ok = f == f_spec;
   const int first_tile = spec_ok ? ft_spec : p.first_tile_of_f[f];
@@ -1009,7 +1015,12 @@ __global__ void __launch_bounds__(kNormBlock, (MODE == kAccum || MODE == kRsAccu
     __syncthreads();
   }
   pdl_launch_dependents();
-  if (AF_TIMING && tid == 0) const_cast<DevState *>(p.state)->tmark[1] = gtimer();
+  if (AF_TIMING && tid == 0) {  // AF_TIMING_FIRST: the FIRST CTA out of tiles (the end phase's start)
+    if (AF_TIMING_FIRST)
+      atomicMin(const_cast<unsigned long long *>(&p.state->tmark[1]), gtimer());
+    else
+      const_cast<DevState *>(p.state)->tmark[1] = gtimer();
+  }
   // finalize: a CTA out of tiles reduces chunks of partials while the grid's last
   // tiles are still streaming; the claimer of the last chunk runs the tail --
   // at once (it waits only on chunk pieces and tile partials, never on the other

@@ -7,6 +7,8 @@ after the decision; dmark[0..6] = the decision's steps).  For each context, sing
 pair around each) and a back-to-back series; prints per-phase medians in us.
 
     AF_NVCC_EXTRA="-DAF_TIMING=1" python tools/end_breakdown_probe.py
+    AF_NVCC_EXTRA="-DAF_TIMING=1 -DAF_TIMING_FIRST=1" ...   # tmark[1] = the FIRST CTA out of tiles:
+                                                           # stream_us then ends where the end phase starts
 """
 import json
 import os
