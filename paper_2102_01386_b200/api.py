@@ -233,7 +233,8 @@ class FreezingModule:
         return decision_to_dict(r, self.n_segments)
 
     def set_debug(self, key, value):
-        """af_ctx_set_debug: test / diagnostic knobs (AF_DEBUG_TAIL_DELAY_NS)."""
+        """af_ctx_set_debug: test / diagnostic knobs (include/af.h): AF_DEBUG_TAIL_DELAY_NS,
+        AF_DEBUG_PEERS_ARRIVED, AF_DEBUG_UNSTAGED_TAIL, AF_DEBUG_FORCE_NCCL."""
         check(lib.af_ctx_set_debug(self._h, int(key), int(value)), "af_ctx_set_debug")
 
     def exchange_rows(self):
