@@ -454,7 +454,8 @@ def run_ours(args, rank, world, local):
         result["rank_shard_p8"] = rank_shard_probe(args, dev)
         # the same emulation at P = 2 and 4 (one rank each): the per-GPU share of the
         # 1/2/4/8-GPU metric on this GPU, exchange stores included, NVLink wait not
-        keep = ("n_local", "interval_end_alone_us", "frac_alone", "interval_end_in_step_us", "frac_in_step")
+        keep = ("n_local", "interval_end_alone_us", "frac_alone", "interval_end_in_step_us", "frac_in_step",
+                "step_pair_us", "step_pair_frac")
         by_world = {}
         for P in (2, 4):
             row = rank_shard_probe(args, dev, P=P, ranks=(P - 1,), rounds=2)["max_over_ranks"]
@@ -971,7 +972,11 @@ def rank_shard_probe(args, dev, P=8, ranks=(0, 3, 7), rounds=3):
                "gbs_alone": round(by / (alone * 1e-3) / 1e9, 1),
                "frac_alone": round(by / (alone * 1e-3) / 1e9 / peak, 4),
                "accumulate_us": round(acc * 1e3, 2),
-               "accumulate_frac": round(n_loc * (s_g + 8) / (acc * 1e-3) / 1e9 / peak, 4)}
+               "accumulate_frac": round(n_loc * (s_g + 8) / (acc * 1e-3) / 1e9 / peak, 4),
+               # the rank's step as a whole: accumulate + interval end back to back (their
+               # L2 interplay makes the in-step marginal split between them arbitrary)
+               "step_pair_us": round(full * 1e3, 2),
+               "step_pair_frac": round((by + n_loc * (s_g + 8)) / (full * 1e-3) / 1e9 / peak, 4)}
         res[f"rank{r}"] = row
         if worst is None or row["interval_end_in_step_us"] > worst["interval_end_in_step_us"]:
             worst = dict(row, rank=r)
